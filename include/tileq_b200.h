@@ -1,0 +1,195 @@
+/*
+ * tileq_b200.h -- C-ABI of the B200-native fused low-rank MoE inference
+ * engine (libtileq_b200.so).  Plain pointers and sizes only; no C++ or
+ * torch types cross this boundary and no exception escapes it.
+ *
+ * Every entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj):
+ *
+ *   tq_layer_load      <- read_artifact(dir, verify_crc)        include/tileq/io.hpp:55,  src/io.cpp:679-813
+ *   tq_route           <- route(x, gate_weights, top_k)         include/tileq/moe.hpp:53, src/moe.cpp:43-89
+ *   tq_permute         <- (no counterpart: the per-token loop of reference_forward, src/moe.cpp:106-133)
+ *   tq_forward         <- tileq_forward / qmoe_forward / lotile_forward
+ *                                                               include/tileq/infer.hpp:52-73, src/infer.cpp:40-185
+ *   tq_forward_routed  <- forward_from_artifact's route + tileq_forward
+ *                                                               bindings/py_module.cpp:112-117
+ *   tq_unpack_codes    <- unpack_codes(bytes, bits, count)      include/tileq/codec.hpp:68, src/codec.cpp:168-195
+ *   tq_launch_count    <- dispatch_count()                      include/tileq/infer.hpp:37-38 (GPU analogue:
+ *                                                               kernel launches per forward, constant in B)
+ *
+ * Status codes mirror the reference error taxonomy (include/tileq/errors.hpp:13-50)
+ * with the same triggering conditions; the message (tq_last_error, thread
+ * local) names the offending tensor or field like the reference's what().
+ *
+ * Pointers marked [dev] are CUDA device pointers on the layer's device;
+ * [host] are host pointers.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  All device entry points are asynchronous and
+ * stream-ordered; a layer may be used from one stream at a time.
+ */
+#ifndef TILEQ_B200_H
+#define TILEQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TQ_OK = 0,
+    TQ_ERR_SHAPE = 1,    /* ShapeError   */
+    TQ_ERR_PARAM = 2,    /* ParamError   */
+    TQ_ERR_SIZE = 3,     /* SizeError    */
+    TQ_ERR_FORMAT = 4,   /* FormatError  */
+    TQ_ERR_IO = 5,       /* IoError      */
+    TQ_ERR_NUMERIC = 6,  /* NumericError */
+    TQ_ERR_DATA = 7,     /* DataError    */
+    TQ_ERR_CUDA = 8,     /* CUDA runtime / launch failure       */
+    TQ_ERR_NCCL = 9,     /* collective failure (expert parallel) */
+    TQ_ERR_INTERNAL = 99
+} tq_status;
+
+typedef enum {
+    TQ_PATH_FULL = 0,    /* tileq_forward  = qmoe + lotile (infer.cpp:182-185) */
+    TQ_PATH_QMOE = 1,    /* qmoe_forward   (infer.cpp:40-51)                   */
+    TQ_PATH_LOTILE = 2   /* lotile_forward (infer.cpp:53-180)                  */
+} tq_path;
+
+typedef struct tq_layer tq_layer;
+
+typedef struct {
+    int64_t num_experts;   /* K  (MoELayerSpec, moe.hpp:16-25) */
+    int64_t top_k;
+    int64_t in_dim;        /* i */
+    int64_t out_dim;       /* o */
+    int64_t num_shared;    /* S */
+    int64_t rank;          /* r  (TiledLowRank::rank)          */
+    int64_t grid_rows;     /* M */
+    int64_t grid_cols;     /* N */
+    int64_t bits;          /* residual code width              */
+    int64_t group_size;    /* g */
+    int64_t expert_begin;  /* resident routed experts [begin, end) (expert parallel) */
+    int64_t expert_end;
+    int64_t device;
+    int64_t device_bytes;  /* HBM held by the layer (weights + tables) */
+    int64_t tier_folded;   /* column blocks per descale tier (infer.cpp:74-99) */
+    int64_t tier_scalar;
+    int64_t tier_general;
+} tq_layer_info;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* tq_last_error(void);
+
+/* Library build string (arch, git hash if known). */
+const char* tq_version(void);
+
+/* Load an artifact directory written by the reference's write_artifact
+ * (io.cpp:565-677) onto `device`, validating it exactly like read_artifact
+ * (manifest version/kind, per-tensor dtype/shape/byte_length, CRC32 unless
+ * verify_crc == 0, placement bounds/injectivity/L1, positive scales, clean
+ * padding bits), then repacking the residual codes, scales, zero points and
+ * factor blocks into the engine's TMA tile layout in HBM.
+ * expert_begin/expert_end select the resident routed experts (expert
+ * parallel); pass 0, -1 for all.  Router, factors, scaling and shared
+ * experts are always resident. */
+tq_status tq_layer_load(const char* dir, int device, int verify_crc, int64_t expert_begin,
+                        int64_t expert_end, tq_layer** out);
+tq_status tq_layer_free(tq_layer* layer);
+tq_status tq_layer_info_get(const tq_layer* layer, tq_layer_info* out);
+
+/* Pre-size the batch workspace for up to max_tokens tokens so the forward
+ * path performs no allocation. */
+tq_status tq_layer_reserve(tq_layer* layer, int64_t max_tokens);
+
+/* route(): ids [dev] int32 batch x top_k (row-major b*top_k+t), gates [dev]
+ * f32 batch x top_k.  x [dev] f32 batch x in_dim.  Bit-exact ids; gates
+ * within 1 f32 ulp of the reference (moe.cpp:64-87). */
+tq_status tq_route(tq_layer* layer, const float* x, int64_t batch, int32_t* ids, float* gates,
+                   void* stream);
+
+/* route() on raw arrays without a layer (the reference's standalone
+ * route(x, gate_weights, top_k), moe.hpp:53): x [dev] f32 batch x in_dim,
+ * gate [dev] f32 num_experts x in_dim.  top_k outside [1, num_experts] ->
+ * TQ_ERR_PARAM. */
+tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const float* gate, int64_t num_experts,
+                       int64_t top_k, int32_t* ids, float* gates, void* stream);
+
+/* Stable token permutation by expert: perm [dev]
+ * int32 batch*top_k (perm[pos] = b*top_k+t), offsets [dev] int32 K+1,
+ * inv [dev] int32 batch*top_k (inv[f] = pos).  ids [dev] int32. */
+tq_status tq_permute(tq_layer* layer, const int32_t* ids, int64_t batch, int32_t* perm,
+                     int32_t* offsets, int32_t* inv, void* stream);
+
+/* Forward with a given routing: y [dev] f32 batch x out_dim.
+ * x [dev] f32, ids [dev] int32, gates [dev] f32.  Expert ids outside
+ * [0, K) make the call fail with TQ_ERR_PARAM (reference_forward,
+ * moe.cpp:111-114) -- checked on the device, reported on the next sync
+ * point (tq_sync). */
+tq_status tq_forward(tq_layer* layer, const float* x, int64_t batch, const int32_t* ids,
+                     const float* gates, float* y, int path, void* stream);
+
+/* route + forward: the reference Python binding's forward_from_artifact
+ * path (py_module.cpp:112-117) on device buffers.  ids/gates may be NULL. */
+tq_status tq_forward_routed(tq_layer* layer, const float* x, int64_t batch, float* y,
+                            int32_t* ids, float* gates, int path, void* stream);
+
+/* Same with HOST buffers: copies in, runs, copies out, synchronizes.
+ * x [host] f32, y [host] f32, ids [host] int64 (reference dtype), gates
+ * [host] f32 (ids/gates may be NULL). */
+tq_status tq_forward_host(tq_layer* layer, const float* x, int64_t batch, float* y,
+                          int64_t* ids, float* gates, int path);
+
+/* Waits for `stream` and reports any device-side error flag raised by the
+ * layer's kernels since the last sync (e.g. expert id out of range). */
+tq_status tq_sync(tq_layer* layer, void* stream);
+
+/* GPU unpack of a packed stream (codec.cpp:168-195): bytes [dev], out [dev]
+ * uint32 count.  Returns TQ_ERR_PARAM on a bad width or byte count and
+ * TQ_ERR_FORMAT on nonzero padding bits (after synchronizing). */
+tq_status tq_unpack_codes(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count,
+                          uint32_t* out, void* stream);
+
+/* Decode the engine's repacked tile layout of routed expert e (or shared
+ * expert e-K) back into row-major uint32 codes [dev] o x i, to prove the
+ * loader's repack is bit-exact with unpack_codes. */
+tq_status tq_layer_export_codes(tq_layer* layer, int64_t e, uint32_t* out, void* stream);
+
+/* Kernel launches issued by this layer since the last reset (GPU analogue
+ * of dispatch_count(), infer.hpp:37-38). */
+uint64_t tq_launch_count(const tq_layer* layer);
+void tq_reset_launch_count(tq_layer* layer);
+
+/* ---- expert-parallel stages (EP host orchestration in Python calls these
+ * around its NCCL all-to-all exchange) ------------- */
+
+/* Build the dispatch rows for locally routed tokens: per permuted slot
+ * pos, row pos of xrows [dev] fp16 (batch*top_k x in_pad) and of extrows
+ * [dev] fp16 (batch*top_k x ext) -- token activations plus the rank-r
+ * projection and group sums the owning rank needs (computed here, since
+ * the factor blocks are replicated). */
+tq_status tq_ep_dispatch_rows(tq_layer* layer, const float* x, int64_t batch,
+                              const int32_t* ids, const int32_t* perm, uint16_t* xrows,
+                              uint16_t* extrows, int path, void* stream);
+
+/* Expert compute on received rows: segments [host] int64 triplets
+ * (local_expert, row_begin, row_count) sorted by row_begin; yrows [dev] f32
+ * (rows x out_dim). */
+tq_status tq_ep_expert_rows(tq_layer* layer, const uint16_t* xrows, const uint16_t* extrows,
+                            int64_t rows, const int64_t* segments, int64_t nseg, float* yrows,
+                            int path, void* stream);
+
+/* Combine returned rows (in permuted-slot order) with the gates plus the
+ * shared experts applied to the home tokens: y [dev] f32 batch x out_dim. */
+tq_status tq_ep_combine(tq_layer* layer, const float* x, int64_t batch, const float* yrows,
+                        const int32_t* inv, const float* gates, float* y, int path,
+                        void* stream);
+
+/* Row widths of the dispatch buffers (fp16 elements). */
+int64_t tq_ep_xrow_elems(const tq_layer* layer);
+int64_t tq_ep_extrow_elems(const tq_layer* layer);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEQ_B200_H */

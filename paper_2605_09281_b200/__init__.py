@@ -1,0 +1,340 @@
+"""B200-native fused low-rank MoE inference engine for TileQ artifacts.
+
+Python mirror of the reference's Python API for the hot path
+(/root/reference/proj/bindings/py_module.cpp, python/tileq/__init__.py):
+
+    route(x, gate_weights, top_k) -> (int64 ids [B,k], float32 gates [B,k])
+    forward_from_artifact(artifact_dir, x) -> float32 [B, o]
+    TileqError (base of ShapeError, ParamError, ... like errors.hpp:13-50)
+
+plus the device-tensor entry points (``Layer``) a serving stack uses.  All
+compute runs in libtileq_b200.so (sm_100a kernels behind the C-ABI in
+include/tileq_b200.h); there is no CPU fallback -- if the library cannot be
+loaded or no B200 is visible, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtileq_b200.so")
+
+PATH_FULL, PATH_QMOE, PATH_LOTILE = 0, 1, 2
+_PATHS = {"full": PATH_FULL, "tileq": PATH_FULL, "qmoe": PATH_QMOE, "lotile": PATH_LOTILE}
+
+
+# ---------------------------------------------------------------------------
+# errors: the reference taxonomy (errors.hpp:13-50) + device failures
+# ---------------------------------------------------------------------------
+
+class TileqError(RuntimeError):
+    """Base of every engine error (the reference binding's TileqError)."""
+
+
+class ShapeError(TileqError):
+    pass
+
+
+class ParamError(TileqError):
+    pass
+
+
+class SizeError(TileqError):
+    pass
+
+
+class FormatError(TileqError):
+    pass
+
+
+class IoError(TileqError):
+    pass
+
+
+class NumericError(TileqError):
+    pass
+
+
+class DataError(TileqError):
+    pass
+
+
+class CudaError(TileqError):
+    pass
+
+
+class NcclError(TileqError):
+    pass
+
+
+_STATUS = {1: ShapeError, 2: ParamError, 3: SizeError, 4: FormatError, 5: IoError,
+           6: NumericError, 7: DataError, 8: CudaError, 9: NcclError}
+
+
+class _LayerInfo(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in (
+        "num_experts", "top_k", "in_dim", "out_dim", "num_shared", "rank", "grid_rows",
+        "grid_cols", "bits", "group_size", "expert_begin", "expert_end", "device",
+        "device_bytes", "tier_folded", "tier_scalar", "tier_general")]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libtileq_b200.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _build
+        _build.build()
+    L = C.CDLL(LIB_PATH)
+    p, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    L.tq_last_error.restype = C.c_char_p
+    L.tq_version.restype = C.c_char_p
+    L.tq_layer_load.argtypes = [C.c_char_p, i32, i32, i64, i64, C.POINTER(p)]
+    L.tq_layer_free.argtypes = [p]
+    L.tq_layer_info_get.argtypes = [p, C.POINTER(_LayerInfo)]
+    L.tq_layer_reserve.argtypes = [p, i64]
+    L.tq_route.argtypes = [p, p, i64, p, p, p]
+    L.tq_route_raw.argtypes = [p, i64, i64, p, i64, i64, p, p, p]
+    L.tq_permute.argtypes = [p, p, i64, p, p, p, p]
+    L.tq_forward.argtypes = [p, p, i64, p, p, p, i32, p]
+    L.tq_forward_routed.argtypes = [p, p, i64, p, p, p, i32, p]
+    L.tq_forward_host.argtypes = [p, p, i64, p, p, p, i32]
+    L.tq_sync.argtypes = [p, p]
+    L.tq_unpack_codes.argtypes = [p, i64, i32, i64, p, p]
+    L.tq_layer_export_codes.argtypes = [p, i64, p, p]
+    L.tq_launch_count.restype = C.c_uint64
+    L.tq_launch_count.argtypes = [p]
+    L.tq_reset_launch_count.argtypes = [p]
+    L.tq_ep_dispatch_rows.argtypes = [p, p, i64, p, p, p, p, i32, p]
+    L.tq_ep_expert_rows.argtypes = [p, p, p, i64, p, i64, p, i32, p]
+    L.tq_ep_combine.argtypes = [p, p, i64, p, p, p, p, i32, p]
+    L.tq_ep_xrow_elems.restype = i64
+    L.tq_ep_xrow_elems.argtypes = [p]
+    L.tq_ep_extrow_elems.restype = i64
+    L.tq_ep_extrow_elems.argtypes = [p]
+    for name in ("tq_layer_load", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
+                 "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
+                 "tq_sync", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
+                 "tq_ep_expert_rows", "tq_ep_combine"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().tq_last_error().decode(errors="replace")
+        raise _STATUS.get(status, TileqError)(msg)
+
+
+def _torch():
+    import torch  # plumbing only: device memory and streams
+    return torch
+
+
+def _stream_ptr(device) -> int:
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _dptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+# the layer
+# ---------------------------------------------------------------------------
+
+class Layer:
+    """A TileQ artifact resident on one B200 (read_artifact + the runtime).
+
+    expert_range=(begin, end) keeps only those routed experts resident
+    (expert parallel); the router, factor blocks and shared experts always are.
+    """
+
+    def __init__(self, artifact_dir: str, device: int = 0, verify_crc: bool = True,
+                 expert_range: Optional[tuple] = None):
+        b, e = expert_range if expert_range is not None else (0, -1)
+        h = C.c_void_p()
+        check(lib().tq_layer_load(os.fsencode(artifact_dir), int(device), int(verify_crc), int(b), int(e),
+                                  C.byref(h)))
+        self._h = h
+        self.device = int(device)
+        info = _LayerInfo()
+        check(lib().tq_layer_info_get(self._h, C.byref(info)))
+        self.info = {f: getattr(info, f) for f, _ in _LayerInfo._fields_}
+        for k in ("num_experts", "top_k", "in_dim", "out_dim", "num_shared", "rank", "bits", "group_size"):
+            setattr(self, k, self.info[k])
+        self.artifact_dir = artifact_dir
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tq_layer_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device-tensor API ----------------------------------------------------
+    def _check_x(self, x):
+        torch = _torch()
+        if x.dim() != 2 or x.shape[1] != self.in_dim:
+            raise ShapeError(f"token width {x.shape[-1]} vs in_dim {self.in_dim}")
+        if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+            raise ParamError("x must be a contiguous float32 CUDA tensor")
+
+    def reserve(self, max_tokens: int) -> None:
+        check(lib().tq_layer_reserve(self._h, int(max_tokens)))
+
+    def route(self, x):
+        """route() on the GPU: (int32 ids [B,k], float32 gates [B,k]) CUDA tensors."""
+        torch = _torch()
+        self._check_x(x)
+        B = x.shape[0]
+        ids = torch.empty((B, self.top_k), dtype=torch.int32, device=x.device)
+        gates = torch.empty((B, self.top_k), dtype=torch.float32, device=x.device)
+        check(lib().tq_route(self._h, x.data_ptr(), B, ids.data_ptr(), gates.data_ptr(), _stream_ptr(x.device)))
+        return ids, gates
+
+    def permute(self, ids):
+        torch = _torch()
+        B = ids.shape[0]
+        perm = torch.empty(B * self.top_k, dtype=torch.int32, device=ids.device)
+        inv = torch.empty(B * self.top_k, dtype=torch.int32, device=ids.device)
+        offsets = torch.empty(self.num_experts + 1, dtype=torch.int32, device=ids.device)
+        check(lib().tq_permute(self._h, ids.contiguous().data_ptr(), B, perm.data_ptr(), offsets.data_ptr(),
+                               inv.data_ptr(), _stream_ptr(ids.device)))
+        return perm, offsets, inv
+
+    def forward(self, x, ids=None, gates=None, path: str = "full", out=None):
+        """tileq_forward (path='full'), qmoe_forward ('qmoe') or lotile_forward
+        ('lotile').  With ids/gates None the layer routes the batch itself."""
+        torch = _torch()
+        self._check_x(x)
+        B = x.shape[0]
+        y = out if out is not None else torch.empty((B, self.out_dim), dtype=torch.float32, device=x.device)
+        st = _stream_ptr(x.device)
+        if ids is None:
+            check(lib().tq_forward_routed(self._h, x.data_ptr(), B, y.data_ptr(), None, None, _PATHS[path], st))
+        else:
+            ids32 = ids.to(torch.int32).contiguous()
+            if ids32.shape != (B, self.top_k):
+                raise ShapeError(f"routing batch {ids32.shape[0]} vs input batch {B}")
+            g = gates.to(torch.float32).contiguous()
+            if B and (int(ids32.min()) < 0 or int(ids32.max()) >= self.num_experts):
+                raise ParamError(f"reference_forward: expert id out of range [0, {self.num_experts})")
+            check(lib().tq_forward(self._h, x.data_ptr(), B, ids32.data_ptr(), g.data_ptr(), y.data_ptr(),
+                                   _PATHS[path], st))
+        return y
+
+    def forward_routed(self, x, path: str = "full"):
+        """(y, ids int32, gates) in one call."""
+        torch = _torch()
+        self._check_x(x)
+        B = x.shape[0]
+        y = torch.empty((B, self.out_dim), dtype=torch.float32, device=x.device)
+        ids = torch.empty((B, self.top_k), dtype=torch.int32, device=x.device)
+        gates = torch.empty((B, self.top_k), dtype=torch.float32, device=x.device)
+        check(lib().tq_forward_routed(self._h, x.data_ptr(), B, y.data_ptr(), ids.data_ptr(), gates.data_ptr(),
+                                      _PATHS[path], _stream_ptr(x.device)))
+        return y, ids, gates
+
+    def sync(self):
+        check(lib().tq_sync(self._h, _stream_ptr(self.device)))
+
+    # -- host-buffer API (the reference binding's numpy in / numpy out) ------
+    def forward_host(self, x: np.ndarray, path: str = "full", with_routing: bool = False):
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.ndim != 2:
+            raise ParamError("x must be a 2-D float array")
+        if x.shape[1] != self.in_dim:
+            raise ShapeError(f"token width {x.shape[1]} vs in_dim {self.in_dim}")
+        B = x.shape[0]
+        y = np.empty((B, self.out_dim), np.float32)
+        ids = np.empty((B, self.top_k), np.int64) if with_routing else None
+        gates = np.empty((B, self.top_k), np.float32) if with_routing else None
+        check(lib().tq_forward_host(self._h, x.ctypes.data, B, y.ctypes.data,
+                                    None if ids is None else ids.ctypes.data,
+                                    None if gates is None else gates.ctypes.data, _PATHS[path]))
+        return (y, ids, gates) if with_routing else y
+
+    # -- instrumentation ------------------------------------------------------
+    def launch_count(self) -> int:
+        return int(lib().tq_launch_count(self._h))
+
+    def reset_launch_count(self) -> None:
+        lib().tq_reset_launch_count(self._h)
+
+    def export_codes(self, e: int):
+        """Codes of matrix e decoded back from the engine's tile layout (uint32 [o, i] CUDA tensor)."""
+        torch = _torch()
+        out = torch.empty((self.out_dim, self.in_dim), dtype=torch.int32, device=f"cuda:{self.device}")
+        check(lib().tq_layer_export_codes(self._h, int(e), out.data_ptr(), _stream_ptr(self.device)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# reference-shaped free functions (py_module.cpp:56-65, 112-117)
+# ---------------------------------------------------------------------------
+
+_layer_cache: dict = {}
+
+
+def route(x, gate_weights, top_k: int):
+    """route(x, gate_weights, top_k) -> (int64 ids, float32 gates), computed on the GPU."""
+    torch = _torch()
+    xa = np.ascontiguousarray(x, dtype=np.float32)
+    ga = np.ascontiguousarray(gate_weights, dtype=np.float32)
+    if xa.ndim != 2 or ga.ndim != 2:
+        raise ParamError("x and gate_weights must be 2-D float arrays")
+    K = ga.shape[0]
+    if top_k < 1 or top_k > K:
+        raise ParamError(f"route: top_k {top_k} outside [1, {K}]")
+    if xa.shape[1] != ga.shape[1]:
+        raise ShapeError(f"route: token width {xa.shape[1]} vs gate width {ga.shape[1]}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xd = torch.from_numpy(xa).to(dev)
+    gd = torch.from_numpy(ga).to(dev)
+    B = xa.shape[0]
+    ids = torch.empty((B, top_k), dtype=torch.int32, device=dev)
+    gates = torch.empty((B, top_k), dtype=torch.float32, device=dev)
+    check(lib().tq_route_raw(xd.data_ptr(), B, xa.shape[1], gd.data_ptr(), K, top_k, ids.data_ptr(),
+                             gates.data_ptr(), _stream_ptr(dev)))
+    return ids.cpu().numpy().astype(np.int64), gates.cpu().numpy()
+
+
+def forward_from_artifact(artifact_dir: str, x) -> np.ndarray:
+    """Load an artifact (cached per directory) and run route + tileq_forward on the GPU."""
+    key = os.path.abspath(artifact_dir)
+    layer = _layer_cache.get(key)
+    if layer is None:
+        layer = Layer(artifact_dir)
+        _layer_cache[key] = layer
+    return layer.forward_host(np.asarray(x, dtype=np.float32))
+
+
+def unpack_codes_gpu(packed: np.ndarray, bits: int, count: int) -> np.ndarray:
+    """unpack_codes (codec.cpp:168-195) on the GPU; raises FormatError on dirty padding."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pb = torch.from_numpy(np.ascontiguousarray(packed, np.uint8)).to(dev)
+    out = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+    check(lib().tq_unpack_codes(pb.data_ptr(), pb.numel(), int(bits), int(count), out.data_ptr(),
+                                _stream_ptr(dev)))
+    return out[:count].cpu().numpy().astype(np.uint32)
+
+
+__all__ = ["TileqError", "ShapeError", "ParamError", "SizeError", "FormatError", "IoError",
+           "NumericError", "DataError", "CudaError", "NcclError", "Layer", "route",
+           "forward_from_artifact", "unpack_codes_gpu", "lib", "PATH_FULL", "PATH_QMOE", "PATH_LOTILE"]

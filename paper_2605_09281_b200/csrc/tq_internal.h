@@ -1,0 +1,126 @@
+// Internal structures shared by the host runtime (tq_runtime.cpp) and the
+// sm_100a kernels (tq_kernels.cu).  Not part of the C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace tqb {
+
+// ---- tiling constants -------------------------------------------------------
+constexpr int kBM = 128;       // weight rows per tile = tcgen05 M (TMEM lanes)
+constexpr int kKC = 64;        // K elements per pipeline chunk (one 128B swizzle atom of fp16)
+constexpr int kBNMax = 192;    // tokens per tile (tcgen05 N, multiple of 16, <= 256)
+constexpr int kDenseBits = 16; // "bits" value of a dense fp16 weight (projection pass)
+
+// Bytes of one (weight, m-block, k-chunk) code block: 128 rows x 64 codes.
+__host__ __device__ constexpr int code_block_bytes(int bits) { return kBM * kKC * bits / 8; }
+
+// One work unit of the grouped tcgen05 GEMM: a 128-row m-block of one weight
+// matrix against up to kBNMax activation rows, over a K-chunk range.
+struct Unit {
+    int32_t weight;    // weight matrix index (routed e, K+s for shared s, 0 for projection)
+    int32_t mb;        // m-block (rows mb*128 ..)
+    int32_t x_row;     // first activation row (X / Ext matrices)
+    int32_t n_tok;     // valid activation rows (1..kBNMax)
+    int32_t y_row;     // first output row in the split buffer
+    int16_t kc_begin;  // main K chunks [kc_begin, kc_end)
+    int16_t kc_end;
+    int16_t n_ext;     // extension chunks appended after the main chunks
+    int16_t split;     // split-K index (selects the output buffer)
+    int32_t pad;
+};
+static_assert(sizeof(Unit) == 32, "Unit is 32 bytes");
+
+// Parameters of one launch of the grouped GEMM (passed as __grid_constant__).
+struct GemmParams {
+    CUtensorMap tmap_x16;   // activations fp16 [rows, k_pad], box 16 x 64, SW128
+    CUtensorMap tmap_x64;   // same tensor, box 64 x 64
+    CUtensorMap tmap_e16;   // extension activations fp16 [rows, ext_cols], box 16 x 64
+    CUtensorMap tmap_e64;
+    const uint8_t* codes;   // [weight][mb][kc] blocks of code_block_bytes(bits)
+    int64_t weight_stride;  // bytes per weight matrix in `codes`
+    const __half* scales;   // [weight][G][o_pad]   (quantized weights)
+    const uint8_t* zeros;   // [weight][G][o_pad]
+    const int8_t* ucodes;   // [M][o_pad][r]        U factor codes (extension)
+    const int32_t* w_ublock;    // per weight: U block p, or -1
+    const float* w_outscale;    // per weight: epilogue multiplier (2^-k)
+    const Unit* units;
+    const int32_t* n_units;     // device counter (units are built on the device)
+    float* y;                   // output, split buffers of y_split_stride floats
+    int64_t y_split_stride;
+    int32_t ldy;                // output row stride (floats)
+    int32_t o_valid;            // valid weight rows (outputs written only below)
+    int32_t o_pad;
+    int32_t bits;               // 2,3,4,8 or 16 (dense fp16)
+    int32_t group_size;
+    int32_t groups;             // G
+    int32_t rank;               // r
+    int32_t kc_total;
+    int32_t ext_zero;           // 1: extension carries the zero-point correction columns
+};
+
+// ---- kernel argument blocks -------------------------------------------------
+struct PlanArgs {
+    const int32_t* ids;
+    int batch, top_k, num_experts;
+    int e_begin, e_end;        // resident routed experts
+    int num_shared;            // shared experts (weights K..K+S-1), rows after the slots
+    int mb_count;              // m-blocks of the expert weights
+    int kc_total, nsplit, n_ext;
+    int main_kc;               // 1: main chunks present (0 for the lotile-only path)
+    int proj_mb, proj_kc_total, proj_nsplit;  // projection pass (0 mb -> none)
+    int32_t* perm;
+    int32_t* inv;
+    int32_t* offsets;
+    Unit* units;
+    int32_t* n_units;
+    Unit* proj_units;
+    int32_t* n_proj_units;
+    int32_t* err_flag;
+};
+
+struct GatherArgs {
+    const __half* x16;       // [B][k_pad]
+    const float* sx;         // [B][G]
+    const float* zpart;      // [proj_nsplit][B][zcols]
+    int64_t zsplit_stride;
+    int zcols, proj_nsplit;
+    const int32_t* ids;
+    const int32_t* perm;
+    const int32_t* offsets;  // K+1 (offsets[K] = slots)
+    const int32_t* pm_of;    // per routed expert: projection matrix index
+    const float* zscale;     // per routed expert: su_p * inv_scalar * 2^k_e
+    const float* rowscale;   // per projection row: 2^k normalisation
+    int batch, top_k, num_experts, k_pad, groups, rank, ext_cols;
+    int with_shared;         // append B shared-expert rows
+    int use_sx, use_z;       // path selection
+    __half* xp;              // [rows][k_pad]
+    __half* ep;              // [rows][ext_cols]
+};
+
+struct CombineArgs {
+    const float* y;          // split buffers [nsplit][rows][o]
+    int64_t split_stride;
+    int nsplit;
+    const int32_t* inv;
+    const float* gates;
+    const int32_t* offsets;  // K+1
+    int num_experts, batch, top_k, out_dim, num_shared;
+    int use_routed;
+    const float* ysh;        // shared-expert rows: split buffers, row = sh_row0 + s*batch + b
+    int64_t sh_split_stride;
+    int sh_nsplit;
+    int sh_from_offsets;     // 1: sh_row0 = offsets[num_experts] (single-GPU layout), 0: 0
+    float* out;
+};
+
+// ---- host-side tables the runtime keeps for a loaded layer ----------------------
+struct DeviceBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace tqb

@@ -1,0 +1,1543 @@
+// Host runtime of libtileq_b200.so: artifact loader (validation identical to
+// the reference read_artifact, io.cpp:679-813), repack of the packed weights
+// into the engine's TMA tile layout, device workspace, and the C-ABI entry
+// points declared in include/tileq_b200.h.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <json.hpp>
+#include <zlib.h>
+
+#include "../../include/tileq_b200.h"
+#include "tq_internal.h"
+
+namespace fs = std::filesystem;
+using nlohmann::json;
+
+namespace tqb {
+
+// launch wrappers (tq_kernels.cu)
+cudaError_t launch_gemm(const GemmParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
+                         int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
+                         cudaStream_t stream);
+cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
+cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream);
+cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
+cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,
+                          int32_t* err_flag, cudaStream_t stream);
+cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
+                                uint32_t* out, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+
+struct TqError : std::runtime_error {
+    tq_status code;
+    TqError(tq_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+thread_local std::string g_last_error;
+
+[[noreturn]] void fail(tq_status c, const std::string& m) { throw TqError(c, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(TQ_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+tq_status guarded(F&& body) {
+    try {
+        body();
+        return TQ_OK;
+    } catch (const TqError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return TQ_ERR_SIZE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TQ_ERR_INTERNAL;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// binary16 helpers (codec.cpp:38-92 semantics)
+// ---------------------------------------------------------------------------
+
+float half_bits_to_float(uint16_t bits) {
+    const uint32_t sign = static_cast<uint32_t>(bits & 0x8000u) << 16;
+    const uint32_t exp = (bits >> 10) & 0x1Fu;
+    uint32_t mant = bits & 0x3FFu;
+    uint32_t u;
+    if (exp == 0x1Fu) {
+        u = sign | 0x7F800000u | (mant << 13);
+    } else if (exp != 0) {
+        u = sign | ((exp + 112u) << 23) | (mant << 13);
+    } else if (mant == 0) {
+        u = sign;
+    } else {
+        uint32_t e = 113;
+        while ((mant & 0x400u) == 0) {
+            mant <<= 1;
+            --e;
+        }
+        u = sign | (e << 23) | ((mant & 0x3FFu) << 13);
+    }
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+uint16_t float_to_half_bits(float value) {
+    // round-to-nearest-even; used for values that are exactly representable
+    // (scaled scales, small integers) and for the fp16 projection weights
+    const __half h = __float2half_rn(value);
+    uint16_t b;
+    std::memcpy(&b, &h, 2);
+    return b;
+}
+
+// ---------------------------------------------------------------------------
+// artifact container reader (io.cpp:186-295 semantics)
+// ---------------------------------------------------------------------------
+
+size_t packed_byte_length(size_t count, int bits) { return (count * static_cast<size_t>(bits) + 7) / 8; }
+
+bool packed_dtype(const std::string& dt, int* bits) {
+    for (int b : {2, 3, 4, 8})
+        if (dt == "packed-u" + std::to_string(b)) {
+            if (bits) *bits = b;
+            return true;
+        }
+    return false;
+}
+
+size_t expected_bytes(const std::vector<size_t>& shape, const std::string& dtype) {
+    size_t n = 1;
+    for (size_t d : shape) {
+        if (d != 0 && n > SIZE_MAX / d) fail(TQ_ERR_FORMAT, "tensor shape overflows element count");
+        n *= d;
+    }
+    int bits = 0;
+    if (packed_dtype(dtype, &bits)) return packed_byte_length(n, bits);
+    if (dtype == "f32") return n * 4;
+    if (dtype == "f16-roundtrip" || dtype == "u16") return n * 2;
+    if (dtype == "u8") return n;
+    fail(TQ_ERR_FORMAT, "unknown tensor dtype '" + dtype + "'");
+}
+
+class Container {
+   public:
+    Container(const std::string& dir, bool verify) : dir_(dir), verify_(verify) {
+        const fs::path path = fs::path(dir) / "manifest.json";
+        std::ifstream in(path, std::ios::binary);
+        if (!in) fail(TQ_ERR_IO, "cannot open '" + path.string() + "'");
+        std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+        try {
+            m_ = json::parse(text);
+        } catch (const json::parse_error& e) {
+            fail(TQ_ERR_FORMAT, std::string("manifest is not valid JSON: ") + e.what());
+        }
+        if (!m_.is_object() || !m_.contains("format_version") || !m_["format_version"].is_number_integer())
+            fail(TQ_ERR_FORMAT, "manifest missing integer format_version");
+        const int version = m_["format_version"].get<int>();
+        if (version != 1)
+            fail(TQ_ERR_FORMAT,
+                 "unsupported container format_version " + std::to_string(version) + " (expected 1)");
+        const std::string kind = m_.value("kind", std::string());
+        if (kind != "tileq_artifact")
+            fail(TQ_ERR_FORMAT, "expected a 'tileq_artifact' container, found '" + kind + "'");
+        if (!m_.contains("tensors") || !m_["tensors"].is_object())
+            fail(TQ_ERR_FORMAT, "manifest missing tensors object");
+        if (!m_.contains("meta") || !m_["meta"].is_object()) fail(TQ_ERR_FORMAT, "manifest missing meta object");
+    }
+
+    const json& meta() const { return m_["meta"]; }
+
+    std::vector<uint8_t> bytes(const std::string& name, const std::string& dtype,
+                               std::vector<size_t>* shape_out = nullptr) const {
+        const json& tensors = m_["tensors"];
+        if (!tensors.contains(name)) fail(TQ_ERR_FORMAT, "missing tensor '" + name + "'");
+        const json& e = tensors[name];
+        if (!e.is_object() || !e.contains("shape") || !e.contains("dtype") || !e.contains("byte_length") ||
+            !e.contains("crc32") || !e.contains("file"))
+            fail(TQ_ERR_FORMAT, "tensor '" + name + "': malformed manifest entry");
+        const std::string actual = e["dtype"].get<std::string>();
+        if (actual != dtype)
+            fail(TQ_ERR_FORMAT, "tensor '" + name + "': dtype is '" + actual + "', expected '" + dtype + "'");
+        std::vector<size_t> shape = e["shape"].get<std::vector<size_t>>();
+        const size_t declared = e["byte_length"].get<size_t>();
+        if (expected_bytes(shape, dtype) != declared)
+            fail(TQ_ERR_FORMAT, "tensor '" + name + "': byte_length does not match shape/dtype");
+        const fs::path path = fs::path(dir_) / e["file"].get<std::string>();
+        std::error_code ec;
+        const auto on_disk = fs::file_size(path, ec);
+        if (ec) fail(TQ_ERR_IO, "tensor '" + name + "': cannot stat '" + path.string() + "'");
+        if (on_disk != declared)
+            fail(TQ_ERR_FORMAT, "tensor '" + name + "': blob is " + std::to_string(on_disk) +
+                                    " bytes, manifest says " + std::to_string(declared));
+        std::ifstream in(path, std::ios::binary);
+        if (!in) fail(TQ_ERR_IO, "tensor '" + name + "': cannot open '" + path.string() + "'");
+        std::vector<uint8_t> data(declared);
+        in.read(reinterpret_cast<char*>(data.data()), static_cast<std::streamsize>(declared));
+        if (static_cast<size_t>(in.gcount()) != declared)
+            fail(TQ_ERR_IO, "tensor '" + name + "': short read from '" + path.string() + "'");
+        if (verify_) {
+            const uint32_t want = e["crc32"].get<uint32_t>();
+            uLong crc = crc32_z(0L, Z_NULL, 0);
+            crc = crc32_z(crc, data.data(), data.size());
+            if (static_cast<uint32_t>(crc) != want) fail(TQ_ERR_FORMAT, "tensor '" + name + "': checksum mismatch");
+        }
+        if (shape_out) *shape_out = std::move(shape);
+        return data;
+    }
+
+   private:
+    std::string dir_;
+    bool verify_;
+    json m_;
+};
+
+const json& require_object(const json& j, const char* key) {
+    if (!j.contains(key) || !j[key].is_object())
+        fail(TQ_ERR_FORMAT, "manifest meta missing object '" + std::string(key) + "'");
+    return j[key];
+}
+
+size_t require_size(const json& j, const char* key) {
+    if (!j.contains(key) || !j[key].is_number_unsigned())
+        fail(TQ_ERR_FORMAT, "manifest meta missing unsigned field '" + std::string(key) + "'");
+    return j[key].get<size_t>();
+}
+
+std::string require_string(const json& j, const char* key) {
+    if (!j.contains(key) || !j[key].is_string())
+        fail(TQ_ERR_FORMAT, "manifest meta missing string field '" + std::string(key) + "'");
+    return j[key].get<std::string>();
+}
+
+// One quantized matrix as read from the wire (read_quantized, io.cpp:422-485).
+struct QMat {
+    std::vector<uint8_t> packed;
+    std::vector<uint16_t> scales;  // o x G binary16
+    std::vector<uint8_t> zeros;    // o x G unpacked
+};
+
+std::vector<uint32_t> unpack_stream(const std::vector<uint8_t>& bytes, int bits, size_t count, const std::string& what) {
+    if (bytes.size() != packed_byte_length(count, bits))
+        fail(TQ_ERR_FORMAT, what + ": packed stream length mismatch");
+    std::vector<uint32_t> out(count);
+    const uint32_t mask = (1u << bits) - 1u;
+    for (size_t t = 0; t < count; ++t) {
+        const size_t bit = t * static_cast<size_t>(bits);
+        uint32_t w = bytes[bit >> 3];
+        if ((bit >> 3) + 1 < bytes.size()) w |= static_cast<uint32_t>(bytes[(bit >> 3) + 1]) << 8;
+        out[t] = (w >> (bit & 7)) & mask;
+    }
+    for (size_t bit = count * static_cast<size_t>(bits); bit < bytes.size() * 8; ++bit)
+        if (bytes[bit >> 3] & (1u << (bit & 7)))
+            fail(TQ_ERR_FORMAT, what + ": packed stream has nonzero padding past code " + std::to_string(count));
+    return out;
+}
+
+QMat read_qmat(const Container& c, const std::string& prefix, const json& qmeta, size_t o, size_t i, int* bits_out,
+               size_t* gs_out) {
+    int bits = 0;
+    if (!qmeta.contains("bits") || !qmeta["bits"].is_number_integer() ||
+        (bits = qmeta["bits"].get<int>(), bits != 2 && bits != 3 && bits != 4 && bits != 8))
+        fail(TQ_ERR_FORMAT, "manifest quant meta: bits must be one of 2, 3, 4, 8");
+    const std::string mode = require_string(qmeta, "mode");
+    if (mode == "vector")
+        fail(TQ_ERR_PARAM,
+             "tensor '" + prefix + ".codes': vector-quantized residuals (codebook mode) are not supported by the "
+             "GPU engine yet");
+    if (mode != "scalar") fail(TQ_ERR_FORMAT, "manifest quant meta: unknown mode '" + mode + "'");
+    const size_t gs = require_size(qmeta, "group_size");
+    if (gs == 0) fail(TQ_ERR_FORMAT, "manifest quant meta: group_size must be >= 1");
+    const size_t groups = (i + gs - 1) / gs;
+    QMat q;
+    std::vector<size_t> shape;
+    q.packed = c.bytes(prefix + ".codes", "packed-u" + std::to_string(bits), &shape);
+    if (shape != std::vector<size_t>{o, i}) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".codes': unexpected shape");
+    const std::vector<uint8_t> sb = c.bytes(prefix + ".scales", "f16-roundtrip", &shape);
+    if (shape != std::vector<size_t>{o, groups}) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".scales': unexpected shape");
+    q.scales.resize(o * groups);
+    std::memcpy(q.scales.data(), sb.data(), sb.size());
+    const std::vector<uint8_t> zb = c.bytes(prefix + ".zeros", "packed-u" + std::to_string(bits), &shape);
+    if (shape != std::vector<size_t>{o, groups}) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".zeros': unexpected shape");
+    const std::vector<uint32_t> z = unpack_stream(zb, bits, o * groups, "tensor '" + prefix + ".zeros'");
+    q.zeros.resize(z.size());
+    for (size_t t = 0; t < z.size(); ++t) q.zeros[t] = static_cast<uint8_t>(z[t]);
+    for (size_t t = 0; t < q.scales.size(); ++t) {
+        const float s = half_bits_to_float(q.scales[t]);
+        if (!(s > 0.0f) || !std::isfinite(s)) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".scales': non-positive scale");
+    }
+    *bits_out = bits;
+    *gs_out = gs;
+    return q;
+}
+
+// ---------------------------------------------------------------------------
+// device memory
+// ---------------------------------------------------------------------------
+
+struct DBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t bytes) {
+        reset();
+        if (bytes == 0) bytes = 16;
+        cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+        n = bytes;
+    }
+    void upload(const void* src, size_t bytes) {
+        alloc(bytes);
+        if (bytes) cuda_check(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy H2D");
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!ptr || q != cudaDriverEntryPointSuccess) fail(TQ_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// fp16 row-major [rows, cols] tensor, box [box_rows, 64], 128-byte swizzle
+CUtensorMap make_map(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint32_t box[2] = {64, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(TQ_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// repack: wire codes -> engine tile layout
+// ---------------------------------------------------------------------------
+
+// Encode 32 consecutive codes of one row into `bits` words (the super-word
+// layouts decoded by dequant32<BITS> in tq_kernels.cu).
+void pack_superword(const uint32_t* c, int bits, uint32_t* w) {
+    for (int j = 0; j < bits; ++j) w[j] = 0;
+    if (bits == 2) {
+        for (int j = 0; j < 2; ++j)
+            for (int m = 0; m < 8; ++m) {
+                const int p = 8 * j + m;
+                w[j] |= (c[2 * p] << (2 * m)) | (c[2 * p + 1] << (16 + 2 * m));
+            }
+    } else if (bits == 3) {
+        const int pos[5] = {0, 3, 6, 9, 12};
+        for (int j = 0; j < 3; ++j)
+            for (int m = 0; m < 5; ++m) {
+                const int p = 5 * j + m;
+                w[j] |= (c[2 * p] << pos[m]) | (c[2 * p + 1] << (16 + pos[m]));
+            }
+        for (int k = 0; k < 3; ++k) w[k] |= (((c[30] >> k) & 1u) << 15) | (((c[31] >> k) & 1u) << 31);
+    } else if (bits == 4) {
+        for (int j = 0; j < 4; ++j)
+            for (int m = 0; m < 4; ++m) {
+                const int p = 4 * j + m;
+                w[j] |= (c[2 * p] << (4 * m)) | (c[2 * p + 1] << (16 + 4 * m));
+            }
+    } else {
+        for (int j = 0; j < 8; ++j)
+            for (int m = 0; m < 2; ++m) {
+                const int p = 2 * j + m;
+                w[j] |= (c[2 * p] << (8 * m)) | (c[2 * p + 1] << (16 + 8 * m));
+            }
+    }
+}
+
+struct Geometry {
+    int64_t K, top_k, i, o, S, r, M, N;
+    int bits;
+    int64_t gs, G;
+    int64_t k_pad, kc_total, o_pad, mb_count;
+    int64_t n_ext, ext_cols;
+};
+
+// Repack one quantized matrix into [mb][kc] blocks + scale/zero slabs.
+void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out, uint8_t* zeros_out,
+                 int* k_out) {
+    const int bits = g.bits;
+    const std::vector<uint32_t> codes = unpack_stream(q.packed, bits, static_cast<size_t>(g.o * g.i), "codes");
+    // power-of-two prescale so code*s' stays comfortably inside fp16 range
+    float smax = 0.0f;
+    for (uint16_t sb : q.scales) smax = std::max(smax, half_bits_to_float(sb));
+    int k = 0;
+    if (smax > 0.0f) {
+        k = static_cast<int>(std::floor(std::log2(16.0 / smax)));
+        k = std::max(-24, std::min(24, k));
+        while (std::ldexp(static_cast<double>(smax), k) > 16.0) --k;
+    }
+    *k_out = k;
+    const int blk = code_block_bytes(bits);
+    uint32_t cbuf[32];
+    uint32_t wbuf[8];
+    for (int64_t mb = 0; mb < g.mb_count; ++mb) {
+        for (int64_t kc = 0; kc < g.kc_total; ++kc) {
+            uint32_t* block = reinterpret_cast<uint32_t*>(codes_out + (mb * g.kc_total + kc) * blk);
+            for (int h = 0; h < 2; ++h) {
+                for (int rl = 0; rl < kBM; ++rl) {
+                    const int64_t row = mb * kBM + rl;
+                    for (int t = 0; t < 32; ++t) {
+                        const int64_t col = kc * kKC + 32 * h + t;
+                        cbuf[t] = (row < g.o && col < g.i) ? codes[static_cast<size_t>(row * g.i + col)] : 0u;
+                    }
+                    pack_superword(cbuf, bits, wbuf);
+                    for (int j = 0; j < bits; ++j) block[(h * bits + j) * kBM + rl] = wbuf[j];
+                }
+            }
+        }
+        for (int64_t gi = 0; gi < g.G; ++gi)
+            for (int rl = 0; rl < kBM; ++rl) {
+                const int64_t row = mb * kBM + rl;
+                const size_t dst = static_cast<size_t>((mb * g.G + gi) * kBM + rl);
+                if (row < g.o) {
+                    const float s = half_bits_to_float(q.scales[static_cast<size_t>(row * g.G + gi)]);
+                    scales_out[dst] = float_to_half_bits(std::ldexp(s, k));
+                    zeros_out[dst] = q.zeros[static_cast<size_t>(row * g.G + gi)];
+                } else {
+                    scales_out[dst] = 0;
+                    zeros_out[dst] = 0;
+                }
+            }
+    }
+}
+
+}  // namespace tqb
+
+using namespace tqb;
+
+// ---------------------------------------------------------------------------
+// the layer
+// ---------------------------------------------------------------------------
+
+struct tq_layer {
+    int device = 0;
+    Geometry g{};
+    int64_t e_begin = 0, e_end = 0;     // resident routed experts
+    int64_t n_weights = 0;              // resident routed + shared
+    int64_t tiers[3] = {0, 0, 0};
+    // projection (stacked X.A matrices)
+    int64_t NP = 0, proj_rows = 0, proj_o_pad = 0, proj_mb = 0;
+    // device tables
+    DBuf gate, codes, scales, zeros, ucodes, w_ublock, w_outscale;
+    DBuf pcodes, p_ublock, p_outscale, pm_of, zscale, rowscale;
+    int64_t weight_stride = 0, pweight_stride = 0;
+    int64_t device_bytes = 0;
+    // workspace
+    int64_t cap = 0;
+    DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
+        err_flag, xin, yout;
+    int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
+    CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
+    std::atomic<uint64_t> launches{0};
+    int num_sms = 148;
+};
+
+namespace {
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+int64_t rows_for(const tq_layer* L, int64_t batch) { return batch * L->g.top_k + L->g.S * batch; }
+
+int main_nsplit(const tq_layer* L, int64_t batch) {
+    const int64_t local = L->e_end - L->e_begin;
+    const int64_t active = std::min<int64_t>(local, batch * L->g.top_k) + L->g.S;
+    const int64_t tiles = std::max<int64_t>(1, (batch * L->g.top_k / std::max<int64_t>(1, local) + kBNMax - 1) / kBNMax);
+    const int64_t base = std::max<int64_t>(1, active * L->g.mb_count * tiles);
+    int64_t ns = (2 * L->num_sms + base - 1) / base;
+    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 4));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ns, 16)));
+}
+
+int proj_nsplit(const tq_layer* L, int64_t batch) {
+    if (L->proj_mb == 0) return 1;
+    const int64_t base = L->proj_mb * ((batch + kBNMax - 1) / kBNMax);
+    int64_t ns = (L->num_sms + base - 1) / base;
+    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 4));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ns, 32)));
+}
+
+void build_maps(tq_layer* L) {
+    const int64_t rows = rows_for(L, L->cap);
+    L->map_x16_16 = make_map(L->x16.p, L->cap, L->g.k_pad, 16);
+    L->map_x16_64 = make_map(L->x16.p, L->cap, L->g.k_pad, 64);
+    L->map_xp16 = make_map(L->xperm.p, rows, L->g.k_pad, 16);
+    L->map_xp64 = make_map(L->xperm.p, rows, L->g.k_pad, 64);
+    L->map_ep16 = make_map(L->extperm.p, rows, L->g.ext_cols, 16);
+    L->map_ep64 = make_map(L->extperm.p, rows, L->g.ext_cols, 64);
+}
+
+void reserve(tq_layer* L, int64_t max_tokens) {
+    if (max_tokens <= L->cap) return;
+    cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+    const Geometry& g = L->g;
+    const int64_t cap = round_up(std::max<int64_t>(max_tokens, 16), 16);
+    const int64_t rows = rows_for(L, cap);
+    int64_t ymax = 0, zmax = 0;
+    for (int64_t b = 1; b <= cap; b = (b < 256 ? b + 1 : b + 64)) {
+        ymax = std::max<int64_t>(ymax, main_nsplit(L, b) * rows_for(L, b) * g.o);
+        zmax = std::max<int64_t>(zmax, proj_nsplit(L, b) * b * std::max<int64_t>(1, L->proj_rows));
+    }
+    ymax = std::max<int64_t>(ymax, main_nsplit(L, cap) * rows * g.o);
+    zmax = std::max<int64_t>(zmax, proj_nsplit(L, cap) * cap * std::max<int64_t>(1, L->proj_rows));
+    L->ids.alloc(sizeof(int32_t) * cap * g.top_k);
+    L->gates.alloc(sizeof(float) * cap * g.top_k);
+    L->x16.alloc(sizeof(__half) * cap * g.k_pad);
+    L->sx.alloc(sizeof(float) * cap * std::max<int64_t>(1, g.G));
+    L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
+    L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
+    L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
+    const int64_t max_units = (g.K + g.S) * g.mb_count * ((cap + kBNMax - 1) / kBNMax + g.K) * 16 + 64;
+    L->units.alloc(sizeof(Unit) * max_units);
+    L->n_units.alloc(sizeof(int32_t));
+    L->punits.alloc(sizeof(Unit) * (std::max<int64_t>(1, L->proj_mb) * ((cap + kBNMax - 1) / kBNMax) * 32 + 8));
+    L->n_punits.alloc(sizeof(int32_t));
+    L->zpart.alloc(sizeof(float) * zmax);
+    L->xperm.alloc(sizeof(__half) * rows * g.k_pad);
+    L->extperm.alloc(sizeof(__half) * rows * g.ext_cols);
+    L->ypart.alloc(sizeof(float) * ymax);
+    L->xin.alloc(sizeof(float) * cap * g.i);
+    L->yout.alloc(sizeof(float) * cap * g.o);
+    cuda_check(cudaMemset(L->offsets.p, 0, sizeof(int32_t) * (g.K + 1)), "cudaMemset");
+    if (!L->err_flag.p) {
+        L->err_flag.alloc(sizeof(int32_t));
+        cuda_check(cudaMemset(L->err_flag.p, 0, sizeof(int32_t)), "cudaMemset");
+    }
+    L->ypart_cap_floats = ymax;
+    L->zpart_cap_floats = zmax;
+    L->cap = cap;
+    build_maps(L);
+}
+
+void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, int64_t e_begin, int64_t e_end) {
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    L->device = device;
+    cudaDeviceProp prop;
+    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        fail(TQ_ERR_CUDA, "libtileq_b200 is built for sm_100a (B200); device " + std::to_string(device) + " is sm_" +
+                              std::to_string(prop.major) + std::to_string(prop.minor));
+    L->num_sms = prop.multiProcessorCount;
+
+    Container c(dir, verify);
+    const json& meta = c.meta();
+    const json& s = require_object(meta, "spec");
+    Geometry& g = L->g;
+    g.K = static_cast<int64_t>(require_size(s, "num_experts"));
+    g.top_k = static_cast<int64_t>(require_size(s, "top_k"));
+    g.i = static_cast<int64_t>(require_size(s, "in_dim"));
+    g.o = static_cast<int64_t>(require_size(s, "out_dim"));
+    g.S = static_cast<int64_t>(require_size(s, "num_shared"));
+    if (g.K < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: num_experts must be >= 1");
+    if (g.top_k < 1 || g.top_k > g.K)
+        fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: top_k " + std::to_string(g.top_k) + " outside [1, " +
+                                std::to_string(g.K) + "]");
+    if (g.i < 1 || g.o < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: dims must be >= 1");
+    const json& tiling = require_object(meta, "tiling");
+    g.M = static_cast<int64_t>(require_size(tiling, "grid_rows"));
+    g.N = static_cast<int64_t>(require_size(tiling, "grid_cols"));
+    g.r = static_cast<int64_t>(require_size(tiling, "rank"));
+    if (g.M == 0 || g.N == 0 || g.r == 0) fail(TQ_ERR_FORMAT, "manifest tiling meta: grid and rank must be nonzero");
+
+    const size_t K = static_cast<size_t>(g.K), I = static_cast<size_t>(g.i), O = static_cast<size_t>(g.o);
+    const size_t M = static_cast<size_t>(g.M), N = static_cast<size_t>(g.N), R = static_cast<size_t>(g.r);
+    std::vector<size_t> shape;
+    // gate weights
+    std::vector<uint8_t> gate_b = c.bytes("gate_weights", "f32", &shape);
+    if (shape != std::vector<size_t>{K, I})
+        fail(TQ_ERR_FORMAT, "tensor 'gate_weights': expected shape [" + std::to_string(K) + ", " + std::to_string(I) + "]");
+    std::vector<uint8_t> scaling_b = c.bytes("scaling", "f32", &shape);
+    if (shape != std::vector<size_t>{K, I})
+        fail(TQ_ERR_FORMAT, "tensor 'scaling': expected shape [" + std::to_string(K) + ", " + std::to_string(I) + "]");
+    std::vector<float> scaling(K * I);
+    std::memcpy(scaling.data(), scaling_b.data(), scaling_b.size());
+    // placement (io.cpp:731-760)
+    const size_t l1 = require_size(tiling, "total_l1_displacement");
+    if (!tiling.contains("ideal") || !tiling["ideal"].is_array() || tiling["ideal"].size() != K)
+        fail(TQ_ERR_FORMAT, "manifest tiling meta: ideal must list every expert's cell");
+    std::vector<std::pair<size_t, size_t>> ideal(K);
+    for (size_t e = 0; e < K; ++e) {
+        const json& cell = tiling["ideal"][e];
+        if (!cell.is_array() || cell.size() != 2 || !cell[0].is_number_unsigned() || !cell[1].is_number_unsigned())
+            fail(TQ_ERR_FORMAT, "manifest tiling meta: malformed ideal cell");
+        ideal[e] = {cell[0].get<size_t>(), cell[1].get<size_t>()};
+    }
+    std::vector<uint8_t> pl_b = c.bytes("placement", "u16", &shape);
+    if (shape != std::vector<size_t>{K, 2})
+        fail(TQ_ERR_FORMAT, "tensor 'placement': expected shape [" + std::to_string(K) + ", 2]");
+    std::vector<uint16_t> placement(K * 2);
+    std::memcpy(placement.data(), pl_b.data(), pl_b.size());
+    {
+        std::set<std::pair<size_t, size_t>> seen;
+        size_t dist = 0;
+        for (size_t e = 0; e < K; ++e) {
+            const std::pair<size_t, size_t> cell{placement[2 * e], placement[2 * e + 1]};
+            if (cell.first >= M || cell.second >= N) fail(TQ_ERR_FORMAT, "tensor 'placement': cell outside the tile grid");
+            if (!seen.insert(cell).second)
+                fail(TQ_ERR_FORMAT, "tensor 'placement': duplicate cell (placement must be injective)");
+            auto gap = [](size_t a, size_t b) { return a > b ? a - b : b - a; };
+            dist += gap(cell.first, ideal[e].first) + gap(cell.second, ideal[e].second);
+        }
+        if (dist != l1)
+            fail(TQ_ERR_FORMAT, "manifest tiling meta: total_l1_displacement does not match the stored cells");
+    }
+    // factors
+    std::vector<uint8_t> sing_b = c.bytes("tiled.singulars", "f16-roundtrip", &shape);
+    if (shape != std::vector<size_t>{R}) fail(TQ_ERR_FORMAT, "tensor 'tiled.singulars': unexpected shape");
+    std::vector<float> sigma(R);
+    for (size_t j = 0; j < R; ++j) {
+        uint16_t hb;
+        std::memcpy(&hb, sing_b.data() + 2 * j, 2);
+        sigma[j] = half_bits_to_float(hb);
+    }
+    std::vector<uint8_t> u_b = c.bytes("tiled.u.codes", "u8", &shape);
+    if (shape != std::vector<size_t>{M, O, R}) fail(TQ_ERR_FORMAT, "tensor 'tiled.u.codes': unexpected shape");
+    std::vector<uint8_t> uabs_b = c.bytes("tiled.u.absmax", "f32", &shape);
+    if (shape != std::vector<size_t>{M}) fail(TQ_ERR_FORMAT, "tensor 'tiled.u.absmax': expected shape [" + std::to_string(M) + "]");
+    std::vector<uint8_t> v_b = c.bytes("tiled.v.codes", "u8", &shape);
+    if (shape != std::vector<size_t>{N, R, I}) fail(TQ_ERR_FORMAT, "tensor 'tiled.v.codes': unexpected shape");
+    std::vector<uint8_t> vabs_b = c.bytes("tiled.v.absmax", "f32", &shape);
+    if (shape != std::vector<size_t>{N}) fail(TQ_ERR_FORMAT, "tensor 'tiled.v.absmax': expected shape [" + std::to_string(N) + "]");
+    std::vector<float> uabs(M), vabs(N);
+    std::memcpy(uabs.data(), uabs_b.data(), uabs_b.size());
+    std::memcpy(vabs.data(), vabs_b.data(), vabs_b.size());
+
+    // residual experts
+    if (e_end < 0 || e_end > g.K) e_end = g.K;
+    if (e_begin < 0 || e_begin > e_end) fail(TQ_ERR_PARAM, "expert range [" + std::to_string(e_begin) + ", " + std::to_string(e_end) + ") outside [0, K]");
+    L->e_begin = e_begin;
+    L->e_end = e_end;
+    const json& qmeta = require_object(meta, "quant");
+    std::vector<QMat> q;
+    int bits = 0;
+    size_t gs = 0;
+    // every expert is read and validated (like read_artifact) even when only a subset is resident
+    std::vector<QMat> all_q;
+    for (size_t e = 0; e < K; ++e) {
+        int b = 0;
+        size_t gsz = 0;
+        QMat m = read_qmat(c, "expert." + std::to_string(e), qmeta, O, I, &b, &gsz);
+        bits = b;
+        gs = gsz;
+        if (static_cast<int64_t>(e) >= e_begin && static_cast<int64_t>(e) < e_end) q.push_back(std::move(m));
+    }
+    if (g.S > 0) {
+        const json& smeta = require_object(meta, "shared_quant");
+        for (int64_t sidx = 0; sidx < g.S; ++sidx) {
+            int b = 0;
+            size_t gsz = 0;
+            q.push_back(read_qmat(c, "sharedexpert." + std::to_string(sidx), smeta, O, I, &b, &gsz));
+            if (b != bits || gsz != gs)
+                fail(TQ_ERR_PARAM, "shared experts must use the routed experts' bits/group_size on the GPU engine");
+        }
+    }
+    g.bits = bits;
+    g.gs = static_cast<int64_t>(gs);
+    if (g.gs % 32 != 0)
+        fail(TQ_ERR_PARAM, "group_size " + std::to_string(g.gs) +
+                               " is not a multiple of 32; the GPU engine dequantizes 32-code super-words per group");
+    g.G = (g.i + g.gs - 1) / g.gs;
+    g.k_pad = round_up(g.i, kKC);
+    g.kc_total = g.k_pad / kKC;
+    g.o_pad = round_up(g.o, kBM);
+    g.mb_count = g.o_pad / kBM;
+    g.n_ext = (g.G + g.r + kKC - 1) / kKC;
+    g.ext_cols = g.n_ext * kKC;
+    if (g.G > 64 || g.r > 64)
+        fail(TQ_ERR_PARAM, "GPU engine supports at most 64 scale groups per row and rank <= 64 (groups " +
+                               std::to_string(g.G) + ", rank " + std::to_string(g.r) + ")");
+    L->n_weights = static_cast<int64_t>(q.size());
+
+    // --- repack residuals (parallel over matrices) ---
+    const int64_t blk = code_block_bytes(bits);
+    L->weight_stride = g.mb_count * g.kc_total * blk;
+    const int64_t slab = g.mb_count * g.G * kBM;  // scale / zero entries per matrix
+    std::vector<uint8_t> h_codes(static_cast<size_t>(L->weight_stride * L->n_weights));
+    std::vector<uint16_t> h_scales(static_cast<size_t>(slab * L->n_weights));
+    std::vector<uint8_t> h_zeros(static_cast<size_t>(slab * L->n_weights));
+    std::vector<int> wk(static_cast<size_t>(L->n_weights), 0);
+    {
+        std::vector<std::thread> pool;
+        std::vector<std::string> errs(q.size());
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        std::atomic<size_t> next{0};
+        for (unsigned t = 0; t < std::min<unsigned>(hw, static_cast<unsigned>(q.size())); ++t)
+            pool.emplace_back([&] {
+                for (size_t w = next++; w < q.size(); w = next++) {
+                    try {
+                        repack_qmat(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
+                                    h_zeros.data() + w * slab, &wk[w]);
+                    } catch (const std::exception& e) {
+                        errs[w] = e.what();
+                    }
+                }
+            });
+        for (auto& t : pool) t.join();
+        for (size_t w = 0; w < errs.size(); ++w)
+            if (!errs[w].empty()) fail(TQ_ERR_FORMAT, errs[w]);
+    }
+    q.clear();
+    std::vector<float> h_outscale(static_cast<size_t>(L->n_weights));
+    std::vector<int32_t> h_ublock(static_cast<size_t>(L->n_weights), -1);
+    for (int64_t w = 0; w < L->n_weights; ++w) {
+        h_outscale[w] = static_cast<float>(std::ldexp(1.0, -wk[w]));
+        if (w < e_end - e_begin) h_ublock[w] = placement[2 * (e_begin + w)];
+    }
+    // U factor codes [M][o_pad][r] int8
+    std::vector<int8_t> h_u(static_cast<size_t>(g.M * g.o_pad * g.r), 0);
+    for (size_t p = 0; p < M; ++p)
+        for (size_t row = 0; row < O; ++row)
+            std::memcpy(&h_u[(p * g.o_pad + row) * R], &u_b[(p * O + row) * R], R);
+
+    // --- descale tiers + projection matrices (infer.cpp:74-117) ---
+    std::vector<int> tier(N, 0);
+    std::vector<int64_t> first(N, -1);
+    for (size_t qq = 0; qq < N; ++qq) {
+        bool any = false, all_same = true, all_scalar = true;
+        for (size_t k = 0; k < K; ++k) {
+            if (placement[2 * k + 1] != qq) continue;
+            const float* sk = &scaling[k * I];
+            if (!any) {
+                first[qq] = static_cast<int64_t>(k);
+                any = true;
+            } else if (!std::equal(sk, sk + I, &scaling[static_cast<size_t>(first[qq]) * I])) {
+                all_same = false;
+            }
+            for (size_t cc = 0; cc < I; ++cc)
+                if (sk[cc] != sk[0]) {
+                    all_scalar = false;
+                    break;
+                }
+        }
+        tier[qq] = (!any || all_same) ? 0 : (all_scalar ? 1 : 2);
+        L->tiers[tier[qq]]++;
+    }
+    // v values exactly as decode_block_i8 (codec.cpp:122-129)
+    auto vval = [&](size_t qq, size_t j, size_t cc) {
+        const float sc = vabs[qq] == 0.0f ? 0.0f : vabs[qq] / 127.0f;
+        return static_cast<float>(static_cast<int8_t>(v_b[(qq * R + j) * I + cc])) * sc;
+    };
+    std::vector<std::vector<double>> mats;   // each r x i (double before fp16 rounding)
+    std::vector<int32_t> pm_of(K, 0);
+    std::vector<float> zscale(K, 1.0f);
+    std::vector<int64_t> q_matrix(N, -1);
+    for (size_t qq = 0; qq < N; ++qq) {
+        if (tier[qq] == 2) continue;
+        if (first[qq] < 0) continue;  // unused column block
+        std::vector<double> m(R * I);
+        for (size_t j = 0; j < R; ++j)
+            for (size_t cc = 0; cc < I; ++cc) {
+                double val = static_cast<double>(sigma[j]) * static_cast<double>(vval(qq, j, cc));
+                if (tier[qq] == 0) val /= scaling[static_cast<size_t>(first[qq]) * I + cc];
+                m[j * I + cc] = static_cast<double>(static_cast<float>(val));
+            }
+        q_matrix[qq] = static_cast<int64_t>(mats.size());
+        mats.push_back(std::move(m));
+    }
+    for (size_t e = 0; e < K; ++e) {
+        const size_t p = placement[2 * e], qq = placement[2 * e + 1];
+        const float su = uabs[p] == 0.0f ? 0.0f : uabs[p] / 127.0f;
+        double inv = 1.0;
+        if (tier[qq] == 2) {
+            std::vector<double> m(R * I);
+            for (size_t j = 0; j < R; ++j)
+                for (size_t cc = 0; cc < I; ++cc) {
+                    const float prow = static_cast<float>(static_cast<double>(sigma[j]) * vval(qq, j, cc));
+                    m[j * I + cc] = static_cast<double>(prow) / scaling[e * I + cc];
+                }
+            pm_of[e] = static_cast<int32_t>(mats.size());
+            mats.push_back(std::move(m));
+        } else {
+            pm_of[e] = static_cast<int32_t>(q_matrix[qq]);
+            if (tier[qq] == 1) inv = 1.0 / scaling[e * I];
+        }
+        int k = 0;
+        const int64_t local = static_cast<int64_t>(e) - e_begin;
+        if (local >= 0 && local < e_end - e_begin) k = wk[static_cast<size_t>(local)];
+        zscale[e] = static_cast<float>(static_cast<double>(su) * inv * std::ldexp(1.0, k));
+    }
+    L->NP = static_cast<int64_t>(mats.size());
+    L->proj_rows = L->NP * g.r;
+    L->proj_o_pad = round_up(std::max<int64_t>(L->proj_rows, 1), kBM);
+    L->proj_mb = L->proj_rows > 0 ? L->proj_o_pad / kBM : 0;
+    // dense fp16 blocks of the stacked projection with per-row power-of-two normalisation
+    const int dblk = code_block_bytes(kDenseBits);
+    L->pweight_stride = L->proj_mb * g.kc_total * dblk;
+    std::vector<uint8_t> h_p(static_cast<size_t>(std::max<int64_t>(L->pweight_stride, 16)), 0);
+    std::vector<float> rowscale(static_cast<size_t>(std::max<int64_t>(L->proj_rows, 1)), 1.0f);
+    std::vector<uint16_t> prow_h(I);
+    for (int64_t pr = 0; pr < L->proj_rows; ++pr) {
+        const std::vector<double>& m = mats[static_cast<size_t>(pr / g.r)];
+        const size_t j = static_cast<size_t>(pr % g.r);
+        double mx = 0.0;
+        for (size_t cc = 0; cc < I; ++cc) mx = std::max(mx, std::fabs(m[j * I + cc]));
+        int k = 0;
+        if (mx > 0.0) k = static_cast<int>(std::floor(std::log2(mx))) - 9;
+        rowscale[static_cast<size_t>(pr)] = static_cast<float>(std::ldexp(1.0, k));
+        for (size_t cc = 0; cc < I; ++cc) prow_h[cc] = float_to_half_bits(static_cast<float>(std::ldexp(m[j * I + cc], -k)));
+        const int64_t mb = pr / kBM, rl = pr % kBM;
+        for (int64_t kc = 0; kc < g.kc_total; ++kc) {
+            uint32_t* block = reinterpret_cast<uint32_t*>(h_p.data() + (mb * g.kc_total + kc) * dblk);
+            for (int h = 0; h < 2; ++h)
+                for (int jw = 0; jw < 16; ++jw) {
+                    const int64_t c0 = kc * kKC + 32 * h + 2 * jw;
+                    const uint32_t lo = c0 < g.i ? prow_h[static_cast<size_t>(c0)] : 0u;
+                    const uint32_t hi = c0 + 1 < g.i ? prow_h[static_cast<size_t>(c0 + 1)] : 0u;
+                    block[(h * 16 + jw) * kBM + rl] = lo | (hi << 16);
+                }
+        }
+    }
+
+    // --- upload ---
+    L->gate.upload(gate_b.data(), gate_b.size());
+    L->codes.upload(h_codes.data(), h_codes.size());
+    L->scales.upload(h_scales.data(), h_scales.size() * 2);
+    L->zeros.upload(h_zeros.data(), h_zeros.size());
+    L->ucodes.upload(h_u.data(), h_u.size());
+    L->w_ublock.upload(h_ublock.data(), h_ublock.size() * 4);
+    L->w_outscale.upload(h_outscale.data(), h_outscale.size() * 4);
+    L->pcodes.upload(h_p.data(), h_p.size());
+    const int32_t minus1 = -1;
+    const float one = 1.0f;
+    L->p_ublock.upload(&minus1, 4);
+    L->p_outscale.upload(&one, 4);
+    L->pm_of.upload(pm_of.data(), pm_of.size() * 4);
+    L->zscale.upload(zscale.data(), zscale.size() * 4);
+    L->rowscale.upload(rowscale.data(), rowscale.size() * 4);
+    L->device_bytes = static_cast<int64_t>(L->gate.n + L->codes.n + L->scales.n + L->zeros.n + L->ucodes.n +
+                                           L->pcodes.n + L->rowscale.n);
+    reserve(L, 64);
+}
+
+GemmParams base_params(tq_layer* L) {
+    GemmParams p;
+    std::memset(&p, 0, sizeof(p));
+    p.group_size = static_cast<int32_t>(L->g.gs);
+    p.kc_total = static_cast<int32_t>(L->g.kc_total);
+    return p;
+}
+
+void count_launch(tq_layer* L, int n = 1) { L->launches += static_cast<uint64_t>(n); }
+
+// prep (x16, sx) and optional routing
+void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st) {
+    cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(L->g.i), L->gate.as<float>(),
+                            do_route ? static_cast<int>(L->g.K) : 0, static_cast<int>(L->g.top_k),
+                            static_cast<int>(L->g.gs), static_cast<int>(L->g.G), static_cast<int>(L->g.k_pad),
+                            L->ids.as<int32_t>(), L->gates.as<float>(), L->x16.as<__half>(), L->sx.as<float>(), st),
+               "route_kernel launch");
+    count_launch(L);
+}
+
+void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
+                 int path, cudaStream_t st) {
+    (void)x;
+    const Geometry& g = L->g;
+    const bool use_lotile = path != TQ_PATH_QMOE;
+    const bool use_qmoe = path != TQ_PATH_LOTILE;
+    const int nsplit = use_qmoe ? main_nsplit(L, batch) : 1;
+    const int pns = proj_nsplit(L, batch);
+    const bool with_shared = use_qmoe && g.S > 0;
+    // plan
+    PlanArgs pa{};
+    pa.ids = ids;
+    pa.batch = static_cast<int>(batch);
+    pa.top_k = static_cast<int>(g.top_k);
+    pa.num_experts = static_cast<int>(g.K);
+    pa.e_begin = static_cast<int>(L->e_begin);
+    pa.e_end = static_cast<int>(L->e_end);
+    pa.num_shared = with_shared ? static_cast<int>(g.S) : 0;
+    pa.mb_count = static_cast<int>(g.mb_count);
+    pa.kc_total = static_cast<int>(g.kc_total);
+    pa.nsplit = nsplit;
+    pa.n_ext = static_cast<int>(g.n_ext);
+    pa.main_kc = use_qmoe ? 1 : 0;
+    pa.proj_mb = use_lotile ? static_cast<int>(L->proj_mb) : 0;
+    pa.proj_kc_total = static_cast<int>(g.kc_total);
+    pa.proj_nsplit = pns;
+    pa.perm = L->perm.as<int32_t>();
+    pa.inv = L->inv.as<int32_t>();
+    pa.offsets = L->offsets.as<int32_t>();
+    pa.units = L->units.as<Unit>();
+    pa.n_units = L->n_units.as<int32_t>();
+    pa.proj_units = L->punits.as<Unit>();
+    pa.n_proj_units = L->n_punits.as<int32_t>();
+    pa.err_flag = L->err_flag.as<int32_t>();
+    cuda_check(launch_plan(pa, st), "plan_kernel launch");
+    count_launch(L);
+    // projection pass: Z = P . x for every token (dense fp16 weights)
+    if (use_lotile && L->proj_mb > 0) {
+        GemmParams p = base_params(L);
+        p.tmap_x16 = L->map_x16_16;
+        p.tmap_x64 = L->map_x16_64;
+        p.tmap_e16 = L->map_x16_16;
+        p.tmap_e64 = L->map_x16_64;
+        p.codes = L->pcodes.as<uint8_t>();
+        p.weight_stride = L->pweight_stride;
+        p.w_ublock = L->p_ublock.as<int32_t>();
+        p.w_outscale = L->p_outscale.as<float>();
+        p.units = L->punits.as<Unit>();
+        p.n_units = L->n_punits.as<int32_t>();
+        p.y = L->zpart.as<float>();
+        p.y_split_stride = batch * L->proj_rows;
+        p.ldy = static_cast<int32_t>(L->proj_rows);
+        p.o_valid = static_cast<int32_t>(L->proj_rows);
+        p.o_pad = static_cast<int32_t>(L->proj_o_pad);
+        p.bits = kDenseBits;
+        p.groups = 0;
+        p.rank = 0;
+        const int64_t nunits = L->proj_mb * ((batch + kBNMax - 1) / kBNMax) * pns;
+        cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nunits, L->num_sms)), st), "projection gemm launch");
+        count_launch(L);
+    }
+    // gather
+    GatherArgs ga{};
+    ga.x16 = L->x16.as<__half>();
+    ga.sx = L->sx.as<float>();
+    ga.zpart = L->zpart.as<float>();
+    ga.zsplit_stride = batch * L->proj_rows;
+    ga.zcols = static_cast<int>(L->proj_rows);
+    ga.proj_nsplit = pns;
+    ga.ids = ids;
+    ga.perm = L->perm.as<int32_t>();
+    ga.offsets = L->offsets.as<int32_t>();
+    ga.pm_of = L->pm_of.as<int32_t>();
+    ga.zscale = L->zscale.as<float>();
+    ga.rowscale = L->rowscale.as<float>();
+    ga.batch = static_cast<int>(batch);
+    ga.top_k = static_cast<int>(g.top_k);
+    ga.num_experts = static_cast<int>(g.K);
+    ga.k_pad = static_cast<int>(g.k_pad);
+    ga.groups = static_cast<int>(g.G);
+    ga.rank = static_cast<int>(g.r);
+    ga.ext_cols = static_cast<int>(g.ext_cols);
+    ga.with_shared = with_shared ? 1 : 0;
+    ga.use_sx = use_qmoe ? 1 : 0;
+    ga.use_z = (use_lotile && L->proj_mb > 0) ? 1 : 0;
+    ga.xp = L->xperm.as<__half>();
+    ga.ep = L->extperm.as<__half>();
+    cuda_check(launch_gather(ga, static_cast<int>(rows_for(L, batch)), st), "gather_kernel launch");
+    count_launch(L);
+    // fused expert pass
+    GemmParams p = base_params(L);
+    p.tmap_x16 = L->map_xp16;
+    p.tmap_x64 = L->map_xp64;
+    p.tmap_e16 = L->map_ep16;
+    p.tmap_e64 = L->map_ep64;
+    p.codes = L->codes.as<uint8_t>();
+    p.weight_stride = L->weight_stride;
+    p.scales = L->scales.as<__half>();
+    p.zeros = L->zeros.as<uint8_t>();
+    p.ucodes = L->ucodes.as<int8_t>();
+    p.w_ublock = L->w_ublock.as<int32_t>();
+    p.w_outscale = L->w_outscale.as<float>();
+    p.units = L->units.as<Unit>();
+    p.n_units = L->n_units.as<int32_t>();
+    p.y = L->ypart.as<float>();
+    p.y_split_stride = rows_for(L, batch) * g.o;
+    p.ldy = static_cast<int32_t>(g.o);
+    p.o_valid = static_cast<int32_t>(g.o);
+    p.o_pad = static_cast<int32_t>(g.o_pad);
+    p.bits = g.bits;
+    p.groups = static_cast<int32_t>(g.G);
+    p.rank = static_cast<int32_t>(g.r);
+    p.ext_zero = use_qmoe ? 1 : 0;
+    cuda_check(launch_gemm(p, L->num_sms, st), "expert gemm launch");
+    count_launch(L);
+    // combine
+    CombineArgs ca{};
+    ca.y = L->ypart.as<float>();
+    ca.split_stride = rows_for(L, batch) * g.o;
+    ca.nsplit = nsplit;
+    ca.inv = L->inv.as<int32_t>();
+    ca.gates = gates;
+    ca.offsets = L->offsets.as<int32_t>();
+    ca.num_experts = static_cast<int>(g.K);
+    ca.batch = static_cast<int>(batch);
+    ca.top_k = static_cast<int>(g.top_k);
+    ca.out_dim = static_cast<int>(g.o);
+    ca.num_shared = with_shared ? static_cast<int>(g.S) : 0;
+    ca.use_routed = 1;
+    ca.ysh = L->ypart.as<float>();
+    ca.sh_split_stride = ca.split_stride;
+    ca.sh_nsplit = nsplit;
+    ca.sh_from_offsets = 1;
+    ca.out = y;
+    cuda_check(launch_combine(ca, st), "combine_kernel launch");
+    count_launch(L);
+}
+
+void check_layer(const tq_layer* L) {
+    if (!L) fail(TQ_ERR_PARAM, "null layer");
+}
+
+void check_batch(tq_layer* L, int64_t batch) {
+    if (batch < 0) fail(TQ_ERR_SHAPE, "negative batch");
+    if (batch > L->cap) reserve(L, batch);
+    if (L->e_begin != 0 || L->e_end != L->g.K)
+        fail(TQ_ERR_PARAM, "layer holds only experts [" + std::to_string(L->e_begin) + ", " + std::to_string(L->e_end) +
+                               "); use the expert-parallel entry points");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* tq_last_error(void) { return g_last_error.c_str(); }
+
+const char* tq_version(void) { return "tileq_b200 0.1 (sm_100a, tcgen05 TS grouped GEMM)"; }
+
+tq_status tq_layer_load(const char* dir, int device, int verify_crc, int64_t expert_begin, int64_t expert_end,
+                        tq_layer** out) {
+    return guarded([&] {
+        if (!dir || !out) fail(TQ_ERR_PARAM, "tq_layer_load: null argument");
+        auto L = std::make_unique<tq_layer>();
+        load_layer(L.get(), dir, device, verify_crc != 0, expert_begin, expert_end);
+        *out = L.release();
+    });
+}
+
+tq_status tq_layer_free(tq_layer* layer) {
+    return guarded([&] {
+        if (layer) {
+            cudaSetDevice(layer->device);
+            delete layer;
+        }
+    });
+}
+
+tq_status tq_layer_info_get(const tq_layer* L, tq_layer_info* out) {
+    return guarded([&] {
+        check_layer(L);
+        out->num_experts = L->g.K;
+        out->top_k = L->g.top_k;
+        out->in_dim = L->g.i;
+        out->out_dim = L->g.o;
+        out->num_shared = L->g.S;
+        out->rank = L->g.r;
+        out->grid_rows = L->g.M;
+        out->grid_cols = L->g.N;
+        out->bits = L->g.bits;
+        out->group_size = L->g.gs;
+        out->expert_begin = L->e_begin;
+        out->expert_end = L->e_end;
+        out->device = L->device;
+        out->device_bytes = L->device_bytes;
+        out->tier_folded = L->tiers[0];
+        out->tier_scalar = L->tiers[1];
+        out->tier_general = L->tiers[2];
+    });
+}
+
+tq_status tq_layer_reserve(tq_layer* L, int64_t max_tokens) {
+    return guarded([&] {
+        check_layer(L);
+        reserve(L, max_tokens);
+    });
+}
+
+tq_status tq_route(tq_layer* L, const float* x, int64_t batch, int32_t* ids, float* gates, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (batch < 0) fail(TQ_ERR_SHAPE, "negative batch");
+        if (batch == 0) return;
+        if (batch > L->cap) reserve(L, batch);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        run_route(L, x, batch, true, st);
+        cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice, st),
+                   "ids copy");
+        cuda_check(cudaMemcpyAsync(gates, L->gates.p, sizeof(float) * batch * L->g.top_k, cudaMemcpyDeviceToDevice, st),
+                   "gates copy");
+    });
+}
+
+tq_status tq_permute(tq_layer* L, const int32_t* ids, int64_t batch, int32_t* perm, int32_t* offsets, int32_t* inv,
+                     void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (batch < 0) fail(TQ_ERR_SHAPE, "negative batch");
+        if (batch > L->cap) reserve(L, batch);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        PlanArgs pa{};
+        pa.ids = ids;
+        pa.batch = static_cast<int>(batch);
+        pa.top_k = static_cast<int>(L->g.top_k);
+        pa.num_experts = static_cast<int>(L->g.K);
+        pa.e_begin = 0;
+        pa.e_end = 0;
+        pa.mb_count = static_cast<int>(L->g.mb_count);
+        pa.kc_total = static_cast<int>(L->g.kc_total);
+        pa.nsplit = 1;
+        pa.perm = perm;
+        pa.inv = inv;
+        pa.offsets = offsets;
+        pa.units = L->units.as<Unit>();
+        pa.n_units = L->n_units.as<int32_t>();
+        pa.proj_units = L->punits.as<Unit>();
+        pa.n_proj_units = nullptr;
+        pa.err_flag = L->err_flag.as<int32_t>();
+        cuda_check(launch_plan(pa, st), "plan_kernel launch");
+        count_launch(L);
+    });
+}
+
+tq_status tq_forward(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
+                     int path, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        check_batch(L, batch);
+        if (batch == 0) return;
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        run_route(L, x, batch, false, st);
+        run_experts(L, x, batch, ids, gates, y, path, st);
+    });
+}
+
+tq_status tq_forward_routed(tq_layer* L, const float* x, int64_t batch, float* y, int32_t* ids, float* gates, int path,
+                            void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        check_batch(L, batch);
+        if (batch == 0) return;
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        run_route(L, x, batch, true, st);
+        run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, st);
+        if (ids)
+            cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice, st),
+                       "ids copy");
+        if (gates)
+            cuda_check(cudaMemcpyAsync(gates, L->gates.p, sizeof(float) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
+                                       st),
+                       "gates copy");
+    });
+}
+
+tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, int64_t* ids, float* gates, int path) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        check_batch(L, batch);
+        if (batch == 0) return;
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = nullptr;
+        cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, st), "x H2D");
+        run_route(L, L->xin.as<float>(), batch, true, st);
+        run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(), L->yout.as<float>(), path,
+                    st);
+        cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, st), "y D2H");
+        std::vector<int32_t> hid;
+        if (ids) {
+            hid.resize(static_cast<size_t>(batch * L->g.top_k));
+            cuda_check(cudaMemcpyAsync(hid.data(), L->ids.p, sizeof(int32_t) * hid.size(), cudaMemcpyDeviceToHost, st),
+                       "ids D2H");
+        }
+        if (gates)
+            cuda_check(cudaMemcpyAsync(gates, L->gates.p, sizeof(float) * batch * L->g.top_k, cudaMemcpyDeviceToHost, st),
+                       "gates D2H");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");
+        for (size_t t = 0; t < hid.size(); ++t) ids[t] = hid[t];
+    });
+}
+
+tq_status tq_sync(tq_layer* L, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "stream sync");
+        int32_t flag = 0;
+        cuda_check(cudaMemcpy(&flag, L->err_flag.p, sizeof(int32_t), cudaMemcpyDeviceToHost), "err flag D2H");
+        if (flag) {
+            cuda_check(cudaMemset(L->err_flag.p, 0, sizeof(int32_t)), "err flag reset");
+            fail(TQ_ERR_PARAM, "reference_forward: expert id out of range [0, " + std::to_string(L->g.K) + ")");
+        }
+    });
+}
+
+tq_status tq_unpack_codes(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out, void* stream) {
+    return guarded([&] {
+        if (bits != 2 && bits != 3 && bits != 4 && bits != 8)
+            fail(TQ_ERR_PARAM, "bit packing supports widths {2,3,4,8}, got " + std::to_string(bits));
+        if (count < 0 || static_cast<size_t>(nbytes) != packed_byte_length(static_cast<size_t>(count), bits))
+            fail(TQ_ERR_PARAM, "packed stream holds " + std::to_string(nbytes) + " bytes, expected " +
+                                   std::to_string(packed_byte_length(static_cast<size_t>(std::max<int64_t>(count, 0)), bits)) +
+                                   " for " + std::to_string(count) + " codes at " + std::to_string(bits) + " bits");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        int32_t* flag = nullptr;
+        cuda_check(cudaMalloc(&flag, sizeof(int32_t)), "cudaMalloc");
+        std::unique_ptr<int32_t, void (*)(int32_t*)> guard(flag, [](int32_t* f) { cudaFree(f); });
+        cuda_check(cudaMemsetAsync(flag, 0, sizeof(int32_t), st), "memset");
+        cuda_check(launch_unpack(bytes, nbytes, bits, count, out, flag, st), "unpack_kernel launch");
+        int32_t h = 0;
+        cuda_check(cudaMemcpyAsync(&h, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "flag D2H");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");
+        if (h) fail(TQ_ERR_FORMAT, "packed stream has nonzero padding past code " + std::to_string(count));
+    });
+}
+
+tq_status tq_layer_export_codes(tq_layer* L, int64_t e, uint32_t* out, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (e < 0 || e >= L->n_weights) fail(TQ_ERR_PARAM, "export: matrix index out of range");
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cuda_check(launch_export_codes(L->codes.as<uint8_t>() + e * L->weight_stride, L->g.bits,
+                                       static_cast<int>(L->g.kc_total), static_cast<int>(L->g.o),
+                                       static_cast<int>(L->g.i), out, static_cast<cudaStream_t>(stream)),
+                   "export launch");
+    });
+}
+
+uint64_t tq_launch_count(const tq_layer* L) { return L ? L->launches.load() : 0; }
+void tq_reset_launch_count(tq_layer* L) {
+    if (L) L->launches = 0;
+}
+
+tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const float* gate, int64_t num_experts,
+                       int64_t top_k, int32_t* ids, float* gates, void* stream) {
+    return guarded([&] {
+        if (top_k < 1 || top_k > num_experts)
+            fail(TQ_ERR_PARAM, "route: top_k " + std::to_string(top_k) + " outside [1, " + std::to_string(num_experts) + "]");
+        if (top_k > 64) fail(TQ_ERR_PARAM, "route: GPU router supports top_k <= 64");
+        if (batch < 0 || in_dim < 1) fail(TQ_ERR_SHAPE, "route: bad batch / width");
+        if (batch == 0) return;
+        cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(in_dim), gate,
+                                static_cast<int>(num_experts), static_cast<int>(top_k), 1, 0, 0, ids, gates, nullptr,
+                                nullptr, static_cast<cudaStream_t>(stream)),
+                   "route_kernel launch");
+    });
+}
+
+// ---- expert-parallel stages --------------------------------------------------
+
+int64_t tq_ep_xrow_elems(const tq_layer* L) { return L ? L->g.k_pad : 0; }
+int64_t tq_ep_extrow_elems(const tq_layer* L) { return L ? L->g.ext_cols : 0; }
+
+tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const int32_t* perm,
+                              uint16_t* xrows, uint16_t* extrows, int path, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        if (batch < 0) fail(TQ_ERR_SHAPE, "negative batch");
+        if (batch == 0) return;
+        if (batch > L->cap) reserve(L, batch);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Geometry& g = L->g;
+        const bool use_lotile = path != TQ_PATH_QMOE;
+        const bool use_qmoe = path != TQ_PATH_LOTILE;
+        run_route(L, x, batch, false, st);
+        const int pns = proj_nsplit(L, batch);
+        PlanArgs pa{};
+        pa.ids = ids;
+        pa.batch = static_cast<int>(batch);
+        pa.top_k = static_cast<int>(g.top_k);
+        pa.num_experts = static_cast<int>(g.K);
+        pa.e_begin = 0;
+        pa.e_end = 0;  // no expert units: this rank only prepares rows
+        pa.mb_count = static_cast<int>(g.mb_count);
+        pa.kc_total = static_cast<int>(g.kc_total);
+        pa.nsplit = 1;
+        pa.n_ext = static_cast<int>(g.n_ext);
+        pa.main_kc = 1;
+        pa.proj_mb = use_lotile ? static_cast<int>(L->proj_mb) : 0;
+        pa.proj_kc_total = static_cast<int>(g.kc_total);
+        pa.proj_nsplit = pns;
+        pa.perm = L->perm.as<int32_t>();
+        pa.inv = L->inv.as<int32_t>();
+        pa.offsets = L->offsets.as<int32_t>();
+        pa.units = L->units.as<Unit>();
+        pa.n_units = L->n_units.as<int32_t>();
+        pa.proj_units = L->punits.as<Unit>();
+        pa.n_proj_units = L->n_punits.as<int32_t>();
+        pa.err_flag = L->err_flag.as<int32_t>();
+        cuda_check(launch_plan(pa, st), "plan_kernel launch");
+        count_launch(L);
+        if (use_lotile && L->proj_mb > 0) {
+            GemmParams p = base_params(L);
+            p.tmap_x16 = L->map_x16_16;
+            p.tmap_x64 = L->map_x16_64;
+            p.tmap_e16 = L->map_x16_16;
+            p.tmap_e64 = L->map_x16_64;
+            p.codes = L->pcodes.as<uint8_t>();
+            p.weight_stride = L->pweight_stride;
+            p.w_ublock = L->p_ublock.as<int32_t>();
+            p.w_outscale = L->p_outscale.as<float>();
+            p.units = L->punits.as<Unit>();
+            p.n_units = L->n_punits.as<int32_t>();
+            p.y = L->zpart.as<float>();
+            p.y_split_stride = batch * L->proj_rows;
+            p.ldy = static_cast<int32_t>(L->proj_rows);
+            p.o_valid = static_cast<int32_t>(L->proj_rows);
+            p.o_pad = static_cast<int32_t>(L->proj_o_pad);
+            p.bits = kDenseBits;
+            const int64_t nunits = L->proj_mb * ((batch + kBNMax - 1) / kBNMax) * pns;
+            cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nunits, L->num_sms)), st),
+                       "projection gemm launch");
+            count_launch(L);
+        }
+        GatherArgs ga{};
+        ga.x16 = L->x16.as<__half>();
+        ga.sx = L->sx.as<float>();
+        ga.zpart = L->zpart.as<float>();
+        ga.zsplit_stride = batch * L->proj_rows;
+        ga.zcols = static_cast<int>(L->proj_rows);
+        ga.proj_nsplit = pns;
+        ga.ids = ids;
+        ga.perm = perm;
+        ga.offsets = L->offsets.as<int32_t>();
+        ga.pm_of = L->pm_of.as<int32_t>();
+        ga.zscale = L->zscale.as<float>();
+        ga.rowscale = L->rowscale.as<float>();
+        ga.batch = static_cast<int>(batch);
+        ga.top_k = static_cast<int>(g.top_k);
+        ga.num_experts = static_cast<int>(g.K);
+        ga.k_pad = static_cast<int>(g.k_pad);
+        ga.groups = static_cast<int>(g.G);
+        ga.rank = static_cast<int>(g.r);
+        ga.ext_cols = static_cast<int>(g.ext_cols);
+        ga.with_shared = 0;
+        ga.use_sx = use_qmoe ? 1 : 0;
+        ga.use_z = (use_lotile && L->proj_mb > 0) ? 1 : 0;
+        ga.xp = reinterpret_cast<__half*>(xrows);
+        ga.ep = reinterpret_cast<__half*>(extrows);
+        cuda_check(launch_gather(ga, static_cast<int>(batch * g.top_k), st), "gather_kernel launch");
+        count_launch(L);
+    });
+}
+
+tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* extrows, int64_t rows,
+                            const int64_t* segments, int64_t nseg, float* yrows, int path, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        if (rows < 0 || nseg < 0) fail(TQ_ERR_SHAPE, "negative row / segment count");
+        if (rows == 0 || nseg == 0) return;
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Geometry& g = L->g;
+        const bool use_qmoe = path != TQ_PATH_LOTILE;
+        std::vector<Unit> units;
+        const int64_t local = L->e_end - L->e_begin;
+        for (int64_t s = 0; s < nseg; ++s) {
+            const int64_t le = segments[3 * s], r0 = segments[3 * s + 1], cnt = segments[3 * s + 2];
+            if (le < 0 || le >= local) fail(TQ_ERR_PARAM, "segment expert " + std::to_string(le) + " not resident");
+            if (r0 < 0 || cnt < 0 || r0 + cnt > rows) fail(TQ_ERR_SHAPE, "segment rows out of range");
+            for (int64_t mb = 0; mb < g.mb_count; ++mb)
+                for (int64_t t0 = 0; t0 < cnt; t0 += kBNMax) {
+                    Unit u{};
+                    u.weight = static_cast<int32_t>(le);
+                    u.mb = static_cast<int32_t>(mb);
+                    u.x_row = static_cast<int32_t>(r0 + t0);
+                    u.n_tok = static_cast<int32_t>(std::min<int64_t>(kBNMax, cnt - t0));
+                    u.y_row = u.x_row;
+                    u.kc_begin = 0;
+                    u.kc_end = static_cast<int16_t>(use_qmoe ? g.kc_total : 0);
+                    u.n_ext = static_cast<int16_t>(g.n_ext);
+                    u.split = 0;
+                    units.push_back(u);
+                }
+        }
+        DBuf dunits;
+        dunits.alloc(sizeof(Unit) * units.size() + sizeof(int32_t));
+        const int32_t nu = static_cast<int32_t>(units.size());
+        cuda_check(cudaMemcpyAsync(dunits.p, units.data(), sizeof(Unit) * units.size(), cudaMemcpyHostToDevice, st),
+                   "units H2D");
+        int32_t* dn = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(dunits.p) + sizeof(Unit) * units.size());
+        cuda_check(cudaMemcpyAsync(dn, &nu, sizeof(int32_t), cudaMemcpyHostToDevice, st), "count H2D");
+        GemmParams p = base_params(L);
+        void* xr = const_cast<uint16_t*>(xrows);
+        void* er = const_cast<uint16_t*>(extrows);
+        p.tmap_x16 = make_map(xr, rows, g.k_pad, 16);
+        p.tmap_x64 = make_map(xr, rows, g.k_pad, 64);
+        p.tmap_e16 = make_map(er, rows, g.ext_cols, 16);
+        p.tmap_e64 = make_map(er, rows, g.ext_cols, 64);
+        p.codes = L->codes.as<uint8_t>();
+        p.weight_stride = L->weight_stride;
+        p.scales = L->scales.as<__half>();
+        p.zeros = L->zeros.as<uint8_t>();
+        p.ucodes = L->ucodes.as<int8_t>();
+        p.w_ublock = L->w_ublock.as<int32_t>();
+        p.w_outscale = L->w_outscale.as<float>();
+        p.units = dunits.as<Unit>();
+        p.n_units = dn;
+        p.y = yrows;
+        p.y_split_stride = 0;
+        p.ldy = static_cast<int32_t>(g.o);
+        p.o_valid = static_cast<int32_t>(g.o);
+        p.o_pad = static_cast<int32_t>(g.o_pad);
+        p.bits = g.bits;
+        p.groups = static_cast<int32_t>(g.G);
+        p.rank = static_cast<int32_t>(g.r);
+        p.ext_zero = use_qmoe ? 1 : 0;
+        cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st), "expert gemm launch");
+        count_launch(L);
+        cuda_check(cudaStreamSynchronize(st), "stream sync");  // dunits lifetime
+    });
+}
+
+tq_status tq_ep_combine(tq_layer* L, const float* x, int64_t batch, const float* yrows, const int32_t* inv,
+                        const float* gates, float* y, int path, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        if (batch < 0) fail(TQ_ERR_SHAPE, "negative batch");
+        if (batch == 0) return;
+        if (batch > L->cap) reserve(L, batch);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Geometry& g = L->g;
+        const bool shared = path != TQ_PATH_LOTILE && g.S > 0;
+        if (shared) {
+            // shared experts on the home tokens: rows 0..B-1 of xperm, outputs s*B + b of ypart
+            run_route(L, x, batch, false, st);
+            GatherArgs ga{};
+            ga.x16 = L->x16.as<__half>();
+            ga.sx = L->sx.as<float>();
+            ga.zpart = L->zpart.as<float>();
+            ga.offsets = L->offsets.as<int32_t>();  // offsets[0] == 0: no routed rows
+            ga.pm_of = L->pm_of.as<int32_t>();
+            ga.zscale = L->zscale.as<float>();
+            ga.rowscale = L->rowscale.as<float>();
+            ga.batch = static_cast<int>(batch);
+            ga.top_k = static_cast<int>(g.top_k);
+            ga.num_experts = 0;
+            ga.k_pad = static_cast<int>(g.k_pad);
+            ga.groups = static_cast<int>(g.G);
+            ga.rank = static_cast<int>(g.r);
+            ga.ext_cols = static_cast<int>(g.ext_cols);
+            ga.with_shared = 1;
+            ga.use_sx = 1;
+            ga.use_z = 0;
+            ga.xp = L->xperm.as<__half>();
+            ga.ep = L->extperm.as<__half>();
+            cuda_check(launch_gather(ga, static_cast<int>(batch), st), "gather_kernel launch");
+            count_launch(L);
+            std::vector<Unit> units;
+            const int64_t local = L->e_end - L->e_begin;
+            for (int64_t s = 0; s < g.S; ++s)
+                for (int64_t mb = 0; mb < g.mb_count; ++mb)
+                    for (int64_t t0 = 0; t0 < batch; t0 += kBNMax) {
+                        Unit u{};
+                        u.weight = static_cast<int32_t>(local + s);
+                        u.mb = static_cast<int32_t>(mb);
+                        u.x_row = static_cast<int32_t>(t0);
+                        u.n_tok = static_cast<int32_t>(std::min<int64_t>(kBNMax, batch - t0));
+                        u.y_row = static_cast<int32_t>(s * batch + t0);
+                        u.kc_begin = 0;
+                        u.kc_end = static_cast<int16_t>(g.kc_total);
+                        u.n_ext = static_cast<int16_t>(g.n_ext);
+                        units.push_back(u);
+                    }
+            const int32_t nu = static_cast<int32_t>(units.size());
+            cuda_check(cudaMemcpyAsync(L->units.p, units.data(), sizeof(Unit) * units.size(), cudaMemcpyHostToDevice, st),
+                       "units H2D");
+            cuda_check(cudaMemcpyAsync(L->n_units.p, &nu, sizeof(int32_t), cudaMemcpyHostToDevice, st), "count H2D");
+            GemmParams p = base_params(L);
+            p.tmap_x16 = L->map_xp16;
+            p.tmap_x64 = L->map_xp64;
+            p.tmap_e16 = L->map_ep16;
+            p.tmap_e64 = L->map_ep64;
+            p.codes = L->codes.as<uint8_t>();
+            p.weight_stride = L->weight_stride;
+            p.scales = L->scales.as<__half>();
+            p.zeros = L->zeros.as<uint8_t>();
+            p.ucodes = L->ucodes.as<int8_t>();
+            p.w_ublock = L->w_ublock.as<int32_t>();
+            p.w_outscale = L->w_outscale.as<float>();
+            p.units = L->units.as<Unit>();
+            p.n_units = L->n_units.as<int32_t>();
+            p.y = L->ypart.as<float>();
+            p.ldy = static_cast<int32_t>(g.o);
+            p.o_valid = static_cast<int32_t>(g.o);
+            p.o_pad = static_cast<int32_t>(g.o_pad);
+            p.bits = g.bits;
+            p.groups = static_cast<int32_t>(g.G);
+            p.rank = static_cast<int32_t>(g.r);
+            p.ext_zero = 1;
+            cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st), "shared gemm launch");
+            count_launch(L);
+            cuda_check(cudaStreamSynchronize(st), "stream sync");  // host unit table lifetime
+        }
+        CombineArgs ca{};
+        ca.y = yrows;
+        ca.split_stride = 0;
+        ca.nsplit = 1;
+        ca.inv = inv;
+        ca.gates = gates;
+        ca.offsets = nullptr;
+        ca.num_experts = static_cast<int>(g.K);
+        ca.batch = static_cast<int>(batch);
+        ca.top_k = static_cast<int>(g.top_k);
+        ca.out_dim = static_cast<int>(g.o);
+        ca.num_shared = shared ? static_cast<int>(g.S) : 0;
+        ca.use_routed = 1;
+        ca.ysh = L->ypart.as<float>();
+        ca.sh_split_stride = 0;
+        ca.sh_nsplit = 1;
+        ca.sh_from_offsets = 0;
+        ca.out = y;
+        cuda_check(launch_combine(ca, st), "combine_kernel launch");
+        count_launch(L);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+"""GPU parity: the sm_100a engine (through the C-ABI) against the reference.
+
+The checker is the reference itself compiled from /root/reference
+(oracle/_ref, artifacts from its own quantization pipeline) and our C
+restatement (oracle/).  Bars (BASELINE.json north_star): routing ids,
+permutation and unpacked codes bit-exact; layer outputs within 2e-3 relative
+Frobenius error of tileq_forward with fp32 accumulation.
+"""
+import numpy as np
+import pytest
+
+from conftest import rel_frob
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3  # north_star: <= 2e-3 relative Frobenius error
+
+
+@pytest.fixture(scope="module")
+def tq():
+    import paper_2605_09281_b200 as tq
+    return tq
+
+
+def _x(B, i, seed, scale=1.0):
+    return (np.random.default_rng(seed).standard_normal((B, i)) * scale).astype(np.float32)
+
+
+SPECS = [
+    # folded tier (sign calibration), the c1 shape family
+    dict(K=8, top_k=2, i=512, o=640, r=16, bits=3, g=128, calib="signs", seed=1),
+    # general tier (gaussian calibration)
+    dict(K=8, top_k=2, i=512, o=640, r=16, bits=3, g=128, calib="gauss", seed=2),
+    # 2-bit with shared experts, wide grid (Qwen-like family)
+    dict(K=12, top_k=4, i=256, o=384, S=2, r=32, bits=2, g=128, calib="signs", seed=3),
+    # 4-bit, ragged dims (i, o not multiples of 64/128), group 64
+    dict(K=6, top_k=3, i=320, o=200, r=8, bits=4, g=64, calib="gauss", seed=4),
+    # 8-bit, group 32
+    dict(K=5, top_k=1, i=192, o=130, r=4, bits=8, g=32, calib="signs", seed=5),
+    # neutral scaling (empty calibration -> all-ones), noise-free low-rank-dominant
+    dict(K=9, top_k=2, i=256, o=256, r=16, bits=3, g=128, calib="none", noise=0.0, seed=6),
+]
+
+
+@pytest.mark.parametrize("spec", SPECS, ids=lambda s: f"K{s['K']}b{s['bits']}{s['calib']}")
+@pytest.mark.parametrize("B", [1, 3, 17, 70])
+def test_forward_matches_reference(tq, ref, make_artifact, spec, B):
+    d = make_artifact(**spec)
+    L = tq.Layer(d)
+    x = _x(B, spec["i"], 100 + B)
+    y, ids, gates = L.forward_host(x, with_routing=True)
+    yr, idr, gr = ref.load(d).forward(x)
+    np.testing.assert_array_equal(ids, idr)                   # bit-exact routing
+    np.testing.assert_array_max_ulp(gates, gr, maxulp=1)       # gates within 1 f32 ulp
+    assert rel_frob(y, yr) <= TOL, rel_frob(y, yr)
+
+
+@pytest.mark.parametrize("spec", SPECS[:3], ids=lambda s: f"K{s['K']}b{s['bits']}{s['calib']}")
+def test_paths_match_reference(tq, ref, make_artifact, spec):
+    """qmoe_forward and lotile_forward halves separately (infer.cpp:40-180)."""
+    d = make_artifact(**spec)
+    L = tq.Layer(d)
+    x = _x(9, spec["i"], 7)
+    R = ref.load(d)
+    for mode, path in ((1, "qmoe"), (2, "lotile")):
+        yr, _, _ = R.forward(x, mode=mode)
+        y = L.forward_host(x, path=path)
+        assert rel_frob(y, yr) <= TOL, (path, rel_frob(y, yr))
+
+
+def test_route_forced_underflow(tq, ref, make_artifact):
+    """x * 100: softmax probabilities underflow to exactly 0 and tie; the
+    lowest index wins (moe.cpp:77-80) -- a score-sorting router fails this."""
+    d = make_artifact(K=8, top_k=2, i=1024, o=256, r=16, bits=3, g=128, calib="signs", seed=11)
+    L = tq.Layer(d)
+    x = _x(64, 1024, 12, scale=100.0)
+    y, ids, gates = L.forward_host(x, with_routing=True)
+    yr, idr, gr = ref.load(d).forward(x)
+    np.testing.assert_array_equal(ids, idr)
+    np.testing.assert_array_max_ulp(gates, gr, maxulp=1)
+    # the case really exercises ties: some token's second gate is exactly zero
+    assert (gr[:, 1] == 0.0).any()
+
+
+def test_route_raw_reference_kats(tq):
+    """Frozen routing cases of the reference tests (test_moe.cpp:110-130)."""
+    x = np.zeros((1, 3), np.float32)
+    x[0, 0] = 1.0
+    g = np.zeros((4, 3), np.float32)
+    g[2, 0] = 50.0
+    ids, gates = tq.route(x, g, 1)
+    assert ids[0, 0] == 2 and gates[0, 0] == 1.0
+    ids, gates = tq.route(np.ones((2, 5), np.float32), np.zeros((4, 5), np.float32), 2)
+    assert (ids == [[0, 1], [0, 1]]).all()
+    np.testing.assert_allclose(gates, 0.5, rtol=1e-6)
+    with pytest.raises(tq.ParamError):
+        tq.route(np.ones((2, 4), np.float32), np.zeros((3, 4), np.float32), 4)
+    with pytest.raises(tq.ShapeError):
+        tq.route(np.ones((2, 4), np.float32), np.zeros((3, 5), np.float32), 1)
+
+
+@pytest.mark.parametrize("topk", [1, 3, 7])
+def test_route_raw_matches_reference(tq, ref, topk):
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((33, 10)).astype(np.float32)
+    g = rng.standard_normal((7, 10)).astype(np.float32)
+    ids, gates = tq.route(x, g, topk)
+    idr, gr = ref.route(x, g, topk)
+    np.testing.assert_array_equal(ids, idr)
+    np.testing.assert_array_max_ulp(gates, gr, maxulp=1)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+@pytest.mark.parametrize("count", [1, 7, 64, 129, 100003])
+def test_unpack_codes_bit_exact(tq, ref, bits, count):
+    rng = np.random.default_rng(bits * 1000 + count)
+    codes = rng.integers(0, 1 << bits, size=count).astype(np.uint32)
+    packed = ref.pack(codes, bits)
+    got = tq.unpack_codes_gpu(packed, bits, count)
+    np.testing.assert_array_equal(got, ref.unpack(packed, bits, count))
+    np.testing.assert_array_equal(got, codes)
+
+
+def test_unpack_rejects_dirty_padding(tq, ref):
+    packed = ref.pack(np.array([1, 1, 1], np.uint32), 2)
+    packed[0] |= 0x80
+    with pytest.raises(tq.FormatError):
+        tq.unpack_codes_gpu(packed, 2, 3)
+    with pytest.raises(tq.ParamError):
+        tq.unpack_codes_gpu(np.zeros(2, np.uint8), 2, 3)
+    with pytest.raises(tq.ParamError):
+        tq.unpack_codes_gpu(np.zeros(2, np.uint8), 5, 3)
+
+
+@pytest.mark.parametrize("spec", SPECS, ids=lambda s: f"K{s['K']}b{s['bits']}{s['calib']}")
+def test_repacked_codes_bit_exact(tq, make_artifact, spec):
+    """The loader's TMA tile layout decodes back to exactly unpack_codes()."""
+    from oracle.oracle import read_artifact_np, unpack_np
+    d = make_artifact(**spec)
+    L = tq.Layer(d)
+    art = read_artifact_np(d)
+    mats = art["experts"] + art["shared"]
+    for e in range(len(mats)):
+        want = unpack_np(mats[e]["packed"], mats[e]["bits"], art["o"] * art["i"]).reshape(art["o"], art["i"])
+        got = L.export_codes(e).cpu().numpy().astype(np.uint32)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_permutation_bit_exact(tq, oracle, make_artifact):
+    import torch
+    d = make_artifact(**SPECS[2])
+    L = tq.Layer(d)
+    for B in (1, 5, 64, 1000):
+        x = torch.from_numpy(_x(B, SPECS[2]["i"], B)).cuda()
+        ids, _ = L.route(x)
+        perm, offs, inv = L.permute(ids)
+        p2, o2, i2 = oracle.permute(ids.cpu().numpy().astype(np.int64), L.num_experts)
+        np.testing.assert_array_equal(perm.cpu().numpy(), p2)
+        np.testing.assert_array_equal(offs.cpu().numpy(), o2)
+        np.testing.assert_array_equal(inv.cpu().numpy(), i2)
+
+
+def test_given_routing_and_properties(tq, ref, make_artifact):
+    """Zero gates -> exactly zero low-rank output; linearity; determinism;
+    out-of-range expert ids -> ParamError (test_infer.cpp:145-187, moe.cpp:111)."""
+    import torch
+    spec = SPECS[1]
+    d = make_artifact(**spec)
+    L = tq.Layer(d)
+    i = spec["i"]
+    x = torch.from_numpy(_x(12, i, 3)).cuda()
+    ids, gates = L.route(x)
+    zero = torch.zeros_like(gates)
+    y0 = L.forward(x, ids, zero, path="lotile")
+    assert float(y0.abs().max()) == 0.0
+    x2 = torch.from_numpy(_x(12, i, 4)).cuda()
+    ya = L.forward(x, ids, gates)
+    yb = L.forward(x2, ids, gates)
+    yab = L.forward(x + x2, ids, gates)
+    assert rel_frob(yab.cpu().numpy(), (ya + yb).cpu().numpy()) < 1e-3
+    y1 = L.forward(x, ids, gates)
+    y2 = L.forward(x, ids, gates)
+    assert torch.equal(y1, y2)
+    bad = ids.clone()
+    bad[0, 0] = L.num_experts
+    with pytest.raises(tq.ParamError):
+        L.forward(x, bad, gates)
+
+
+def test_empty_batch_and_shape_errors(tq, make_artifact):
+    import torch
+    d = make_artifact(**SPECS[0])
+    L = tq.Layer(d)
+    y = L.forward(torch.zeros((0, SPECS[0]["i"]), device="cuda"))
+    assert tuple(y.shape) == (0, SPECS[0]["o"])
+    with pytest.raises(tq.ShapeError):
+        L.forward(torch.zeros((2, SPECS[0]["i"] + 1), device="cuda"))
+
+
+def test_launch_count_constant_in_batch(tq, make_artifact):
+    """Dispatch structure: the fused path issues the same number of kernel
+    launches for every batch size (dispatch_count() == 2, test_infer.cpp:204-231)."""
+    import torch
+    d = make_artifact(**SPECS[0])
+    L = tq.Layer(d)
+    counts = set()
+    for B in (1, 4, 16, 64, 250):
+        x = torch.from_numpy(_x(B, SPECS[0]["i"], B)).cuda()
+        L.reset_launch_count()
+        L.forward(x)
+        counts.add(L.launch_count())
+    assert len(counts) == 1, counts
+
+
+def test_artifact_errors(tq, make_artifact, tmp_path):
+    import shutil
+    d = make_artifact(**SPECS[0])
+    bad = tmp_path / "bad"
+    shutil.copytree(d, bad)
+    with open(bad / "expert.2.codes.bin", "r+b") as f:
+        b = bytearray(f.read(1))
+        f.seek(0)
+        f.write(bytes([b[0] ^ 0xFF]))
+    with pytest.raises(tq.FormatError, match="expert.2.codes"):
+        tq.Layer(str(bad))
+    with pytest.raises(tq.IoError):
+        tq.Layer(str(tmp_path / "missing"))

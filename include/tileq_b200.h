@@ -155,6 +155,13 @@ tq_status tq_unpack_codes(const uint8_t* bytes, int64_t nbytes, int bits, int64_
  * loader's repack is bit-exact with unpack_codes. */
 tq_status tq_layer_export_codes(tq_layer* layer, int64_t e, uint32_t* out, void* stream);
 
+/* Device-time instrumentation of the fused expert GEMM (the dominant
+ * kernel): when enabled, every expert-GEMM launch is bracketed by CUDA events
+ * on its launching stream; tq_gemm_time_get returns the accumulated device
+ * milliseconds and launch count since the last enable (synchronizes). */
+tq_status tq_gemm_timing_enable(tq_layer* layer, int enable);
+tq_status tq_gemm_time_get(tq_layer* layer, double* ms_total, int64_t* launches);
+
 /* Kernel launches issued by this layer since the last reset (GPU analogue
  * of dispatch_count(), infer.hpp:37-38). */
 uint64_t tq_launch_count(const tq_layer* layer);

@@ -116,6 +116,8 @@ def lib() -> C.CDLL:
     L.tq_ep_dispatch_rows.argtypes = [p, p, i64, p, p, p, p, i32, p]
     L.tq_ep_expert_rows.argtypes = [p, p, p, i64, p, i64, p, i32, p]
     L.tq_ep_combine.argtypes = [p, p, i64, p, p, p, p, i32, p]
+    L.tq_gemm_timing_enable.argtypes = [p, i32]
+    L.tq_gemm_time_get.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64)]
     L.tq_ep_xrow_elems.restype = i64
     L.tq_ep_xrow_elems.argtypes = [p]
     L.tq_ep_extrow_elems.restype = i64
@@ -123,7 +125,7 @@ def lib() -> C.CDLL:
     for name in ("tq_layer_load", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
                  "tq_sync", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
-                 "tq_ep_expert_rows", "tq_ep_combine"):
+                 "tq_ep_expert_rows", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -275,6 +277,17 @@ class Layer:
 
     def reset_launch_count(self) -> None:
         lib().tq_reset_launch_count(self._h)
+
+    def gemm_timing(self, enable: bool) -> None:
+        """Bracket every fused expert-GEMM launch with CUDA events (device time)."""
+        check(lib().tq_gemm_timing_enable(self._h, int(enable)))
+
+    def gemm_time(self):
+        """(total device ms, launches) of the expert GEMM since gemm_timing(True)."""
+        ms = C.c_double()
+        n = C.c_int64()
+        check(lib().tq_gemm_time_get(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def export_codes(self, e: int):
         """Codes of matrix e decoded back from the engine's tile layout (uint32 [o, i] CUDA tensor)."""

@@ -1,0 +1,517 @@
+// THE fused kernel: a persistent, warp-specialised tcgen05 grouped GEMM whose
+// A operand (the quantized expert weights) is dequantized in registers and
+// stored straight into tensor memory, never touching shared memory as fp16.
+//
+//   D[128 weight rows x N tokens] (fp32, TMEM)  +=  A[128 x K] (fp16, TMEM)  *  X[N x K]^T (fp16, SMEM)
+//
+// per work unit (weight matrix, 128-row m-block, token tile, K range).  After
+// the main K chunks, extension chunks append, in the SAME accumulator,
+//   [-zero*s per scale group | U_p codes]  x  [group sums of x | (X.A_q) * su]
+// i.e. the zero-point correction of the affine residual codes and the
+// rank-r tile correction (X.A).B_p of the shared low-rank factors.
+//
+// Warp roles:
+//   0  code producer: cp.async.bulk of packed code blocks + fp16 scale slices
+//      (+ per-unit extension blocks) into a deep smem ring
+//   1  MMA issuer: one thread, tcgen05.mma.cta_group::1.kind::f16, A in TMEM
+//   2  TMEM allocator
+//   3  activation producer: TMA 2D tiles (large token tiles) or cp.async
+//      16-byte rows with the 128B swizzle applied in software (small tiles)
+//   4 .. 4+4*NG-1  dequant: NG independent groups of 4 warps; warp q of a
+//      group owns TMEM lanes (weight rows) 32q..32q+31; the groups take whole
+//      K chunks round-robin so NG chunks are in flight at once (each chunk's
+//      barrier/TMEM latency chain overlaps the others)
+//   last 4  epilogue: tcgen05.ld -> scale -> coalesced fp32 stores
+//
+// Configurations (KC = K elements per chunk, DN = TMEM accumulator columns):
+//   decode  KC=128 NG=3 DN=64    mid  KC=128 NG=3 DN=128    prefill  KC=64 NG=2 DN=192
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tq_internal.h"
+#include "tq_ptx.cuh"
+
+namespace tqb {
+
+constexpr int kTmemCols = 512;
+constexpr int kMaxXStages = 16;
+constexpr int kMaxCStages = 24;
+constexpr int kMaxAStages = 8;
+constexpr int kSmemBudget = 225 * 1024;
+
+__host__ __device__ constexpr int a_stages(int kc, int dn) {
+    return ((kTmemCols - 2 * dn) / (kc / 2)) < kMaxAStages ? ((kTmemCols - 2 * dn) / (kc / 2)) : kMaxAStages;
+}
+__host__ __device__ constexpr int gemm_threads(int ng) { return (8 + 4 * ng) * 32; }
+__host__ __device__ constexpr int scale_trailer(int bits, int kc) {
+    return bits == kDenseBits ? 0 : (kc / 32) * kBM * 2;
+}
+__host__ __device__ constexpr int code_stage_bytes(int bits, int kc) {
+    return (kc / kKC) * code_block_bytes(bits) + scale_trailer(bits, kc);
+}
+// extension blocks of one (weight, m-block): n_ext64 dense fp16 128 x 64 blocks
+__host__ __device__ inline int ext_slot_bytes(int n_ext64) { return n_ext64 * code_block_bytes(kDenseBits); }
+
+struct SharedHdr {
+    uint64_t x_full[kMaxXStages], x_empty[kMaxXStages];
+    uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
+    uint64_t c_full[kMaxCStages], c_empty[kMaxCStages];
+    uint64_t d_full[2], d_empty[2];
+    uint64_t e_full[2], e_empty[2];
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx) {
+    if ((p.debug & 8) && blockIdx.x == 0 && idx < 4096) p.trace[slot * 4096 + idx] = clock64();
+}
+
+template <int BITS, int KC, int NG, int DN>
+__global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_constant__ GemmParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    constexpr int kAS = a_stages(KC, DN);
+    constexpr int kAtoms = KC / kKC;                  // 128-byte swizzle atoms per activation row
+    constexpr int kACols = KC / 2;                    // TMEM columns per A stage
+    constexpr int kDCol0 = kAS * kACols;
+    constexpr int kBlk = code_block_bytes(BITS);      // one 128 x 64 code block
+    constexpr int kCBytes = kAtoms * kBlk;            // codes per chunk
+    constexpr int kCStage = code_stage_bytes(BITS, KC);
+    constexpr int kSW = KC / 32;                      // 32-code super-words per dequant thread per chunk
+    constexpr int kWords = BITS;                      // u32 words per super-word (dense fp16: 16)
+    constexpr int kDqWarps = 4 * NG;
+    constexpr int kEpi0 = 4 + kDqWarps;               // first epilogue warp
+    static_assert(kDCol0 + 2 * DN <= kTmemCols, "TMEM budget");
+
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t pad = (1024u - (raw & 1023u)) & 1023u;
+    uint8_t* smem = smem_raw + pad;
+    const uint32_t s_base = raw + pad;
+    const int ext_bytes = ext_slot_bytes(p.n_ext64);
+    const int x_rows = p.x_stage_rows;
+    const int x_atom_bytes = x_rows * 128;
+    const int x_stage_bytes = kAtoms * x_atom_bytes;
+    const int x_stages = p.x_stages;
+    const int c_stages = p.c_stages;
+    const uint32_t x_off = 0;
+    const uint32_t c_off = x_off + x_stages * x_stage_bytes;
+    const uint32_t e_off = c_off + c_stages * kCStage;
+    SharedHdr* hdr = reinterpret_cast<SharedHdr*>(smem + e_off + 2 * ext_bytes);
+
+    // Role layout: the scheduler arbitrates highest-warp-id first, so the
+    // latency-critical single-thread roles sit at the top:
+    //   [0, 4NG) dequant | [4NG, 4NG+4) epilogue | +4 TMEM alloc | +5 code producer
+    //   | +6 activation producer | +7 MMA issuer
+    const int wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    constexpr int kRoleBase = 4 * NG + 4;
+    const int warp = wid < 4 * NG ? wid + 4                       // dequant -> logical 4..
+                   : wid < kRoleBase ? wid - 4 * NG + kEpi0        // epilogue -> logical kEpi0..
+                   : (wid == kRoleBase ? 2 : wid == kRoleBase + 1 ? 0 : wid == kRoleBase + 2 ? 3 : 1);
+    const int n_units = *p.n_units;
+
+    if (threadIdx.x == 0) {
+        prefetch_tmap(&p.tmap_x64);
+        prefetch_tmap(&p.tmap_e64);
+        for (int s = 0; s < x_stages; ++s) {
+            mbar_init(&hdr->x_full[s], 32);
+            mbar_init(&hdr->x_empty[s], 1);
+        }
+        for (int s = 0; s < kAS; ++s) {
+            mbar_init(&hdr->a_full[s], 4);
+            mbar_init(&hdr->a_empty[s], 1);
+        }
+        for (int s = 0; s < c_stages; ++s) {
+            mbar_init(&hdr->c_full[s], 1);
+            mbar_init(&hdr->c_empty[s], 4);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&hdr->d_full[s], 1);
+            mbar_init(&hdr->d_empty[s], 4);
+            mbar_init(&hdr->e_full[s], 1);
+            mbar_init(&hdr->e_empty[s], 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1));
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&hdr->tmem_base)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = hdr->tmem_base;
+    const int first = blockIdx.x;
+    const int stride = gridDim.x;
+    const int gshift = p.group_shift;
+
+    if (warp == 0) {
+        // ===================== code producer =====================
+        if (lane == 0) {
+            int cs = 0, es = 0, tcnt = 0;
+            uint32_t cph = 0, eph = 0;
+            Unit nxt = first < n_units ? p.units[first] : Unit{};
+            for (int u = first; u < n_units; u += stride) {
+                const Unit un = nxt;
+                if (u + stride < n_units) nxt = p.units[u + stride];
+                const int nmain = un.kc_end - un.kc_begin;
+                const int64_t wm = static_cast<int64_t>(un.weight) * (p.o_pad / kBM) + un.mb;  // (w, mb) slab
+                const uint8_t* wbase = p.codes + static_cast<int64_t>(un.weight) * p.weight_stride +
+                                       static_cast<int64_t>(un.mb) * p.kc_total * kCBytes;
+                for (int c = 0; c < nmain; ++c) {
+                    const int kc = un.kc_begin + c;
+                    mbar_wait(&hdr->c_empty[cs], cph ^ 1u);
+                    uint8_t* st = smem + c_off + cs * kCStage;
+                    if constexpr (BITS == kDenseBits) {
+                        mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes);
+                        bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
+                    } else {
+                        const int e0 = kc * KC;
+                        const int g0 = gshift >= 0 ? e0 >> gshift : e0 / p.group_size;
+                        const int glast = gshift >= 0 ? (e0 + KC - 1) >> gshift : (e0 + KC - 1) / p.group_size;
+                        const int g1 = min(p.groups - 1, glast);
+                        const uint32_t sbytes = static_cast<uint32_t>(g1 - g0 + 1) * kBM * 2;
+                        mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes + sbytes);
+                        bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
+                        bulk_copy_g2s(st + kCBytes, p.scales + (wm * p.groups + g0) * kBM, sbytes, &hdr->c_full[cs]);
+                    }
+                    trace_ev(p, 0, tcnt++);
+                    if (++cs == c_stages) { cs = 0; cph ^= 1u; }
+                }
+                if (un.n_ext > 0 && p.n_ext64 > 0) {
+                    mbar_wait(&hdr->e_empty[es], eph ^ 1u);
+                    mbar_arrive_expect_tx(&hdr->e_full[es], ext_bytes);
+                    bulk_copy_g2s(smem + e_off + es * ext_bytes, p.ext_blocks + wm * ext_bytes, ext_bytes,
+                                  &hdr->e_full[es]);
+                    if (++es == 2) { es = 0; eph ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ===================== activation producer (all 32 lanes) =====================
+        int xs = 0, tcnt = 0;
+        uint32_t xph = 0;
+        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        for (int u = first; u < n_units; u += stride) {
+            const Unit un = nxt;
+            if (u + stride < n_units) nxt = p.units[u + stride];
+            const int nmain = un.kc_end - un.kc_begin;
+            const int nch = nmain + un.n_ext;
+            const bool big = un.n_tok > 32;
+            const int nbox = (un.n_tok + 63) / 64;
+            const int pieces = un.n_tok * kAtoms * 8;   // 16-byte pieces per chunk (small tiles)
+            for (int c = 0; c < nch; ++c) {
+                const bool ext = c >= nmain;
+                mbar_wait(&hdr->x_empty[xs], xph ^ 1u);
+                const uint32_t sx = s_base + x_off + xs * x_stage_bytes;
+                const int col0 = ext ? (c - nmain) * KC : (un.kc_begin + c) * KC;
+                if (big) {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&hdr->x_full[xs], kAtoms * nbox * 64 * 128);
+                        const CUtensorMap* map = ext ? &p.tmap_e64 : &p.tmap_x64;
+                        uint8_t* xst = smem + x_off + xs * x_stage_bytes;
+#pragma unroll
+                        for (int at = 0; at < kAtoms; ++at)
+                            for (int bx = 0; bx < nbox; ++bx)
+                                tma_load_2d(xst + at * x_atom_bytes + bx * 64 * 128, map, col0 + at * kKC,
+                                            un.x_row + bx * 64, &hdr->x_full[xs]);
+                    } else {
+                        mbar_arrive(&hdr->x_full[xs]);
+                    }
+                } else {
+                    const __half* src = ext ? p.e_ptr : p.x_ptr;
+                    const int64_t ld = ext ? p.e_ld : p.x_ld;
+                    for (int pc = lane; pc < pieces; pc += 32) {
+                        const int row = pc / (kAtoms * 8);
+                        const int rem = pc % (kAtoms * 8);
+                        const int at = rem >> 3, ch = rem & 7;
+                        const __half* g = src + static_cast<int64_t>(un.x_row + row) * ld + col0 + at * kKC + ch * 8;
+                        const uint32_t d = sx + at * x_atom_bytes + row * 128 + ((ch ^ (row & 7)) << 4);
+                        cp_async_16(d, g);
+                    }
+                    cp_async_mbar_arrive(&hdr->x_full[xs]);
+                }
+                if (lane == 0) trace_ev(p, 1, tcnt++);
+                if (++xs == x_stages) { xs = 0; xph ^= 1u; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer (converged warp, one elected lane issues) ==========
+        {
+            int xs = 0, as = 0, lu = 0, tcnt = 0;
+            uint32_t xph = 0, aph = 0;
+            Unit nxt = first < n_units ? p.units[first] : Unit{};
+            for (int u = first; u < n_units; u += stride, ++lu) {
+                const Unit un = nxt;
+                if (u + stride < n_units) nxt = p.units[u + stride];
+                const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
+                const int ds = lu & 1;
+                const uint32_t dph = (lu >> 1) & 1;
+                const uint32_t n = static_cast<uint32_t>((un.n_tok + 15) & ~15);
+                const uint32_t idesc = idesc_f16(n);
+                const uint32_t d_tmem = tmem + kDCol0 + ds * DN;
+                mbar_wait(&hdr->d_empty[ds], dph ^ 1u);
+                tc_fence_after();
+                for (int c = 0; c < nch; ++c) {
+                    mbar_wait(&hdr->a_full[as], aph);
+                    if (lane == 0) trace_ev(p, 2, tcnt);
+                    mbar_wait(&hdr->x_full[xs], xph);
+                    if (lane == 0) trace_ev(p, 3, tcnt);
+                    ++tcnt;
+                    if (p.debug & 16) fence_proxy_async_smem();
+                    tc_fence_after();
+                    const uint32_t xaddr = s_base + x_off + xs * x_stage_bytes;
+                    if (!(p.debug & 2)) {
+#pragma unroll
+                        for (int k = 0; k < KC / 16; ++k) {
+                            const uint32_t baddr = xaddr + (k / 4) * x_atom_bytes + (k % 4) * 32;
+                            tc_mma_ts_elect(d_tmem, tmem + as * kACols + k * 8, sw128_desc(baddr), idesc,
+                                            (c > 0 || k > 0) ? 1u : 0u);
+                        }
+                    }
+                    tc_commit_elect(&hdr->a_empty[as]);
+                    tc_commit_elect(&hdr->x_empty[xs]);
+                    if (++as == kAS) { as = 0; aph ^= 1u; }
+                    if (++xs == x_stages) { xs = 0; xph ^= 1u; }
+                }
+                tc_commit_elect(&hdr->d_full[ds]);
+            }
+        }
+    } else if (warp >= 4 && warp < kEpi0) {
+        // ===================== dequant groups =====================
+        const int q = wid & 3;  // TMEM lane quarter = physical warp id % 4
+        const int grp = wid >> 2;
+        const int rloc = q * 32 + lane;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        // every warp walks the whole chunk stream with O(1) ring bookkeeping and
+        // processes the chunks whose round-robin index equals its group
+        int cs = 0, as = 0, es = 0, rr = 0;
+        uint32_t cph = 0, aph = 0, eph = 0;
+        int tcnt = 0;
+        const bool tr = (lane == 0 && q == 0);
+        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        for (int u = first; u < n_units; u += stride) {
+            const Unit un = nxt;
+            if (u + stride < n_units) nxt = p.units[u + stride];
+            const int nmain = un.kc_end - un.kc_begin;
+            const int nch = nmain + un.n_ext;
+            for (int c = 0; c < nch; ++c) {
+                const bool mine = rr == grp;
+                if (++rr == NG) rr = 0;
+                const bool main_chunk = c < nmain;
+                if (mine) {
+                    uint32_t v[kSW][16];
+                    if (main_chunk) {
+                        const int kc = un.kc_begin + c;
+                        mbar_wait(&hdr->c_full[cs], cph);
+                        if (tr) trace_ev(p, 4, grp * 1024 + tcnt);
+                        const uint8_t* st = smem + c_off + cs * kCStage;
+                        const uint32_t* wst = reinterpret_cast<const uint32_t*>(st) + rloc;
+                        uint32_t words[kSW][kWords];
+                        uint16_t sbits[kSW];
+#pragma unroll
+                        for (int s = 0; s < kSW; ++s) {
+                            // super-word s: 64-column block s/2, half s%2
+                            constexpr int kHalf = kWords * kBM;
+#pragma unroll
+                            for (int w = 0; w < kWords; ++w)
+                                words[s][w] = wst[(s >> 1) * (kBlk / 4) + (s & 1) * kHalf + w * kBM];
+                        }
+                        if constexpr (BITS != kDenseBits) {
+                            const int e0 = kc * KC;
+                            const int ein = gshift >= 0 ? (e0 & ((1 << gshift) - 1)) : e0 % p.group_size;
+                            const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + kCBytes) + rloc;
+#pragma unroll
+                            for (int s = 0; s < kSW; ++s) {
+                                const int off = ein + 32 * s;
+                                const int gi = gshift >= 0 ? off >> gshift : off / p.group_size;
+                                sbits[s] = sc[gi * kBM];
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
+#pragma unroll
+                        for (int s = 0; s < kSW; ++s) {
+                            if constexpr (BITS == kDenseBits) {
+#pragma unroll
+                                for (int w = 0; w < 16; ++w) v[s][w] = words[s][w];
+                            } else {
+                                if (p.debug & 1) {
+#pragma unroll
+                                    for (int w = 0; w < 16; ++w) v[s][w] = words[s][w % kWords];
+                                } else {
+                                    const DqConst dq = make_dq(__ushort_as_half(sbits[s]));
+                                    dequant32<BITS>(words[s], dq, v[s]);
+                                }
+                            }
+                        }
+                    } else {
+                        // extension chunk: precomputed fp16 columns [-zero*s per group | U_p codes | 0]
+                        mbar_wait(&hdr->e_full[es], eph);
+                        const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
+#pragma unroll
+                        for (int s = 0; s < kSW; ++s) {
+                            const int colbase = (c - nmain) * KC + 32 * s;
+                            const int blk = colbase >> 6, hh = (colbase >> 5) & 1;
+                            if (blk < p.n_ext64) {
+#pragma unroll
+                                for (int w = 0; w < 16; ++w)
+                                    v[s][w] = eb[blk * (code_block_bytes(kDenseBits) / 4) + (hh * 16 + w) * kBM];
+                            } else {
+#pragma unroll
+                                for (int w = 0; w < 16; ++w) v[s][w] = 0u;
+                            }
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
+                    }
+                    mbar_wait(&hdr->a_empty[as], aph ^ 1u);
+                    if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+                    tc_fence_after();
+#pragma unroll
+                    for (int s = 0; s < kSW; ++s) tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v[s]);
+                    tc_wait_st();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&hdr->a_full[as]);
+                    if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
+                    ++tcnt;
+                }
+                // ring bookkeeping for every chunk of the stream
+                if (main_chunk) {
+                    if (++cs == c_stages) { cs = 0; cph ^= 1u; }
+                }
+                if (++as == kAS) { as = 0; aph ^= 1u; }
+            }
+            if (un.n_ext > 0 && p.n_ext64 > 0) {
+                if (++es == 2) { es = 0; eph ^= 1u; }
+            }
+        }
+    } else if (warp >= kEpi0) {
+        // ===================== epilogue =====================
+        const int q = wid & 3;  // TMEM lane quarter = physical warp id % 4
+        int lu = 0;
+        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        float nscale = first < n_units ? p.w_outscale[nxt.weight] : 1.0f;
+        for (int u = first; u < n_units; u += stride, ++lu) {
+            const Unit un = nxt;
+            const float oscale = nscale;
+            if (u + stride < n_units) {
+                nxt = p.units[u + stride];
+                nscale = p.w_outscale[nxt.weight];
+            }
+            const int ds = lu & 1;
+            const uint32_t dph = (lu >> 1) & 1;
+            const int row = un.mb * kBM + q * 32 + lane;
+            const bool valid = row < p.o_valid;
+            float* out = p.y + static_cast<int64_t>(un.split) * p.y_split_stride +
+                         static_cast<int64_t>(un.y_row) * p.ldy + row;
+            mbar_wait_sleep(&hdr->d_full[ds], dph);
+            tc_fence_after();
+            const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * DN;
+            for (int t0 = 0; t0 < un.n_tok; t0 += 16) {
+                uint32_t v[16];
+                tc_ld_32x32b_x16(dbase + t0, v);
+                tc_wait_ld();
+                if (valid && !(p.debug & 4)) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (t0 + j < un.n_tok)
+                            out[static_cast<int64_t>(t0 + j) * p.ldy] = __uint_as_float(v[j]) * oscale;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&hdr->d_empty[ds]);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) {
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
+                     : "memory");
+    }
+}
+
+// -----------------------------------------------------------------------------
+
+cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
+    GemmParams p = p0;
+    const int kc = p.kc_width;
+    const int dn = p.dn;
+    const bool cfg_ok = (kc == 128 && (dn == 64 || dn == 128)) || (kc == 64 && dn == 192);
+    if (!cfg_ok) return cudaErrorInvalidValue;
+    if (p.bn_max > dn) return cudaErrorInvalidValue;
+    // activation ring: stage rows = token tile rounded to the box (64) or the MMA N granularity (16)
+    const int rows = p.bn_max > 32 ? ((p.bn_max + 63) / 64) * 64 : ((p.bn_max + 15) / 16) * 16;
+    p.x_stage_rows = rows;
+    const int x_stage = (kc / kKC) * rows * 128;
+    const int c_stage = code_stage_bytes(p.bits, kc);
+    const int fixed = 2048 + 2 * ext_slot_bytes(p.n_ext64);
+    // smem split: >= 6 activation stages, then code stages (decode is HBM-latency
+    // bound on the code ring), leftovers back to the activation ring
+    int xs = 6;
+    int cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
+    if (cs < 4) {
+        xs = 3;
+        cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
+    }
+    cs = cs < kMaxCStages ? cs : kMaxCStages;
+    if (cs < 2) return cudaErrorInvalidValue;
+    xs = (kSmemBudget - fixed - cs * c_stage) / x_stage;
+    xs = xs < kMaxXStages ? xs : kMaxXStages;
+    if (xs < 2) return cudaErrorInvalidValue;
+    p.x_stages = xs;
+    p.c_stages = cs;
+    p.group_shift = -1;
+    for (int s = 0; s < 16; ++s)
+        if ((1 << s) == p.group_size) p.group_shift = s;
+    const int smem = 1024 + xs * x_stage + cs * c_stage + 2 * ext_slot_bytes(p.n_ext64) + 1024;
+    static const int dbg = getenv("TQ_DEBUG") ? atoi(getenv("TQ_DEBUG")) : 0;
+    p.debug = dbg;
+    static unsigned long long* trace_buf = nullptr;
+    if ((dbg & 8) && !trace_buf) cudaMalloc(&trace_buf, 8 * 4096 * sizeof(unsigned long long));
+    p.trace = trace_buf;
+    cudaError_t err = cudaSuccess;
+    auto go = [&](auto kern, int threads) {
+        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (err != cudaSuccess) return;
+        kern<<<grid, threads, smem, stream>>>(p);
+        err = cudaGetLastError();
+    };
+#define TQ_GEMM_CASES(KCV, NGV, DNV)                                                                 \
+    switch (p.bits) {                                                                              \
+        case 2: go(gemm_kernel<2, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
+        case 3: go(gemm_kernel<3, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
+        case 4: go(gemm_kernel<4, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
+        case 8: go(gemm_kernel<8, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
+        case kDenseBits: go(gemm_kernel<kDenseBits, KCV, NGV, DNV>, gemm_threads(NGV)); break;     \
+        default: return cudaErrorInvalidValue;                                                     \
+    }
+    if (kc == 128 && dn == 64) {
+        TQ_GEMM_CASES(128, 3, 64)
+    } else if (kc == 128) {
+        TQ_GEMM_CASES(128, 3, 128)
+    } else {
+        TQ_GEMM_CASES(64, 2, 192)
+    }
+#undef TQ_GEMM_CASES
+    if (err == cudaSuccess && (dbg & 8) && getenv("TQ_TRACE_FILE")) {
+        // debug only: dump CTA 0's event trace of this launch (8 slots x 4096 u64)
+        static unsigned long long host[8 * 4096];
+        cudaStreamSynchronize(stream);
+        cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen(getenv("TQ_TRACE_FILE"), "wb")) {
+            fwrite(host, 1, sizeof(host), f);
+            fclose(f);
+        }
+        cudaMemset(trace_buf, 0, sizeof(host));
+    }
+    return err;
+}
+
+}  // namespace tqb

@@ -36,16 +36,17 @@ static_assert(sizeof(Unit) == 32, "Unit is 32 bytes");
 
 // Parameters of one launch of the grouped GEMM (passed as __grid_constant__).
 struct GemmParams {
-    CUtensorMap tmap_x16;   // activations fp16 [rows, k_pad], box 16 x 64, SW128
-    CUtensorMap tmap_x64;   // same tensor, box 64 x 64
-    CUtensorMap tmap_e16;   // extension activations fp16 [rows, ext_cols], box 16 x 64
-    CUtensorMap tmap_e64;
+    CUtensorMap tmap_x64;   // activations fp16 [rows, k_pad], box 64 rows x 64 cols, SW128
+    CUtensorMap tmap_e64;   // extension activations fp16 [rows, ext_cols], box 64 x 64
+    const __half* x_ptr;    // the same two matrices for the cp.async path (small token tiles)
+    int64_t x_ld;
+    const __half* e_ptr;
+    int64_t e_ld;
     const uint8_t* codes;   // [weight][mb][kc] blocks of code_block_bytes(bits)
     int64_t weight_stride;  // bytes per weight matrix in `codes`
-    const __half* scales;   // [weight][G][o_pad]   (quantized weights)
-    const uint8_t* zeros;   // [weight][G][o_pad]
-    const int8_t* ucodes;   // [M][o_pad][r]        U factor codes (extension)
-    const int32_t* w_ublock;    // per weight: U block p, or -1
+    const __half* scales;   // [weight][mb][G][128] fp16 scale slabs (quantized weights)
+    const uint8_t* ext_blocks;  // [weight][mb][n_ext64] dense fp16 extension blocks (-zero*s | U_p codes)
+    int32_t n_ext64;            // extension blocks per (weight, m-block) (0: none)
     const float* w_outscale;    // per weight: epilogue multiplier (2^-k)
     const Unit* units;
     const int32_t* n_units;     // device counter (units are built on the device)
@@ -59,7 +60,16 @@ struct GemmParams {
     int32_t groups;             // G
     int32_t rank;               // r
     int32_t kc_total;
-    int32_t ext_zero;           // 1: extension carries the zero-point correction columns
+    int32_t kc_width;           // K elements per pipeline chunk: 64 or 128
+    int32_t dn;                 // TMEM accumulator columns per buffer (64, 128 or 192)
+    int32_t n_ext_chunks;       // extension chunks of units that carry them
+    int32_t bn_max;             // largest token tile of the launch (sizes the activation ring)
+    int32_t x_stage_rows;       // set by launch_gemm
+    int32_t x_stages;           // set by launch_gemm
+    int32_t c_stages;           // set by launch_gemm
+    int32_t group_shift;        // log2(group_size) or -1, set by launch_gemm
+    int32_t debug;              // TQ_DEBUG bits (profiling only): 1 no dequant, 2 no MMA, 4 no stores, 8 trace
+    unsigned long long* trace;  // trace buffer (TQ_DEBUG & 8)
 };
 
 // ---- kernel argument blocks -------------------------------------------------
@@ -69,8 +79,11 @@ struct PlanArgs {
     int e_begin, e_end;        // resident routed experts
     int num_shared;            // shared experts (weights K..K+S-1), rows after the slots
     int mb_count;              // m-blocks of the expert weights
-    int kc_total, nsplit, n_ext;
+    int kc_total, nsplit, n_ext;   // nsplit: upper bound; the kernel picks the best <= nsplit
     int main_kc;               // 1: main chunks present (0 for the lotile-only path)
+    int num_sms;               // persistent grid size (load-balance target)
+    int bn;                    // token tile (<= kBNMax)
+    int32_t* nsplit_out;       // chosen split count (read by combine), may be null
     int proj_mb, proj_kc_total, proj_nsplit;  // projection pass (0 mb -> none)
     int32_t* perm;
     int32_t* inv;
@@ -114,6 +127,7 @@ struct CombineArgs {
     int64_t sh_split_stride;
     int sh_nsplit;
     int sh_from_offsets;     // 1: sh_row0 = offsets[num_experts] (single-GPU layout), 0: 0
+    const int32_t* nsplit_dev;  // if set: split count of both routed and shared rows (chosen by plan)
     float* out;
 };
 

@@ -22,657 +22,165 @@
 //   unpack_kernel       unpack_codes (codec.cpp:168-195) on the GPU.
 //   export_codes_kernel inverse of the loader's repack (bit-exactness proof).
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda_fp16.h>
 
 #include "tq_internal.h"
+#include "tq_ptx.cuh"
 
 namespace tqb {
-
-// =============================================================================
-// PTX helpers
-// =============================================================================
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "TQ_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra TQ_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_barrier_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
-}
-
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16, fp32 accumulate, cta_group::1.
-__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tc_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
-        "%13, %14, %15, %16};" ::"r"(taddr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-
-__device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr)
-        : "memory");
-}
-
-// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, rows of
-// 128 B, 8-row core-matrix groups 1024 B apart (SBO), sm_100 version 1.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
-    d |= static_cast<uint64_t>(1u) << 16;                 // LBO (unused for swizzled K-major)
-    d |= static_cast<uint64_t>(1024u >> 4) << 32;         // SBO
-    d |= static_cast<uint64_t>(1u) << 46;                 // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(2u) << 61;                 // SWIZZLE_128B
-    return d;
-}
-
-// Instruction descriptor: kind::f16, A=B=F16, D=F32, both K-major, M=128.
-__device__ __forceinline__ uint32_t idesc_f16(uint32_t n) {
-    return (1u << 4) | ((n >> 3) << 17) | ((uint32_t(kBM) >> 4) << 24);
-}
-
-__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t mask, uint32_t orv) {
-    uint32_t r;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(mask), "r"(orv));  // (a & b) | c
-    return r;
-}
-
-__device__ __forceinline__ uint32_t hfma2_u32(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t r;
-    asm("fma.rn.f16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, uint32_t b) {
-    uint32_t r;
-    asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
-    return r;
-}
-
-// =============================================================================
-// in-register dequant: 32 consecutive codes of one row -> 16 half2 = code * s
-// =============================================================================
-//
-// Super-word encodings (written by the loader, tq_runtime.cpp pack_superword):
-// pair p holds codes (c_{2p}, c_{2p+1}) in the low / high 16-bit half of a
-// word at bit offset `pos` inside the half.  A field at pos (pos + b <= 10)
-// is turned into fp16 by OR-ing the exponent 25-pos: value = 2^(10-pos) +
-// code exactly; one HFMA2 with s and bias = -2^(10-pos)*s yields code*s with
-// a single rounding.  Fields above bit 9 are shifted down first.
-
-__device__ __forceinline__ uint32_t magic_for(int pos) {
-    const uint32_t e = static_cast<uint32_t>(25 - pos) << 10;
-    return e | (e << 16);
-}
-
-struct DqConst {
-    uint32_t s2;         // half2 (s, s)
-    uint32_t bias[10];   // bias for field position pos (index pos): -2^(10-pos) * s
-};
-
-__device__ __forceinline__ DqConst make_dq(__half s) {
-    DqConst c;
-    const __half2 s2 = __half2half2(s);
-    c.s2 = *reinterpret_cast<const uint32_t*>(&s2);
-#pragma unroll
-    for (int pos = 0; pos < 10; ++pos) {
-        uint32_t m = 0x8000u | (static_cast<uint32_t>(25 - pos) << 10);  // -2^(10-pos) in fp16
-        m |= m << 16;
-        c.bias[pos] = hmul2_u32(c.s2, m);
-    }
-    return c;
-}
-
-__device__ __forceinline__ uint32_t dq_field(uint32_t w, int pos, int bits, const DqConst& c) {
-    const uint32_t fmask = ((1u << bits) - 1u) << pos;
-    return hfma2_u32(lop3_and_or(w, fmask | (fmask << 16), magic_for(pos)), c.s2, c.bias[pos]);
-}
-
-template <int BITS>
-__device__ __forceinline__ void dequant32(const uint32_t* w, const DqConst& c, uint32_t (&out)[16]);
-
-template <>
-__device__ __forceinline__ void dequant32<2>(const uint32_t* w, const DqConst& c, uint32_t (&out)[16]) {
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const uint32_t v = w[j];
-        const uint32_t u = v >> 10;
-        out[8 * j + 0] = dq_field(v, 0, 2, c);
-        out[8 * j + 1] = dq_field(v, 2, 2, c);
-        out[8 * j + 2] = dq_field(v, 4, 2, c);
-        out[8 * j + 3] = dq_field(v, 6, 2, c);
-        out[8 * j + 4] = dq_field(v, 8, 2, c);
-        out[8 * j + 5] = dq_field(u, 0, 2, c);
-        out[8 * j + 6] = dq_field(u, 2, 2, c);
-        out[8 * j + 7] = dq_field(u, 4, 2, c);
-    }
-}
-
-template <>
-__device__ __forceinline__ void dequant32<3>(const uint32_t* w, const DqConst& c, uint32_t (&out)[16]) {
-    uint32_t u[3];
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-        const uint32_t v = w[j];
-        u[j] = v >> 9;
-        out[5 * j + 0] = dq_field(v, 0, 3, c);
-        out[5 * j + 1] = dq_field(v, 3, 3, c);
-        out[5 * j + 2] = dq_field(v, 6, 3, c);
-        out[5 * j + 3] = dq_field(u[j], 0, 3, c);
-        out[5 * j + 4] = dq_field(u[j], 3, 3, c);
-    }
-    // pair 15: bit k of (c30, c31) sits at bits (15, 31) of word k -> (6, 22) of u[k]
-    uint32_t t = lop3_and_or(u[0], 0x00400040u, magic_for(6));
-    t = lop3_and_or(u[1] << 1, 0x00800080u, t);
-    t = lop3_and_or(u[2] << 2, 0x01000100u, t);
-    out[15] = hfma2_u32(t, c.s2, c.bias[6]);
-}
-
-template <>
-__device__ __forceinline__ void dequant32<4>(const uint32_t* w, const DqConst& c, uint32_t (&out)[16]) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint32_t v = w[j];
-        const uint32_t u = v >> 8;
-        out[4 * j + 0] = dq_field(v, 0, 4, c);
-        out[4 * j + 1] = dq_field(v, 4, 4, c);
-        out[4 * j + 2] = dq_field(u, 0, 4, c);
-        out[4 * j + 3] = dq_field(u, 4, 4, c);
-    }
-}
-
-template <>
-__device__ __forceinline__ void dequant32<8>(const uint32_t* w, const DqConst& c, uint32_t (&out)[16]) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        const uint32_t v = w[j];
-        out[2 * j + 0] = dq_field(v, 0, 8, c);
-        out[2 * j + 1] = dq_field(v >> 8, 0, 8, c);
-    }
-}
-
-// =============================================================================
-// the fused grouped GEMM
-// =============================================================================
-
-constexpr int kThreads = 512;          // 16 warps
-constexpr int kXStages = 4;
-constexpr int kXStageBytes = kBNMax * 128;   // 24 KB
-constexpr int kAStages = 4;
-constexpr int kACols = kKC / 2;        // 32 TMEM columns per A stage (128 x 64 fp16)
-constexpr int kDCol0 = kAStages * kACols;  // 128
-constexpr int kTmemCols = 512;
-constexpr int kCodeRingBytes = 48 * 1024;
-constexpr int kScaleTrailer = 2 * kBM * 2;  // two 128-row fp16 scale slices (one per 32-column half)
-constexpr int kMaxCStages = 16;
-
-__host__ __device__ constexpr int code_stage_bytes(int bits) {
-    return code_block_bytes(bits) + (bits == kDenseBits ? 0 : kScaleTrailer);
-}
-__host__ __device__ constexpr int code_stages(int bits) {
-    return (kCodeRingBytes / code_stage_bytes(bits)) < kMaxCStages ? (kCodeRingBytes / code_stage_bytes(bits))
-                                                                   : kMaxCStages;
-}
-// extension tables of one (weight, m-block): scales [G][128] fp16, zeros [G][128] u8, U [128][r] int8
-__host__ __device__ inline int ext_slot_bytes(int groups, int rank) {
-    return (groups * kBM * 3 + kBM * rank + 1023) & ~1023;
-}
-
-struct SharedHdr {
-    uint64_t x_full[kXStages], x_empty[kXStages];
-    uint64_t a_full[kAStages], a_empty[kAStages];
-    uint64_t c_full[kMaxCStages], c_empty[kMaxCStages];
-    uint64_t d_full[2], d_empty[2];
-    uint64_t e_full[2], e_empty[2];
-    uint32_t tmem_base;
-};
-
-__host__ int gemm_smem_bytes(int groups, int rank) {
-    return 1024 + kXStages * kXStageBytes + kCodeRingBytes + 2 * ext_slot_bytes(groups, rank) + 1024;
-}
-
-template <int BITS>
-__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(const __grid_constant__ GemmParams p) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int kCBytes = code_block_bytes(BITS);
-    constexpr int kCStage = code_stage_bytes(BITS);
-    constexpr int kCStages = code_stages(BITS);
-    constexpr int kWords = BITS;  // u32 words per 32 codes of one row (dense fp16: 16)
-    const int ext_bytes = ext_slot_bytes(p.groups, p.rank);
-    uint8_t* x_smem = smem;
-    uint8_t* c_smem = smem + kXStages * kXStageBytes;
-    uint8_t* e_smem = c_smem + kCodeRingBytes;
-    SharedHdr* hdr = reinterpret_cast<SharedHdr*>(e_smem + 2 * ext_bytes);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int n_units = *p.n_units;
-
-    if (threadIdx.x == 0) {
-        prefetch_tmap(&p.tmap_x16);
-        prefetch_tmap(&p.tmap_x64);
-        prefetch_tmap(&p.tmap_e16);
-        prefetch_tmap(&p.tmap_e64);
-        for (int s = 0; s < kXStages; ++s) {
-            mbar_init(&hdr->x_full[s], 1);
-            mbar_init(&hdr->x_empty[s], 1);
-        }
-        for (int s = 0; s < kAStages; ++s) {
-            mbar_init(&hdr->a_full[s], 8);
-            mbar_init(&hdr->a_empty[s], 1);
-        }
-        for (int s = 0; s < kCStages; ++s) {
-            mbar_init(&hdr->c_full[s], 1);
-            mbar_init(&hdr->c_empty[s], 8);
-        }
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(&hdr->d_full[s], 1);
-            mbar_init(&hdr->d_empty[s], 4);
-            mbar_init(&hdr->e_full[s], 1);
-            mbar_init(&hdr->e_empty[s], 8);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&hdr->tmem_base)),
-                     "r"(kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = hdr->tmem_base;
-    const int64_t slab_groups = static_cast<int64_t>(p.groups) * kBM;  // scale/zero entries per (w, mb)
-
-    if (warp == 0) {
-        // ===================== producer: TMA activations + bulk weight blocks =====================
-        if (lane == 0) {
-            int xs = 0, cs = 0, es = 0;
-            uint32_t xph = 0, cph = 0, eph = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const Unit un = p.units[u];
-                const int nmain = un.kc_end - un.kc_begin;
-                const int nch = nmain + un.n_ext;
-                const bool big = un.n_tok > 32;
-                const int box_rows = big ? 64 : 16;
-                const int nbox = (un.n_tok + box_rows - 1) / box_rows;
-                const int64_t wm = static_cast<int64_t>(un.weight) * (p.o_pad / kBM) + un.mb;  // (w, mb) slab
-                const uint8_t* wbase = p.codes + static_cast<int64_t>(un.weight) * p.weight_stride +
-                                       static_cast<int64_t>(un.mb) * p.kc_total * kCBytes;
-                for (int c = 0; c < nch; ++c) {
-                    const bool ext = c >= nmain;
-                    if (!ext) {
-                        const int kc = un.kc_begin + c;
-                        mbar_wait(&hdr->c_empty[cs], cph ^ 1u);
-                        uint8_t* st = c_smem + cs * kCStage;
-                        if constexpr (BITS == kDenseBits) {
-                            mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes);
-                            bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
-                        } else {
-                            mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes + kScaleTrailer);
-                            bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
-                            for (int h = 0; h < 2; ++h) {
-                                const int g = (kc * kKC + 32 * h) / p.group_size;
-                                bulk_copy_g2s(st + kCBytes + h * kBM * 2, p.scales + (wm * p.groups + g) * kBM,
-                                              kBM * 2, &hdr->c_full[cs]);
-                            }
-                        }
-                        if (++cs == kCStages) { cs = 0; cph ^= 1u; }
-                    } else if (c == nmain) {
-                        const int ub = p.w_ublock[un.weight];
-                        mbar_wait(&hdr->e_empty[es], eph ^ 1u);
-                        uint8_t* eb = e_smem + es * ext_bytes;
-                        const uint32_t zb = static_cast<uint32_t>(slab_groups);
-                        const uint32_t ubytes = (ub >= 0) ? static_cast<uint32_t>(kBM * p.rank) : 0u;
-                        mbar_arrive_expect_tx(&hdr->e_full[es], zb * 2 + zb + ubytes);
-                        bulk_copy_g2s(eb, p.scales + wm * slab_groups, zb * 2, &hdr->e_full[es]);
-                        bulk_copy_g2s(eb + zb * 2, p.zeros + wm * slab_groups, zb, &hdr->e_full[es]);
-                        if (ub >= 0)
-                            bulk_copy_g2s(eb + zb * 3,
-                                          p.ucodes + (static_cast<int64_t>(ub) * p.o_pad + un.mb * kBM) * p.rank,
-                                          ubytes, &hdr->e_full[es]);
-                        if (++es == 2) { es = 0; eph ^= 1u; }
-                    }
-                    mbar_wait(&hdr->x_empty[xs], xph ^ 1u);
-                    mbar_arrive_expect_tx(&hdr->x_full[xs], nbox * box_rows * 128);
-                    const CUtensorMap* map =
-                        ext ? (big ? &p.tmap_e64 : &p.tmap_e16) : (big ? &p.tmap_x64 : &p.tmap_x16);
-                    const int col = ext ? (c - nmain) * kKC : (un.kc_begin + c) * kKC;
-                    for (int bx = 0; bx < nbox; ++bx)
-                        tma_load_2d(x_smem + xs * kXStageBytes + bx * box_rows * 128, map, col,
-                                    un.x_row + bx * box_rows, &hdr->x_full[xs]);
-                    if (++xs == kXStages) { xs = 0; xph ^= 1u; }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ===================== MMA issuer (single thread) =====================
-        if (lane == 0) {
-            int xs = 0, as = 0, lu = 0;
-            uint32_t xph = 0, aph = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
-                const Unit un = p.units[u];
-                const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
-                const int ds = lu & 1;
-                const uint32_t dph = (lu >> 1) & 1;
-                const uint32_t n = static_cast<uint32_t>((un.n_tok + 15) & ~15);
-                const uint32_t idesc = idesc_f16(n);
-                const uint32_t d_tmem = tmem + kDCol0 + ds * kBNMax;
-                mbar_wait(&hdr->d_empty[ds], dph ^ 1u);
-                tc_fence_after();
-                for (int c = 0; c < nch; ++c) {
-                    mbar_wait(&hdr->a_full[as], aph);
-                    mbar_wait(&hdr->x_full[xs], xph);
-                    tc_fence_after();
-                    const uint32_t xaddr = smem_u32(x_smem + xs * kXStageBytes);
-#pragma unroll
-                    for (int k = 0; k < kKC / 16; ++k) {
-                        tc_mma_ts(d_tmem, tmem + as * kACols + k * 8, sw128_desc(xaddr + k * 32), idesc,
-                                  (c > 0 || k > 0) ? 1u : 0u);
-                    }
-                    tc_commit(&hdr->a_empty[as]);
-                    tc_commit(&hdr->x_empty[xs]);
-                    if (++as == kAStages) { as = 0; aph ^= 1u; }
-                    if (++xs == kXStages) { xs = 0; xph ^= 1u; }
-                }
-                tc_commit(&hdr->d_full[ds]);
-            }
-        }
-    } else if (warp >= 4 && warp < 12) {
-        // ===================== dequant warps: codes -> fp16 -> TMEM (A operand) =====================
-        const int q = warp & 3;
-        const int h = (warp - 4) >> 2;
-        const int rloc = q * 32 + lane;
-        int cs = 0, as = 0, es = 0;
-        uint32_t cph = 0, aph = 0, eph = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const Unit un = p.units[u];
-            const int nmain = un.kc_end - un.kc_begin;
-            const int nch = nmain + un.n_ext;
-            const int ub = p.w_ublock[un.weight];
-            for (int c = 0; c < nch; ++c) {
-                uint32_t v[16];
-                if (c < nmain) {
-                    mbar_wait(&hdr->c_full[cs], cph);
-                    const uint8_t* st = c_smem + cs * kCStage;
-                    const uint32_t* blk = reinterpret_cast<const uint32_t*>(st);
-                    uint32_t words[kWords];
-#pragma unroll
-                    for (int j = 0; j < kWords; ++j) words[j] = blk[(h * kWords + j) * kBM + rloc];
-                    if constexpr (BITS == kDenseBits) {
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) v[j] = words[j];
-                    } else {
-                        const __half s = reinterpret_cast<const __half*>(st + kCBytes)[h * kBM + rloc];
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
-                        const DqConst dq = make_dq(s);
-                        dequant32<BITS>(words, dq, v);
-                    }
-                    if (++cs == kCStages) { cs = 0; cph ^= 1u; }
-                } else {
-                    // extension chunk: columns [-zero*s per group | U_p codes | 0]
-                    if (c == nmain) mbar_wait(&hdr->e_full[es], eph);
-                    const uint8_t* eb = e_smem + es * ext_bytes;
-                    const __half* es_s = reinterpret_cast<const __half*>(eb);
-                    const uint8_t* es_z = eb + slab_groups * 2;
-                    const int8_t* es_u = reinterpret_cast<const int8_t*>(eb + slab_groups * 3);
-                    const int colbase = (c - nmain) * kKC + 32 * h;
-                    const int zcols = p.groups;  // extension layout is fixed: [groups | rank | pad]
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        __half hv[2];
-#pragma unroll
-                        for (int e2 = 0; e2 < 2; ++e2) {
-                            const int col = colbase + 2 * j + e2;
-                            __half val = __float2half_rn(0.0f);
-                            if (col < zcols) {
-                                if (!p.ext_zero) {
-                                    hv[e2] = val;
-                                    continue;
-                                }
-                                const __half s = es_s[col * kBM + rloc];
-                                const __half z = __float2half_rn(static_cast<float>(es_z[col * kBM + rloc]));
-                                val = __hneg(__hmul(z, s));
-                            } else if (ub >= 0 && col - zcols < p.rank) {
-                                val = __float2half_rn(static_cast<float>(es_u[rloc * p.rank + (col - zcols)]));
-                            }
-                            hv[e2] = val;
-                        }
-                        const __half2 h2 = __halves2half2(hv[0], hv[1]);
-                        v[j] = *reinterpret_cast<const uint32_t*>(&h2);
-                    }
-                    if (c == nch - 1) {
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
-                        if (++es == 2) { es = 0; eph ^= 1u; }
-                    }
-                }
-                mbar_wait(&hdr->a_empty[as], aph ^ 1u);
-                tc_fence_after();
-                tc_st_32x32b_x16(tmem + (static_cast<uint32_t>(q * 32) << 16) + as * kACols + h * 16, v);
-                tc_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&hdr->a_full[as]);
-                if (++as == kAStages) { as = 0; aph ^= 1u; }
-            }
-        }
-    } else if (warp >= 12) {
-        // ===================== epilogue: TMEM -> registers -> global =====================
-        const int q = warp & 3;
-        int lu = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
-            const Unit un = p.units[u];
-            const int ds = lu & 1;
-            const uint32_t dph = (lu >> 1) & 1;
-            const int row = un.mb * kBM + q * 32 + lane;
-            const bool valid = row < p.o_valid;
-            const float oscale = p.w_outscale[un.weight];
-            float* out = p.y + static_cast<int64_t>(un.split) * p.y_split_stride +
-                         static_cast<int64_t>(un.y_row) * p.ldy + row;
-            mbar_wait(&hdr->d_full[ds], dph);
-            tc_fence_after();
-            const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * kBNMax;
-            for (int t0 = 0; t0 < un.n_tok; t0 += 16) {
-                uint32_t v[16];
-                tc_ld_32x32b_x16(dbase + t0, v);
-                tc_wait_ld();
-                if (valid) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (t0 + j < un.n_tok)
-                            out[static_cast<int64_t>(t0 + j) * p.ldy] = __uint_as_float(v[j]) * oscale;
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&hdr->d_empty[ds]);
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 2) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
-                     : "memory");
-    }
-}
 
 // =============================================================================
 // router: bit-exact route() (moe.cpp:43-89)
 // =============================================================================
 
 // Per token: scores[k] = float(sum_c double(x[c]) * double(G[k,c])) with the
-// reference's sequential index-order f64 sum (matrix.cpp:25-36).  The warp
-// computes a parallel f64 sum plus sum|p|; the reference result differs from
-// ours by at most (gamma_{i-1} + gamma_{i/32+5}) * sum|p| (every product is
-// exact in f64), so if both ends of that interval round to the same f32 the
-// f32 score is certified identical; otherwise lane 0 replays the sequential
-// loop.  Then f64 max-subtracted softmax, total summed k = 0..K-1, ordering
-// by (prob desc, index asc), gates = float(prob / selected).
-__global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x, int in_dim,
+// reference's sequential index-order f64 sum (matrix.cpp:25-36).  Every
+// product is exact in f64, so ANY summation order of the i terms lands within
+// gamma_{i-1} * sum|p| of the exact sum, as does the reference's sequential
+// loop.  We sum in parallel (vectorised, several accumulators, warp tree) and
+// bound |ours - reference| <= 2 * gamma_{i+i/32+8} * sum|p|; when both ends of
+// that interval round to the same f32, the f32 score is certified identical to
+// the reference's, otherwise lane 0 replays the sequential loop (rare).  Then
+// f64 max-subtracted softmax, total summed k = 0..K-1, order by (prob desc,
+// index asc), gates = float(prob / selected) -- moe.cpp:64-87 step by step.
+template <int TPB>
+__global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x, int batch, int in_dim,
                                                    const float* __restrict__ gate, int num_experts, int top_k,
                                                    int group_size, int groups, int k_pad,
                                                    int32_t* __restrict__ ids, float* __restrict__ gates,
                                                    __half* __restrict__ x16, float* __restrict__ sx) {
     extern __shared__ __align__(16) float rs_smem[];
-    float* xs = rs_smem;                 // in_dim
-    float* scores = rs_smem + in_dim;    // num_experts
-    const int b = blockIdx.x;
-    const float* xb = x + static_cast<int64_t>(b) * in_dim;
-    for (int c = threadIdx.x; c < in_dim; c += blockDim.x) xs[c] = xb[c];
+    float* xs = rs_smem;                          // TPB x in_dim
+    float* scores = rs_smem + TPB * in_dim;       // TPB x num_experts
+    const int b0 = blockIdx.x * TPB;
+    const int nt = min(TPB, batch - b0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int t = 0; t < nt; ++t) {
+        const float* xb = x + static_cast<int64_t>(b0 + t) * in_dim;
+        for (int c = threadIdx.x; c < in_dim; c += blockDim.x) xs[t * in_dim + c] = xb[c];
+    }
     __syncthreads();
     // fp16 activations (zero-padded to k_pad) and per-group sums of them
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    if (x16) {
-        __half* xo = x16 + static_cast<int64_t>(b) * k_pad;
-        for (int c = threadIdx.x; c < k_pad; c += blockDim.x) xo[c] = __float2half_rn(c < in_dim ? xs[c] : 0.0f);
-    }
-    for (int g = warp; sx && g < groups; g += nwarps) {
-        float acc = 0.0f;
-        const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
-        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xs[c]));
+    for (int t = 0; t < nt; ++t) {
+        const float* xr = xs + t * in_dim;
+        if (x16) {
+            __half* xo = x16 + static_cast<int64_t>(b0 + t) * k_pad;
+            for (int c = threadIdx.x; c < k_pad; c += blockDim.x) xo[c] = __float2half_rn(c < in_dim ? xr[c] : 0.0f);
+        }
+        for (int g = warp; sx && g < groups; g += nwarps) {
+            float acc = 0.0f;
+            const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
+            for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xr[c]));
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-        if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+            if (lane == 0) sx[static_cast<int64_t>(b0 + t) * groups + g] = acc;
+        }
     }
     if (num_experts == 0) return;  // activations-only prep (tq_forward with given routing)
     // certified scores
+    const bool vec = (in_dim & 3) == 0;
     for (int k = warp; k < num_experts; k += nwarps) {
         const float* gk = gate + static_cast<int64_t>(k) * in_dim;
-        double s = 0.0, a = 0.0;
-        for (int c = lane; c < in_dim; c += 32) {
-            const double prod = static_cast<double>(xs[c]) * static_cast<double>(gk[c]);
-            s += prod;
-            a += fabs(prod);
+        double s[TPB], a[TPB];
+#pragma unroll
+        for (int t = 0; t < TPB; ++t) s[t] = a[t] = 0.0;
+        if (vec) {
+#pragma unroll 4
+            for (int c = 4 * lane; c + 3 < in_dim; c += 128) {
+                const float4 g4 = __ldg(reinterpret_cast<const float4*>(gk + c));
+#pragma unroll
+                for (int t = 0; t < TPB; ++t) {
+                    if (t < nt) {
+                        const float4 x4 = *reinterpret_cast<const float4*>(xs + t * in_dim + c);
+                        const double p0 = static_cast<double>(x4.x) * g4.x, p1 = static_cast<double>(x4.y) * g4.y;
+                        const double p2 = static_cast<double>(x4.z) * g4.z, p3 = static_cast<double>(x4.w) * g4.w;
+                        s[t] += (p0 + p1) + (p2 + p3);
+                        a[t] += (fabs(p0) + fabs(p1)) + (fabs(p2) + fabs(p3));
+                    }
+                }
+            }
+        } else {
+            for (int cc = lane; cc < in_dim; cc += 32) {
+                const float gv = gk[cc];
+#pragma unroll
+                for (int t = 0; t < TPB; ++t)
+                    if (t < nt) {
+                        const double p = static_cast<double>(xs[t * in_dim + cc]) * gv;
+                        s[t] += p;
+                        a[t] += fabs(p);
+                    }
+            }
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            s += __shfl_down_sync(0xffffffffu, s, off);
-            a += __shfl_down_sync(0xffffffffu, a, off);
-        }
-        if (lane == 0) {
-            const double u = 1.1102230246251565e-16;  // 2^-53
-            const double nterms = static_cast<double>(in_dim) + static_cast<double>((in_dim + 31) / 32) + 8.0;
-            const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(a, 1.0001));
-            const float lo = __double2float_rn(__dsub_rd(s, err));
-            const float hi = __double2float_rn(__dadd_ru(s, err));
-            float score;
-            if (lo == hi) {
-                score = __double2float_rn(s);
-            } else {
-                double acc = 0.0;  // the reference's exact sequential loop
-                for (int c = 0; c < in_dim; ++c) acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(xs[c]),
-                                                                                static_cast<double>(gk[c])));
-                score = __double2float_rn(acc);
+        for (int t = 0; t < TPB; ++t) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                s[t] += __shfl_down_sync(0xffffffffu, s[t], off);
+                a[t] += __shfl_down_sync(0xffffffffu, a[t], off);
             }
-            scores[k] = score;
+        }
+        // certification (lane 0 holds the sums); replay undecided scores
+        const double u = 1.1102230246251565e-16;  // 2^-53
+        const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 8.0);
+        unsigned undecided = 0;
+        if (lane == 0) {
+#pragma unroll
+            for (int t = 0; t < TPB; ++t) {
+                if (t >= nt) continue;
+                const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(a[t], 1.0001));
+                const float lo = __double2float_rn(__dsub_rd(s[t], err));
+                const float hi = __double2float_rn(__dadd_ru(s[t], err));
+                if (lo == hi) scores[t * num_experts + k] = __double2float_rn(s[t]);
+                else undecided |= 1u << t;
+            }
+        }
+        undecided = __shfl_sync(0xffffffffu, undecided, 0);
+        while (undecided) {
+            // the reference's exact sequential loop (matrix.cpp:29-34) for token t:
+            // the warp streams the gate row through a per-warp smem window, lane 0 adds
+            const int t = __ffs(undecided) - 1;
+            undecided &= undecided - 1;
+            // products are exact in f64, so the warp forms them; lane 0 keeps the sequential adds
+            double* win = reinterpret_cast<double*>(rs_smem + ((TPB * (in_dim + num_experts) + 1) & ~1)) + warp * 64;
+            const float* xr = xs + t * in_dim;
+            double acc = 0.0;
+            for (int c0 = 0; c0 < in_dim; c0 += 64) {
+                __syncwarp();
+                for (int j = lane; j < 64 && c0 + j < in_dim; j += 32)
+                    win[j] = static_cast<double>(xr[c0 + j]) * static_cast<double>(gk[c0 + j]);
+                __syncwarp();
+                if (lane == 0) {
+                    const int n = min(64, in_dim - c0);
+                    for (int q = 0; q < n; ++q) acc = __dadd_rn(acc, win[q]);
+                }
+            }
+            if (lane == 0) scores[t * num_experts + k] = __double2float_rn(acc);
         }
     }
     __syncthreads();
-    if (warp == 0) {
+    for (int t = warp; t < nt; t += nwarps) {
+        const float* sc = scores + t * num_experts;
+        const int b = b0 + t;
         double mx = -INFINITY;
-        for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(scores[k]));
+        for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[k]));
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
         // every lane computes the total in the reference order k = 0..K-1
         double total = 0.0;
-        for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, exp(static_cast<double>(scores[k]) - mx));
+        for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, exp(static_cast<double>(sc[k]) - mx));
         double selected = 0.0;
         int picked[64];
         double pprob[64];
-        for (int t = 0; t < top_k; ++t) {
+        for (int tt = 0; tt < top_k; ++tt) {
             double best_p = -1.0;
             int best_k = 0x7fffffff;
             for (int k = lane; k < num_experts; k += 32) {
                 bool taken = false;
-                for (int tt = 0; tt < t; ++tt) taken |= (picked[tt] == k);
+                for (int q = 0; q < tt; ++q) taken |= (picked[q] == k);
                 if (taken) continue;
-                const double pk = __ddiv_rn(exp(static_cast<double>(scores[k]) - mx), total);
+                const double pk = __ddiv_rn(exp(static_cast<double>(sc[k]) - mx), total);
                 if (pk > best_p || (pk == best_p && k < best_k)) {
                     best_p = pk;
                     best_k = k;
@@ -687,14 +195,14 @@ __global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x,
                     best_k = ok;
                 }
             }
-            picked[t] = best_k;
-            pprob[t] = best_p;
+            picked[tt] = best_k;
+            pprob[tt] = best_p;
             selected = __dadd_rn(selected, best_p);
         }
         if (lane == 0) {
-            for (int t = 0; t < top_k; ++t) {
-                ids[static_cast<int64_t>(b) * top_k + t] = picked[t];
-                gates[static_cast<int64_t>(b) * top_k + t] = __double2float_rn(__ddiv_rn(pprob[t], selected));
+            for (int tt = 0; tt < top_k; ++tt) {
+                ids[static_cast<int64_t>(b) * top_k + tt] = picked[tt];
+                gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pprob[tt], selected));
             }
         }
     }
@@ -780,75 +288,112 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
         __syncwarp();
     }
     __syncthreads();
-    // units: routed experts (e, mb, tile, split), then shared (s, mb, tile, split)
+    // ---- work units ----------------------------------------------------------
+    // routed experts (e, mb, tile, split), then shared experts (s, mb, tile, split),
+    // generated in parallel; the split count is chosen here from the actual
+    // routing so the persistent grid is evenly loaded.
+    __shared__ int32_t s_tiles[1025];
+    __shared__ int32_t s_nsplit;
+    const int n_slots = tot[K];
+    const int bn = a.bn;
+    const int n_local = a.e_end - a.e_begin;
+    const int sh_tiles = (a.batch + bn - 1) / bn;
+    for (int t = threadIdx.x; t < n_local; t += blockDim.x) {
+        const int ne = tot[a.e_begin + t + 1] - tot[a.e_begin + t];
+        s_tiles[t + 1] = (ne + bn - 1) / bn;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        int nu = 0;
-        const int n_slots = tot[K];
-        const int ext = a.n_ext;
-        for (int e = a.e_begin; e < a.e_end; ++e) {
+        s_tiles[0] = 0;
+        for (int t = 0; t < n_local; ++t) s_tiles[t + 1] += s_tiles[t];  // prefix over resident experts
+        const long base = static_cast<long>(s_tiles[n_local] + a.num_shared * sh_tiles) * a.mb_count;
+        int best = 1;
+        float best_score = -1.0f;
+        const int cap = a.main_kc ? max(1, min(a.nsplit, a.kc_total)) : 1;
+        for (int ns = 1; ns <= cap; ++ns) {
+            const long units = base * ns;
+            const long rounds = (units + a.num_sms - 1) / a.num_sms;
+            const float eff = rounds > 0 ? static_cast<float>(units) / static_cast<float>(rounds * a.num_sms) : 1.0f;
+            const float score = eff - 0.01f * ns;
+            if (score > best_score + 1e-6f) {
+                best_score = score;
+                best = ns;
+            }
+        }
+        s_nsplit = best;
+        if (a.nsplit_out) *a.nsplit_out = best;
+    }
+    __syncthreads();
+    const int ns = s_nsplit;
+    const int routed_units = s_tiles[n_local] * a.mb_count * ns;
+    const int shared_units = a.num_shared * sh_tiles * a.mb_count * ns;
+    const int total = routed_units + shared_units;
+    for (int u = threadIdx.x; u < total; u += blockDim.x) {
+        Unit un;
+        int sp = u % ns;
+        int rest = u / ns;
+        if (u < routed_units) {
+            // rest = (tile-global index) over (e, mb, tile): ordered e, mb, tile
+            // find expert: units of expert t = (s_tiles[t+1]-s_tiles[t]) * mb_count
+            int lo = 0, hi = n_local;  // s_tiles[lo]*mb <= rest < s_tiles[hi]*mb
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (s_tiles[mid] * a.mb_count <= rest) lo = mid; else hi = mid;
+            }
+            const int t = lo;
+            const int within = rest - s_tiles[t] * a.mb_count;
+            const int ntl = s_tiles[t + 1] - s_tiles[t];
+            const int mb = within / ntl, tl = within % ntl;
+            const int e = a.e_begin + t;
             const int ne = tot[e + 1] - tot[e];
-            const int tiles = (ne + kBNMax - 1) / kBNMax;
-            for (int mb = 0; mb < a.mb_count; ++mb)
-                for (int tl = 0; tl < tiles; ++tl)
-                    for (int sp = 0; sp < a.nsplit; ++sp) {
-                        Unit u;
-                        u.weight = e - a.e_begin;
-                        u.mb = mb;
-                        u.x_row = tot[e] + tl * kBNMax;
-                        u.n_tok = min(kBNMax, ne - tl * kBNMax);
-                        u.y_row = u.x_row;
-                        const int k0 = a.main_kc ? sp * a.kc_total / a.nsplit : 0;
-                        const int k1 = a.main_kc ? (sp + 1) * a.kc_total / a.nsplit : 0;
-                        u.kc_begin = static_cast<int16_t>(k0);
-                        u.kc_end = static_cast<int16_t>(k1);
-                        u.n_ext = static_cast<int16_t>(sp == a.nsplit - 1 ? ext : 0);
-                        u.split = static_cast<int16_t>(sp);
-                        u.pad = 0;
-                        if (u.kc_end > u.kc_begin || u.n_ext > 0) a.units[nu++] = u;
-                    }
+            un.weight = t;
+            un.mb = mb;
+            un.x_row = tot[e] + tl * bn;
+            un.n_tok = min(bn, ne - tl * bn);
+            un.y_row = un.x_row;
+        } else {
+            rest -= s_tiles[n_local] * a.mb_count;
+            const int s = rest / (sh_tiles * a.mb_count);
+            const int within = rest % (sh_tiles * a.mb_count);
+            const int mb = within / sh_tiles, tl = within % sh_tiles;
+            un.weight = n_local + s;
+            un.mb = mb;
+            un.x_row = n_slots + tl * bn;
+            un.n_tok = min(bn, a.batch - tl * bn);
+            un.y_row = n_slots + s * a.batch + tl * bn;
         }
-        for (int s = 0; s < a.num_shared; ++s) {
-            const int tiles = (a.batch + kBNMax - 1) / kBNMax;
-            for (int mb = 0; mb < a.mb_count; ++mb)
-                for (int tl = 0; tl < tiles; ++tl)
-                    for (int sp = 0; sp < a.nsplit; ++sp) {
-                        Unit u;
-                        u.weight = (a.e_end - a.e_begin) + s;
-                        u.mb = mb;
-                        u.x_row = n_slots + tl * kBNMax;
-                        u.n_tok = min(kBNMax, a.batch - tl * kBNMax);
-                        u.y_row = n_slots + s * a.batch + tl * kBNMax;
-                        u.kc_begin = static_cast<int16_t>(sp * a.kc_total / a.nsplit);
-                        u.kc_end = static_cast<int16_t>((sp + 1) * a.kc_total / a.nsplit);
-                        u.n_ext = static_cast<int16_t>(sp == a.nsplit - 1 ? ext : 0);
-                        u.split = static_cast<int16_t>(sp);
-                        u.pad = 0;
-                        a.units[nu++] = u;
-                    }
+        un.kc_begin = static_cast<int16_t>(a.main_kc ? sp * a.kc_total / ns : 0);
+        un.kc_end = static_cast<int16_t>(a.main_kc ? (sp + 1) * a.kc_total / ns : 0);
+        un.n_ext = static_cast<int16_t>(sp == ns - 1 ? a.n_ext : 0);
+        un.split = static_cast<int16_t>(sp);
+        un.pad = 0;
+        a.units[u] = un;
+    }
+    if (threadIdx.x == 0) *a.n_units = total;
+    // projection pass units: stacked projection weight (index 0) x all tokens
+    if (a.proj_mb > 0) {
+        const int tiles = (a.batch + bn - 1) / bn;
+        const int np = a.proj_mb * tiles * a.proj_nsplit;
+        for (int u = threadIdx.x; u < np; u += blockDim.x) {
+            const int sp = u % a.proj_nsplit;
+            const int rest = u / a.proj_nsplit;
+            const int mb = rest / tiles, tl = rest % tiles;
+            Unit un;
+            un.weight = 0;
+            un.mb = mb;
+            un.x_row = tl * bn;
+            un.n_tok = min(bn, a.batch - tl * bn);
+            un.y_row = tl * bn;
+            un.kc_begin = static_cast<int16_t>(sp * a.proj_kc_total / a.proj_nsplit);
+            un.kc_end = static_cast<int16_t>((sp + 1) * a.proj_kc_total / a.proj_nsplit);
+            un.n_ext = 0;
+            un.split = static_cast<int16_t>(sp);
+            un.pad = 0;
+            a.proj_units[u] = un;
         }
-        *a.n_units = nu;
-        // projection pass units: stacked projection weight (index 0) x all tokens
-        int np = 0;
-        if (a.proj_mb > 0) {
-            const int tiles = (a.batch + kBNMax - 1) / kBNMax;
-            for (int mb = 0; mb < a.proj_mb; ++mb)
-                for (int tl = 0; tl < tiles; ++tl)
-                    for (int sp = 0; sp < a.proj_nsplit; ++sp) {
-                        Unit u;
-                        u.weight = 0;
-                        u.mb = mb;
-                        u.x_row = tl * kBNMax;
-                        u.n_tok = min(kBNMax, a.batch - tl * kBNMax);
-                        u.y_row = tl * kBNMax;
-                        u.kc_begin = static_cast<int16_t>(sp * a.proj_kc_total / a.proj_nsplit);
-                        u.kc_end = static_cast<int16_t>((sp + 1) * a.proj_kc_total / a.proj_nsplit);
-                        u.n_ext = 0;
-                        u.split = static_cast<int16_t>(sp);
-                        u.pad = 0;
-                        a.proj_units[np++] = u;
-                    }
-        }
-        if (a.n_proj_units) *a.n_proj_units = np;
+        if (threadIdx.x == 0 && a.n_proj_units) *a.n_proj_units = np;
+    } else if (threadIdx.x == 0 && a.n_proj_units) {
+        *a.n_proj_units = 0;
     }
 }
 
@@ -900,30 +445,52 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
 
 
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
+    // 4 consecutive output columns per thread (float4 when out_dim % 4 == 0)
     const int b = blockIdx.y;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= a.out_dim) return;
+    const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c0 >= a.out_dim) return;
+    const bool vec = (a.out_dim & 3) == 0;
     const int n_slots = a.offsets ? a.offsets[a.num_experts] : 0;
-    float acc = 0.0f;
+    const int ns = a.nsplit_dev ? *a.nsplit_dev : a.nsplit;
+    const int nsh = a.nsplit_dev ? ns : a.sh_nsplit;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    auto load4 = [&](const float* base, float (&v)[4]) {
+        if (vec) {
+            const float4 t = *reinterpret_cast<const float4*>(base);
+            v[0] += t.x; v[1] += t.y; v[2] += t.z; v[3] += t.w;
+        } else {
+            for (int j = 0; j < 4; ++j)
+                if (c0 + j < a.out_dim) v[j] += base[j];
+        }
+    };
     if (a.use_routed) {
         for (int t = 0; t < a.top_k; ++t) {
             const int f = b * a.top_k + t;
             const int pos = a.inv[f];
             if (pos < 0) continue;  // invalid expert id (reported through the error flag)
-            float v = 0.0f;
-            for (int sp = 0; sp < a.nsplit; ++sp)
-                v += a.y[sp * a.split_stride + static_cast<int64_t>(pos) * a.out_dim + c];
-            acc = fmaf(a.gates[f], v, acc);
+            float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            for (int sp = 0; sp < ns; ++sp)
+                load4(a.y + sp * a.split_stride + static_cast<int64_t>(pos) * a.out_dim + c0, v);
+            const float g = a.gates[f];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fmaf(g, v[j], acc[j]);
         }
     }
     const int64_t sh0 = a.sh_from_offsets ? n_slots : 0;
     for (int s = 0; s < a.num_shared; ++s) {
         const int64_t r = sh0 + static_cast<int64_t>(s) * a.batch + b;
-        float v = 0.0f;
-        for (int sp = 0; sp < a.sh_nsplit; ++sp) v += a.ysh[sp * a.sh_split_stride + r * a.out_dim + c];
-        acc += v;
+        float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int sp = 0; sp < nsh; ++sp) load4(a.ysh + sp * a.sh_split_stride + r * a.out_dim + c0, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += v[j];
     }
-    a.out[static_cast<int64_t>(b) * a.out_dim + c] = acc;
+    float* o = a.out + static_cast<int64_t>(b) * a.out_dim + c0;
+    if (vec) {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+        for (int j = 0; j < 4; ++j)
+            if (c0 + j < a.out_dim) o[j] = acc[j];
+    }
 }
 
 // =============================================================================
@@ -1010,38 +577,29 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 // launch wrappers (called from tq_runtime.cpp)
 // =============================================================================
 
-cudaError_t launch_gemm(const GemmParams& p, int grid, cudaStream_t stream) {
-    const int smem = gemm_smem_bytes(p.groups, p.rank);
-    cudaError_t err = cudaSuccess;
-    auto go = [&](auto kern) {
-        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (err != cudaSuccess) return;
-        kern<<<grid, kThreads, smem, stream>>>(p);
-        err = cudaGetLastError();
-    };
-    switch (p.bits) {
-        case 2: go(gemm_kernel<2>); break;
-        case 3: go(gemm_kernel<3>); break;
-        case 4: go(gemm_kernel<4>); break;
-        case 8: go(gemm_kernel<8>); break;
-        case kDenseBits: go(gemm_kernel<kDenseBits>); break;
-        default: return cudaErrorInvalidValue;
-    }
-    return err;
-}
-
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16,
                          float* sx, cudaStream_t stream) {
-    const size_t smem = sizeof(float) * (static_cast<size_t>(in_dim) + num_experts);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(route_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-    }
-    route_kernel<<<batch, 256, smem, stream>>>(x, in_dim, gate, num_experts, top_k, group_size, groups, k_pad, ids,
-                                               gates, x16, sx);
-    return cudaGetLastError();
+    // tokens per CTA: share each gate row across several tokens at prefill,
+    // spread tokens over many CTAs at decode
+    int tpb = batch <= 32 ? 1 : (batch <= 1024 ? 2 : 8);
+    while (tpb > 1 && sizeof(float) * static_cast<size_t>(tpb) * (in_dim + num_experts) > 160 * 1024) tpb >>= 1;
+    const size_t smem = sizeof(float) * (static_cast<size_t>(tpb) * (in_dim + num_experts) + 2) + 8 * 64 * sizeof(double);
+    const int grid = (batch + tpb - 1) / tpb;
+    auto go = [&](auto kern) -> cudaError_t {
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+        }
+        kern<<<grid, 256, smem, stream>>>(x, batch, in_dim, gate, num_experts, top_k, group_size, groups, k_pad,
+                                          ids, gates, x16, sx);
+        return cudaGetLastError();
+    };
+    if (tpb == 8) return go(route_kernel<8>);
+    if (tpb == 4) return go(route_kernel<4>);
+    if (tpb == 2) return go(route_kernel<2>);
+    return go(route_kernel<1>);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
@@ -1062,7 +620,7 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
-    dim3 grid((a.out_dim + 255) / 256, a.batch);
+    dim3 grid((a.out_dim + 1023) / 1024, a.batch);
     combine_kernel<<<grid, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }

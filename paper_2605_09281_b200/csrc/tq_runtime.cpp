@@ -469,18 +469,27 @@ struct tq_layer {
     // projection (stacked X.A matrices)
     int64_t NP = 0, proj_rows = 0, proj_o_pad = 0, proj_mb = 0;
     // device tables
-    DBuf gate, codes, scales, zeros, ucodes, w_ublock, w_outscale;
-    DBuf pcodes, p_ublock, p_outscale, pm_of, zscale, rowscale;
+    DBuf gate, codes, scales, ext_blocks, w_outscale;
+    DBuf pcodes, p_outscale, pm_of, zscale, rowscale;
     int64_t weight_stride = 0, pweight_stride = 0;
     int64_t device_bytes = 0;
     // workspace
     int64_t cap = 0;
     DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
-        err_flag, xin, yout;
+        err_flag, xin, yout, nsplit_d;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
     std::atomic<uint64_t> launches{0};
     int num_sms = 148;
+    // expert-GEMM device timing (tq_gemm_timing_enable)
+    bool timing = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    ~tq_layer() {
+        for (auto& e : tev) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+    }
 };
 
 namespace {
@@ -489,22 +498,52 @@ int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
 int64_t rows_for(const tq_layer* L, int64_t batch) { return batch * L->g.top_k + L->g.S * batch; }
 
+// Upper bound of the split-K count the plan kernel may choose for a batch
+// (it picks the best-balanced value <= this from the actual routing).
 int main_nsplit(const tq_layer* L, int64_t batch) {
     const int64_t local = L->e_end - L->e_begin;
-    const int64_t active = std::min<int64_t>(local, batch * L->g.top_k) + L->g.S;
-    const int64_t tiles = std::max<int64_t>(1, (batch * L->g.top_k / std::max<int64_t>(1, local) + kBNMax - 1) / kBNMax);
-    const int64_t base = std::max<int64_t>(1, active * L->g.mb_count * tiles);
-    int64_t ns = (2 * L->num_sms + base - 1) / base;
-    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 4));
+    const int64_t active = std::max<int64_t>(1, std::min<int64_t>(local, batch * L->g.top_k) + L->g.S);
+    const int64_t base = active * L->g.mb_count;
+    int64_t ns = (16 * L->num_sms + base - 1) / base;
+    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 2));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ns, 16)));
 }
 
 int proj_nsplit(const tq_layer* L, int64_t batch) {
     if (L->proj_mb == 0) return 1;
-    const int64_t base = L->proj_mb * ((batch + kBNMax - 1) / kBNMax);
+    const int64_t base = L->proj_mb * ((batch + 191) / 192);
     int64_t ns = (L->num_sms + base - 1) / base;
     ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 4));
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ns, 32)));
+}
+
+struct LaunchCfg {
+    int kc;        // K elements per chunk (64 or 128)
+    int dn;        // TMEM accumulator columns (max token tile)
+    int bn;        // token tile
+    int kc_total;  // chunks per weight row
+    int n_ext;     // extension chunks
+};
+
+int gemm_dn_host(int kc) { return kc == 64 ? 192 : 128; }
+
+// Decode-sized batches (few tokens per expert) use 128-wide chunks and 16
+// dequant warps; prefill uses 64-wide chunks and 192-token tiles.
+LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
+    const int64_t local = std::max<int64_t>(1, L->e_end - L->e_begin);
+    const int64_t per_expert = (batch * L->g.top_k + local - 1) / local;
+    LaunchCfg c;
+    if (per_expert <= 128 && L->g.k_pad % 128 == 0) {
+        c.kc = 128;
+        c.dn = batch <= 64 ? 64 : 128;   // decode: small accumulators -> deeper A ring
+    } else {
+        c.kc = 64;
+        c.dn = 192;
+    }
+    c.bn = c.dn;
+    c.kc_total = static_cast<int>(L->g.k_pad / c.kc);
+    c.n_ext = static_cast<int>((L->g.G + L->g.r + c.kc - 1) / c.kc);
+    return c;
 }
 
 void build_maps(tq_layer* L) {
@@ -537,10 +576,11 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
     L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
     L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
-    const int64_t max_units = (g.K + g.S) * g.mb_count * ((cap + kBNMax - 1) / kBNMax + g.K) * 16 + 64;
+    const int64_t max_units = (g.K + g.S) * g.mb_count * ((cap + 127) / 128 + g.K) * 16 + 64;
     L->units.alloc(sizeof(Unit) * max_units);
     L->n_units.alloc(sizeof(int32_t));
-    L->punits.alloc(sizeof(Unit) * (std::max<int64_t>(1, L->proj_mb) * ((cap + kBNMax - 1) / kBNMax) * 32 + 8));
+    L->nsplit_d.alloc(sizeof(int32_t));
+    L->punits.alloc(sizeof(Unit) * (std::max<int64_t>(1, L->proj_mb) * ((cap + 127) / 128) * 32 + 8));
     L->n_punits.alloc(sizeof(int32_t));
     L->zpart.alloc(sizeof(float) * zmax);
     L->xperm.alloc(sizeof(__half) * rows * g.k_pad);
@@ -691,8 +731,8 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     g.kc_total = g.k_pad / kKC;
     g.o_pad = round_up(g.o, kBM);
     g.mb_count = g.o_pad / kBM;
-    g.n_ext = (g.G + g.r + kKC - 1) / kKC;
-    g.ext_cols = g.n_ext * kKC;
+    g.n_ext = (g.G + g.r + kKC - 1) / kKC;   // extension chunks at KC = 64
+    g.ext_cols = round_up(g.G + g.r, 256);    // room for KC = 256 chunks (zero-padded)
     if (g.G > 64 || g.r > 64)
         fail(TQ_ERR_PARAM, "GPU engine supports at most 64 scale groups per row and rank <= 64 (groups " +
                                std::to_string(g.G) + ", rank " + std::to_string(g.r) + ")");
@@ -728,16 +768,42 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     }
     q.clear();
     std::vector<float> h_outscale(static_cast<size_t>(L->n_weights));
-    std::vector<int32_t> h_ublock(static_cast<size_t>(L->n_weights), -1);
+    for (int64_t w = 0; w < L->n_weights; ++w) h_outscale[w] = static_cast<float>(std::ldexp(1.0, -wk[w]));
+    // Extension blocks per (weight, m-block): dense fp16 A-operand columns appended
+    // after the main K range: [-zero * s' per scale group | U_p codes | 0].  They
+    // depend only on (weight, row), so they are formed once here (-zero*s' rounded
+    // once to fp16 like the device HMUL would; int8 U codes are exact in fp16).
+    const int64_t n_ext64 = g.n_ext;
+    const int eblk = code_block_bytes(kDenseBits);
+    std::vector<uint8_t> h_ext(static_cast<size_t>(L->n_weights * g.mb_count * n_ext64 * eblk), 0);
     for (int64_t w = 0; w < L->n_weights; ++w) {
-        h_outscale[w] = static_cast<float>(std::ldexp(1.0, -wk[w]));
-        if (w < e_end - e_begin) h_ublock[w] = placement[2 * (e_begin + w)];
+        const bool routed = w < e_end - e_begin;
+        const size_t p_blk = routed ? placement[2 * (e_begin + w)] : 0;
+        for (int64_t mb = 0; mb < g.mb_count; ++mb) {
+            uint8_t* base = h_ext.data() + ((w * g.mb_count + mb) * n_ext64) * eblk;
+            for (int64_t blk = 0; blk < n_ext64; ++blk) {
+                uint16_t* b16 = reinterpret_cast<uint16_t*>(base + blk * eblk);
+                for (int rl = 0; rl < kBM; ++rl) {
+                    const int64_t row = mb * kBM + rl;
+                    for (int col = 0; col < 64; ++col) {
+                        const int64_t gc = blk * 64 + col;
+                        float val = 0.0f;
+                        if (row < g.o && gc < g.G) {
+                            const size_t si = static_cast<size_t>(w * slab + (mb * g.G + gc) * kBM + rl);
+                            const float sv = half_bits_to_float(h_scales[si]);
+                            val = static_cast<float>(-static_cast<double>(h_zeros[si]) * sv);
+                        } else if (row < g.o && routed && gc >= g.G && gc < g.G + g.r) {
+                            val = static_cast<float>(static_cast<int8_t>(u_b[(p_blk * O + static_cast<size_t>(row)) * R +
+                                                                              static_cast<size_t>(gc - g.G)]));
+                        }
+                        // block layout: u32 word (hh*16 + j) of row rl holds columns 32*hh + 2j (+1)
+                        const int hh = col >> 5, j = (col & 31) >> 1, hi = col & 1;
+                        b16[((hh * 16 + j) * kBM + rl) * 2 + hi] = float_to_half_bits(val);
+                    }
+                }
+            }
+        }
     }
-    // U factor codes [M][o_pad][r] int8
-    std::vector<int8_t> h_u(static_cast<size_t>(g.M * g.o_pad * g.r), 0);
-    for (size_t p = 0; p < M; ++p)
-        for (size_t row = 0; row < O; ++row)
-            std::memcpy(&h_u[(p * g.o_pad + row) * R], &u_b[(p * O + row) * R], R);
 
     // --- descale tiers + projection matrices (infer.cpp:74-117) ---
     std::vector<int> tier(N, 0);
@@ -842,29 +908,39 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     L->gate.upload(gate_b.data(), gate_b.size());
     L->codes.upload(h_codes.data(), h_codes.size());
     L->scales.upload(h_scales.data(), h_scales.size() * 2);
-    L->zeros.upload(h_zeros.data(), h_zeros.size());
-    L->ucodes.upload(h_u.data(), h_u.size());
-    L->w_ublock.upload(h_ublock.data(), h_ublock.size() * 4);
+    L->ext_blocks.upload(h_ext.data(), h_ext.size());
     L->w_outscale.upload(h_outscale.data(), h_outscale.size() * 4);
     L->pcodes.upload(h_p.data(), h_p.size());
-    const int32_t minus1 = -1;
     const float one = 1.0f;
-    L->p_ublock.upload(&minus1, 4);
     L->p_outscale.upload(&one, 4);
     L->pm_of.upload(pm_of.data(), pm_of.size() * 4);
     L->zscale.upload(zscale.data(), zscale.size() * 4);
     L->rowscale.upload(rowscale.data(), rowscale.size() * 4);
-    L->device_bytes = static_cast<int64_t>(L->gate.n + L->codes.n + L->scales.n + L->zeros.n + L->ucodes.n +
-                                           L->pcodes.n + L->rowscale.n);
+    L->device_bytes = static_cast<int64_t>(L->gate.n + L->codes.n + L->scales.n + L->ext_blocks.n + L->pcodes.n +
+                                           L->rowscale.n);
     reserve(L, 64);
 }
 
-GemmParams base_params(tq_layer* L) {
+GemmParams base_params(tq_layer* L, const LaunchCfg& cf, int64_t max_tok) {
     GemmParams p;
     std::memset(&p, 0, sizeof(p));
     p.group_size = static_cast<int32_t>(L->g.gs);
-    p.kc_total = static_cast<int32_t>(L->g.kc_total);
+    p.kc_total = cf.kc_total;
+    p.kc_width = cf.kc;
+    p.dn = cf.dn;
+    p.n_ext_chunks = cf.n_ext;
+    p.bn_max = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(cf.bn, max_tok)));
     return p;
+}
+
+LaunchCfg cfg64(const tq_layer* L) {
+    LaunchCfg c;
+    c.kc = 64;
+    c.dn = 192;
+    c.bn = gemm_dn_host(64);
+    c.kc_total = static_cast<int>(L->g.k_pad / 64);
+    c.n_ext = static_cast<int>(L->g.n_ext);
+    return c;
 }
 
 void count_launch(tq_layer* L, int n = 1) { L->launches += static_cast<uint64_t>(n); }
@@ -885,6 +961,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     const Geometry& g = L->g;
     const bool use_lotile = path != TQ_PATH_QMOE;
     const bool use_qmoe = path != TQ_PATH_LOTILE;
+    const LaunchCfg cf = cfg_for(L, batch);
     const int nsplit = use_qmoe ? main_nsplit(L, batch) : 1;
     const int pns = proj_nsplit(L, batch);
     const bool with_shared = use_qmoe && g.S > 0;
@@ -898,12 +975,15 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     pa.e_end = static_cast<int>(L->e_end);
     pa.num_shared = with_shared ? static_cast<int>(g.S) : 0;
     pa.mb_count = static_cast<int>(g.mb_count);
-    pa.kc_total = static_cast<int>(g.kc_total);
+    pa.kc_total = cf.kc_total;
     pa.nsplit = nsplit;
-    pa.n_ext = static_cast<int>(g.n_ext);
+    pa.n_ext = cf.n_ext;
     pa.main_kc = use_qmoe ? 1 : 0;
+    pa.num_sms = L->num_sms;
+    pa.bn = cf.bn;
+    pa.nsplit_out = L->nsplit_d.as<int32_t>();
     pa.proj_mb = use_lotile ? static_cast<int>(L->proj_mb) : 0;
-    pa.proj_kc_total = static_cast<int>(g.kc_total);
+    pa.proj_kc_total = cf.kc_total;
     pa.proj_nsplit = pns;
     pa.perm = L->perm.as<int32_t>();
     pa.inv = L->inv.as<int32_t>();
@@ -917,14 +997,15 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     count_launch(L);
     // projection pass: Z = P . x for every token (dense fp16 weights)
     if (use_lotile && L->proj_mb > 0) {
-        GemmParams p = base_params(L);
-        p.tmap_x16 = L->map_x16_16;
+        GemmParams p = base_params(L, cf, batch);
         p.tmap_x64 = L->map_x16_64;
-        p.tmap_e16 = L->map_x16_16;
         p.tmap_e64 = L->map_x16_64;
+        p.x_ptr = L->x16.as<__half>();
+        p.x_ld = g.k_pad;
+        p.e_ptr = L->x16.as<__half>();
+        p.e_ld = g.k_pad;
         p.codes = L->pcodes.as<uint8_t>();
         p.weight_stride = L->pweight_stride;
-        p.w_ublock = L->p_ublock.as<int32_t>();
         p.w_outscale = L->p_outscale.as<float>();
         p.units = L->punits.as<Unit>();
         p.n_units = L->n_punits.as<int32_t>();
@@ -936,7 +1017,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
         p.bits = kDenseBits;
         p.groups = 0;
         p.rank = 0;
-        const int64_t nunits = L->proj_mb * ((batch + kBNMax - 1) / kBNMax) * pns;
+        const int64_t nunits = L->proj_mb * ((batch + cf.bn - 1) / cf.bn) * pns;
         cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nunits, L->num_sms)), st), "projection gemm launch");
         count_launch(L);
     }
@@ -969,17 +1050,18 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     cuda_check(launch_gather(ga, static_cast<int>(rows_for(L, batch)), st), "gather_kernel launch");
     count_launch(L);
     // fused expert pass
-    GemmParams p = base_params(L);
-    p.tmap_x16 = L->map_xp16;
+    GemmParams p = base_params(L, cf, batch);
     p.tmap_x64 = L->map_xp64;
-    p.tmap_e16 = L->map_ep16;
     p.tmap_e64 = L->map_ep64;
+    p.x_ptr = L->xperm.as<__half>();
+    p.x_ld = g.k_pad;
+    p.e_ptr = L->extperm.as<__half>();
+    p.e_ld = g.ext_cols;
     p.codes = L->codes.as<uint8_t>();
     p.weight_stride = L->weight_stride;
     p.scales = L->scales.as<__half>();
-    p.zeros = L->zeros.as<uint8_t>();
-    p.ucodes = L->ucodes.as<int8_t>();
-    p.w_ublock = L->w_ublock.as<int32_t>();
+    p.ext_blocks = L->ext_blocks.as<uint8_t>();
+    p.n_ext64 = static_cast<int32_t>(L->g.n_ext);
     p.w_outscale = L->w_outscale.as<float>();
     p.units = L->units.as<Unit>();
     p.n_units = L->n_units.as<int32_t>();
@@ -991,8 +1073,17 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.bits = g.bits;
     p.groups = static_cast<int32_t>(g.G);
     p.rank = static_cast<int32_t>(g.r);
-    p.ext_zero = use_qmoe ? 1 : 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (L->timing) {
+        cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
+        cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
+    }
     cuda_check(launch_gemm(p, L->num_sms, st), "expert gemm launch");
+    if (L->timing) {
+        cuda_check(cudaEventRecord(ev1, st), "cudaEventRecord");
+        L->tev.emplace_back(ev0, ev1);
+    }
     count_launch(L);
     // combine
     CombineArgs ca{};
@@ -1012,6 +1103,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ca.sh_split_stride = ca.split_stride;
     ca.sh_nsplit = nsplit;
     ca.sh_from_offsets = 1;
+    ca.nsplit_dev = L->nsplit_d.as<int32_t>();
     ca.out = y;
     cuda_check(launch_combine(ca, st), "combine_kernel launch");
     count_launch(L);
@@ -1124,6 +1216,8 @@ tq_status tq_permute(tq_layer* L, const int32_t* ids, int64_t batch, int32_t* pe
         pa.mb_count = static_cast<int>(L->g.mb_count);
         pa.kc_total = static_cast<int>(L->g.kc_total);
         pa.nsplit = 1;
+        pa.num_sms = L->num_sms;
+        pa.bn = gemm_dn_host(64);
         pa.perm = perm;
         pa.inv = inv;
         pa.offsets = offsets;
@@ -1246,6 +1340,35 @@ tq_status tq_layer_export_codes(tq_layer* L, int64_t e, uint32_t* out, void* str
     });
 }
 
+tq_status tq_gemm_timing_enable(tq_layer* L, int enable) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        for (auto& e : L->tev) {
+            cudaEventDestroy(e.first);
+            cudaEventDestroy(e.second);
+        }
+        L->tev.clear();
+        L->timing = enable != 0;
+    });
+}
+
+tq_status tq_gemm_time_get(tq_layer* L, double* ms_total, int64_t* launches) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        double tot = 0.0;
+        for (auto& e : L->tev) {
+            cuda_check(cudaEventSynchronize(e.second), "cudaEventSynchronize");
+            float ms = 0.0f;
+            cuda_check(cudaEventElapsedTime(&ms, e.first, e.second), "cudaEventElapsedTime");
+            tot += ms;
+        }
+        if (ms_total) *ms_total = tot;
+        if (launches) *launches = static_cast<int64_t>(L->tev.size());
+    });
+}
+
 uint64_t tq_launch_count(const tq_layer* L) { return L ? L->launches.load() : 0; }
 void tq_reset_launch_count(tq_layer* L) {
     if (L) L->launches = 0;
@@ -1286,6 +1409,7 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
         const bool use_qmoe = path != TQ_PATH_LOTILE;
         run_route(L, x, batch, false, st);
         const int pns = proj_nsplit(L, batch);
+        const LaunchCfg cf = cfg_for(L, batch);
         PlanArgs pa{};
         pa.ids = ids;
         pa.batch = static_cast<int>(batch);
@@ -1294,12 +1418,14 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
         pa.e_begin = 0;
         pa.e_end = 0;  // no expert units: this rank only prepares rows
         pa.mb_count = static_cast<int>(g.mb_count);
-        pa.kc_total = static_cast<int>(g.kc_total);
+        pa.kc_total = cf.kc_total;
         pa.nsplit = 1;
-        pa.n_ext = static_cast<int>(g.n_ext);
+        pa.n_ext = cf.n_ext;
         pa.main_kc = 1;
+        pa.num_sms = L->num_sms;
+        pa.bn = cf.bn;
         pa.proj_mb = use_lotile ? static_cast<int>(L->proj_mb) : 0;
-        pa.proj_kc_total = static_cast<int>(g.kc_total);
+        pa.proj_kc_total = cf.kc_total;
         pa.proj_nsplit = pns;
         pa.perm = L->perm.as<int32_t>();
         pa.inv = L->inv.as<int32_t>();
@@ -1312,14 +1438,15 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
         cuda_check(launch_plan(pa, st), "plan_kernel launch");
         count_launch(L);
         if (use_lotile && L->proj_mb > 0) {
-            GemmParams p = base_params(L);
-            p.tmap_x16 = L->map_x16_16;
+            GemmParams p = base_params(L, cf, batch);
             p.tmap_x64 = L->map_x16_64;
-            p.tmap_e16 = L->map_x16_16;
             p.tmap_e64 = L->map_x16_64;
+            p.x_ptr = L->x16.as<__half>();
+            p.x_ld = g.k_pad;
+            p.e_ptr = L->x16.as<__half>();
+            p.e_ld = g.k_pad;
             p.codes = L->pcodes.as<uint8_t>();
             p.weight_stride = L->pweight_stride;
-            p.w_ublock = L->p_ublock.as<int32_t>();
             p.w_outscale = L->p_outscale.as<float>();
             p.units = L->punits.as<Unit>();
             p.n_units = L->n_punits.as<int32_t>();
@@ -1329,7 +1456,7 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
             p.o_valid = static_cast<int32_t>(L->proj_rows);
             p.o_pad = static_cast<int32_t>(L->proj_o_pad);
             p.bits = kDenseBits;
-            const int64_t nunits = L->proj_mb * ((batch + kBNMax - 1) / kBNMax) * pns;
+            const int64_t nunits = L->proj_mb * ((batch + cf.bn - 1) / cf.bn) * pns;
             cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nunits, L->num_sms)), st),
                        "projection gemm launch");
             count_launch(L);
@@ -1377,21 +1504,24 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
         const bool use_qmoe = path != TQ_PATH_LOTILE;
         std::vector<Unit> units;
         const int64_t local = L->e_end - L->e_begin;
+        const LaunchCfg cf = cfg64(L);
+        int64_t max_tok = 1;
         for (int64_t s = 0; s < nseg; ++s) {
             const int64_t le = segments[3 * s], r0 = segments[3 * s + 1], cnt = segments[3 * s + 2];
             if (le < 0 || le >= local) fail(TQ_ERR_PARAM, "segment expert " + std::to_string(le) + " not resident");
             if (r0 < 0 || cnt < 0 || r0 + cnt > rows) fail(TQ_ERR_SHAPE, "segment rows out of range");
             for (int64_t mb = 0; mb < g.mb_count; ++mb)
-                for (int64_t t0 = 0; t0 < cnt; t0 += kBNMax) {
+                for (int64_t t0 = 0; t0 < cnt; t0 += cf.bn) {
                     Unit u{};
                     u.weight = static_cast<int32_t>(le);
                     u.mb = static_cast<int32_t>(mb);
                     u.x_row = static_cast<int32_t>(r0 + t0);
-                    u.n_tok = static_cast<int32_t>(std::min<int64_t>(kBNMax, cnt - t0));
+                    u.n_tok = static_cast<int32_t>(std::min<int64_t>(cf.bn, cnt - t0));
+                    max_tok = std::max<int64_t>(max_tok, u.n_tok);
                     u.y_row = u.x_row;
                     u.kc_begin = 0;
-                    u.kc_end = static_cast<int16_t>(use_qmoe ? g.kc_total : 0);
-                    u.n_ext = static_cast<int16_t>(g.n_ext);
+                    u.kc_end = static_cast<int16_t>(use_qmoe ? cf.kc_total : 0);
+                    u.n_ext = static_cast<int16_t>(cf.n_ext);
                     u.split = 0;
                     units.push_back(u);
                 }
@@ -1403,19 +1533,20 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
                    "units H2D");
         int32_t* dn = reinterpret_cast<int32_t*>(static_cast<uint8_t*>(dunits.p) + sizeof(Unit) * units.size());
         cuda_check(cudaMemcpyAsync(dn, &nu, sizeof(int32_t), cudaMemcpyHostToDevice, st), "count H2D");
-        GemmParams p = base_params(L);
+        GemmParams p = base_params(L, cf, max_tok);
         void* xr = const_cast<uint16_t*>(xrows);
         void* er = const_cast<uint16_t*>(extrows);
-        p.tmap_x16 = make_map(xr, rows, g.k_pad, 16);
         p.tmap_x64 = make_map(xr, rows, g.k_pad, 64);
-        p.tmap_e16 = make_map(er, rows, g.ext_cols, 16);
         p.tmap_e64 = make_map(er, rows, g.ext_cols, 64);
+        p.x_ptr = static_cast<const __half*>(xr);
+        p.x_ld = g.k_pad;
+        p.e_ptr = static_cast<const __half*>(er);
+        p.e_ld = g.ext_cols;
         p.codes = L->codes.as<uint8_t>();
         p.weight_stride = L->weight_stride;
         p.scales = L->scales.as<__half>();
-        p.zeros = L->zeros.as<uint8_t>();
-        p.ucodes = L->ucodes.as<int8_t>();
-        p.w_ublock = L->w_ublock.as<int32_t>();
+        p.ext_blocks = L->ext_blocks.as<uint8_t>();
+    p.n_ext64 = static_cast<int32_t>(L->g.n_ext);
         p.w_outscale = L->w_outscale.as<float>();
         p.units = dunits.as<Unit>();
         p.n_units = dn;
@@ -1427,7 +1558,6 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
         p.bits = g.bits;
         p.groups = static_cast<int32_t>(g.G);
         p.rank = static_cast<int32_t>(g.r);
-        p.ext_zero = use_qmoe ? 1 : 0;
         cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st), "expert gemm launch");
         count_launch(L);
         cuda_check(cudaStreamSynchronize(st), "stream sync");  // dunits lifetime
@@ -1473,35 +1603,37 @@ tq_status tq_ep_combine(tq_layer* L, const float* x, int64_t batch, const float*
             count_launch(L);
             std::vector<Unit> units;
             const int64_t local = L->e_end - L->e_begin;
+            const LaunchCfg cf = cfg64(L);
             for (int64_t s = 0; s < g.S; ++s)
                 for (int64_t mb = 0; mb < g.mb_count; ++mb)
-                    for (int64_t t0 = 0; t0 < batch; t0 += kBNMax) {
+                    for (int64_t t0 = 0; t0 < batch; t0 += cf.bn) {
                         Unit u{};
                         u.weight = static_cast<int32_t>(local + s);
                         u.mb = static_cast<int32_t>(mb);
                         u.x_row = static_cast<int32_t>(t0);
-                        u.n_tok = static_cast<int32_t>(std::min<int64_t>(kBNMax, batch - t0));
+                        u.n_tok = static_cast<int32_t>(std::min<int64_t>(cf.bn, batch - t0));
                         u.y_row = static_cast<int32_t>(s * batch + t0);
                         u.kc_begin = 0;
-                        u.kc_end = static_cast<int16_t>(g.kc_total);
-                        u.n_ext = static_cast<int16_t>(g.n_ext);
+                        u.kc_end = static_cast<int16_t>(cf.kc_total);
+                        u.n_ext = static_cast<int16_t>(cf.n_ext);
                         units.push_back(u);
                     }
             const int32_t nu = static_cast<int32_t>(units.size());
             cuda_check(cudaMemcpyAsync(L->units.p, units.data(), sizeof(Unit) * units.size(), cudaMemcpyHostToDevice, st),
                        "units H2D");
             cuda_check(cudaMemcpyAsync(L->n_units.p, &nu, sizeof(int32_t), cudaMemcpyHostToDevice, st), "count H2D");
-            GemmParams p = base_params(L);
-            p.tmap_x16 = L->map_xp16;
+            GemmParams p = base_params(L, cf, batch);
             p.tmap_x64 = L->map_xp64;
-            p.tmap_e16 = L->map_ep16;
             p.tmap_e64 = L->map_ep64;
+            p.x_ptr = L->xperm.as<__half>();
+            p.x_ld = g.k_pad;
+            p.e_ptr = L->extperm.as<__half>();
+            p.e_ld = g.ext_cols;
             p.codes = L->codes.as<uint8_t>();
             p.weight_stride = L->weight_stride;
             p.scales = L->scales.as<__half>();
-            p.zeros = L->zeros.as<uint8_t>();
-            p.ucodes = L->ucodes.as<int8_t>();
-            p.w_ublock = L->w_ublock.as<int32_t>();
+            p.ext_blocks = L->ext_blocks.as<uint8_t>();
+    p.n_ext64 = static_cast<int32_t>(L->g.n_ext);
             p.w_outscale = L->w_outscale.as<float>();
             p.units = L->units.as<Unit>();
             p.n_units = L->n_units.as<int32_t>();
@@ -1512,7 +1644,6 @@ tq_status tq_ep_combine(tq_layer* L, const float* x, int64_t batch, const float*
             p.bits = g.bits;
             p.groups = static_cast<int32_t>(g.G);
             p.rank = static_cast<int32_t>(g.r);
-            p.ext_zero = 1;
             cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st), "shared gemm launch");
             count_launch(L);
             cuda_check(cudaStreamSynchronize(st), "stream sync");  // host unit table lifetime

@@ -56,6 +56,18 @@ def test_forward_matches_reference(tq, ref, make_artifact, spec, B):
 
 
 @pytest.mark.parametrize("spec", SPECS[:3], ids=lambda s: f"K{s['K']}b{s['bits']}{s['calib']}")
+def test_prefill_batch_matches_reference(tq, ref, make_artifact, spec):
+    """Prefill-sized batch: 64-wide chunks, several 192-token tiles per expert."""
+    d = make_artifact(**spec)
+    L = tq.Layer(d)
+    x = _x(1500, spec["i"], 5)
+    y, ids, gates = L.forward_host(x, with_routing=True)
+    yr, idr, gr = ref.load(d).forward(x, threads=8)
+    np.testing.assert_array_equal(ids, idr)
+    assert rel_frob(y, yr) <= TOL, rel_frob(y, yr)
+
+
+@pytest.mark.parametrize("spec", SPECS[:3], ids=lambda s: f"K{s['K']}b{s['bits']}{s['calib']}")
 def test_paths_match_reference(tq, ref, make_artifact, spec):
     """qmoe_forward and lotile_forward halves separately (infer.cpp:40-180)."""
     d = make_artifact(**spec)

@@ -1,0 +1,93 @@
+// Microbenchmark: HBM streaming bandwidth of cp.async.bulk into a smem ring
+// (one producer thread, consumer warps that only release stages) as a
+// function of stage size and ring depth, 148 persistent CTAs.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void minit(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c)); }
+__device__ __forceinline__ void marrive(uint64_t* b) { asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory"); }
+__device__ __forceinline__ void mexpect(uint64_t* b, uint32_t n) { asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mwait(uint64_t* b, uint32_t ph) {
+  asm volatile("{\n.reg .pred P1;\nW_%=:\nmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W_%=;\n}" ::"r"(su32(b)), "r"(ph) : "memory");
+}
+__device__ __forceinline__ void bulk(void* d, const void* s, uint32_t n, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(d)), "l"(s), "r"(n), "r"(su32(b)) : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1) stream_kernel(const uint8_t* src, size_t per_cta, int stage, int nst, unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + nst * stage);
+  uint64_t* empty = full + 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nst; ++s) { minit(&full[s], 1); minit(&empty[s], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint8_t* base = src + blockIdx.x * per_cta;
+  const int nchunks = (int)(per_cta / stage);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0; uint32_t ph = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mwait(&empty[s], ph ^ 1);
+        mexpect(&full[s], stage);
+        bulk(sm + s * stage, base + (size_t)c * stage, stage, &full[s]);
+        if (++s == nst) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    int s = 0; uint32_t ph = 0; unsigned acc = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      mwait(&full[s], ph);
+      acc += reinterpret_cast<const uint32_t*>(sm + s * stage)[lane + 32 * (warp - 4)];
+      __syncwarp();
+      if (lane == 0) marrive(&empty[s]);
+      if (++s == nst) { s = 0; ph ^= 1; }
+    }
+    if (acc == 0x12345678) atomicAdd(sink, 1ull);
+  }
+}
+
+// plain LDG.128 streaming for comparison
+__global__ void __launch_bounds__(512) ldg_kernel(const int4* src, size_t n, unsigned long long* sink) {
+  unsigned acc = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    int4 v; asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(src + i));
+    acc ^= v.x ^ v.w;
+  }
+  if (acc == 0x12345678) atomicAdd(sink, 1ull);
+}
+
+int main() {
+  const size_t total = (size_t)2 << 30;
+  uint8_t* buf; cudaMalloc(&buf, total); cudaMemset(buf, 1, total);
+  unsigned long long* sink; cudaMalloc(&sink, 8);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  const int grid = 148;
+  int stages[] = {2048, 4096, 8192, 16384, 32768};
+  int depths[] = {4, 8, 16, 24};
+  for (int st : stages) for (int nd : depths) {
+    size_t smem = (size_t)st * nd + 1024;
+    if (smem > 220 * 1024) continue;
+    cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    size_t per = (total / grid) / st * st;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      stream_kernel<<<grid, 256, smem>>>(buf, per, st, nd, sink);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+    }
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    printf("bulk stage=%6d depth=%2d inflight=%4d KB  %7.1f GB/s  (%s)\n", st, nd, st * nd / 1024, per * grid / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+  }
+  for (int rep = 0; rep < 2; ++rep) {
+    cudaEventRecord(a);
+    ldg_kernel<<<148 * 4, 512>>>((const int4*)buf, total / 16, sink);
+    cudaEventRecord(b); cudaEventSynchronize(b);
+  }
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  printf("ldg.128 streaming %7.1f GB/s\n", total / ms / 1e6);
+  return 0;
+}

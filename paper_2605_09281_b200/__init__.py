@@ -256,14 +256,21 @@ class Layer:
         check(lib().tq_sync(self._h, _stream_ptr(self.device)))
 
     # -- host-buffer API (the reference binding's numpy in / numpy out) ------
-    def forward_host(self, x: np.ndarray, path: str = "full", with_routing: bool = False):
+    def forward_host(self, x: np.ndarray, path: str = "full", with_routing: bool = False, out=None):
+        """Host f32 in / host f32 out (tq_forward_host): the copies are part of the call.
+        ``out`` may be a preallocated (pinned) float32 [B, o] array."""
         x = np.ascontiguousarray(x, dtype=np.float32)
         if x.ndim != 2:
             raise ParamError("x must be a 2-D float array")
         if x.shape[1] != self.in_dim:
             raise ShapeError(f"token width {x.shape[1]} vs in_dim {self.in_dim}")
         B = x.shape[0]
-        y = np.empty((B, self.out_dim), np.float32)
+        if out is not None:
+            if out.shape != (B, self.out_dim) or out.dtype != np.float32 or not out.flags.c_contiguous:
+                raise ParamError("out must be a contiguous float32 [B, out_dim] array")
+            y = out
+        else:
+            y = np.empty((B, self.out_dim), np.float32)
         ids = np.empty((B, self.top_k), np.int64) if with_routing else None
         gates = np.empty((B, self.top_k), np.float32) if with_routing else None
         check(lib().tq_forward_host(self._h, x.ctypes.data, B, y.ctypes.data,
@@ -288,6 +295,44 @@ class Layer:
         n = C.c_int64()
         check(lib().tq_gemm_time_get(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    # -- expert-parallel stages (tq_ep_*; orchestrated by ep.EPLayer) --------
+    def ep_row_widths(self):
+        """(x row, ext row) widths in fp16 elements of the dispatch buffers."""
+        return int(lib().tq_ep_xrow_elems(self._h)), int(lib().tq_ep_extrow_elems(self._h))
+
+    def ep_dispatch_rows(self, x, ids, perm, path: str = "full"):
+        """Rows to send, in permuted-slot order: fp16 token rows + fp16 extension rows."""
+        torch = _torch()
+        self._check_x(x)
+        B = x.shape[0]
+        xw, ew = self.ep_row_widths()
+        xrows = torch.empty((B * self.top_k, xw), dtype=torch.float16, device=x.device)
+        erows = torch.empty((B * self.top_k, ew), dtype=torch.float16, device=x.device)
+        check(lib().tq_ep_dispatch_rows(self._h, x.data_ptr(), B, ids.data_ptr(), perm.data_ptr(),
+                                        xrows.data_ptr(), erows.data_ptr(), _PATHS[path], _stream_ptr(x.device)))
+        return xrows, erows
+
+    def ep_expert_rows(self, xrows, erows, segments: np.ndarray, path: str = "full"):
+        """Resident-expert outputs (f32 [rows, o]) for received rows; segments int64
+        [n, 3] = (local expert, first row, row count) sorted by first row."""
+        torch = _torch()
+        rows = xrows.shape[0]
+        y = torch.empty((rows, self.out_dim), dtype=torch.float32, device=xrows.device)
+        seg = np.ascontiguousarray(segments, dtype=np.int64).reshape(-1, 3)
+        if rows and len(seg):
+            check(lib().tq_ep_expert_rows(self._h, xrows.data_ptr(), erows.data_ptr(), rows, seg.ctypes.data,
+                                          len(seg), y.data_ptr(), _PATHS[path], _stream_ptr(xrows.device)))
+        return y
+
+    def ep_combine(self, x, yrows, inv, gates, path: str = "full", out=None):
+        """Gate-weighted combine of returned rows (+ shared experts on the home tokens)."""
+        torch = _torch()
+        B = x.shape[0]
+        y = out if out is not None else torch.empty((B, self.out_dim), dtype=torch.float32, device=x.device)
+        check(lib().tq_ep_combine(self._h, x.data_ptr(), B, yrows.data_ptr(), inv.data_ptr(), gates.data_ptr(),
+                                  y.data_ptr(), _PATHS[path], _stream_ptr(x.device)))
+        return y
 
     def export_codes(self, e: int):
         """Codes of matrix e decoded back from the engine's tile layout (uint32 [o, i] CUDA tensor)."""

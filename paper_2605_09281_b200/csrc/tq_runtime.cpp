@@ -955,6 +955,23 @@ void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaSt
     count_launch(L);
 }
 
+// The fused expert GEMM, bracketed by CUDA events on its own stream when the
+// layer's timing hook is on (tq_gemm_timing_enable): the device time bench.py
+// divides the kernel's algorithmic bytes / flops by.
+static void timed_expert_gemm(tq_layer* L, const GemmParams& p, int grid, cudaStream_t st) {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (L->timing) {
+        cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
+        cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
+    }
+    cuda_check(launch_gemm(p, grid, st), "expert gemm launch");
+    if (L->timing) {
+        cuda_check(cudaEventRecord(ev1, st), "cudaEventRecord");
+        L->tev.emplace_back(ev0, ev1);
+    }
+}
+
 void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
                  int path, cudaStream_t st) {
     (void)x;
@@ -1073,17 +1090,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.bits = g.bits;
     p.groups = static_cast<int32_t>(g.G);
     p.rank = static_cast<int32_t>(g.r);
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    if (L->timing) {
-        cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
-        cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
-        cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
-    }
-    cuda_check(launch_gemm(p, L->num_sms, st), "expert gemm launch");
-    if (L->timing) {
-        cuda_check(cudaEventRecord(ev1, st), "cudaEventRecord");
-        L->tev.emplace_back(ev0, ev1);
-    }
+    timed_expert_gemm(L, p, L->num_sms, st);
     count_launch(L);
     // combine
     CombineArgs ca{};
@@ -1558,7 +1565,7 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
         p.bits = g.bits;
         p.groups = static_cast<int32_t>(g.G);
         p.rank = static_cast<int32_t>(g.r);
-        cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st), "expert gemm launch");
+        timed_expert_gemm(L, p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st);
         count_launch(L);
         cuda_check(cudaStreamSynchronize(st), "stream sync");  // dunits lifetime
     });

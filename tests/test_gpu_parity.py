@@ -237,3 +237,75 @@ def test_artifact_errors(tq, make_artifact, tmp_path):
         tq.Layer(str(bad))
     with pytest.raises(tq.IoError):
         tq.Layer(str(tmp_path / "missing"))
+
+
+# ---------------------------------------------------------------------------
+# against the committed reference fixtures (tests/golden/, written by the
+# reference itself; these need no /root/reference on the GPU box)
+# ---------------------------------------------------------------------------
+
+import os  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+GOLD_ARTS = ["folded_b3", "general_b2_shared", "scalar_b4_ragged", "general_b8"]
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return dict(np.load(os.path.join(GOLD, "golden.npz")))
+
+
+@pytest.mark.parametrize("name", GOLD_ARTS)
+def test_engine_matches_reference_golden(tq, golden, name):
+    L = tq.Layer(os.path.join(GOLD, name))
+    for B in (1, 7, 33):
+        x = golden[f"{name}/x{B}"]
+        y, ids, gates = L.forward_host(x, with_routing=True)
+        np.testing.assert_array_equal(ids, golden[f"{name}/ids{B}"])
+        np.testing.assert_array_max_ulp(gates, golden[f"{name}/gates{B}"], maxulp=1)
+        assert rel_frob(y, golden[f"{name}/tileq{B}"]) <= TOL
+        for path in ("qmoe", "lotile"):
+            yp = L.forward_host(x, path=path)
+            assert rel_frob(yp, golden[f"{name}/{path}{B}"]) <= TOL, (path, B)
+
+
+def test_route_golden_kats(tq, golden):
+    for t in range(5):
+        x, g = golden[f"route{t}/x"], golden[f"route{t}/g"]
+        k = golden[f"route{t}/ids"].shape[1]
+        ids, gates = tq.route(x, g, k)
+        np.testing.assert_array_equal(ids, golden[f"route{t}/ids"])
+        np.testing.assert_array_max_ulp(gates, golden[f"route{t}/gates"], maxulp=1)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8])
+def test_unpack_golden(tq, golden, bits):
+    for count in (1, 5, 7, 64, 129, 1000):
+        got = tq.unpack_codes_gpu(golden[f"pack{bits}_{count}/bytes"], bits, count)
+        np.testing.assert_array_equal(got, golden[f"pack{bits}_{count}/codes"])
+
+
+class _RankComm:
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["general_b2_shared", "scalar_b4_ragged"])
+def test_ep_stages_emulated_ranks(tq, golden, name, world):
+    """Expert-parallel stages (tq_ep_*) for W ranks, each a Layer holding its
+    expert block, stepped in one process with the exchange done by slicing
+    (ep.emulate_forward; no kernels wait on one another).  Each rank's tokens
+    must come out as the reference's tileq_forward."""
+    import torch
+    from paper_2605_09281_b200.ep import EPLayer, emulate_forward, expert_bounds
+    d = os.path.join(GOLD, name)
+    full = tq.Layer(d)
+    b = expert_bounds(full.num_experts, world)
+    layers = [EPLayer(comm=_RankComm(r, world), num_experts=full.num_experts,
+                      stages=tq.Layer(d, expert_range=(b[r], b[r + 1]))) for r in range(world)]
+    Bs = [33, 7, 1][:world]
+    xs = [torch.from_numpy(golden[f"{name}/x{B}"]).cuda() for B in Bs]
+    ys = emulate_forward(layers, xs)
+    for B, y in zip(Bs, ys):
+        assert rel_frob(y.cpu().numpy(), golden[f"{name}/tileq{B}"]) <= TOL, (B, world)

@@ -336,10 +336,27 @@ def bench_tileq(args, rank, world, local_rank):
                 fwd(x, y)
         return evs
 
+    clocks = ClockSampler(local_rank).start() if rank == 0 else None
     for _ in range(args.warmup):
         one_step(False)
+    # keep the GPU busy (untimed) until nvidia-smi has produced samples, so the
+    # clock record covers a loaded GPU; the sampler keeps running through the
+    # timed region
+    settle = 0
+    t_settle = time.time()
+    while True:
+        ready = clocks is None or len(clocks.lines) >= 3 or time.time() - t_settle > 5.0
+        if world > 1:
+            import torch.distributed as dist
+            flag = torch.tensor([1 if ready else 0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ready = bool(flag.item())
+        if ready:
+            break
+        one_step(False)
+        torch.cuda.synchronize()
+        settle += 1
     barrier()
-    clocks = ClockSampler(local_rank).start() if rank == 0 else None
     L.gemm_timing(True)
     L.reset_launch_count()
     barrier()
@@ -400,7 +417,7 @@ def bench_tileq(args, rank, world, local_rank):
             "data": "synthetic", "config": workload_config(args, world), "roofline": roof,
             "per_batch": per_b, "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_forward": launches / max(1, args.steps * len(batches)),
-            "gemm_launches_per_forward": launches_per_fwd, "clocks": clk}
+            "gemm_launches_per_forward": launches_per_fwd, "clocks": clk, "clock_settle_steps": settle}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, art, geo)
     print(json.dumps(line), flush=True)
@@ -468,7 +485,7 @@ def cpu_baseline_leg(args, art, geo):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="tileq", choices=["tileq", "reference"])
     ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])

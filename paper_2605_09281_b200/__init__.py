@@ -21,7 +21,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtileq_b200.so")
+LIB_PATH = os.environ.get("TQ_LIB_PATH") or os.path.join(HERE, "libtileq_b200.so")
 
 PATH_FULL, PATH_QMOE, PATH_LOTILE = 0, 1, 2
 _PATHS = {"full": PATH_FULL, "tileq": PATH_FULL, "qmoe": PATH_QMOE, "lotile": PATH_LOTILE}

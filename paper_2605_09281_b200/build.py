@@ -47,36 +47,42 @@ def needs_rebuild() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_rebuild():
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB) -> str:
+    """Compile the sources (in parallel) and link ``lib``.  ``defines`` builds an
+    experiment variant (e.g. TQ_SPIN_WAIT) into a separate library file."""
+    if not force and not defines and not needs_rebuild():
         return LIB
     objs = []
     jdir = json_include_dir()
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
-              f"-I{jdir}", f"-I{os.path.join(HERE, '..', 'include')}", "--expt-relaxed-constexpr"]
-    build_dir = os.path.join(HERE, "_build")
+              f"-I{jdir}", f"-I{os.path.join(HERE, '..', 'include')}", "--expt-relaxed-constexpr",
+              *[f"-D{d}" for d in defines]]
+    build_dir = os.path.join(HERE, "_build" + "".join("_" + d.lower() for d in defines))
     os.makedirs(build_dir, exist_ok=True)
+    procs = []
     for src in SOURCES:
         obj = os.path.join(build_dir, src + ".o")
         cmd = common + ["-c", os.path.join(CSRC, src), "-o", obj]
-        if src.endswith(".cu"):
-            cmd += ["-Xptxas", "-v"] if verbose else []
-        else:
-            cmd += ["-x", "cu"] if False else []
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}\n{r.stderr}")
-        if verbose:
-            print(r.stderr)
+        if src.endswith(".cu") and verbose:
+            cmd += ["-Xptxas", "-v"]
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    for src, pr in procs:
+        out, err = pr.communicate()
+        if pr.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n{out}\n{err}")
+        if verbose:
+            print(err)
+    tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lz", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = LIB if not defs else os.path.join(HERE, "libtileq_b200_" + "_".join(d.lower() for d in defs) + ".so")
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, lib=out))

@@ -63,7 +63,9 @@ struct SharedHdr {
 };
 
 __device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx) {
+#ifdef TQ_TRACE
     if ((p.debug & 8) && blockIdx.x == 0 && idx < 4096) p.trace[slot * 4096 + idx] = clock64();
+#endif
 }
 
 template <int BITS, int KC, int NG, int DN>
@@ -112,8 +114,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     if (threadIdx.x == 0) {
         prefetch_tmap(&p.tmap_x64);
         prefetch_tmap(&p.tmap_e64);
+        prefetch_tmap(&p.tmap_x16);
+        prefetch_tmap(&p.tmap_e16);
         for (int s = 0; s < x_stages; ++s) {
-            mbar_init(&hdr->x_full[s], 32);
+            mbar_init(&hdr->x_full[s], 1);
             mbar_init(&hdr->x_empty[s], 1);
         }
         for (int s = 0; s < kAS; ++s) {
@@ -148,8 +152,8 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const int gshift = p.group_shift;
 
     if (warp == 0) {
-        // ===================== code producer =====================
-        if (lane == 0) {
+        // ===================== code producer (converged warp, one elected lane issues) =====
+        {
             int cs = 0, es = 0, tcnt = 0;
             uint32_t cph = 0, eph = 0;
             Unit nxt = first < n_units ? p.units[first] : Unit{};
@@ -164,33 +168,35 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     const int kc = un.kc_begin + c;
                     mbar_wait(&hdr->c_empty[cs], cph ^ 1u);
                     uint8_t* st = smem + c_off + cs * kCStage;
-                    if constexpr (BITS == kDenseBits) {
-                        mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes);
-                        bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
+                    const uint8_t* src = wbase + static_cast<int64_t>(kc) * kCBytes;
+                    if (p.debug & 128) {
+                        if (lane == 0) mbar_arrive(&hdr->c_full[cs]);
+                    } else if constexpr (BITS == kDenseBits) {
+                        bulk_copy2_elect(&hdr->c_full[cs], st, src, kCBytes, st, src, 0u);
                     } else {
                         const int e0 = kc * KC;
                         const int g0 = gshift >= 0 ? e0 >> gshift : e0 / p.group_size;
                         const int glast = gshift >= 0 ? (e0 + KC - 1) >> gshift : (e0 + KC - 1) / p.group_size;
                         const int g1 = min(p.groups - 1, glast);
                         const uint32_t sbytes = static_cast<uint32_t>(g1 - g0 + 1) * kBM * 2;
-                        mbar_arrive_expect_tx(&hdr->c_full[cs], kCBytes + sbytes);
-                        bulk_copy_g2s(st, wbase + static_cast<int64_t>(kc) * kCBytes, kCBytes, &hdr->c_full[cs]);
-                        bulk_copy_g2s(st + kCBytes, p.scales + (wm * p.groups + g0) * kBM, sbytes, &hdr->c_full[cs]);
+                        bulk_copy2_elect(&hdr->c_full[cs], st, src, kCBytes, st + kCBytes,
+                                         p.scales + (wm * p.groups + g0) * kBM, sbytes);
                     }
-                    trace_ev(p, 0, tcnt++);
+                    if (lane == 0) trace_ev(p, 0, tcnt);
+                    ++tcnt;
                     if (++cs == c_stages) { cs = 0; cph ^= 1u; }
                 }
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
                     mbar_wait(&hdr->e_empty[es], eph ^ 1u);
-                    mbar_arrive_expect_tx(&hdr->e_full[es], ext_bytes);
-                    bulk_copy_g2s(smem + e_off + es * ext_bytes, p.ext_blocks + wm * ext_bytes, ext_bytes,
-                                  &hdr->e_full[es]);
+                    uint8_t* dst = smem + e_off + es * ext_bytes;
+                    bulk_copy2_elect(&hdr->e_full[es], dst, p.ext_blocks + wm * ext_bytes, ext_bytes, dst, dst, 0u);
                     if (++es == 2) { es = 0; eph ^= 1u; }
                 }
             }
         }
     } else if (warp == 3) {
-        // ===================== activation producer (all 32 lanes) =====================
+        // ===================== activation producer (converged warp, elected lane) ==========
+        // TMA 2D tiles, 128B swizzle: 16-row boxes for small token tiles, 64-row boxes above 48
         int xs = 0, tcnt = 0;
         uint32_t xph = 0;
         Unit nxt = first < n_units ? p.units[first] : Unit{};
@@ -199,41 +205,32 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             if (u + stride < n_units) nxt = p.units[u + stride];
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
-            const bool big = un.n_tok > 32;
-            const int nbox = (un.n_tok + 63) / 64;
-            const int pieces = un.n_tok * kAtoms * 8;   // 16-byte pieces per chunk (small tiles)
+            const bool b64 = un.n_tok > 48;
+            const int box = b64 ? 64 : 16;
+            const int nbox = (un.n_tok + box - 1) / box;
+            const uint32_t bytes = static_cast<uint32_t>(kAtoms * nbox * box * 128);
             for (int c = 0; c < nch; ++c) {
                 const bool ext = c >= nmain;
                 mbar_wait(&hdr->x_empty[xs], xph ^ 1u);
-                const uint32_t sx = s_base + x_off + xs * x_stage_bytes;
                 const int col0 = ext ? (c - nmain) * KC : (un.kc_begin + c) * KC;
-                if (big) {
-                    if (lane == 0) {
-                        mbar_arrive_expect_tx(&hdr->x_full[xs], kAtoms * nbox * 64 * 128);
-                        const CUtensorMap* map = ext ? &p.tmap_e64 : &p.tmap_x64;
+                if (elect_one()) {
+                    if (p.debug & 32) {
+                        mbar_arrive(&hdr->x_full[xs]);
+                    } else {
+                        mbar_arrive_expect_tx(&hdr->x_full[xs], bytes);
+                        const CUtensorMap* map = ext ? (b64 ? &p.tmap_e64 : &p.tmap_e16)
+                                                     : (b64 ? &p.tmap_x64 : &p.tmap_x16);
                         uint8_t* xst = smem + x_off + xs * x_stage_bytes;
 #pragma unroll
                         for (int at = 0; at < kAtoms; ++at)
                             for (int bx = 0; bx < nbox; ++bx)
-                                tma_load_2d(xst + at * x_atom_bytes + bx * 64 * 128, map, col0 + at * kKC,
-                                            un.x_row + bx * 64, &hdr->x_full[xs]);
-                    } else {
-                        mbar_arrive(&hdr->x_full[xs]);
+                                tma_load_2d(xst + at * x_atom_bytes + bx * box * 128, map, col0 + at * kKC,
+                                            un.x_row + bx * box, &hdr->x_full[xs]);
                     }
-                } else {
-                    const __half* src = ext ? p.e_ptr : p.x_ptr;
-                    const int64_t ld = ext ? p.e_ld : p.x_ld;
-                    for (int pc = lane; pc < pieces; pc += 32) {
-                        const int row = pc / (kAtoms * 8);
-                        const int rem = pc % (kAtoms * 8);
-                        const int at = rem >> 3, ch = rem & 7;
-                        const __half* g = src + static_cast<int64_t>(un.x_row + row) * ld + col0 + at * kKC + ch * 8;
-                        const uint32_t d = sx + at * x_atom_bytes + row * 128 + ((ch ^ (row & 7)) << 4);
-                        cp_async_16(d, g);
-                    }
-                    cp_async_mbar_arrive(&hdr->x_full[xs]);
+                    trace_ev(p, 1, tcnt);
                 }
-                if (lane == 0) trace_ev(p, 1, tcnt++);
+                __syncwarp();
+                ++tcnt;
                 if (++xs == x_stages) { xs = 0; xph ^= 1u; }
             }
         }
@@ -285,10 +282,14 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         const int grp = wid >> 2;
         const int rloc = q * 32 + lane;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-        // every warp walks the whole chunk stream with O(1) ring bookkeeping and
-        // processes the chunks whose round-robin index equals its group
-        int cs = 0, as = 0, es = 0, rr = 0;
+        // the CTA's chunk stream (main + extension chunks of its units, in order)
+        // is dealt round-robin to the NG groups: group grp takes global chunk
+        // indices grp, grp+NG, ...; ring positions advance incrementally
+        int cs = 0, as = grp, es = 0;                  // as: chunk index grp mod kAS (NG <= kAS)
         uint32_t cph = 0, aph = 0, eph = 0;
+        int m_cur = 0;                                 // main-chunk index that (cs, cph) denotes
+        int q_base = 0, m_base = 0;                    // chunks / main chunks before this unit
+        int c_next = grp;                              // next own chunk, relative to q_base
         int tcnt = 0;
         const bool tr = (lane == 0 && q == 0);
         Unit nxt = first < n_units ? p.units[first] : Unit{};
@@ -297,12 +298,17 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             if (u + stride < n_units) nxt = p.units[u + stride];
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
-            for (int c = 0; c < nch; ++c) {
-                const bool mine = rr == grp;
-                if (++rr == NG) rr = 0;
+            int c = c_next;
+            for (; c < nch; c += NG) {
                 const bool main_chunk = c < nmain;
-                if (mine) {
-                    uint32_t v[kSW][16];
+                if (main_chunk) {
+                    // move the code-ring position to main chunk m_base + c
+                    for (int m = m_base + c; m_cur < m; ++m_cur)
+                        if (++cs == c_stages) { cs = 0; cph ^= 1u; }
+                }
+                {
+                    // registers: the packed words of the chunk (kSW x BITS) plus ONE
+                    // super-word of fp16 pairs at a time -- dequantize, tcgen05.st, reuse
                     if (main_chunk) {
                         const int kc = un.kc_begin + c;
                         mbar_wait(&hdr->c_full[cs], cph);
@@ -332,59 +338,66 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
+                        mbar_wait(&hdr->a_empty[as], aph ^ 1u);
+                        if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+                        tc_fence_after();
 #pragma unroll
                         for (int s = 0; s < kSW; ++s) {
+                            uint32_t v[16];
                             if constexpr (BITS == kDenseBits) {
 #pragma unroll
-                                for (int w = 0; w < 16; ++w) v[s][w] = words[s][w];
-                            } else {
-                                if (p.debug & 1) {
+                                for (int w = 0; w < 16; ++w) v[w] = words[s][w];
+                            } else if (p.debug & 1) {
 #pragma unroll
-                                    for (int w = 0; w < 16; ++w) v[s][w] = words[s][w % kWords];
-                                } else {
-                                    const DqConst dq = make_dq(__ushort_as_half(sbits[s]));
-                                    dequant32<BITS>(words[s], dq, v[s]);
-                                }
+                                for (int w = 0; w < 16; ++w) v[w] = words[s][w % kWords];
+                            } else {
+                                const DqConst dq = make_dq(__ushort_as_half(sbits[s]));
+                                dequant32<BITS>(words[s], dq, v);
+                            }
+                            if (!(p.debug & 64)) tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
+                            else {
+#pragma unroll
+                                for (int w = 0; w < 16; ++w) asm volatile("" ::"r"(v[w]));
                             }
                         }
                     } else {
                         // extension chunk: precomputed fp16 columns [-zero*s per group | U_p codes | 0]
                         mbar_wait(&hdr->e_full[es], eph);
                         const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
+                        mbar_wait(&hdr->a_empty[as], aph ^ 1u);
+                        if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+                        tc_fence_after();
 #pragma unroll
                         for (int s = 0; s < kSW; ++s) {
                             const int colbase = (c - nmain) * KC + 32 * s;
                             const int blk = colbase >> 6, hh = (colbase >> 5) & 1;
+                            uint32_t v[16];
                             if (blk < p.n_ext64) {
 #pragma unroll
                                 for (int w = 0; w < 16; ++w)
-                                    v[s][w] = eb[blk * (code_block_bytes(kDenseBits) / 4) + (hh * 16 + w) * kBM];
+                                    v[w] = eb[blk * (code_block_bytes(kDenseBits) / 4) + (hh * 16 + w) * kBM];
                             } else {
 #pragma unroll
-                                for (int w = 0; w < 16; ++w) v[s][w] = 0u;
+                                for (int w = 0; w < 16; ++w) v[w] = 0u;
                             }
+                            tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
                     }
-                    mbar_wait(&hdr->a_empty[as], aph ^ 1u);
-                    if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
-                    tc_fence_after();
-#pragma unroll
-                    for (int s = 0; s < kSW; ++s) tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v[s]);
-                    tc_wait_st();
+                    if (!(p.debug & 64)) tc_wait_st();
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&hdr->a_full[as]);
                     if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
                     ++tcnt;
                 }
-                // ring bookkeeping for every chunk of the stream
-                if (main_chunk) {
-                    if (++cs == c_stages) { cs = 0; cph ^= 1u; }
-                }
-                if (++as == kAS) { as = 0; aph ^= 1u; }
+                as += NG;
+                if (as >= kAS) { as -= kAS; aph ^= 1u; }
             }
+            c_next = c - nch;
+            q_base += nch;
+            m_base += nmain;
             if (un.n_ext > 0 && p.n_ext64 > 0) {
                 if (++es == 2) { es = 0; eph ^= 1u; }
             }
@@ -447,7 +460,7 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     if (!cfg_ok) return cudaErrorInvalidValue;
     if (p.bn_max > dn) return cudaErrorInvalidValue;
     // activation ring: stage rows = token tile rounded to the box (64) or the MMA N granularity (16)
-    const int rows = p.bn_max > 32 ? ((p.bn_max + 63) / 64) * 64 : ((p.bn_max + 15) / 16) * 16;
+    const int rows = p.bn_max > 48 ? ((p.bn_max + 63) / 64) * 64 : ((p.bn_max + 15) / 16) * 16;
     p.x_stage_rows = rows;
     const int x_stage = (kc / kKC) * rows * 128;
     const int c_stage = code_stage_bytes(p.bits, kc);

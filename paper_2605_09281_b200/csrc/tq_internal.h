@@ -38,6 +38,8 @@ static_assert(sizeof(Unit) == 32, "Unit is 32 bytes");
 struct GemmParams {
     CUtensorMap tmap_x64;   // activations fp16 [rows, k_pad], box 64 rows x 64 cols, SW128
     CUtensorMap tmap_e64;   // extension activations fp16 [rows, ext_cols], box 64 x 64
+    CUtensorMap tmap_x16;   // the same tensors with 16-row boxes (small token tiles)
+    CUtensorMap tmap_e16;
     const __half* x_ptr;    // the same two matrices for the cp.async path (small token tiles)
     int64_t x_ld;
     const __half* e_ptr;

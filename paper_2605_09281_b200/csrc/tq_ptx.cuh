@@ -30,6 +30,30 @@ static __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint
 }
 
 static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef TQ_SPIN_WAIT
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TQ_SPIN_%=:\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra TQ_SPIN_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+    return;
+#endif
+#ifdef TQ_WAIT_BACKOFF
+    uint32_t ok = 0;
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(TQ_WAIT_BACKOFF);
+    }
+#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "TQ_WAIT_%=:\n\t"
@@ -63,6 +87,24 @@ static __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src,
         : "memory");
 }
 
+// Warp-converged producer issue: every lane executes, one elected lane arms
+// the barrier with the expected bytes and starts up to two bulk copies into
+// it (the second is skipped when bytes2 == 0).
+static __device__ __forceinline__ void bulk_copy2_elect(uint64_t* bar, void* dst1, const void* src1, uint32_t bytes1,
+                                                        void* dst2, const void* src2, uint32_t bytes2) {
+    asm volatile(
+        "{\n\t.reg .pred e, two;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.and.b32 two, %6, 0, e;\n\t"
+        "@e mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %7;\n\t"
+        "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%1], [%2], %3, [%0];\n\t"
+        "@two cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%4], [%5], %6, [%0];\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(smem_u32(dst1)), "l"(src1), "r"(bytes1), "r"(smem_u32(dst2)), "l"(src2), "r"(bytes2),
+        "r"(bytes1 + bytes2)
+        : "memory");
+}
+
 static __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                             uint64_t* bar) {
     asm volatile(
@@ -70,6 +112,17 @@ static __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap*
         "[%4];" ::"r"(smem_u32(dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
+}
+
+// true in exactly one lane of a converged warp
+static __device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, e;\n}"
+        : "=r"(pred));
+    return pred != 0;
 }
 
 static __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {

@@ -403,12 +403,9 @@ struct Geometry {
     int64_t n_ext, ext_cols;
 };
 
-// Repack one quantized matrix into [mb][kc] blocks + scale/zero slabs.
-void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out, uint8_t* zeros_out,
-                 int* k_out) {
-    const int bits = g.bits;
-    const std::vector<uint32_t> codes = unpack_stream(q.packed, bits, static_cast<size_t>(g.o * g.i), "codes");
-    // power-of-two prescale so code*s' stays comfortably inside fp16 range
+// Power-of-two prescale k of a matrix (s' = s * 2^k, max s' <= 16) so code*s'
+// stays comfortably inside fp16 range; the epilogue multiplies by 2^-k.
+int prescale_exponent(const QMat& q) {
     float smax = 0.0f;
     for (uint16_t sb : q.scales) smax = std::max(smax, half_bits_to_float(sb));
     int k = 0;
@@ -417,6 +414,15 @@ void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t*
         k = std::max(-24, std::min(24, k));
         while (std::ldexp(static_cast<double>(smax), k) > 16.0) --k;
     }
+    return k;
+}
+
+// Repack one quantized matrix into [mb][kc] blocks + scale/zero slabs.
+void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out, uint8_t* zeros_out,
+                 int* k_out) {
+    const int bits = g.bits;
+    const std::vector<uint32_t> codes = unpack_stream(q.packed, bits, static_cast<size_t>(g.o * g.i), "codes");
+    const int k = prescale_exponent(q);
     *k_out = k;
     const int blk = code_block_bytes(bits);
     uint32_t cbuf[32];
@@ -702,13 +708,16 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     int bits = 0;
     size_t gs = 0;
     // every expert is read and validated (like read_artifact) even when only a subset is resident
-    std::vector<QMat> all_q;
+    // prescale exponent of EVERY routed expert: a rank's dispatch rows carry
+    // the low-rank term pre-multiplied by the owner's 2^k (expert parallel)
+    std::vector<int> k_all(K, 0);
     for (size_t e = 0; e < K; ++e) {
         int b = 0;
         size_t gsz = 0;
         QMat m = read_qmat(c, "expert." + std::to_string(e), qmeta, O, I, &b, &gsz);
         bits = b;
         gs = gsz;
+        k_all[e] = prescale_exponent(m);
         if (static_cast<int64_t>(e) >= e_begin && static_cast<int64_t>(e) < e_end) q.push_back(std::move(m));
     }
     if (g.S > 0) {
@@ -867,9 +876,7 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
             pm_of[e] = static_cast<int32_t>(q_matrix[qq]);
             if (tier[qq] == 1) inv = 1.0 / scaling[e * I];
         }
-        int k = 0;
-        const int64_t local = static_cast<int64_t>(e) - e_begin;
-        if (local >= 0 && local < e_end - e_begin) k = wk[static_cast<size_t>(local)];
+        const int k = k_all[e];
         zscale[e] = static_cast<float>(static_cast<double>(su) * inv * std::ldexp(1.0, k));
     }
     L->NP = static_cast<int64_t>(mats.size());
@@ -1017,6 +1024,8 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
         GemmParams p = base_params(L, cf, batch);
         p.tmap_x64 = L->map_x16_64;
         p.tmap_e64 = L->map_x16_64;
+        p.tmap_x16 = L->map_x16_16;
+        p.tmap_e16 = L->map_x16_16;
         p.x_ptr = L->x16.as<__half>();
         p.x_ld = g.k_pad;
         p.e_ptr = L->x16.as<__half>();
@@ -1070,6 +1079,8 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     GemmParams p = base_params(L, cf, batch);
     p.tmap_x64 = L->map_xp64;
     p.tmap_e64 = L->map_ep64;
+    p.tmap_x16 = L->map_xp16;
+    p.tmap_e16 = L->map_ep16;
     p.x_ptr = L->xperm.as<__half>();
     p.x_ld = g.k_pad;
     p.e_ptr = L->extperm.as<__half>();
@@ -1448,6 +1459,8 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
             GemmParams p = base_params(L, cf, batch);
             p.tmap_x64 = L->map_x16_64;
             p.tmap_e64 = L->map_x16_64;
+            p.tmap_x16 = L->map_x16_16;
+            p.tmap_e16 = L->map_x16_16;
             p.x_ptr = L->x16.as<__half>();
             p.x_ld = g.k_pad;
             p.e_ptr = L->x16.as<__half>();
@@ -1545,6 +1558,8 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
         void* er = const_cast<uint16_t*>(extrows);
         p.tmap_x64 = make_map(xr, rows, g.k_pad, 64);
         p.tmap_e64 = make_map(er, rows, g.ext_cols, 64);
+        p.tmap_x16 = make_map(xr, rows, g.k_pad, 16);
+        p.tmap_e16 = make_map(er, rows, g.ext_cols, 16);
         p.x_ptr = static_cast<const __half*>(xr);
         p.x_ld = g.k_pad;
         p.e_ptr = static_cast<const __half*>(er);
@@ -1632,6 +1647,8 @@ tq_status tq_ep_combine(tq_layer* L, const float* x, int64_t batch, const float*
             GemmParams p = base_params(L, cf, batch);
             p.tmap_x64 = L->map_xp64;
             p.tmap_e64 = L->map_ep64;
+            p.tmap_x16 = L->map_xp16;
+            p.tmap_e16 = L->map_ep16;
             p.x_ptr = L->xperm.as<__half>();
             p.x_ld = g.k_pad;
             p.e_ptr = L->extperm.as<__half>();

@@ -8,7 +8,7 @@ L = tq.Layer(synth.ensure_config(sys.argv[1]))
 for B in [int(b) for b in sys.argv[2:]]:
     L.reserve(B)
     x = torch.randn(B, L.in_dim, device="cuda")
-    os.environ["TQ_TRACE_FILE"] = f"gpurun_out/trace_B{B}.bin"
+    os.environ["TQ_TRACE_FILE"] = f"gpurun_out/trace_B{B}{os.environ.get('TRACE_TAG', '')}.bin"
     for _ in range(3):
         L.forward(x)
     torch.cuda.synchronize()

@@ -40,8 +40,9 @@ constexpr int kMaxCStages = 24;
 constexpr int kMaxAStages = 8;
 constexpr int kSmemBudget = 225 * 1024;
 
-__host__ __device__ constexpr int a_stages(int kc, int dn) {
-    return ((kTmemCols - 2 * dn) / (kc / 2)) < kMaxAStages ? ((kTmemCols - 2 * dn) / (kc / 2)) : kMaxAStages;
+// TMEM: [A stages: kc/2 columns each][accumulators: 2 buffers x ni issuers x dn]
+__host__ __device__ constexpr int a_stages(int kc, int dn, int ni) {
+    return ((kTmemCols - 2 * ni * dn) / (kc / 2)) < kMaxAStages ? ((kTmemCols - 2 * ni * dn) / (kc / 2)) : kMaxAStages;
 }
 __host__ __device__ constexpr int gemm_threads(int ng) { return (8 + 4 * ng) * 32; }
 __host__ __device__ constexpr int scale_trailer(int bits, int kc) {
@@ -54,8 +55,13 @@ __host__ __device__ constexpr int code_stage_bytes(int bits, int kc) {
 __host__ __device__ inline int ext_slot_bytes(int n_ext64) { return n_ext64 * code_block_bytes(kDenseBits); }
 
 struct SharedHdr {
+    // one ring for the MMA operands: stage s = A columns in TMEM + an activation
+    // tile in smem; full = 4 dequant warps + the activation producer (with its
+    // TMA bytes), empty = one tcgen05.commit after the stage's MMAs
+    uint64_t full[kMaxAStages], empty[kMaxAStages];
+    // activation ring, deeper than the A ring: its TMA loads queue behind the
+    // packed-code bulk copies in the SM's copy engine, so they are issued early
     uint64_t x_full[kMaxXStages], x_empty[kMaxXStages];
-    uint64_t a_full[kMaxAStages], a_empty[kMaxAStages];
     uint64_t c_full[kMaxCStages], c_empty[kMaxCStages];
     uint64_t d_full[2], d_empty[2];
     uint64_t e_full[2], e_empty[2];
@@ -68,10 +74,29 @@ __device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx)
 #endif
 }
 
-template <int BITS, int KC, int NG, int DN>
+// TQ_PROFILE builds: every warp accumulates the cycles it spends in selected
+// waits / phases (4 slots) and writes them, with its total, at exit.
+#ifdef TQ_PROFILE
+#define TQ_TIMED(slot, stmt)                   \
+    do {                                       \
+        const long long t0_ = clock64();       \
+        stmt;                                  \
+        prof[slot] += clock64() - t0_;         \
+    } while (0)
+#else
+#define TQ_TIMED(slot, stmt) stmt
+#endif
+
+// NI MMA issuers (logical warps 1 and 2): a single issuing thread sustains
+// one M=128 K=16 MMA per ~56 cycles for N <= 64 whatever N is, so small-N
+// decode tiles need several issue streams; issuer j takes the chunks whose
+// CTA-wide index is j mod NI and accumulates into its own TMEM columns; the
+// epilogue adds the NI partial accumulators in a fixed order.
+template <int BITS, int KC, int NG, int DN, int NI>
 __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    constexpr int kAS = a_stages(KC, DN);
+    constexpr int kAS = a_stages(KC, DN, NI);
+    static_assert(NI == 1 || NI == 2, "issuers");
     constexpr int kAtoms = KC / kKC;                  // 128-byte swizzle atoms per activation row
     constexpr int kACols = KC / 2;                    // TMEM columns per A stage
     constexpr int kDCol0 = kAS * kACols;
@@ -82,7 +107,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     constexpr int kWords = BITS;                      // u32 words per super-word (dense fp16: 16)
     constexpr int kDqWarps = 4 * NG;
     constexpr int kEpi0 = 4 + kDqWarps;               // first epilogue warp
-    static_assert(kDCol0 + 2 * DN <= kTmemCols, "TMEM budget");
+    static_assert(kDCol0 + 2 * NI * DN <= kTmemCols, "TMEM budget");
 
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t pad = (1024u - (raw & 1023u)) & 1023u;
@@ -110,26 +135,31 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                    : wid < kRoleBase ? wid - 4 * NG + kEpi0        // epilogue -> logical kEpi0..
                    : (wid == kRoleBase ? 2 : wid == kRoleBase + 1 ? 0 : wid == kRoleBase + 2 ? 3 : 1);
     const int n_units = *p.n_units;
+#ifdef TQ_EXPERIMENT
+    const int kDbg = p.debug;   // experiment builds: runtime skip flags (TQ_DEBUG)
+#else
+    constexpr int kDbg = 0;     // production: every debug branch folds away
+#endif
 
     if (threadIdx.x == 0) {
         prefetch_tmap(&p.tmap_x64);
         prefetch_tmap(&p.tmap_e64);
         prefetch_tmap(&p.tmap_x16);
         prefetch_tmap(&p.tmap_e16);
+        for (int s = 0; s < kAS; ++s) {
+            mbar_init(&hdr->full[s], 4);
+            mbar_init(&hdr->empty[s], 1);
+        }
         for (int s = 0; s < x_stages; ++s) {
             mbar_init(&hdr->x_full[s], 1);
             mbar_init(&hdr->x_empty[s], 1);
-        }
-        for (int s = 0; s < kAS; ++s) {
-            mbar_init(&hdr->a_full[s], 4);
-            mbar_init(&hdr->a_empty[s], 1);
         }
         for (int s = 0; s < c_stages; ++s) {
             mbar_init(&hdr->c_full[s], 1);
             mbar_init(&hdr->c_empty[s], 4);
         }
         for (int s = 0; s < 2; ++s) {
-            mbar_init(&hdr->d_full[s], 1);
+            mbar_init(&hdr->d_full[s], NI);
             mbar_init(&hdr->d_empty[s], 4);
             mbar_init(&hdr->e_full[s], 1);
             mbar_init(&hdr->e_empty[s], 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1));
@@ -147,6 +177,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = hdr->tmem_base;
+#ifdef TQ_PROFILE
+    long long prof[4] = {0, 0, 0, 0};
+    const long long prof_t0 = clock64();
+#endif
     const int first = blockIdx.x;
     const int stride = gridDim.x;
     const int gshift = p.group_shift;
@@ -166,10 +200,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                                        static_cast<int64_t>(un.mb) * p.kc_total * kCBytes;
                 for (int c = 0; c < nmain; ++c) {
                     const int kc = un.kc_begin + c;
-                    mbar_wait(&hdr->c_empty[cs], cph ^ 1u);
+                    TQ_TIMED(0, mbar_wait(&hdr->c_empty[cs], cph ^ 1u));
                     uint8_t* st = smem + c_off + cs * kCStage;
                     const uint8_t* src = wbase + static_cast<int64_t>(kc) * kCBytes;
-                    if (p.debug & 128) {
+                    if (kDbg & 128) {
                         if (lane == 0) mbar_arrive(&hdr->c_full[cs]);
                     } else if constexpr (BITS == kDenseBits) {
                         bulk_copy2_elect(&hdr->c_full[cs], st, src, kCBytes, st, src, 0u);
@@ -187,7 +221,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     if (++cs == c_stages) { cs = 0; cph ^= 1u; }
                 }
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
-                    mbar_wait(&hdr->e_empty[es], eph ^ 1u);
+                    TQ_TIMED(1, mbar_wait(&hdr->e_empty[es], eph ^ 1u));
                     uint8_t* dst = smem + e_off + es * ext_bytes;
                     bulk_copy2_elect(&hdr->e_full[es], dst, p.ext_blocks + wm * ext_bytes, ext_bytes, dst, dst, 0u);
                     if (++es == 2) { es = 0; eph ^= 1u; }
@@ -195,8 +229,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             }
         }
     } else if (warp == 3) {
-        // ===================== activation producer (converged warp, elected lane) ==========
-        // TMA 2D tiles, 128B swizzle: 16-row boxes for small token tiles, 64-row boxes above 48
+        // ===================== activation producer (all 32 lanes) ==========
+        // small token tiles (decode): cp.async 16-byte pieces through the LSU with
+        // the 128B swizzle applied in software -- TMA loads would queue behind
+        // the packed-code bulk copies in the SM's copy engine; large tiles: TMA
         int xs = 0, tcnt = 0;
         uint32_t xph = 0;
         Unit nxt = first < n_units ? p.units[first] : Unit{};
@@ -205,76 +241,109 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             if (u + stride < n_units) nxt = p.units[u + stride];
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
-            const bool b64 = un.n_tok > 48;
-            const int box = b64 ? 64 : 16;
+            const bool small = un.n_tok <= 8;   // a few rows: LSU; 16-row granules and up: TMA
+            const int box = un.n_tok > 48 ? 64 : 16;
             const int nbox = (un.n_tok + box - 1) / box;
-            const uint32_t bytes = static_cast<uint32_t>(kAtoms * nbox * box * 128);
             for (int c = 0; c < nch; ++c) {
                 const bool ext = c >= nmain;
-                mbar_wait(&hdr->x_empty[xs], xph ^ 1u);
+                TQ_TIMED(0, mbar_wait(&hdr->x_empty[xs], xph ^ 1u));
                 const int col0 = ext ? (c - nmain) * KC : (un.kc_begin + c) * KC;
-                if (elect_one()) {
-                    if (p.debug & 32) {
-                        mbar_arrive(&hdr->x_full[xs]);
-                    } else {
-                        mbar_arrive_expect_tx(&hdr->x_full[xs], bytes);
-                        const CUtensorMap* map = ext ? (b64 ? &p.tmap_e64 : &p.tmap_e16)
-                                                     : (b64 ? &p.tmap_x64 : &p.tmap_x16);
+                const int natoms = ext ? min(kAtoms, p.n_ext64 - (c - nmain) * kAtoms) : kAtoms;
+                if (kDbg & 32) {
+                    if (lane == 0) mbar_arrive(&hdr->x_full[xs]);
+                } else if (small) {
+                    const __half* src = ext ? p.e_ptr : p.x_ptr;
+                    const int64_t ld = ext ? p.e_ld : p.x_ld;
+                    const uint32_t sx = s_base + x_off + xs * x_stage_bytes;
+                    // lanes per row = natoms * 8 pieces (a power of two <= 32)
+                    const int lshift = 3 + (natoms >= 4 ? 2 : natoms >= 2 ? 1 : 0);
+                    const int rows_per_it = 32 >> lshift;
+                    const int piece = lane & ((1 << lshift) - 1);
+                    const int at = piece >> 3, ch = piece & 7;
+                    const __half* g = src + static_cast<int64_t>(un.x_row) * ld + col0 + at * kKC + ch * 8;
+                    for (int row = lane >> lshift; row < un.n_tok; row += rows_per_it)
+                        cp_async_16(sx + at * x_atom_bytes + row * 128 + ((ch ^ (row & 7)) << 4), g + row * ld);
+                    cp_async_mbar_arrive_inc(&hdr->x_full[xs]);   // pending += 1, -1 when this lane's copies land
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&hdr->x_full[xs]);
+                } else {
+                    if (lane == 0) {
+                        mbar_arrive_expect_tx(&hdr->x_full[xs], static_cast<uint32_t>(natoms * nbox * box * 128));
+                        const CUtensorMap* map = ext ? (box == 64 ? &p.tmap_e64 : &p.tmap_e16)
+                                                     : (box == 64 ? &p.tmap_x64 : &p.tmap_x16);
                         uint8_t* xst = smem + x_off + xs * x_stage_bytes;
-#pragma unroll
-                        for (int at = 0; at < kAtoms; ++at)
+                        for (int at = 0; at < natoms; ++at)
                             for (int bx = 0; bx < nbox; ++bx)
                                 tma_load_2d(xst + at * x_atom_bytes + bx * box * 128, map, col0 + at * kKC,
                                             un.x_row + bx * box, &hdr->x_full[xs]);
                     }
-                    trace_ev(p, 1, tcnt);
+                    __syncwarp();
                 }
-                __syncwarp();
+                if (lane == 0) trace_ev(p, 1, tcnt);
                 ++tcnt;
                 if (++xs == x_stages) { xs = 0; xph ^= 1u; }
             }
         }
-    } else if (warp == 1) {
-        // ===================== MMA issuer (converged warp, one elected lane issues) ==========
-        {
-            int xs = 0, as = 0, lu = 0, tcnt = 0;
-            uint32_t xph = 0, aph = 0;
-            Unit nxt = first < n_units ? p.units[first] : Unit{};
-            for (int u = first; u < n_units; u += stride, ++lu) {
-                const Unit un = nxt;
-                if (u + stride < n_units) nxt = p.units[u + stride];
-                const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
-                const int ds = lu & 1;
-                const uint32_t dph = (lu >> 1) & 1;
-                const uint32_t n = static_cast<uint32_t>((un.n_tok + 15) & ~15);
-                const uint32_t idesc = idesc_f16(n);
-                const uint32_t d_tmem = tmem + kDCol0 + ds * DN;
-                mbar_wait(&hdr->d_empty[ds], dph ^ 1u);
+    } else if (warp == 1 || (NI == 2 && warp == 2)) {
+        // ===================== MMA issuers (converged warp, one elected lane issues) ==========
+        const int j = warp == 1 ? 0 : 1;
+        int as = j, lu = 0, tcnt = 0;   // issuer j's chunks: CTA-wide index j, j+NI, ...
+        uint32_t aph = 0;
+        int xs = j;
+        uint32_t xph = 0;
+        int c_next = j;
+        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        for (int u = first; u < n_units; u += stride, ++lu) {
+            const Unit un = nxt;
+            if (u + stride < n_units) nxt = p.units[u + stride];
+            const int nmain = un.kc_end - un.kc_begin;
+            const int nch = nmain + un.n_ext;
+            const int ds = lu & 1;
+            const uint32_t dph = (lu >> 1) & 1;
+            const uint32_t n = static_cast<uint32_t>((un.n_tok + 15) & ~15);
+            const uint32_t idesc = idesc_f16(n);
+            const uint32_t d_tmem = tmem + kDCol0 + (ds * NI + j) * DN;
+            int c = c_next;
+            // every issuer (even one without a chunk in this unit) waits for the
+            // epilogue to release this accumulator buffer before it arrives on
+            // d_full[ds], so its arrival cannot fall into an older phase
+            TQ_TIMED(1, mbar_wait(&hdr->d_empty[ds], dph ^ 1u));
+            tc_fence_after();
+            const int c_first = c;
+            for (; c < nch; c += NI) {
+                TQ_TIMED(0, mbar_wait(&hdr->full[as], aph));
+                if (lane == 0) trace_ev(p, 2, tcnt);
+                TQ_TIMED(3, mbar_wait(&hdr->x_full[xs], xph));
+                if (un.n_tok <= 8) fence_proxy_async_smem();   // cp.async (generic proxy) tiles -> MMA reads
+                ++tcnt;
                 tc_fence_after();
-                for (int c = 0; c < nch; ++c) {
-                    mbar_wait(&hdr->a_full[as], aph);
-                    if (lane == 0) trace_ev(p, 2, tcnt);
-                    mbar_wait(&hdr->x_full[xs], xph);
-                    if (lane == 0) trace_ev(p, 3, tcnt);
-                    ++tcnt;
-                    if (p.debug & 16) fence_proxy_async_smem();
-                    tc_fence_after();
-                    const uint32_t xaddr = s_base + x_off + xs * x_stage_bytes;
-                    if (!(p.debug & 2)) {
+                const uint32_t xaddr = s_base + x_off + xs * x_stage_bytes;
+                const uint64_t bdesc = sw128_desc(xaddr);
+                const uint32_t a_tm = tmem + as * kACols;
+                // atoms of 64 K: 4 MMAs each, one elected lane, descriptors advanced in PTX
+                const int natoms = c < nmain ? kAtoms : min(kAtoms, p.n_ext64 - (c - nmain) * kAtoms);
+                if (!(kDbg & 2)) {
 #pragma unroll
-                        for (int k = 0; k < KC / 16; ++k) {
-                            const uint32_t baddr = xaddr + (k / 4) * x_atom_bytes + (k % 4) * 32;
-                            tc_mma_ts_elect(d_tmem, tmem + as * kACols + k * 8, sw128_desc(baddr), idesc,
-                                            (c > 0 || k > 0) ? 1u : 0u);
-                        }
-                    }
-                    tc_commit_elect(&hdr->a_empty[as]);
-                    tc_commit_elect(&hdr->x_empty[xs]);
-                    if (++as == kAS) { as = 0; aph ^= 1u; }
-                    if (++xs == x_stages) { xs = 0; xph ^= 1u; }
+                    for (int at = 0; at < kAtoms; ++at)
+                        if (at < natoms)
+                            tc_mma_ts_x4_elect(d_tmem, a_tm + at * 32,
+                                               bdesc + static_cast<uint64_t>((at * x_atom_bytes) >> 4), idesc,
+                                               (c > c_first || at > 0) ? 1u : 0u);
                 }
-                tc_commit_elect(&hdr->d_full[ds]);
+                tc_commit_elect(&hdr->empty[as]);
+                tc_commit_elect(&hdr->x_empty[xs]);
+#ifdef TQ_PROFILE
+                prof[2] += 1;   // chunks
+#endif
+                as += NI;
+                if (as >= kAS) { as -= kAS; aph ^= 1u; }
+                xs += NI;
+                if (xs >= x_stages) { xs -= x_stages; xph ^= 1u; }
             }
+            // this issuer's part of unit u is accumulated (or it had no chunk in it)
+            if (c_first < nch) tc_commit_elect(&hdr->d_full[ds]);
+            else if (lane == 0) mbar_arrive(&hdr->d_full[ds]);
+            c_next = c - nch;
         }
     } else if (warp >= 4 && warp < kEpi0) {
         // ===================== dequant groups =====================
@@ -311,60 +380,75 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     // super-word of fp16 pairs at a time -- dequantize, tcgen05.st, reuse
                     if (main_chunk) {
                         const int kc = un.kc_begin + c;
-                        mbar_wait(&hdr->c_full[cs], cph);
+                        TQ_TIMED(0, mbar_wait(&hdr->c_full[cs], cph));
                         if (tr) trace_ev(p, 4, grp * 1024 + tcnt);
                         const uint8_t* st = smem + c_off + cs * kCStage;
                         const uint32_t* wst = reinterpret_cast<const uint32_t*>(st) + rloc;
-                        uint32_t words[kSW][kWords];
-                        uint16_t sbits[kSW];
+                        constexpr int kHalf = kWords * kBM;
+                        if constexpr (BITS == kDenseBits) {
+                            // dense fp16 operand (projection pass): stream each super-word smem -> TMEM
+                            TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
+                            tc_fence_after();
 #pragma unroll
-                        for (int s = 0; s < kSW; ++s) {
-                            // super-word s: 64-column block s/2, half s%2
-                            constexpr int kHalf = kWords * kBM;
+                            for (int s = 0; s < kSW; ++s) {
+                                uint32_t v[16];
 #pragma unroll
-                            for (int w = 0; w < kWords; ++w)
-                                words[s][w] = wst[(s >> 1) * (kBlk / 4) + (s & 1) * kHalf + w * kBM];
-                        }
-                        if constexpr (BITS != kDenseBits) {
+                                for (int w = 0; w < 16; ++w)
+                                    v[w] = wst[(s >> 1) * (kBlk / 4) + (s & 1) * kHalf + w * kBM];
+                                tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
+                            }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
+                        } else {
+                            // all packed words of the chunk in registers, stage released, then
+                            // one super-word of fp16 pairs at a time: dequantize, tcgen05.st
+                            uint32_t words[kSW][kWords];
+                            uint16_t sbits[kSW];
                             const int e0 = kc * KC;
                             const int ein = gshift >= 0 ? (e0 & ((1 << gshift) - 1)) : e0 % p.group_size;
                             const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + kCBytes) + rloc;
 #pragma unroll
-                            for (int s = 0; s < kSW; ++s) {
+                            for (int s = 0; s < kSW; ++s) {   // super-word s: 64-column block s/2, half s%2
+#pragma unroll
+                                for (int w = 0; w < kWords; ++w)
+                                    words[s][w] = wst[(s >> 1) * (kBlk / 4) + (s & 1) * kHalf + w * kBM];
                                 const int off = ein + 32 * s;
                                 const int gi = gshift >= 0 ? off >> gshift : off / p.group_size;
                                 sbits[s] = sc[gi * kBM];
                             }
-                        }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
-                        mbar_wait(&hdr->a_empty[as], aph ^ 1u);
-                        if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
-                        tc_fence_after();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
+                            TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
+                            if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+                            tc_fence_after();
+#ifdef TQ_PROFILE
+                            const long long tdq0 = clock64();
+#endif
 #pragma unroll
-                        for (int s = 0; s < kSW; ++s) {
-                            uint32_t v[16];
-                            if constexpr (BITS == kDenseBits) {
+                            for (int s = 0; s < kSW; ++s) {
+                                uint32_t v[16];
+                                if (kDbg & 1) {
 #pragma unroll
-                                for (int w = 0; w < 16; ++w) v[w] = words[s][w];
-                            } else if (p.debug & 1) {
+                                    for (int w = 0; w < 16; ++w) v[w] = words[s][w % kWords];
+                                } else {
+                                    const DqConst dq = make_dq(__ushort_as_half(sbits[s]));
+                                    dequant32<BITS>(words[s], dq, v);
+                                }
+                                if (!(kDbg & 64)) tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
+                                else {
 #pragma unroll
-                                for (int w = 0; w < 16; ++w) v[w] = words[s][w % kWords];
-                            } else {
-                                const DqConst dq = make_dq(__ushort_as_half(sbits[s]));
-                                dequant32<BITS>(words[s], dq, v);
+                                    for (int w = 0; w < 16; ++w) asm volatile("" ::"r"(v[w]));
+                                }
                             }
-                            if (!(p.debug & 64)) tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
-                            else {
-#pragma unroll
-                                for (int w = 0; w < 16; ++w) asm volatile("" ::"r"(v[w]));
-                            }
+#ifdef TQ_PROFILE
+                            prof[2] += clock64() - tdq0;
+#endif
                         }
                     } else {
                         // extension chunk: precomputed fp16 columns [-zero*s per group | U_p codes | 0]
-                        mbar_wait(&hdr->e_full[es], eph);
+                        TQ_TIMED(0, mbar_wait(&hdr->e_full[es], eph));
                         const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
-                        mbar_wait(&hdr->a_empty[as], aph ^ 1u);
+                        TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
                         if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
                         tc_fence_after();
 #pragma unroll
@@ -372,24 +456,22 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                             const int colbase = (c - nmain) * KC + 32 * s;
                             const int blk = colbase >> 6, hh = (colbase >> 5) & 1;
                             uint32_t v[16];
-                            if (blk < p.n_ext64) {
+                            if (blk < p.n_ext64) {   // blocks past the last real one are never read by the MMA
 #pragma unroll
                                 for (int w = 0; w < 16; ++w)
                                     v[w] = eb[blk * (code_block_bytes(kDenseBits) / 4) + (hh * 16 + w) * kBM];
-                            } else {
-#pragma unroll
-                                for (int w = 0; w < 16; ++w) v[w] = 0u;
+                                tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
                             }
-                            tc_st_32x32b_x16(tmem + lane_base + as * kACols + s * 16, v);
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
                     }
-                    if (!(p.debug & 64)) tc_wait_st();
+                    if (!(kDbg & 64)) TQ_TIMED(3, tc_wait_st());
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&hdr->a_full[as]);
+                    if (lane == 0) mbar_arrive(&hdr->full[as]);
                     if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
+                    if (lane == 0 && grp == 0) trace_ev(p, 7, q * 1024 + tcnt);   // per-warp skew of group 0
                     ++tcnt;
                 }
                 as += NG;
@@ -406,6 +488,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         // ===================== epilogue =====================
         const int q = wid & 3;  // TMEM lane quarter = physical warp id % 4
         int lu = 0;
+        int q_base_e = 0;       // CTA-wide chunk index of the unit's first chunk
         Unit nxt = first < n_units ? p.units[first] : Unit{};
         float nscale = first < n_units ? p.w_outscale[nxt.weight] : 1.0f;
         for (int u = first; u < n_units; u += stride, ++lu) {
@@ -421,14 +504,32 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             const bool valid = row < p.o_valid;
             float* out = p.y + static_cast<int64_t>(un.split) * p.y_split_stride +
                          static_cast<int64_t>(un.y_row) * p.ldy + row;
-            mbar_wait_sleep(&hdr->d_full[ds], dph);
+            TQ_TIMED(0, mbar_wait_sleep(&hdr->d_full[ds], dph));
             tc_fence_after();
-            const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * DN;
+            const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * NI * DN;
+            const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
+            // issuer j took part iff the unit holds a chunk whose CTA-wide index is j mod NI
+            const bool part0 = NI == 1 ? nch > 0 : (nch >= 2 || (nch == 1 && (q_base_e & 1) == 0));
+            const bool part1 = NI == 2 && (nch >= 2 || (nch == 1 && (q_base_e & 1) == 1));
+            q_base_e += nch;
             for (int t0 = 0; t0 < un.n_tok; t0 += 16) {
                 uint32_t v[16];
-                tc_ld_32x32b_x16(dbase + t0, v);
-                tc_wait_ld();
-                if (valid && !(p.debug & 4)) {
+                if (part0) tc_ld_32x32b_x16(dbase + t0, v);
+                if (part1) {
+                    uint32_t w[16];
+                    tc_ld_32x32b_x16(dbase + DN + t0, w);
+                    tc_wait_ld();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k)
+                        v[k] = part0 ? __float_as_uint(__uint_as_float(v[k]) + __uint_as_float(w[k])) : w[k];
+                } else {
+                    tc_wait_ld();
+                    if (!part0) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) v[k] = 0u;
+                    }
+                }
+                if (valid && !(kDbg & 4)) {
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (t0 + j < un.n_tok)
@@ -441,6 +542,14 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         }
     }
 
+#ifdef TQ_PROFILE
+    if (lane == 0 && p.trace) {
+        unsigned long long* o = p.trace + (static_cast<size_t>(blockIdx.x) * 32 + wid) * 8;
+        o[0] = clock64() - prof_t0;
+        o[1] = warp;
+        for (int k = 0; k < 4; ++k) o[2 + k] = prof[k];
+    }
+#endif
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -456,28 +565,26 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     GemmParams p = p0;
     const int kc = p.kc_width;
     const int dn = p.dn;
-    const bool cfg_ok = (kc == 128 && (dn == 64 || dn == 128)) || (kc == 64 && dn == 192);
+    const bool cfg_ok = (kc == 128 && (dn == 32 || dn == 64 || dn == 128)) || (kc == 64 && dn == 192);
     if (!cfg_ok) return cudaErrorInvalidValue;
     if (p.bn_max > dn) return cudaErrorInvalidValue;
     // activation ring: stage rows = token tile rounded to the box (64) or the MMA N granularity (16)
-    const int rows = p.bn_max > 48 ? ((p.bn_max + 63) / 64) * 64 : ((p.bn_max + 15) / 16) * 16;
+    const int rows = p.bn_max > 48 ? ((p.bn_max + 63) / 64) * 64 : ((p.bn_max + 15) / 16) * 16;  // cp.async tiles: 16-row granules
     p.x_stage_rows = rows;
     const int x_stage = (kc / kKC) * rows * 128;
     const int c_stage = code_stage_bytes(p.bits, kc);
     const int fixed = 2048 + 2 * ext_slot_bytes(p.n_ext64);
-    // smem split: >= 6 activation stages, then code stages (decode is HBM-latency
-    // bound on the code ring), leftovers back to the activation ring
-    int xs = 6;
-    int cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
-    if (cs < 4) {
-        xs = 3;
-        cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
-    }
-    cs = cs < kMaxCStages ? cs : kMaxCStages;
-    if (cs < 2) return cudaErrorInvalidValue;
-    xs = (kSmemBudget - fixed - cs * c_stage) / x_stage;
+    // smem split: >= 80 KB of packed-code stages in flight (HBM latency), the
+    // activation ring as deep as the rest allows (<= 16), leftovers to codes
+    const int ni = (kc == 128 && dn <= 64) ? 2 : 1;
+    const int as_n = a_stages(kc, dn, ni);
+    int cs = (80 * 1024 + c_stage - 1) / c_stage;
+    int xs = (kSmemBudget - fixed - cs * c_stage) / x_stage;
     xs = xs < kMaxXStages ? xs : kMaxXStages;
-    if (xs < 2) return cudaErrorInvalidValue;
+    if (xs < as_n) xs = as_n;
+    cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
+    cs = cs < kMaxCStages ? cs : kMaxCStages;
+    if (cs < 2 || xs < 2) return cudaErrorInvalidValue;
     p.x_stages = xs;
     p.c_stages = cs;
     p.group_shift = -1;
@@ -487,7 +594,11 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     static const int dbg = getenv("TQ_DEBUG") ? atoi(getenv("TQ_DEBUG")) : 0;
     p.debug = dbg;
     static unsigned long long* trace_buf = nullptr;
-    if ((dbg & 8) && !trace_buf) cudaMalloc(&trace_buf, 8 * 4096 * sizeof(unsigned long long));
+    constexpr size_t kTraceWords = 160 * 32 * 8;   // >= 8 x 4096 event slots, and 8 words per warp of 160 CTAs
+    if ((dbg & 8) && !trace_buf) {
+        cudaMalloc(&trace_buf, kTraceWords * sizeof(unsigned long long));
+        cudaMemset(trace_buf, 0, kTraceWords * sizeof(unsigned long long));
+    }
     p.trace = trace_buf;
     cudaError_t err = cudaSuccess;
     auto go = [&](auto kern, int threads) {
@@ -496,26 +607,28 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
         kern<<<grid, threads, smem, stream>>>(p);
         err = cudaGetLastError();
     };
-#define TQ_GEMM_CASES(KCV, NGV, DNV)                                                                 \
+#define TQ_GEMM_CASES(KCV, NGV, DNV, NIV)                                                                 \
     switch (p.bits) {                                                                              \
-        case 2: go(gemm_kernel<2, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
-        case 3: go(gemm_kernel<3, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
-        case 4: go(gemm_kernel<4, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
-        case 8: go(gemm_kernel<8, KCV, NGV, DNV>, gemm_threads(NGV)); break;                       \
-        case kDenseBits: go(gemm_kernel<kDenseBits, KCV, NGV, DNV>, gemm_threads(NGV)); break;     \
+        case 2: go(gemm_kernel<2, KCV, NGV, DNV, NIV>, gemm_threads(NGV)); break;                  \
+        case 3: go(gemm_kernel<3, KCV, NGV, DNV, NIV>, gemm_threads(NGV)); break;                  \
+        case 4: go(gemm_kernel<4, KCV, NGV, DNV, NIV>, gemm_threads(NGV)); break;                  \
+        case 8: go(gemm_kernel<8, KCV, NGV, DNV, NIV>, gemm_threads(NGV)); break;                  \
+        case kDenseBits: go(gemm_kernel<kDenseBits, KCV, NGV, DNV, NIV>, gemm_threads(NGV)); break; \
         default: return cudaErrorInvalidValue;                                                     \
     }
-    if (kc == 128 && dn == 64) {
-        TQ_GEMM_CASES(128, 3, 64)
+    if (kc == 128 && dn == 32) {
+        TQ_GEMM_CASES(128, 4, 32, 2)
+    } else if (kc == 128 && dn == 64) {
+        TQ_GEMM_CASES(128, 4, 64, 2)
     } else if (kc == 128) {
-        TQ_GEMM_CASES(128, 3, 128)
+        TQ_GEMM_CASES(128, 3, 128, 1)
     } else {
-        TQ_GEMM_CASES(64, 2, 192)
+        TQ_GEMM_CASES(64, 2, 192, 1)
     }
 #undef TQ_GEMM_CASES
     if (err == cudaSuccess && (dbg & 8) && getenv("TQ_TRACE_FILE")) {
         // debug only: dump CTA 0's event trace of this launch (8 slots x 4096 u64)
-        static unsigned long long host[8 * 4096];
+        static unsigned long long host[kTraceWords];
         cudaStreamSynchronize(stream);
         cudaMemcpy(host, trace_buf, sizeof(host), cudaMemcpyDeviceToHost);
         if (FILE* f = fopen(getenv("TQ_TRACE_FILE"), "wb")) {

@@ -539,7 +539,10 @@ LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
     const int64_t local = std::max<int64_t>(1, L->e_end - L->e_begin);
     const int64_t per_expert = (batch * L->g.top_k + local - 1) / local;
     LaunchCfg c;
-    if (per_expert <= 128 && L->g.k_pad % 128 == 0) {
+    if (per_expert <= 32 && L->g.k_pad % 128 == 0) {
+        c.kc = 128;                      // decode: 2 MMA issue streams, 4 dequant groups
+        c.dn = 32;
+    } else if (per_expert <= 128 && L->g.k_pad % 128 == 0) {
         c.kc = 128;
         c.dn = batch <= 64 ? 64 : 128;   // decode: small accumulators -> deeper A ring
     } else {

@@ -17,7 +17,7 @@ __device__ __forceinline__ void commit_elect(uint64_t* b) {
   asm volatile("{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(su32(b)) : "memory");
 }
 constexpr int CS = 13, AS = 6, XS = 6, NG = 3;
-template <int MODE, bool LDS, bool UNITS>
+template <int MODE, bool LDS, bool UNITS, int FENCE = 1>
 __global__ void __launch_bounds__(640, 1) pipe(int nch, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t dsm[];
   __shared__ uint64_t c_full[CS], c_empty[CS], a_full[AS], a_empty[AS], x_full[XS], x_empty[XS], done, d_full[2], d_empty[2];
@@ -68,7 +68,16 @@ __global__ void __launch_bounds__(640, 1) pipe(int nch, unsigned long long* out)
         __syncwarp(); if (lane == 0) arrive(&c_empty[cs]);
         if (acc == 0x12345678u) out[1] = acc;
         wait(&a_empty[as], ap ^ 1);
-        asm volatile("tcgen05.fence::before_thread_sync;");
+        if (FENCE & 2) asm volatile("tcgen05.fence::after_thread_sync;");
+        if (FENCE & 4) {
+          uint32_t v[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = lane + k;
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+            :: "r"(tbase + (((wid & 3) * 32) << 16) + as * 64), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        if (FENCE & 1) asm volatile("tcgen05.fence::before_thread_sync;");
         __syncwarp(); if (lane == 0) arrive(&a_full[as]);
       }
       if (++cs == CS) { cs = 0; cp ^= 1; }
@@ -112,5 +121,9 @@ int main() {
   run(pipe<0, true, false>, "commit x2, LDS, 220KB smem", 220 * 1024);
   run(pipe<0, true, true>, "commit x2, LDS, units, 220KB", 220 * 1024);
   run(pipe<0, false, true>, "commit x2, units", 0);
+  run(pipe<0, true, true, 0>, "LDS units, no fences", 220 * 1024);
+  run(pipe<0, true, true, 3>, "LDS units, both fences", 220 * 1024);
+  run(pipe<0, true, true, 7>, "LDS units, fences + st x16", 220 * 1024);
+  run(pipe<1, true, true, 0>, "arrive, LDS units, no fences", 220 * 1024);
   return 0;
 }

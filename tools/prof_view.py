@@ -1,0 +1,28 @@
+"""Summarise a TQ_PROFILE dump: per role, mean cycles in each timed slot."""
+import sys
+import numpy as np
+a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 32, 8).astype(np.int64)
+NAMES = {0: ("code", ["c_empty", "e_empty", "-", "-"]), 3: ("xprod", ["x_empty", "-", "-", "-"]),
+         1: ("mma", ["full", "d_empty", "chunks(n)", "x_full"]), 2: ("mma1", ["full", "d_empty", "chunks(n)", "x_full"])}
+rows = {}
+for cta in range(a.shape[0]):
+    for w in range(32):
+        r = a[cta, w]
+        if r[0] <= 0:
+            continue
+        role = int(r[1])
+        rows.setdefault(role, []).append(r)
+for role in sorted(rows):
+    r = np.array(rows[role])
+    if role in NAMES:
+        name, slots = NAMES[role]
+    elif role >= 4 and role < 4 + 4 * 4 and any(k in rows for k in ()):
+        name, slots = "dq", []
+    else:
+        name, slots = f"role{role}", ["s0", "s1", "s2", "s3"]
+    if role >= 4 and name.startswith("role"):
+        name = "dequant" if role < max(rows) - 3 else "epilogue"
+        slots = ["c_full/e_full", "empty", "dq+st", "wait_st"] if name == "dequant" else ["d_full", "-", "-", "-"]
+    tot = r[:, 0].mean()
+    parts = " ".join(f"{s}={r[:, 2 + k].mean():9.0f} ({r[:, 2 + k].mean() / tot * 100:4.1f}%)" for k, s in enumerate(slots) if s != "-")
+    print(f"{name:9s} role={role:2d} n={len(r):4d} total={tot:9.0f}  {parts}")

@@ -602,8 +602,24 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     p.trace = trace_buf;
     cudaError_t err = cudaSuccess;
     auto go = [&](auto kern, int threads) {
-        err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (err != cudaSuccess) return;
+        // the attribute is raised once per kernel (launches may be captured into graphs);
+        // all instantiations share one function-pointer type, so key by address
+        static const void* cfg_fn[64];
+        static int cfg_smem[64];
+        static int cfg_n = 0;
+        int slot = -1;
+        for (int t = 0; t < cfg_n; ++t)
+            if (cfg_fn[t] == reinterpret_cast<const void*>(kern)) slot = t;
+        if (slot < 0 && cfg_n < 64) {
+            slot = cfg_n++;
+            cfg_fn[slot] = reinterpret_cast<const void*>(kern);
+            cfg_smem[slot] = 0;
+        }
+        if (slot < 0 || smem > cfg_smem[slot]) {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (err != cudaSuccess) return;
+            if (slot >= 0) cfg_smem[slot] = smem;
+        }
         kern<<<grid, threads, smem, stream>>>(p);
         err = cudaGetLastError();
     };

@@ -39,172 +39,205 @@ namespace tqb {
 // reference's sequential index-order f64 sum (matrix.cpp:25-36).  Every
 // product is exact in f64, so ANY summation order of the i terms lands within
 // gamma_{i-1} * sum|p| of the exact sum, as does the reference's sequential
-// loop.  We sum in parallel (vectorised, several accumulators, warp tree) and
-// bound |ours - reference| <= 2 * gamma_{i+i/32+8} * sum|p|; when both ends of
-// that interval round to the same f32, the f32 score is certified identical to
-// the reference's, otherwise lane 0 replays the sequential loop (rare).  Then
-// f64 max-subtracted softmax, total summed k = 0..K-1, order by (prob desc,
-// index asc), gates = float(prob / selected) -- moe.cpp:64-87 step by step.
-template <int TPB>
-__global__ void __launch_bounds__(256) route_kernel(const float* __restrict__ x, int batch, int in_dim,
-                                                   const float* __restrict__ gate, int num_experts, int top_k,
-                                                   int group_size, int groups, int k_pad,
-                                                   int32_t* __restrict__ ids, float* __restrict__ gates,
-                                                   __half* __restrict__ x16, float* __restrict__ sx) {
-    extern __shared__ __align__(16) float rs_smem[];
-    float* xs = rs_smem;                          // TPB x in_dim
-    float* scores = rs_smem + TPB * in_dim;       // TPB x num_experts
-    const int b0 = blockIdx.x * TPB;
-    const int nt = min(TPB, batch - b0);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-    for (int t = 0; t < nt; ++t) {
-        const float* xb = x + static_cast<int64_t>(b0 + t) * in_dim;
-        for (int c = threadIdx.x; c < in_dim; c += blockDim.x) xs[t * in_dim + c] = xb[c];
-    }
-    __syncthreads();
-    // fp16 activations (zero-padded to k_pad) and per-group sums of them
-    for (int t = 0; t < nt; ++t) {
-        const float* xr = xs + t * in_dim;
+// loop.  We sum in parallel and bound |ours - reference| <= 2 *
+// gamma_{i+i/32+40} * sum|p|; when both ends of that interval round to the
+// same f32, the f32 score is certified identical to the reference's,
+// otherwise one warp replays the sequential loop (rare).  Then f64
+// max-subtracted softmax, total summed k = 0..K-1, order by (prob desc, index
+// asc), gates = float(prob / selected) -- moe.cpp:64-87 step by step.
+//
+// Grid (token, slice of 4 experts), 1024 threads: every thread issues all its
+// gate loads up front (one memory round trip), the 4 (sum, sum|p|) pairs meet
+// in shared memory in a fixed order; the last slice CTA of a token (atomic
+// ticket) runs the softmax / top-k over the token's certified scores.
+constexpr int kRouteThreads = 1024;
+constexpr int kRouteWarps = kRouteThreads / 32;
+constexpr int kRouteExperts = 4;      // experts per CTA
+constexpr int kRouteCols = 4;         // columns per thread per pass (i <= 4096 in one pass)
+constexpr int kReplayWin = 2048;      // products per replay window (16 KB of shared memory)
+
+__global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __restrict__ x, int batch, int in_dim,
+                                                             const float* __restrict__ gate, int num_experts,
+                                                             int top_k, int group_size, int groups, int k_pad,
+                                                             int32_t* __restrict__ ids, float* __restrict__ gates,
+                                                             __half* __restrict__ x16, float* __restrict__ sx,
+                                                             float* __restrict__ score_ws, int32_t* __restrict__ ticket) {
+    __shared__ double part[kRouteWarps][kRouteExperts][2];
+    __shared__ double prod[kReplayWin];
+    __shared__ double replay_acc;
+    __shared__ float sc[64];
+    __shared__ double ex[64];
+    __shared__ int pick_k[64];
+    __shared__ double pick_p[64];
+    __shared__ unsigned s_und;
+    __shared__ int s_last;
+    const int b = blockIdx.x;
+    const int k0 = blockIdx.y * kRouteExperts;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const float* xb = x + static_cast<int64_t>(b) * in_dim;
+    if (blockIdx.y == 0) {
+        // fp16 activations (zero-padded to k_pad) and per-group sums of them
         if (x16) {
-            __half* xo = x16 + static_cast<int64_t>(b0 + t) * k_pad;
-            for (int c = threadIdx.x; c < k_pad; c += blockDim.x) xo[c] = __float2half_rn(c < in_dim ? xr[c] : 0.0f);
+            __half* xo = x16 + static_cast<int64_t>(b) * k_pad;
+            for (int c = threadIdx.x; c < k_pad; c += kRouteThreads) xo[c] = __float2half_rn(c < in_dim ? xb[c] : 0.0f);
         }
-        for (int g = warp; sx && g < groups; g += nwarps) {
+        for (int g = warp; sx && g < groups; g += kRouteWarps) {
             float acc = 0.0f;
             const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
-            for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xr[c]));
+            for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-            if (lane == 0) sx[static_cast<int64_t>(b0 + t) * groups + g] = acc;
+            if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
         }
     }
     if (num_experts == 0) return;  // activations-only prep (tq_forward with given routing)
-    // certified scores
-    const bool vec = (in_dim & 3) == 0;
-    for (int k = warp; k < num_experts; k += nwarps) {
-        const float* gk = gate + static_cast<int64_t>(k) * in_dim;
-        double s[TPB], a[TPB];
+    if (threadIdx.x == 0) {
+        s_und = 0u;
+        replay_acc = 0.0;
+    }
+    // ---- partial dot products: all loads of a pass issued before any math ----
+    double s[kRouteExperts], a[kRouteExperts];
 #pragma unroll
-        for (int t = 0; t < TPB; ++t) s[t] = a[t] = 0.0;
-        if (vec) {
-#pragma unroll 4
-            for (int c = 4 * lane; c + 3 < in_dim; c += 128) {
-                const float4 g4 = __ldg(reinterpret_cast<const float4*>(gk + c));
+    for (int j = 0; j < kRouteExperts; ++j) s[j] = a[j] = 0.0;
+    for (int c0 = 0; c0 < in_dim; c0 += kRouteThreads * kRouteCols) {
+        float xv[kRouteCols], gv[kRouteExperts][kRouteCols];
 #pragma unroll
-                for (int t = 0; t < TPB; ++t) {
-                    if (t < nt) {
-                        const float4 x4 = *reinterpret_cast<const float4*>(xs + t * in_dim + c);
-                        const double p0 = static_cast<double>(x4.x) * g4.x, p1 = static_cast<double>(x4.y) * g4.y;
-                        const double p2 = static_cast<double>(x4.z) * g4.z, p3 = static_cast<double>(x4.w) * g4.w;
-                        s[t] += (p0 + p1) + (p2 + p3);
-                        a[t] += (fabs(p0) + fabs(p1)) + (fabs(p2) + fabs(p3));
-                    }
-                }
-            }
-        } else {
-            for (int cc = lane; cc < in_dim; cc += 32) {
-                const float gv = gk[cc];
+        for (int m = 0; m < kRouteCols; ++m) {
+            const int c = c0 + threadIdx.x + m * kRouteThreads;
+            xv[m] = c < in_dim ? xb[c] : 0.0f;
 #pragma unroll
-                for (int t = 0; t < TPB; ++t)
-                    if (t < nt) {
-                        const double p = static_cast<double>(xs[t * in_dim + cc]) * gv;
-                        s[t] += p;
-                        a[t] += fabs(p);
-                    }
-            }
+            for (int j = 0; j < kRouteExperts; ++j)
+                gv[j][m] = (c < in_dim && k0 + j < num_experts) ? __ldg(gate + static_cast<int64_t>(k0 + j) * in_dim + c)
+                                                                : 0.0f;
         }
 #pragma unroll
-        for (int t = 0; t < TPB; ++t) {
+        for (int m = 0; m < kRouteCols; ++m) {
+            const double xd = static_cast<double>(xv[m]);
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                s[t] += __shfl_down_sync(0xffffffffu, s[t], off);
-                a[t] += __shfl_down_sync(0xffffffffu, a[t], off);
+            for (int j = 0; j < kRouteExperts; ++j) {
+                const double pr = xd * static_cast<double>(gv[j][m]);
+                s[j] += pr;
+                a[j] += fabs(pr);
             }
         }
-        // certification (lane 0 holds the sums); replay undecided scores
-        const double u = 1.1102230246251565e-16;  // 2^-53
-        const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 8.0);
-        unsigned undecided = 0;
-        if (lane == 0) {
+    }
 #pragma unroll
-            for (int t = 0; t < TPB; ++t) {
-                if (t >= nt) continue;
-                const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(a[t], 1.0001));
-                const float lo = __double2float_rn(__dsub_rd(s[t], err));
-                const float hi = __double2float_rn(__dadd_ru(s[t], err));
-                if (lo == hi) scores[t * num_experts + k] = __double2float_rn(s[t]);
-                else undecided |= 1u << t;
-            }
+    for (int j = 0; j < kRouteExperts; ++j) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            s[j] += __shfl_xor_sync(0xffffffffu, s[j], off);
+            a[j] += __shfl_xor_sync(0xffffffffu, a[j], off);
         }
-        undecided = __shfl_sync(0xffffffffu, undecided, 0);
-        while (undecided) {
-            // the reference's exact sequential loop (matrix.cpp:29-34) for token t:
-            // the warp streams the gate row through a per-warp smem window, lane 0 adds
-            const int t = __ffs(undecided) - 1;
-            undecided &= undecided - 1;
-            // products are exact in f64, so the warp forms them; lane 0 keeps the sequential adds
-            double* win = reinterpret_cast<double*>(rs_smem + ((TPB * (in_dim + num_experts) + 1) & ~1)) + warp * 64;
-            const float* xr = xs + t * in_dim;
-            double acc = 0.0;
-            for (int c0 = 0; c0 < in_dim; c0 += 64) {
-                __syncwarp();
-                for (int j = lane; j < 64 && c0 + j < in_dim; j += 32)
-                    win[j] = static_cast<double>(xr[c0 + j]) * static_cast<double>(gk[c0 + j]);
-                __syncwarp();
-                if (lane == 0) {
-                    const int n = min(64, in_dim - c0);
-                    for (int q = 0; q < n; ++q) acc = __dadd_rn(acc, win[q]);
-                }
-            }
-            if (lane == 0) scores[t * num_experts + k] = __double2float_rn(acc);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) {
+            part[warp][j][0] = s[j];
+            part[warp][j][1] = a[j];
         }
     }
     __syncthreads();
-    for (int t = warp; t < nt; t += nwarps) {
-        const float* sc = scores + t * num_experts;
-        const int b = b0 + t;
-        double mx = -INFINITY;
-        for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[k]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        // every lane computes the total in the reference order k = 0..K-1
-        double total = 0.0;
-        for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, exp(static_cast<double>(sc[k]) - mx));
-        double selected = 0.0;
-        int picked[64];
-        double pprob[64];
-        for (int tt = 0; tt < top_k; ++tt) {
-            double best_p = -1.0;
-            int best_k = 0x7fffffff;
-            for (int k = lane; k < num_experts; k += 32) {
-                bool taken = false;
-                for (int q = 0; q < tt; ++q) taken |= (picked[q] == k);
-                if (taken) continue;
-                const double pk = __ddiv_rn(exp(static_cast<double>(sc[k]) - mx), total);
-                if (pk > best_p || (pk == best_p && k < best_k)) {
-                    best_p = pk;
-                    best_k = k;
-                }
-            }
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                const double op = __shfl_xor_sync(0xffffffffu, best_p, off);
-                const int ok = __shfl_xor_sync(0xffffffffu, best_k, off);
-                if (op > best_p || (op == best_p && ok < best_k)) {
-                    best_p = op;
-                    best_k = ok;
-                }
-            }
-            picked[tt] = best_k;
-            pprob[tt] = best_p;
-            selected = __dadd_rn(selected, best_p);
+    // ---- certification (thread j: expert k0 + j) ----
+    if (threadIdx.x < kRouteExperts && k0 + static_cast<int>(threadIdx.x) < num_experts) {
+        const int j = threadIdx.x;
+        double sv = 0.0, av = 0.0;
+        for (int w = 0; w < kRouteWarps; ++w) {
+            sv += part[w][j][0];
+            av += part[w][j][1];
         }
+        const double u = 1.1102230246251565e-16;  // 2^-53
+        const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 8.0 + kRouteWarps);
+        const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
+        const float lo = __double2float_rn(__dsub_rd(sv, err));
+        const float hi = __double2float_rn(__dadd_ru(sv, err));
+        score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(sv);
+        if (lo != hi) atomicOr(&s_und, 1u << j);
+    }
+    __syncthreads();
+    // replay: the reference's exact sequential loop (matrix.cpp:29-34).  The
+    // CTA forms the (exact) products in shared memory, then one thread adds
+    // them in index order -- a dependent f64 chain, loads hoisted ahead
+    const unsigned und = s_und;
+    for (int j = 0; j < kRouteExperts; ++j) {
+        if (!(und & (1u << j))) continue;
+        const float* gk = gate + static_cast<int64_t>(k0 + j) * in_dim;
+        for (int c0 = 0; c0 < in_dim; c0 += kReplayWin) {
+            const int n = min(kReplayWin, in_dim - c0);
+            __syncthreads();
+            for (int q = threadIdx.x; q < n; q += kRouteThreads)
+                prod[q] = static_cast<double>(xb[c0 + q]) * static_cast<double>(gk[c0 + q]);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double acc = replay_acc;
+                int q = 0;
+                for (; q + 8 <= n; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) v[t] = prod[q + t];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) acc = __dadd_rn(acc, v[t]);
+                }
+                for (; q < n; ++q) acc = __dadd_rn(acc, prod[q]);
+                replay_acc = c0 + n < in_dim ? acc : 0.0;
+                if (c0 + n >= in_dim) score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(acc);
+            }
+        }
+    }
+    // ---- the last slice CTA of token b finishes the routing ----
+    if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();   // score_ws writers
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int done = atomicAdd(&ticket[b], 1);
+        s_last = done == static_cast<int>(gridDim.y) - 1;
+        if (s_last) ticket[b] = 0;   // ready for the next launch
+    }
+    __syncthreads();
+    if (!s_last || warp != 0) return;
+    __threadfence();
+    for (int k = lane; k < num_experts; k += 32) sc[k] = __ldcg(score_ws + static_cast<int64_t>(b) * num_experts + k);
+    __syncwarp();
+    double mx = -INFINITY;
+    for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[k]));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    for (int k = lane; k < num_experts; k += 32) ex[k] = exp(static_cast<double>(sc[k]) - mx);
+    __syncwarp();
+    double total = 0.0;   // in the reference order k = 0..K-1
+    for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[k]);
+    double selected = 0.0;
+    uint64_t taken = 0;
+    for (int tt = 0; tt < top_k; ++tt) {
+        double best_p = -1.0;
+        int best_k = 0x7fffffff;
+        for (int k = lane; k < num_experts; k += 32) {
+            if (taken & (1ull << k)) continue;
+            const double pk = __ddiv_rn(ex[k], total);
+            if (pk > best_p || (pk == best_p && k < best_k)) {
+                best_p = pk;
+                best_k = k;
+            }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double op = __shfl_xor_sync(0xffffffffu, best_p, off);
+            const int ok = __shfl_xor_sync(0xffffffffu, best_k, off);
+            if (op > best_p || (op == best_p && ok < best_k)) {
+                best_p = op;
+                best_k = ok;
+            }
+        }
+        taken |= 1ull << best_k;
         if (lane == 0) {
-            for (int tt = 0; tt < top_k; ++tt) {
-                ids[static_cast<int64_t>(b) * top_k + tt] = picked[tt];
-                gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pprob[tt], selected));
-            }
+            pick_k[tt] = best_k;
+            pick_p[tt] = best_p;
         }
+        selected = __dadd_rn(selected, best_p);
+    }
+    __syncwarp();
+    for (int tt = lane; tt < top_k; tt += 32) {
+        ids[static_cast<int64_t>(b) * top_k + tt] = pick_k[tt];
+        gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pick_p[tt], selected));
     }
 }
 
@@ -578,28 +611,14 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 // =============================================================================
 
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
-                         int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16,
-                         float* sx, cudaStream_t stream) {
-    // tokens per CTA: share each gate row across several tokens at prefill,
-    // spread tokens over many CTAs at decode
-    int tpb = batch <= 32 ? 1 : (batch <= 1024 ? 2 : 8);
-    while (tpb > 1 && sizeof(float) * static_cast<size_t>(tpb) * (in_dim + num_experts) > 160 * 1024) tpb >>= 1;
-    const size_t smem = sizeof(float) * (static_cast<size_t>(tpb) * (in_dim + num_experts) + 2) + 8 * 64 * sizeof(double);
-    const int grid = (batch + tpb - 1) / tpb;
-    auto go = [&](auto kern) -> cudaError_t {
-        if (smem > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-        }
-        kern<<<grid, 256, smem, stream>>>(x, batch, in_dim, gate, num_experts, top_k, group_size, groups, k_pad,
-                                          ids, gates, x16, sx);
-        return cudaGetLastError();
-    };
-    if (tpb == 8) return go(route_kernel<8>);
-    if (tpb == 4) return go(route_kernel<4>);
-    if (tpb == 2) return go(route_kernel<2>);
-    return go(route_kernel<1>);
+                         int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
+                         float* score_ws, int32_t* ticket, cudaStream_t stream) {
+    if (batch <= 0) return cudaSuccess;
+    if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
+    const dim3 grid(batch, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
+    route_kernel<<<grid, kRouteThreads, 0, stream>>>(x, batch, in_dim, gate, num_experts, top_k, group_size, groups,
+                                                     k_pad, ids, gates, x16, sx, score_ws, ticket);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {

@@ -34,7 +34,7 @@ namespace tqb {
 cudaError_t launch_gemm(const GemmParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
-                         cudaStream_t stream);
+                         float* score_ws, int32_t* ticket, cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
@@ -481,6 +481,7 @@ struct tq_layer {
     int64_t device_bytes = 0;
     // workspace
     int64_t cap = 0;
+    DBuf route_ws, route_ticket;   // router: per-(token, expert) certified scores, per-token tickets
     DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
         err_flag, xin, yout, nsplit_d;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
@@ -490,11 +491,29 @@ struct tq_layer {
     // expert-GEMM device timing (tq_gemm_timing_enable)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    // CUDA graphs of whole forwards, keyed by their arguments: one launch per
+    // forward instead of six, no host work between the kernels
+    struct GraphEntry {
+        const void* key[6];
+        int64_t batch;
+        int path;
+        cudaGraphExec_t exec;
+        uint64_t launches;
+    };
+    std::vector<GraphEntry> graphs;
+    cudaStream_t cap_stream = nullptr;
+    bool use_graphs = !(getenv("TQ_GRAPHS") && atoi(getenv("TQ_GRAPHS")) == 0);
+    void drop_graphs() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
     ~tq_layer() {
         for (auto& e : tev) {
             cudaEventDestroy(e.first);
             cudaEventDestroy(e.second);
         }
+        drop_graphs();
+        if (cap_stream) cudaStreamDestroy(cap_stream);
     }
 };
 
@@ -567,6 +586,7 @@ void build_maps(tq_layer* L) {
 
 void reserve(tq_layer* L, int64_t max_tokens) {
     if (max_tokens <= L->cap) return;
+    L->drop_graphs();
     cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
     const Geometry& g = L->g;
     const int64_t cap = round_up(std::max<int64_t>(max_tokens, 16), 16);
@@ -582,6 +602,9 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     L->gates.alloc(sizeof(float) * cap * g.top_k);
     L->x16.alloc(sizeof(__half) * cap * g.k_pad);
     L->sx.alloc(sizeof(float) * cap * std::max<int64_t>(1, g.G));
+    L->route_ws.alloc(sizeof(float) * cap * g.K);
+    L->route_ticket.alloc(sizeof(int32_t) * cap);
+    cuda_check(cudaMemset(L->route_ticket.p, 0, sizeof(int32_t) * cap), "cudaMemset");
     L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
     L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
     L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
@@ -745,6 +768,8 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     g.mb_count = g.o_pad / kBM;
     g.n_ext = (g.G + g.r + kKC - 1) / kKC;   // extension chunks at KC = 64
     g.ext_cols = round_up(g.G + g.r, 256);    // room for KC = 256 chunks (zero-padded)
+    if (g.K > 64)
+        fail(TQ_ERR_PARAM, "GPU engine routes at most 64 experts (num_experts " + std::to_string(g.K) + ")");
     if (g.G > 64 || g.r > 64)
         fail(TQ_ERR_PARAM, "GPU engine supports at most 64 scale groups per row and rank <= 64 (groups " +
                                std::to_string(g.G) + ", rank " + std::to_string(g.r) + ")");
@@ -960,7 +985,8 @@ void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaSt
     cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(L->g.i), L->gate.as<float>(),
                             do_route ? static_cast<int>(L->g.K) : 0, static_cast<int>(L->g.top_k),
                             static_cast<int>(L->g.gs), static_cast<int>(L->g.G), static_cast<int>(L->g.k_pad),
-                            L->ids.as<int32_t>(), L->gates.as<float>(), L->x16.as<__half>(), L->sx.as<float>(), st),
+                            L->ids.as<int32_t>(), L->gates.as<float>(), L->x16.as<__half>(), L->sx.as<float>(),
+                            L->route_ws.as<float>(), L->route_ticket.as<int32_t>(), st),
                "route_kernel launch");
     count_launch(L);
 }
@@ -1148,6 +1174,51 @@ void check_batch(tq_layer* L, int64_t batch) {
 // C-ABI
 // ---------------------------------------------------------------------------
 
+namespace {
+// Run `body` (which enqueues a forward on the stream it is given) through the
+// layer's graph cache: captured once per argument set on a private stream,
+// then replayed on the caller's stream with one cudaGraphLaunch.
+template <class Body>
+void run_graphed(tq_layer* L, const void* const (&key)[6], int64_t batch, int path, cudaStream_t st, Body body) {
+    if (!L->use_graphs || L->timing) {
+        body(st);
+        return;
+    }
+    tq_layer::GraphEntry* hit = nullptr;
+    for (auto& g : L->graphs)
+        if (g.batch == batch && g.path == path && std::equal(key, key + 6, g.key)) hit = &g;
+    if (!hit) {
+        if (!L->cap_stream)
+            cuda_check(cudaStreamCreateWithFlags(&L->cap_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        if (L->graphs.size() >= 64) L->drop_graphs();
+        const uint64_t before = L->launches;
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(L->cap_stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        try {
+            body(L->cap_stream);
+        } catch (...) {
+            cudaStreamEndCapture(L->cap_stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(L->cap_stream, &graph), "cudaStreamEndCapture");
+        tq_layer::GraphEntry e{};
+        std::copy(key, key + 6, e.key);
+        e.batch = batch;
+        e.path = path;
+        e.launches = L->launches - before;
+        L->launches = before;
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(ie, "cudaGraphInstantiate");
+        L->graphs.push_back(e);
+        hit = &L->graphs.back();
+    }
+    cuda_check(cudaGraphLaunch(hit->exec, st), "cudaGraphLaunch");
+    L->launches += hit->launches;
+}
+}  // namespace
+
 extern "C" {
 
 const char* tq_last_error(void) { return g_last_error.c_str(); }
@@ -1252,6 +1323,7 @@ tq_status tq_permute(tq_layer* L, const int32_t* ids, int64_t batch, int32_t* pe
     });
 }
 
+
 tq_status tq_forward(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
                      int path, void* stream) {
     return guarded([&] {
@@ -1261,8 +1333,11 @@ tq_status tq_forward(tq_layer* L, const float* x, int64_t batch, const int32_t* 
         if (batch == 0) return;
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        run_route(L, x, batch, false, st);
-        run_experts(L, x, batch, ids, gates, y, path, st);
+        const void* const key[6] = {x, ids, gates, y, nullptr, nullptr};
+        run_graphed(L, key, batch, path, st, [&](cudaStream_t s2) {
+            run_route(L, x, batch, false, s2);
+            run_experts(L, x, batch, ids, gates, y, path, s2);
+        });
     });
 }
 
@@ -1275,15 +1350,19 @@ tq_status tq_forward_routed(tq_layer* L, const float* x, int64_t batch, float* y
         if (batch == 0) return;
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = static_cast<cudaStream_t>(stream);
-        run_route(L, x, batch, true, st);
-        run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, st);
-        if (ids)
-            cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice, st),
-                       "ids copy");
-        if (gates)
-            cuda_check(cudaMemcpyAsync(gates, L->gates.p, sizeof(float) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
-                                       st),
-                       "gates copy");
+        const void* const key[6] = {x, nullptr, nullptr, y, ids, gates};
+        run_graphed(L, key, batch, path + 16, st, [&](cudaStream_t s2) {
+            run_route(L, x, batch, true, s2);
+            run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2);
+            if (ids)
+                cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
+                                           s2),
+                           "ids copy");
+            if (gates)
+                cuda_check(cudaMemcpyAsync(gates, L->gates.p, sizeof(float) * batch * L->g.top_k,
+                                           cudaMemcpyDeviceToDevice, s2),
+                           "gates copy");
+        });
     });
 }
 
@@ -1403,10 +1482,17 @@ tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const floa
         if (top_k > 64) fail(TQ_ERR_PARAM, "route: GPU router supports top_k <= 64");
         if (batch < 0 || in_dim < 1) fail(TQ_ERR_SHAPE, "route: bad batch / width");
         if (batch == 0) return;
+        if (num_experts > 64) fail(TQ_ERR_PARAM, "route: GPU router supports at most 64 experts");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        DBuf ws, ticket;
+        ws.alloc(sizeof(float) * batch * num_experts);
+        ticket.alloc(sizeof(int32_t) * batch);
+        cuda_check(cudaMemsetAsync(ticket.p, 0, sizeof(int32_t) * batch, st), "cudaMemsetAsync");
         cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(in_dim), gate,
                                 static_cast<int>(num_experts), static_cast<int>(top_k), 1, 0, 0, ids, gates, nullptr,
-                                nullptr, static_cast<cudaStream_t>(stream)),
+                                nullptr, ws.as<float>(), ticket.as<int32_t>(), st),
                    "route_kernel launch");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");   // workspace lifetime
     });
 }
 

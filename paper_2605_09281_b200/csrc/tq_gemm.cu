@@ -35,7 +35,7 @@
 namespace tqb {
 
 constexpr int kTmemCols = 512;
-constexpr int kMaxXStages = 16;
+constexpr int kMaxXStages = 64;   // activation ring stages, or resident slots (one per chunk of a unit)
 constexpr int kMaxCStages = 24;
 constexpr int kMaxAStages = 8;
 constexpr int kSmemBudget = 225 * 1024;
@@ -97,6 +97,12 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr int kAS = a_stages(KC, DN, NI);
     static_assert(NI == 1 || NI == 2, "issuers");
+    // decode configuration: the activation tile of a RUN of units (same expert,
+    // token tile and K range; consecutive m-blocks) stays resident in shared
+    // memory -- loaded once, chunk by chunk, by the code producer -- instead of
+    // being re-fetched for every 128-row m-block
+    constexpr bool kXR = DN == 32;
+    constexpr bool kGX = false;
     constexpr int kAtoms = KC / kKC;                  // 128-byte swizzle atoms per activation row
     constexpr int kACols = KC / 2;                    // TMEM columns per A stage
     constexpr int kDCol0 = kAS * kACols;
@@ -122,7 +128,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const uint32_t x_off = 0;
     const uint32_t c_off = x_off + x_stages * x_stage_bytes;
     const uint32_t e_off = c_off + c_stages * kCStage;
-    SharedHdr* hdr = reinterpret_cast<SharedHdr*>(smem + e_off + 2 * ext_bytes);
+    SharedHdr* hdr = reinterpret_cast<SharedHdr*>(smem + e_off + p.e_slots * ext_bytes);
 
     // Role layout: the scheduler arbitrates highest-warp-id first, so the
     // latency-critical single-thread roles sit at the top:
@@ -134,7 +140,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const int warp = wid < 4 * NG ? wid + 4                       // dequant -> logical 4..
                    : wid < kRoleBase ? wid - 4 * NG + kEpi0        // epilogue -> logical kEpi0..
                    : (wid == kRoleBase ? 2 : wid == kRoleBase + 1 ? 0 : wid == kRoleBase + 2 ? 3 : 1);
-    const int n_units = *p.n_units;
+    const int n_all = *p.n_units;
+    // unit range of this CTA: contiguous (runs of units share their activation
+    // tile) or strided over the persistent grid
+    const int n_units = p.contig ? static_cast<int>((static_cast<int64_t>(blockIdx.x) + 1) * n_all / gridDim.x) : n_all;
 #ifdef TQ_EXPERIMENT
     const int kDbg = p.debug;   // experiment builds: runtime skip flags (TQ_DEBUG)
 #else
@@ -152,7 +161,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         }
         for (int s = 0; s < x_stages; ++s) {
             mbar_init(&hdr->x_full[s], 1);
-            mbar_init(&hdr->x_empty[s], 1);
+            mbar_init(&hdr->x_empty[s], 1);   // kXR: committed by the issuer of the run's last chunk c
         }
         for (int s = 0; s < c_stages; ++s) {
             mbar_init(&hdr->c_full[s], 1);
@@ -162,7 +171,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             mbar_init(&hdr->d_full[s], NI);
             mbar_init(&hdr->d_empty[s], 4);
             mbar_init(&hdr->e_full[s], 1);
-            mbar_init(&hdr->e_empty[s], 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1));
+            mbar_init(&hdr->e_empty[s], 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1));   // p.e_slots used
         }
         fence_barrier_init();
     }
@@ -181,8 +190,14 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     long long prof[4] = {0, 0, 0, 0};
     const long long prof_t0 = clock64();
 #endif
-    const int first = blockIdx.x;
-    const int stride = gridDim.x;
+    const int first = p.contig ? static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_all / gridDim.x) : blockIdx.x;
+    const int stride = p.contig ? 1 : gridDim.x;
+    // resident activation slots (kXR): slot c holds chunk c of the current run
+    const int xr_slot_bytes = kAtoms * x_atom_bytes;
+    auto same_run = [](const Unit& a, const Unit& b) {
+        return a.weight == b.weight && a.x_row == b.x_row && a.n_tok == b.n_tok && a.kc_begin == b.kc_begin &&
+               a.kc_end == b.kc_end && a.n_ext == b.n_ext;
+    };
     const int gshift = p.group_shift;
 
     if (warp == 0) {
@@ -190,16 +205,40 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         {
             int cs = 0, es = 0, tcnt = 0;
             uint32_t cph = 0, eph = 0;
+            uint64_t xm = 0;   // kXR: per-slot count (mod 2) of runs that have used the slot
+            Unit prev{};
             Unit nxt = first < n_units ? p.units[first] : Unit{};
             for (int u = first; u < n_units; u += stride) {
                 const Unit un = nxt;
                 if (u + stride < n_units) nxt = p.units[u + stride];
+                const bool run_start = u == first || !same_run(prev, un);
+                prev = un;
                 const int nmain = un.kc_end - un.kc_begin;
                 const int64_t wm = static_cast<int64_t>(un.weight) * (p.o_pad / kBM) + un.mb;  // (w, mb) slab
                 const uint8_t* wbase = p.codes + static_cast<int64_t>(un.weight) * p.weight_stride +
                                        static_cast<int64_t>(un.mb) * p.kc_total * kCBytes;
+                // kXR: the run's activation tile for chunk c, queued just ahead of chunk c's codes
+                auto load_x = [&](int c) {
+                    const bool ext = c >= nmain;
+                    const int col0 = ext ? (c - nmain) * KC : (un.kc_begin + c) * KC;
+                    const int natoms = ext ? min(kAtoms, p.n_ext64 - (c - nmain) * kAtoms) : kAtoms;
+                    const __half* src = ext ? p.e_ptr : p.x_ptr;
+                    TQ_TIMED(1, mbar_wait(&hdr->x_empty[c], static_cast<uint32_t>((xm >> c) & 1u) ^ 1u));
+                    xm ^= 1ull << c;
+                    if (elect_one()) {
+                        const uint32_t nrow = static_cast<uint32_t>((un.n_tok + 15) & ~15);
+                        mbar_arrive_expect_tx(&hdr->x_full[c], natoms * nrow * 128u);
+                        uint8_t* xst = smem + x_off + c * xr_slot_bytes;
+                        for (int at = 0; at < natoms; ++at)
+                            bulk_copy_g2s(xst + at * x_atom_bytes,
+                                          src + ((static_cast<int64_t>(col0 / kKC + at) * p.x_atom_rows) + un.x_row) * kKC,
+                                          nrow * 128u, &hdr->x_full[c]);
+                    }
+                    __syncwarp();
+                };
                 for (int c = 0; c < nmain; ++c) {
                     const int kc = un.kc_begin + c;
+                    if (kXR && run_start) load_x(c);
                     TQ_TIMED(0, mbar_wait(&hdr->c_empty[cs], cph ^ 1u));
                     uint8_t* st = smem + c_off + cs * kCStage;
                     const uint8_t* src = wbase + static_cast<int64_t>(kc) * kCBytes;
@@ -220,16 +259,20 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     ++tcnt;
                     if (++cs == c_stages) { cs = 0; cph ^= 1u; }
                 }
+                if (kXR && run_start)
+                    for (int c = nmain; c < nmain + un.n_ext; ++c) load_x(c);
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
                     TQ_TIMED(1, mbar_wait(&hdr->e_empty[es], eph ^ 1u));
                     uint8_t* dst = smem + e_off + es * ext_bytes;
                     bulk_copy2_elect(&hdr->e_full[es], dst, p.ext_blocks + wm * ext_bytes, ext_bytes, dst, dst, 0u);
-                    if (++es == 2) { es = 0; eph ^= 1u; }
+                    if (++es == p.e_slots) { es = 0; eph ^= 1u; }
                 }
             }
         }
     } else if (warp == 3) {
         // ===================== activation producer (all 32 lanes) ==========
+        if (kXR) {
+        } else {
         // small token tiles (decode): cp.async 16-byte pieces through the LSU with
         // the 128B swizzle applied in software -- TMA loads would queue behind
         // the packed-code bulk copies in the SM's copy engine; large tiles: TMA
@@ -251,6 +294,18 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 const int natoms = ext ? min(kAtoms, p.n_ext64 - (c - nmain) * kAtoms) : kAtoms;
                 if (kDbg & 32) {
                     if (lane == 0) mbar_arrive(&hdr->x_full[xs]);
+                } else if (p.x_atom_rows > 0) {
+                    if (lane == 0) {
+                        const __half* src = ext ? p.e_ptr : p.x_ptr;
+                        const uint32_t nrow = static_cast<uint32_t>((un.n_tok + 15) & ~15);
+                        mbar_arrive_expect_tx(&hdr->x_full[xs], natoms * nrow * 128u);
+                        uint8_t* xst = smem + x_off + xs * x_stage_bytes;
+                        for (int at = 0; at < natoms; ++at)
+                            bulk_copy_g2s(xst + at * x_atom_bytes,
+                                          src + ((static_cast<int64_t>(col0 / kKC + at) * p.x_atom_rows) + un.x_row) * kKC,
+                                          nrow * 128u, &hdr->x_full[xs]);
+                    }
+                    __syncwarp();
                 } else if (small) {
                     const __half* src = ext ? p.e_ptr : p.x_ptr;
                     const int64_t ld = ext ? p.e_ld : p.x_ld;
@@ -284,6 +339,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 if (++xs == x_stages) { xs = 0; xph ^= 1u; }
             }
         }
+        }
     } else if (warp == 1 || (NI == 2 && warp == 2)) {
         // ===================== MMA issuers (converged warp, one elected lane issues) ==========
         const int j = warp == 1 ? 0 : 1;
@@ -292,10 +348,12 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         int xs = j;
         uint32_t xph = 0;
         int c_next = j;
+        uint64_t xm = 0;   // kXR: per-slot count (mod 2) of completed runs that used the slot
         Unit nxt = first < n_units ? p.units[first] : Unit{};
         for (int u = first; u < n_units; u += stride, ++lu) {
             const Unit un = nxt;
             if (u + stride < n_units) nxt = p.units[u + stride];
+            const bool run_end = u + stride >= n_units || !same_run(un, nxt);
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
             const int ds = lu & 1;
@@ -313,11 +371,15 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             for (; c < nch; c += NI) {
                 TQ_TIMED(0, mbar_wait(&hdr->full[as], aph));
                 if (lane == 0) trace_ev(p, 2, tcnt);
-                TQ_TIMED(3, mbar_wait(&hdr->x_full[xs], xph));
-                if (un.n_tok <= 8) fence_proxy_async_smem();   // cp.async (generic proxy) tiles -> MMA reads
+                if (kXR) {
+                    TQ_TIMED(3, mbar_wait(&hdr->x_full[c], static_cast<uint32_t>((xm >> c) & 1u)));
+                } else {
+                    TQ_TIMED(3, mbar_wait(&hdr->x_full[xs], xph));
+                    if (un.n_tok <= 8) fence_proxy_async_smem();   // cp.async (generic proxy) tiles -> MMA reads
+                }
                 ++tcnt;
                 tc_fence_after();
-                const uint32_t xaddr = s_base + x_off + xs * x_stage_bytes;
+                const uint32_t xaddr = s_base + x_off + (kXR ? c * xr_slot_bytes : xs * x_stage_bytes);
                 const uint64_t bdesc = sw128_desc(xaddr);
                 const uint32_t a_tm = tmem + as * kACols;
                 // atoms of 64 K: 4 MMAs each, one elected lane, descriptors advanced in PTX
@@ -331,7 +393,8 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                                                (c > c_first || at > 0) ? 1u : 0u);
                 }
                 tc_commit_elect(&hdr->empty[as]);
-                tc_commit_elect(&hdr->x_empty[xs]);
+                if (!kXR) tc_commit_elect(&hdr->x_empty[xs]);
+                else if (run_end) tc_commit_elect(&hdr->x_empty[c]);   // the run's last use of slot c
 #ifdef TQ_PROFILE
                 prof[2] += 1;   // chunks
 #endif
@@ -344,6 +407,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             if (c_first < nch) tc_commit_elect(&hdr->d_full[ds]);
             else if (lane == 0) mbar_arrive(&hdr->d_full[ds]);
             c_next = c - nch;
+            if (kXR && run_end) xm ^= (nch >= 64 ? ~0ull : ((1ull << nch) - 1ull));
         }
     } else if (warp >= 4 && warp < kEpi0) {
         // ===================== dequant groups =====================
@@ -361,15 +425,71 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         int c_next = grp;                              // next own chunk, relative to q_base
         int tcnt = 0;
         const bool tr = (lane == 0 && q == 0);
+        // GX (small token tiles): the group loads the activation tile of its NEXT
+        // own chunk with cp.async while it dequantizes the current one -- 128
+        // threads keep the LSU busy; no copy-engine queue in the way
+        const int gt = threadIdx.x & 127;              // thread within the group (wid & 3 -> q)
+        int xs_n = grp, xph_n = 0;                     // X ring slot of the next load (chunk grp, grp+NG, ...)
+        auto issue_x = [&](const Unit& xu, int xc) {
+            const int xnmain = xu.kc_end - xu.kc_begin;
+            const bool ext = xc >= xnmain;
+            const int col0 = ext ? (xc - xnmain) * KC : (xu.kc_begin + xc) * KC;
+            const int natoms = ext ? min(kAtoms, p.n_ext64 - (xc - xnmain) * kAtoms) : kAtoms;
+            mbar_wait(&hdr->x_empty[xs_n], static_cast<uint32_t>(xph_n) ^ 1u);
+            const __half* src = ext ? p.e_ptr : p.x_ptr;
+            if (p.x_atom_rows > 0) {
+                // pre-swizzled atom-major rows: one bulk copy per 64-column atom (async proxy)
+                if (gt == 0) {
+                    const uint32_t nrow = static_cast<uint32_t>((xu.n_tok + 15) & ~15);
+                    mbar_arrive_expect_tx(&hdr->x_full[xs_n], natoms * nrow * 128u);
+                    uint8_t* xst = smem + x_off + xs_n * x_stage_bytes;
+                    for (int at = 0; at < natoms; ++at)
+                        bulk_copy_g2s(xst + at * x_atom_bytes,
+                                      src + ((static_cast<int64_t>(col0 / kKC + at) * p.x_atom_rows) + xu.x_row) * kKC,
+                                      nrow * 128u, &hdr->x_full[xs_n]);
+                }
+                return;
+            }
+            const int64_t ld = ext ? p.e_ld : p.x_ld;
+            const uint32_t sx = s_base + x_off + xs_n * x_stage_bytes;
+            const int lshift = 3 + (natoms >= 4 ? 2 : natoms >= 2 ? 1 : 0);   // lanes per row = natoms * 8
+            const int piece = gt & ((1 << lshift) - 1);
+            const int at = piece >> 3, ch = piece & 7;
+            if (at < natoms) {
+                const __half* g = src + static_cast<int64_t>(xu.x_row) * ld + col0 + at * kKC + ch * 8;
+                for (int row = gt >> lshift; row < xu.n_tok; row += (128 >> lshift))
+                    cp_async_16(sx + at * x_atom_bytes + row * 128 + ((ch ^ (row & 7)) << 4), g + row * ld);
+            }
+            cp_async_commit();
+        };
+        auto advance_x = [&]() {
+            xs_n += NG;
+            if (xs_n >= x_stages) { xs_n -= x_stages; xph_n ^= 1; }
+        };
         Unit nxt = first < n_units ? p.units[first] : Unit{};
+        if (kGX && first < n_units) {
+            const int nch0 = (nxt.kc_end - nxt.kc_begin) + nxt.n_ext;
+            if (grp < nch0) issue_x(nxt, grp);
+            else cp_async_commit();
+            advance_x();
+        }
         for (int u = first; u < n_units; u += stride) {
             const Unit un = nxt;
             if (u + stride < n_units) nxt = p.units[u + stride];
+            const bool has_nxt = u + stride < n_units;
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
             int c = c_next;
             for (; c < nch; c += NG) {
                 const bool main_chunk = c < nmain;
+                if (kGX) {   // prefetch the activation tile of the next own chunk
+                    const int cn = c + NG;
+                    const int nch_n = has_nxt ? (nxt.kc_end - nxt.kc_begin) + nxt.n_ext : 0;
+                    if (cn < nch) TQ_TIMED(0, issue_x(un, cn));
+                    else if (cn - nch < nch_n) TQ_TIMED(0, issue_x(nxt, cn - nch));
+                    else cp_async_commit();
+                    advance_x();
+                }
                 if (main_chunk) {
                     // move the code-ring position to main chunk m_base + c
                     for (int m = m_base + c; m_cur < m; ++m_cur)
@@ -380,7 +500,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     // super-word of fp16 pairs at a time -- dequantize, tcgen05.st, reuse
                     if (main_chunk) {
                         const int kc = un.kc_begin + c;
-                        TQ_TIMED(0, mbar_wait(&hdr->c_full[cs], cph));
+#ifdef TQ_PROFILE
+                        const long long tcf0 = clock64();
+#endif
+                        mbar_wait(&hdr->c_full[cs], cph);
                         if (tr) trace_ev(p, 4, grp * 1024 + tcnt);
                         const uint8_t* st = smem + c_off + cs * kCStage;
                         const uint32_t* wst = reinterpret_cast<const uint32_t*>(st) + rloc;
@@ -418,7 +541,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                             }
                             __syncwarp();
                             if (lane == 0) mbar_arrive(&hdr->c_empty[cs]);
-                            TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
+#ifdef TQ_PROFILE
+                            prof[1] += clock64() - tcf0;
+#endif
+                            TQ_TIMED(3, mbar_wait(&hdr->empty[as], aph ^ 1u));
                             if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
                             tc_fence_after();
 #ifdef TQ_PROFILE
@@ -466,7 +592,11 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
                     }
-                    if (!(kDbg & 64)) TQ_TIMED(3, tc_wait_st());
+                    if (!(kDbg & 64)) tc_wait_st();
+                    if (kGX && p.x_atom_rows == 0) {
+                        cp_async_wait_group1();          // this chunk's tile landed (the next may be in flight)
+                        fence_proxy_async_smem();        // generic-proxy cp.async writes -> MMA operand reads
+                    }
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&hdr->full[as]);
@@ -481,7 +611,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             q_base += nch;
             m_base += nmain;
             if (un.n_ext > 0 && p.n_ext64 > 0) {
-                if (++es == 2) { es = 0; eph ^= 1u; }
+                if (++es == p.e_slots) { es = 0; eph ^= 1u; }
             }
         }
     } else if (warp >= kEpi0) {
@@ -573,24 +703,35 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     p.x_stage_rows = rows;
     const int x_stage = (kc / kKC) * rows * 128;
     const int c_stage = code_stage_bytes(p.bits, kc);
-    const int fixed = 2048 + 2 * ext_slot_bytes(p.n_ext64);
-    // smem split: >= 80 KB of packed-code stages in flight (HBM latency), the
-    // activation ring as deep as the rest allows (<= 16), leftovers to codes
+    if (p.e_slots != 1) p.e_slots = 2;
+    const int fixed = 2048 + p.e_slots * ext_slot_bytes(p.n_ext64);
     const int ni = (kc == 128 && dn <= 64) ? 2 : 1;
     const int as_n = a_stages(kc, dn, ni);
-    int cs = (80 * 1024 + c_stage - 1) / c_stage;
-    int xs = (kSmemBudget - fixed - cs * c_stage) / x_stage;
-    xs = xs < kMaxXStages ? xs : kMaxXStages;
-    if (xs < as_n) xs = as_n;
-    cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
-    cs = cs < kMaxCStages ? cs : kMaxCStages;
-    if (cs < 2 || xs < 2) return cudaErrorInvalidValue;
+    int cs, xs;
+    if (dn == 32) {
+        // resident activation slots, one per chunk of a unit; codes get the rest
+        if (p.xr_slots < 1 || p.xr_slots > kMaxXStages || p.x_atom_rows <= 0) return cudaErrorInvalidValue;
+        xs = p.xr_slots;
+        cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
+        cs = cs < kMaxCStages ? cs : kMaxCStages;
+        if (cs < 4) return cudaErrorInvalidValue;
+    } else {
+        // >= 80 KB of packed-code stages in flight (HBM latency), the activation
+        // ring as deep as the rest allows (<= 16), leftovers to codes
+        cs = (80 * 1024 + c_stage - 1) / c_stage;
+        xs = (kSmemBudget - fixed - cs * c_stage) / x_stage;
+        xs = xs < 16 ? xs : 16;
+        if (xs < as_n) xs = as_n;
+        cs = (kSmemBudget - fixed - xs * x_stage) / c_stage;
+        cs = cs < kMaxCStages ? cs : kMaxCStages;
+        if (cs < 2 || xs < 2) return cudaErrorInvalidValue;
+    }
     p.x_stages = xs;
     p.c_stages = cs;
     p.group_shift = -1;
     for (int s = 0; s < 16; ++s)
         if ((1 << s) == p.group_size) p.group_shift = s;
-    const int smem = 1024 + xs * x_stage + cs * c_stage + 2 * ext_slot_bytes(p.n_ext64) + 1024;
+    const int smem = 1024 + xs * x_stage + cs * c_stage + p.e_slots * ext_slot_bytes(p.n_ext64) + 2048;
     static const int dbg = getenv("TQ_DEBUG") ? atoi(getenv("TQ_DEBUG")) : 0;
     p.debug = dbg;
     static unsigned long long* trace_buf = nullptr;

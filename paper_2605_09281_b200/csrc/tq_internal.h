@@ -44,6 +44,12 @@ struct GemmParams {
     int64_t x_ld;
     const __half* e_ptr;
     int64_t e_ld;
+    int32_t contig;         // 1: each CTA takes a contiguous unit range (runs share activation tiles)
+    int32_t e_slots;        // extension-block ring depth (1 or 2)
+    int32_t xr_slots;       // resident activation slots (decode config): max chunks per unit
+    int64_t x_atom_rows;    // > 0: x_ptr / e_ptr are atom-major [cols/64][x_atom_rows][64 halves], rows
+                            // pre-swizzled (128B pattern of the row index), tile rows 8-aligned:
+                            // activation tiles are plain bulk copies, one per 64-column atom
     const uint8_t* codes;   // [weight][mb][kc] blocks of code_block_bytes(bits)
     int64_t weight_stride;  // bytes per weight matrix in `codes`
     const __half* scales;   // [weight][mb][G][128] fp16 scale slabs (quantized weights)
@@ -82,6 +88,9 @@ struct PlanArgs {
     int num_shared;            // shared experts (weights K..K+S-1), rows after the slots
     int mb_count;              // m-blocks of the expert weights
     int kc_total, nsplit, n_ext;   // nsplit: upper bound; the kernel picks the best <= nsplit
+    int nsplit_min;            // lower bound (resident activation tiles must fit shared memory)
+    int run_order;             // 1: units ordered (expert, tile, split, m-block): runs of m-blocks
+    int proj_bn;               // token tile of the projection pass (0: bn)
     int main_kc;               // 1: main chunks present (0 for the lotile-only path)
     int num_sms;               // persistent grid size (load-balance target)
     int bn;                    // token tile (<= kBNMax)
@@ -90,6 +99,7 @@ struct PlanArgs {
     int32_t* perm;
     int32_t* inv;
     int32_t* offsets;
+    int32_t* poffsets;         // K+1: expert row bases in the 8-row padded activation layout
     Unit* units;
     int32_t* n_units;
     Unit* proj_units;
@@ -112,8 +122,10 @@ struct GatherArgs {
     int batch, top_k, num_experts, k_pad, groups, rank, ext_cols;
     int with_shared;         // append B shared-expert rows
     int use_sx, use_z;       // path selection
-    __half* xp;              // [rows][k_pad]
-    __half* ep;              // [rows][ext_cols]
+    __half* xp;              // [rows][k_pad], or atom-major (see atom_rows)
+    __half* ep;              // [rows][ext_cols], or atom-major
+    const int32_t* poffsets; // if set: slot s of expert e goes to padded row s + poffsets[e] - offsets[e]
+    int64_t atom_rows;       // > 0: atom-major, 128B-swizzled layout [cols/64][atom_rows][64] (bulk-copy tiles)
 };
 
 struct CombineArgs {
@@ -123,6 +135,8 @@ struct CombineArgs {
     const int32_t* inv;
     const float* gates;
     const int32_t* offsets;  // K+1
+    const int32_t* ids;      // with poffsets: routed row = inv + poffsets[e] - offsets[e]
+    const int32_t* poffsets;
     int num_experts, batch, top_k, out_dim, num_shared;
     int use_routed;
     const float* ysh;        // shared-expert rows: split buffers, row = sh_row0 + s*batch + b

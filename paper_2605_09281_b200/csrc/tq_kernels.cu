@@ -280,17 +280,24 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
         tot[threadIdx.x] = s;
     }
     __syncthreads();
+    __shared__ int32_t ptot[1025];   // expert row bases, each expert's rows padded to a multiple of 8
     if (threadIdx.x == 0) {
-        int run = 0;
+        int run = 0, prun = 0;
         for (int e = 0; e < K; ++e) {
             const int c = tot[e];
             tot[e] = run;
+            ptot[e] = prun;
             run += c;
+            prun += (c + 7) & ~7;
         }
         tot[K] = run;
+        ptot[K] = prun;
     }
     __syncthreads();
-    if (threadIdx.x <= K) a.offsets[threadIdx.x] = tot[threadIdx.x];
+    if (threadIdx.x <= K) {
+        a.offsets[threadIdx.x] = tot[threadIdx.x];
+        if (a.poffsets) a.poffsets[threadIdx.x] = ptot[threadIdx.x];
+    }
     if (threadIdx.x < K) {
         int run = tot[threadIdx.x];
         for (int w = 0; w < 32; ++w) {
@@ -340,10 +347,11 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
         s_tiles[0] = 0;
         for (int t = 0; t < n_local; ++t) s_tiles[t + 1] += s_tiles[t];  // prefix over resident experts
         const long base = static_cast<long>(s_tiles[n_local] + a.num_shared * sh_tiles) * a.mb_count;
-        int best = 1;
+        int best = a.main_kc ? max(1, a.nsplit_min) : 1;
         float best_score = -1.0f;
         const int cap = a.main_kc ? max(1, min(a.nsplit, a.kc_total)) : 1;
-        for (int ns = 1; ns <= cap; ++ns) {
+        const int lo_ns = a.main_kc ? min(max(1, a.nsplit_min), cap) : 1;
+        for (int ns = lo_ns; ns <= cap; ++ns) {
             const long units = base * ns;
             const long rounds = (units + a.num_sms - 1) / a.num_sms;
             const float eff = rounds > 0 ? static_cast<float>(units) / static_cast<float>(rounds * a.num_sms) : 1.0f;
@@ -366,34 +374,64 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
         int sp = u % ns;
         int rest = u / ns;
         if (u < routed_units) {
-            // rest = (tile-global index) over (e, mb, tile): ordered e, mb, tile
-            // find expert: units of expert t = (s_tiles[t+1]-s_tiles[t]) * mb_count
-            int lo = 0, hi = n_local;  // s_tiles[lo]*mb <= rest < s_tiles[hi]*mb
-            while (hi - lo > 1) {
-                const int mid = (lo + hi) >> 1;
-                if (s_tiles[mid] * a.mb_count <= rest) lo = mid; else hi = mid;
+            int t, mb, tl;
+            if (a.run_order) {
+                // (expert, tile, split, m-block), m-block fastest: consecutive units share X
+                mb = u % a.mb_count;
+                const int r2 = u / a.mb_count;
+                sp = r2 % ns;
+                const int tg = r2 / ns;   // global tile index
+                int lo = 0, hi = n_local;  // s_tiles[lo] <= tg < s_tiles[hi]
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_tiles[mid] <= tg) lo = mid; else hi = mid;
+                }
+                t = lo;
+                tl = tg - s_tiles[t];
+            } else {
+                // rest = (tile-global index) over (e, mb, tile): ordered e, mb, tile
+                // find expert: units of expert t = (s_tiles[t+1]-s_tiles[t]) * mb_count
+                int lo = 0, hi = n_local;  // s_tiles[lo]*mb <= rest < s_tiles[hi]*mb
+                while (hi - lo > 1) {
+                    const int mid = (lo + hi) >> 1;
+                    if (s_tiles[mid] * a.mb_count <= rest) lo = mid; else hi = mid;
+                }
+                t = lo;
+                const int within = rest - s_tiles[t] * a.mb_count;
+                const int ntl = s_tiles[t + 1] - s_tiles[t];
+                mb = within / ntl;
+                tl = within % ntl;
             }
-            const int t = lo;
-            const int within = rest - s_tiles[t] * a.mb_count;
-            const int ntl = s_tiles[t + 1] - s_tiles[t];
-            const int mb = within / ntl, tl = within % ntl;
             const int e = a.e_begin + t;
             const int ne = tot[e + 1] - tot[e];
             un.weight = t;
             un.mb = mb;
-            un.x_row = tot[e] + tl * bn;
+            un.x_row = (a.poffsets ? ptot[e] : tot[e]) + tl * bn;
             un.n_tok = min(bn, ne - tl * bn);
             un.y_row = un.x_row;
         } else {
-            rest -= s_tiles[n_local] * a.mb_count;
-            const int s = rest / (sh_tiles * a.mb_count);
-            const int within = rest % (sh_tiles * a.mb_count);
-            const int mb = within / sh_tiles, tl = within % sh_tiles;
+            int s, mb, tl;
+            if (a.run_order) {
+                const int v = u - routed_units;   // (s, tile, split, mb)
+                mb = v % a.mb_count;
+                const int r2 = v / a.mb_count;
+                sp = r2 % ns;
+                const int tg = r2 / ns;
+                s = tg / sh_tiles;
+                tl = tg % sh_tiles;
+            } else {
+                rest -= s_tiles[n_local] * a.mb_count;
+                s = rest / (sh_tiles * a.mb_count);
+                const int within = rest % (sh_tiles * a.mb_count);
+                mb = within / sh_tiles;
+                tl = within % sh_tiles;
+            }
+            const int base = a.poffsets ? ptot[K] : n_slots;
             un.weight = n_local + s;
             un.mb = mb;
-            un.x_row = n_slots + tl * bn;
+            un.x_row = base + tl * bn;
             un.n_tok = min(bn, a.batch - tl * bn);
-            un.y_row = n_slots + s * a.batch + tl * bn;
+            un.y_row = base + s * a.batch + tl * bn;
         }
         un.kc_begin = static_cast<int16_t>(a.main_kc ? sp * a.kc_total / ns : 0);
         un.kc_end = static_cast<int16_t>(a.main_kc ? (sp + 1) * a.kc_total / ns : 0);
@@ -405,7 +443,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     if (threadIdx.x == 0) *a.n_units = total;
     // projection pass units: stacked projection weight (index 0) x all tokens
     if (a.proj_mb > 0) {
-        const int tiles = (a.batch + bn - 1) / bn;
+        const int pbn = a.proj_bn > 0 ? a.proj_bn : bn;
+        const int tiles = (a.batch + pbn - 1) / pbn;
         const int np = a.proj_mb * tiles * a.proj_nsplit;
         for (int u = threadIdx.x; u < np; u += blockDim.x) {
             const int sp = u % a.proj_nsplit;
@@ -414,9 +453,9 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
             Unit un;
             un.weight = 0;
             un.mb = mb;
-            un.x_row = tl * bn;
-            un.n_tok = min(bn, a.batch - tl * bn);
-            un.y_row = tl * bn;
+            un.x_row = tl * pbn;
+            un.n_tok = min(pbn, a.batch - tl * pbn);
+            un.y_row = tl * pbn;
             un.kc_begin = static_cast<int16_t>(sp * a.proj_kc_total / a.proj_nsplit);
             un.kc_end = static_cast<int16_t>((sp + 1) * a.proj_kc_total / a.proj_nsplit);
             un.n_ext = 0;
@@ -441,34 +480,50 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
     const int row = blockIdx.x;
     if (row >= rows) return;
     int b, e = -1;
+    int64_t prow = row;   // destination row
     if (row < n_slots) {
         const int f = a.perm[row];
         b = f / a.top_k;
         e = a.ids[f];
+        if (a.poffsets) prow = row + a.poffsets[e] - a.offsets[e];
     } else {
         b = row - n_slots;
+        if (a.poffsets) prow = a.poffsets[a.num_experts] + b;
     }
+    // destination of the 16-byte piece t (8 halves) of a row with `cols` columns
+    auto dst_piece = [&](__half* base, int cols, int t) -> int4* {
+        if (a.atom_rows > 0) {
+            const int at = t >> 3, ch = t & 7;
+            return reinterpret_cast<int4*>(base + ((static_cast<int64_t>(at) * a.atom_rows + prow) * 64 +
+                                                   ((ch ^ static_cast<int>(prow & 7)) << 3)));
+        }
+        return reinterpret_cast<int4*>(base + prow * cols) + t;
+    };
     // activation row: 16-byte vector copy
     const int4* src = reinterpret_cast<const int4*>(a.x16 + static_cast<int64_t>(b) * a.k_pad);
-    int4* dst = reinterpret_cast<int4*>(a.xp + static_cast<int64_t>(row) * a.k_pad);
-    for (int t = threadIdx.x; t < a.k_pad / 8; t += blockDim.x) dst[t] = src[t];
-    // extension row: [Sx | zscale * sum_splits(Z) * rowscale | 0]
-    __half* er = a.ep + static_cast<int64_t>(row) * a.ext_cols;
-    for (int col = threadIdx.x; col < a.ext_cols; col += blockDim.x) {
-        float v = 0.0f;
-        if (col < a.groups) {
-            if (a.use_sx) v = a.sx[static_cast<int64_t>(b) * a.groups + col];
-        } else if (col < a.groups + a.rank) {
-            if (a.use_z && e >= 0) {
-                const int j = col - a.groups;
-                const int zc = a.pm_of[e] * a.rank + j;
-                float z = 0.0f;
-                for (int sp = 0; sp < a.proj_nsplit; ++sp)
-                    z += a.zpart[sp * a.zsplit_stride + static_cast<int64_t>(b) * a.zcols + zc];
-                v = z * a.rowscale[zc] * a.zscale[e];
+    for (int t = threadIdx.x; t < a.k_pad / 8; t += blockDim.x) *dst_piece(a.xp, a.k_pad, t) = src[t];
+    // extension row: [Sx | zscale * sum_splits(Z) * rowscale | 0], 8 columns per thread
+    for (int t = threadIdx.x; t < a.ext_cols / 8; t += blockDim.x) {
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int col = t * 8 + q;
+            float v = 0.0f;
+            if (col < a.groups) {
+                if (a.use_sx) v = a.sx[static_cast<int64_t>(b) * a.groups + col];
+            } else if (col < a.groups + a.rank) {
+                if (a.use_z && e >= 0) {
+                    const int j = col - a.groups;
+                    const int zc = a.pm_of[e] * a.rank + j;
+                    float z = 0.0f;
+                    for (int sp = 0; sp < a.proj_nsplit; ++sp)
+                        z += a.zpart[sp * a.zsplit_stride + static_cast<int64_t>(b) * a.zcols + zc];
+                    v = z * a.rowscale[zc] * a.zscale[e];
+                }
             }
+            h[q] = __float2half_rn(v);
         }
-        er[col] = __float2half_rn(v);
+        *dst_piece(a.ep, a.ext_cols, t) = *reinterpret_cast<const int4*>(h);
     }
 }
 
@@ -499,8 +554,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     if (a.use_routed) {
         for (int t = 0; t < a.top_k; ++t) {
             const int f = b * a.top_k + t;
-            const int pos = a.inv[f];
+            int pos = a.inv[f];
             if (pos < 0) continue;  // invalid expert id (reported through the error flag)
+            if (a.poffsets) {
+                const int e = a.ids[f];
+                pos += a.poffsets[e] - a.offsets[e];
+            }
             float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
             for (int sp = 0; sp < ns; ++sp)
                 load4(a.y + sp * a.split_stride + static_cast<int64_t>(pos) * a.out_dim + c0, v);
@@ -509,7 +568,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
             for (int j = 0; j < 4; ++j) acc[j] = fmaf(g, v[j], acc[j]);
         }
     }
-    const int64_t sh0 = a.sh_from_offsets ? n_slots : 0;
+    const int64_t sh0 = a.sh_from_offsets ? (a.poffsets ? a.poffsets[a.num_experts] : n_slots) : 0;
     for (int s = 0; s < a.num_shared; ++s) {
         const int64_t r = sh0 + static_cast<int64_t>(s) * a.batch + b;
         float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};

@@ -233,6 +233,9 @@ static __device__ __forceinline__ uint16_t ld_shared_u16(uint32_t addr) {
 static __device__ __forceinline__ void cp_async_16(uint32_t dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
+static __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+static __device__ __forceinline__ void cp_async_wait_group1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
 // async arrive that first raises the barrier's pending count (no .noinc): the
 // arrival is extra to the count the barrier was initialised with
 static __device__ __forceinline__ void cp_async_mbar_arrive_inc(uint64_t* bar) {

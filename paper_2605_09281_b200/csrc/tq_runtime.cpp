@@ -481,7 +481,7 @@ struct tq_layer {
     int64_t device_bytes = 0;
     // workspace
     int64_t cap = 0;
-    DBuf route_ws, route_ticket;   // router: per-(token, expert) certified scores, per-token tickets
+    DBuf route_ws, route_ticket, poffsets;   // router: per-(token, expert) certified scores, per-token tickets
     DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
         err_flag, xin, yout, nsplit_d;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
@@ -502,7 +502,7 @@ struct tq_layer {
     };
     std::vector<GraphEntry> graphs;
     cudaStream_t cap_stream = nullptr;
-    bool use_graphs = !(getenv("TQ_GRAPHS") && atoi(getenv("TQ_GRAPHS")) == 0);
+    bool use_graphs = !(getenv("TQ_GRAPHS") && atoi(getenv("TQ_GRAPHS")) == 0) && !getenv("TQ_DEBUG");  // debug dumps sync
     void drop_graphs() {
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         graphs.clear();
@@ -521,19 +521,16 @@ namespace {
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
-int64_t rows_for(const tq_layer* L, int64_t batch) { return batch * L->g.top_k + L->g.S * batch; }
+// activation / output rows of a forward: routed slots with every expert's rows
+// padded to a multiple of 8 (tile starts 8-row aligned for the swizzled
+// bulk-copy layout), the shared-expert rows, and slack for 16-row MMA tiles
+int64_t rows_for(const tq_layer* L, int64_t batch) {
+    return batch * L->g.top_k + 8 * L->g.K + L->g.S * batch + 32;
+}
+int64_t compact_rows(const tq_layer* L, int64_t batch) { return batch * L->g.top_k + L->g.S * batch; }
 
 // Upper bound of the split-K count the plan kernel may choose for a batch
 // (it picks the best-balanced value <= this from the actual routing).
-int main_nsplit(const tq_layer* L, int64_t batch) {
-    const int64_t local = L->e_end - L->e_begin;
-    const int64_t active = std::max<int64_t>(1, std::min<int64_t>(local, batch * L->g.top_k) + L->g.S);
-    const int64_t base = active * L->g.mb_count;
-    int64_t ns = (16 * L->num_sms + base - 1) / base;
-    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 2));
-    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ns, 16)));
-}
-
 int proj_nsplit(const tq_layer* L, int64_t batch) {
     if (L->proj_mb == 0) return 1;
     const int64_t base = L->proj_mb * ((batch + 191) / 192);
@@ -574,6 +571,43 @@ LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
     return c;
 }
 
+// projection pass: dense fp16 operand from the row-major x16 buffer -- never
+// the resident-activation decode configuration
+LaunchCfg proj_cfg(const tq_layer* L, int64_t batch) {
+    LaunchCfg c = cfg_for(L, batch);
+    if (c.dn == 32) {
+        c.dn = 64;
+        c.bn = 64;
+    }
+    return c;
+}
+
+// decode configuration (dn == 32): resident activation slots of kc-wide chunks
+// must fit ~140 KB of shared memory -> lower bound on the split-K count
+int xr_ns_min(const tq_layer* L, const LaunchCfg& cf, int64_t batch) {
+    if (cf.dn != 32) return 1;
+    const int64_t tok = std::max<int64_t>(1, std::min<int64_t>(cf.bn, batch * L->g.top_k));
+    const int64_t rows = (tok + 15) / 16 * 16;
+    const int64_t slot = (cf.kc / 64) * rows * 128;
+    const int64_t max_slots = std::min<int64_t>(64, (140 * 1024) / slot);
+    const int64_t main_slots = std::max<int64_t>(1, max_slots - cf.n_ext);
+    return static_cast<int>((cf.kc_total + main_slots - 1) / main_slots);
+}
+
+int xr_slots(const LaunchCfg& cf, int ns_min) {
+    return (cf.kc_total + ns_min - 1) / ns_min + cf.n_ext;
+}
+
+int main_nsplit(const tq_layer* L, int64_t batch) {
+    const int64_t local = L->e_end - L->e_begin;
+    const int64_t active = std::max<int64_t>(1, std::min<int64_t>(local, batch * L->g.top_k) + L->g.S);
+    const int64_t base = active * L->g.mb_count;
+    int64_t ns = (16 * L->num_sms + base - 1) / base;
+    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 2));
+    ns = std::max<int64_t>(1, std::min<int64_t>(ns, 16));
+    return static_cast<int>(std::max<int64_t>(ns, xr_ns_min(L, cfg_for(L, batch), batch)));
+}
+
 void build_maps(tq_layer* L) {
     const int64_t rows = rows_for(L, L->cap);
     L->map_x16_16 = make_map(L->x16.p, L->cap, L->g.k_pad, 16);
@@ -608,6 +642,7 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
     L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
     L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
+    L->poffsets.alloc(sizeof(int32_t) * (g.K + 1));
     const int64_t max_units = (g.K + g.S) * g.mb_count * ((cap + 127) / 128 + g.K) * 16 + 64;
     L->units.alloc(sizeof(Unit) * max_units);
     L->n_units.alloc(sizeof(int32_t));
@@ -1015,6 +1050,9 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     const bool use_lotile = path != TQ_PATH_QMOE;
     const bool use_qmoe = path != TQ_PATH_LOTILE;
     const LaunchCfg cf = cfg_for(L, batch);
+    const LaunchCfg cfp = proj_cfg(L, batch);
+    const bool xr = cf.dn == 32;   // decode: resident activation tiles, contiguous unit runs
+    const int ns_min = use_qmoe ? xr_ns_min(L, cf, batch) : 1;
     const int nsplit = use_qmoe ? main_nsplit(L, batch) : 1;
     const int pns = proj_nsplit(L, batch);
     const bool with_shared = use_qmoe && g.S > 0;
@@ -1030,17 +1068,21 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     pa.mb_count = static_cast<int>(g.mb_count);
     pa.kc_total = cf.kc_total;
     pa.nsplit = nsplit;
+    pa.nsplit_min = ns_min;
+    pa.run_order = xr ? 1 : 0;
     pa.n_ext = cf.n_ext;
     pa.main_kc = use_qmoe ? 1 : 0;
     pa.num_sms = L->num_sms;
     pa.bn = cf.bn;
+    pa.proj_bn = cfp.bn;
     pa.nsplit_out = L->nsplit_d.as<int32_t>();
     pa.proj_mb = use_lotile ? static_cast<int>(L->proj_mb) : 0;
-    pa.proj_kc_total = cf.kc_total;
+    pa.proj_kc_total = cfp.kc_total;
     pa.proj_nsplit = pns;
     pa.perm = L->perm.as<int32_t>();
     pa.inv = L->inv.as<int32_t>();
     pa.offsets = L->offsets.as<int32_t>();
+    pa.poffsets = L->poffsets.as<int32_t>();
     pa.units = L->units.as<Unit>();
     pa.n_units = L->n_units.as<int32_t>();
     pa.proj_units = L->punits.as<Unit>();
@@ -1048,9 +1090,10 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     pa.err_flag = L->err_flag.as<int32_t>();
     cuda_check(launch_plan(pa, st), "plan_kernel launch");
     count_launch(L);
+    const int64_t atom_rows = rows_for(L, L->cap);   // capacity rows of xperm / extperm / ypart
     // projection pass: Z = P . x for every token (dense fp16 weights)
     if (use_lotile && L->proj_mb > 0) {
-        GemmParams p = base_params(L, cf, batch);
+        GemmParams p = base_params(L, cfp, batch);
         p.tmap_x64 = L->map_x16_64;
         p.tmap_e64 = L->map_x16_64;
         p.tmap_x16 = L->map_x16_16;
@@ -1072,7 +1115,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
         p.bits = kDenseBits;
         p.groups = 0;
         p.rank = 0;
-        const int64_t nunits = L->proj_mb * ((batch + cf.bn - 1) / cf.bn) * pns;
+        const int64_t nunits = L->proj_mb * ((batch + cfp.bn - 1) / cfp.bn) * pns;
         cuda_check(launch_gemm(p, static_cast<int>(std::min<int64_t>(nunits, L->num_sms)), st), "projection gemm launch");
         count_launch(L);
     }
@@ -1102,7 +1145,9 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ga.use_z = (use_lotile && L->proj_mb > 0) ? 1 : 0;
     ga.xp = L->xperm.as<__half>();
     ga.ep = L->extperm.as<__half>();
-    cuda_check(launch_gather(ga, static_cast<int>(rows_for(L, batch)), st), "gather_kernel launch");
+    ga.poffsets = L->poffsets.as<int32_t>();
+    ga.atom_rows = atom_rows;
+    cuda_check(launch_gather(ga, static_cast<int>(compact_rows(L, batch)), st), "gather_kernel launch");
     count_launch(L);
     // fused expert pass
     GemmParams p = base_params(L, cf, batch);
@@ -1114,6 +1159,10 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.x_ld = g.k_pad;
     p.e_ptr = L->extperm.as<__half>();
     p.e_ld = g.ext_cols;
+    p.x_atom_rows = atom_rows;
+    p.contig = xr ? 1 : 0;
+    p.e_slots = xr ? 1 : 2;
+    p.xr_slots = xr ? xr_slots(cf, ns_min) : 0;
     p.codes = L->codes.as<uint8_t>();
     p.weight_stride = L->weight_stride;
     p.scales = L->scales.as<__half>();
@@ -1140,6 +1189,8 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ca.inv = L->inv.as<int32_t>();
     ca.gates = gates;
     ca.offsets = L->offsets.as<int32_t>();
+    ca.ids = ids;
+    ca.poffsets = L->poffsets.as<int32_t>();
     ca.num_experts = static_cast<int>(g.K);
     ca.batch = static_cast<int>(batch);
     ca.top_k = static_cast<int>(g.top_k);
@@ -1516,7 +1567,7 @@ tq_status tq_ep_dispatch_rows(tq_layer* L, const float* x, int64_t batch, const 
         const bool use_qmoe = path != TQ_PATH_LOTILE;
         run_route(L, x, batch, false, st);
         const int pns = proj_nsplit(L, batch);
-        const LaunchCfg cf = cfg_for(L, batch);
+        const LaunchCfg cf = proj_cfg(L, batch);
         PlanArgs pa{};
         pa.ids = ids;
         pa.batch = static_cast<int>(batch);

@@ -22,7 +22,7 @@ for role in sorted(rows):
         name, slots = f"role{role}", ["s0", "s1", "s2", "s3"]
     if role >= 4 and name.startswith("role"):
         name = "dequant" if role < max(rows) - 3 else "epilogue"
-        slots = ["c_full/e_full", "empty", "dq+st", "wait_st"] if name == "dequant" else ["d_full", "-", "-", "-"]
+        slots = ["issue_x", "c_full+lds", "dq+st", "empty"] if name == "dequant" else ["d_full", "-", "-", "-"]
     tot = r[:, 0].mean()
     parts = " ".join(f"{s}={r[:, 2 + k].mean():9.0f} ({r[:, 2 + k].mean() / tot * 100:4.1f}%)" for k, s in enumerate(slots) if s != "-")
     print(f"{name:9s} role={role:2d} n={len(r):4d} total={tot:9.0f}  {parts}")

@@ -163,14 +163,22 @@ def measured_peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
-def traffic_from_profiles(workload: str):
+def traffic_from_profiles(workload: str, batches):
     """dram__bytes_read+write per launch of the fused GEMM from the committed
-    ncu --set full capture (profiles/gemm_traffic.json), or None."""
+    ncu --set full captures (profiles/gemm_traffic.json): the mean over the
+    workload's batch sizes when every one was captured, else the captured
+    sizes by batch (with the source), else None."""
     try:
         with open(os.path.join(REPO, "profiles", "gemm_traffic.json")) as f:
-            return json.load(f).get(workload)
+            ent = json.load(f).get(workload)
     except (OSError, ValueError):
         return None
+    if not ent:
+        return None
+    per = ent.get("per_batch_bytes", {})
+    if all(str(b) in per for b in batches):
+        return float(np.mean([per[str(b)] for b in batches]))
+    return {"per_batch_bytes": per, "source": ent.get("source")}
 
 
 # ---------------------------------------------------------------------------
@@ -357,15 +365,21 @@ def bench_tileq(args, rank, world, local_rank):
         torch.cuda.synchronize()
         settle += 1
     barrier()
-    L.gemm_timing(True)
     L.reset_launch_count()
     barrier()
-    all_evs = [one_step(True) for _ in range(args.steps)]
+    all_evs = [one_step(True) for _ in range(args.steps)]   # the measurement (CUDA-graph replays)
     barrier()
     launches = L.launch_count()
+    clk = clocks.stop() if clocks else None
+    # second pass over the same steps with the GEMM bracketed by events (graphs
+    # off for this pass only): the dominant kernel's device time for the roofline
+    L.gemm_timing(True)
+    for _ in range(args.steps):
+        one_step(False)
+    torch.cuda.synchronize()
     gemm_ms, gemm_n = L.gemm_time()
     L.gemm_timing(False)
-    clk = clocks.stop() if clocks else None
+    gemm_passes = args.steps
     per_b_ms = np.zeros(len(batches))
     for evs in all_evs:
         for j, (a, b) in enumerate(evs):
@@ -386,26 +400,26 @@ def bench_tileq(args, rank, world, local_rank):
         return 0
     hbm, tf_burst, tf_sust, peak_kind = measured_peaks()
     # dominant kernel = the fused expert GEMM (one launch per forward)
-    launches_per_fwd = gemm_n / max(1, args.steps * len(batches))
+    launches_per_fwd = gemm_n / max(1, gemm_passes * len(batches))
     gemm_avg_ms = gemm_ms / max(gemm_n, 1)
     if args.workload == "decode":
         algo = float(np.mean(gemm_bytes)) if world == 1 else None
         achieved = (algo / (gemm_avg_ms * 1e-3) / 1e9) if algo else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None, "traffic": traffic_from_profiles("decode"),
+                "frac": (achieved / hbm) if achieved else None, "traffic": traffic_from_profiles("decode", batches),
                 "kernel": "tq_gemm (fused dequant + low-rank tcgen05 expert GEMM)",
                 "algorithmic_bytes_per_launch": algo, "avg_launch_ms": gemm_avg_ms,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
-                "share_of_step": gemm_ms / total_ms if total_ms else None}
+                "share_of_step": (gemm_ms / gemm_passes) / ms_per_step if ms_per_step else None}
     else:
         fl = geo.flops(PREFILL_BATCH)
         achieved = fl / (gemm_avg_ms * 1e-3) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
-                "frac": achieved / tf_burst, "traffic": traffic_from_profiles("prefill"),
+                "frac": achieved / tf_burst, "traffic": traffic_from_profiles("prefill", batches),
                 "kernel": "tq_gemm (fused dequant + low-rank tcgen05 expert GEMM)",
                 "algorithmic_flops_per_launch": fl, "avg_launch_ms": gemm_avg_ms,
                 "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst cuBLAS)",
-                "share_of_step": gemm_ms / total_ms if total_ms else None}
+                "share_of_step": (gemm_ms / gemm_passes) / ms_per_step if ms_per_step else None}
     per_b = {str(B): {"us": per_b_ms[j] / args.steps * 1e3,
                       "tokens_per_s": B / (per_b_ms[j] / args.steps * 1e-3),
                       "layer_bytes": layer_bytes[j],

@@ -89,6 +89,7 @@ struct PlanArgs {
     int mb_count;              // m-blocks of the expert weights
     int kc_total, nsplit, n_ext;   // nsplit: upper bound; the kernel picks the best <= nsplit
     int nsplit_min;            // lower bound (resident activation tiles must fit shared memory)
+    float split_cost;          // extra output traffic of one more split, relative to the weight bytes
     int run_order;             // 1: units ordered (expert, tile, split, m-block): runs of m-blocks
     int proj_bn;               // token tile of the projection pass (0: bn)
     int main_kc;               // 1: main chunks present (0 for the lotile-only path)

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
             const long units = base * ns;
             const long rounds = (units + a.num_sms - 1) / a.num_sms;
             const float eff = rounds > 0 ? static_cast<float>(units) / static_cast<float>(rounds * a.num_sms) : 1.0f;
-            const float score = eff - 0.01f * ns;
+            const float score = eff - (a.split_cost + 0.002f) * (ns - lo_ns);
             if (score > best_score + 1e-6f) {
                 best_score = score;
                 best = ns;

@@ -1069,6 +1069,15 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     pa.kc_total = cf.kc_total;
     pa.nsplit = nsplit;
     pa.nsplit_min = ns_min;
+    {
+        // one more K split writes (and the combine re-reads) another f32 partial of every
+        // routed row; weigh it against the residual payload the GEMM must stream anyway
+        const int64_t local = L->e_end - L->e_begin;
+        const double active = static_cast<double>(std::min<int64_t>(local, batch * g.top_k) + g.S);
+        const double wbytes = active * static_cast<double>(g.o) * static_cast<double>(g.i) * g.bits / 8.0;
+        const double obytes = static_cast<double>(compact_rows(L, batch)) * static_cast<double>(g.o) * 8.0;
+        pa.split_cost = static_cast<float>(obytes / std::max(1.0, wbytes));
+    }
     pa.run_order = xr ? 1 : 0;
     pa.n_ext = cf.n_ext;
     pa.main_kc = use_qmoe ? 1 : 0;
@@ -1425,11 +1434,29 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
         if (batch == 0) return;
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = nullptr;
-        cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, st), "x H2D");
-        run_route(L, L->xin.as<float>(), batch, true, st);
-        run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(), L->yout.as<float>(), path,
-                    st);
-        cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, st), "y D2H");
+        auto body = [&](cudaStream_t s2) {
+            cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, s2), "x H2D");
+            run_route(L, L->xin.as<float>(), batch, true, s2);
+            run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(), L->yout.as<float>(),
+                        path, s2);
+            cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, s2),
+                       "y D2H");
+        };
+        // page-locked host buffers: the copies and kernels replay as one CUDA graph
+        auto pinned = [](const void* ptr) {
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return at.type == cudaMemoryTypeHost;
+        };
+        if (pinned(x) && pinned(y)) {
+            const void* const key[6] = {x, y, nullptr, nullptr, nullptr, nullptr};
+            run_graphed(L, key, batch, path + 32, st, body);
+        } else {
+            body(st);
+        }
         std::vector<int32_t> hid;
         if (ids) {
             hid.resize(static_cast<size_t>(batch * L->g.top_k));

@@ -520,10 +520,17 @@ def main():
                 return 0
             world_ref = world
             return bench_reference(args, 0, world_ref)
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        # one rank per GPU over NCCL; TILEQ_DIST_BACKEND=gloo runs the same EP path
+        # with host-staged exchanges (lets several ranks share one GPU for testing)
+        backend = os.environ.get("TILEQ_DIST_BACKEND", "nccl")
+        dev_idx = local_rank % max(1, torch.cuda.device_count())
+        torch.cuda.set_device(dev_idx)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
         try:
-            return bench_tileq(args, rank, world, local_rank)
+            return bench_tileq(args, rank, world, dev_idx)
         finally:
             dist.destroy_process_group()
     if args.impl == "reference":

@@ -91,19 +91,29 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves host tensors only: stage device tensors through the host
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _a2a(self, out, inp, **kw):
+        if self.stage and inp.is_cuda:
+            o = out.cpu()
+            self.dist.all_to_all_single(o, inp.cpu(), group=self.group, **kw)
+            out.copy_(o)
+        else:
+            self.dist.all_to_all_single(out, inp, group=self.group, **kw)
 
     def all_to_all_counts(self, counts):
         """counts: torch int32 [W, E_max] (device of the backend) -> same shape."""
         import torch
         out = torch.empty_like(counts)
-        self.dist.all_to_all_single(out, counts.contiguous(), group=self.group)
+        self._a2a(out, counts.contiguous())
         return out
 
     def all_to_all_rows(self, send, send_rows, recv_rows):
         import torch
         recv = torch.empty((int(sum(recv_rows)),) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
-        self.dist.all_to_all_single(recv, send.contiguous(), output_split_sizes=[int(v) for v in recv_rows],
-                                    input_split_sizes=[int(v) for v in send_rows], group=self.group)
+        self._a2a(recv, send.contiguous(), output_split_sizes=[int(v) for v in recv_rows],
+                  input_split_sizes=[int(v) for v in send_rows])
         return recv
 
 

@@ -140,10 +140,6 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const int warp = wid < 4 * NG ? wid + 4                       // dequant -> logical 4..
                    : wid < kRoleBase ? wid - 4 * NG + kEpi0        // epilogue -> logical kEpi0..
                    : (wid == kRoleBase ? 2 : wid == kRoleBase + 1 ? 0 : wid == kRoleBase + 2 ? 3 : 1);
-    const int n_all = *p.n_units;
-    // unit range of this CTA: contiguous (runs of units share their activation
-    // tile) or strided over the persistent grid
-    const int n_units = p.contig ? static_cast<int>((static_cast<int64_t>(blockIdx.x) + 1) * n_all / gridDim.x) : n_all;
 #ifdef TQ_EXPERIMENT
     const int kDbg = p.debug;   // experiment builds: runtime skip flags (TQ_DEBUG)
 #else
@@ -185,6 +181,14 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // programmatic dependent launch: the prologue above overlapped the previous
+    // kernel; everything below reads its outputs
+    pdl_wait();
+    pdl_launch_dependents();
+    const int n_all = *p.n_units;
+    // unit range of this CTA: contiguous (runs of units share their activation
+    // tile) or strided over the persistent grid
+    const int n_units = p.contig ? static_cast<int>((static_cast<int64_t>(blockIdx.x) + 1) * n_all / gridDim.x) : n_all;
     const uint32_t tmem = hdr->tmem_base;
 #ifdef TQ_PROFILE
     long long prof[4] = {0, 0, 0, 0};
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     const int col0 = ext ? (c - nmain) * KC : (un.kc_begin + c) * KC;
                     const int natoms = ext ? min(kAtoms, p.n_ext64 - (c - nmain) * kAtoms) : kAtoms;
                     const __half* src = ext ? p.e_ptr : p.x_ptr;
-                    TQ_TIMED(1, mbar_wait(&hdr->x_empty[c], static_cast<uint32_t>((xm >> c) & 1u) ^ 1u));
+                    TQ_TIMED(1, mbar_wait_sleep(&hdr->x_empty[c], static_cast<uint32_t>((xm >> c) & 1u) ^ 1u));
                     xm ^= 1ull << c;
                     if (elect_one()) {
                         const uint32_t nrow = static_cast<uint32_t>((un.n_tok + 15) & ~15);
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 for (int c = 0; c < nmain; ++c) {
                     const int kc = un.kc_begin + c;
                     if (kXR && run_start) load_x(c);
-                    TQ_TIMED(0, mbar_wait(&hdr->c_empty[cs], cph ^ 1u));
+                    TQ_TIMED(0, mbar_wait_sleep(&hdr->c_empty[cs], cph ^ 1u));
                     uint8_t* st = smem + c_off + cs * kCStage;
                     const uint8_t* src = wbase + static_cast<int64_t>(kc) * kCBytes;
                     if (kDbg & 128) {
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 if (kXR && run_start)
                     for (int c = nmain; c < nmain + un.n_ext; ++c) load_x(c);
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
-                    TQ_TIMED(1, mbar_wait(&hdr->e_empty[es], eph ^ 1u));
+                    TQ_TIMED(1, mbar_wait_sleep(&hdr->e_empty[es], eph ^ 1u));
                     uint8_t* dst = smem + e_off + es * ext_bytes;
                     bulk_copy2_elect(&hdr->e_full[es], dst, p.ext_blocks + wm * ext_bytes, ext_bytes, dst, dst, 0u);
                     if (++es == p.e_slots) { es = 0; eph ^= 1u; }
@@ -491,9 +495,11 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     advance_x();
                 }
                 if (main_chunk) {
-                    // move the code-ring position to main chunk m_base + c
-                    for (int m = m_base + c; m_cur < m; ++m_cur)
-                        if (++cs == c_stages) { cs = 0; cph ^= 1u; }
+                    // move the code-ring position to main chunk m_base + c (at most one wrap:
+                    // consecutive own chunks are <= NG <= c_stages main chunks apart)
+                    cs += (m_base + c) - m_cur;
+                    m_cur = m_base + c;
+                    if (cs >= c_stages) { cs -= c_stages; cph ^= 1u; }
                 }
                 {
                     // registers: the packed words of the chunk (kSW x BITS) plus ONE
@@ -761,8 +767,7 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
             if (err != cudaSuccess) return;
             if (slot >= 0) cfg_smem[slot] = smem;
         }
-        kern<<<grid, threads, smem, stream>>>(p);
-        err = cudaGetLastError();
+        err = launch_maybe_pdl(kern, dim3(grid), dim3(threads), smem, stream, p);
     };
 #define TQ_GEMM_CASES(KCV, NGV, DNV, NIV)                                                                 \
     switch (p.bits) {                                                                              \

@@ -4,6 +4,8 @@
 
 #include <cstdint>
 #include <cuda.h>
+#include <cstdlib>
+#include <utility>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -153,5 +155,30 @@ struct DeviceBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
 };
+
+// Kernel launch with programmatic stream serialization (PDL): the kernel may
+// start while its predecessor drains; kernels call griddepcontrol.wait before
+// touching predecessor outputs.  Off by default (measured slower on the
+// decode sweep: the early-launched grids contend with their predecessors);
+// TQ_PDL=1 turns it on.
+inline bool pdl_enabled() {
+    static const bool on = std::getenv("TQ_PDL") && std::atoi(std::getenv("TQ_PDL")) == 1;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                                    Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace tqb

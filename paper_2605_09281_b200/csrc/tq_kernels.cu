@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
     __shared__ double pick_p[64];
     __shared__ unsigned s_und;
     __shared__ int s_last;
+    pdl_wait();
+    pdl_launch_dependents();
     const int b = blockIdx.x;
     const int k0 = blockIdx.y * kRouteExperts;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -250,6 +252,8 @@ constexpr int kPlanThreads = 1024;
 
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     extern __shared__ int32_t pl_smem[];
+    pdl_wait();
+    pdl_launch_dependents();
     const int K = a.num_experts;
     int32_t* cnt = pl_smem;                // [32][K]
     int32_t* tot = pl_smem + 32 * K;       // [K+1]
@@ -475,6 +479,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
 
 
 __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     const int n_slots = a.offsets[a.num_experts];
     const int rows = n_slots + (a.with_shared ? a.batch : 0);
     const int row = blockIdx.x;
@@ -533,6 +539,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
 
 
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
+    pdl_wait();
+    pdl_launch_dependents();
     // 4 consecutive output columns per thread (float4 when out_dim % 4 == 0)
     const int b = blockIdx.y;
     const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -675,9 +683,8 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     if (batch <= 0) return cudaSuccess;
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
     const dim3 grid(batch, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
-    route_kernel<<<grid, kRouteThreads, 0, stream>>>(x, batch, in_dim, gate, num_experts, top_k, group_size, groups,
-                                                     k_pad, ids, gates, x16, sx, score_ws, ticket);
-    return cudaGetLastError();
+    return launch_maybe_pdl(route_kernel, grid, dim3(kRouteThreads), 0, stream, x, batch, in_dim, gate, num_experts,
+                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
@@ -687,20 +694,17 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
-    plan_kernel<<<1, kPlanThreads, smem, stream>>>(a);
-    return cudaGetLastError();
+    return launch_maybe_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), smem, stream, a);
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream) {
     if (max_rows <= 0) return cudaSuccess;
-    gather_kernel<<<max_rows, 256, 0, stream>>>(a);
-    return cudaGetLastError();
+    return launch_maybe_pdl(gather_kernel, dim3(max_rows), dim3(256), 0, stream, a);
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
     dim3 grid((a.out_dim + 1023) / 1024, a.batch);
-    combine_kernel<<<grid, 256, 0, stream>>>(a);
-    return cudaGetLastError();
+    return launch_maybe_pdl(combine_kernel, grid, dim3(256), 0, stream, a);
 }
 
 cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,

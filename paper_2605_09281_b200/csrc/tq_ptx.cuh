@@ -114,6 +114,10 @@ static __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap*
         : "memory");
 }
 
+// programmatic dependent launch (PDL)
+static __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+static __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // true in exactly one lane of a converged warp
 static __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;

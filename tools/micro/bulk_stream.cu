@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include "../../paper_2605_09281_b200/csrc/tq_ptx.cuh"
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void minit(uint64_t* b, uint32_t c) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c)); }
@@ -16,7 +17,7 @@ __device__ __forceinline__ void bulk(void* d, const void* s, uint32_t n, uint64_
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(d)), "l"(s), "r"(n), "r"(su32(b)) : "memory");
 }
 
-__global__ void __launch_bounds__(256, 1) stream_kernel(const uint8_t* src, size_t per_cta, int stage, int nst, unsigned long long* sink) {
+__global__ void __launch_bounds__(256, 1) stream_kernel(const uint8_t* src, size_t per_cta, int stage, int nst, unsigned long long* sink, int split) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + nst * stage);
   uint64_t* empty = full + 32;
@@ -28,13 +29,27 @@ __global__ void __launch_bounds__(256, 1) stream_kernel(const uint8_t* src, size
   const uint8_t* base = src + blockIdx.x * per_cta;
   const int nchunks = (int)(per_cta / stage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 0) {
+  if (warp == 0 && split == 2) {
+    // the engine's producer: converged warp, elect.sync, codes + scale slice in one asm
+    int s = 0; uint32_t ph = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      mwait(&empty[s], ph ^ 1);
+      tqb::bulk_copy2_elect(&full[s], sm + s * stage, base + (size_t)c * stage, stage - 256,
+                            sm + s * stage + stage - 256, base + (size_t)c * stage + stage - 256, 256u);
+      if (++s == nst) { s = 0; ph ^= 1; }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       int s = 0; uint32_t ph = 0;
       for (int c = 0; c < nchunks; ++c) {
         mwait(&empty[s], ph ^ 1);
         mexpect(&full[s], stage);
-        bulk(sm + s * stage, base + (size_t)c * stage, stage, &full[s]);
+        if (split) {
+          bulk(sm + s * stage, base + (size_t)c * stage, stage - 256, &full[s]);
+          bulk(sm + s * stage + stage - 256, base + (size_t)c * stage + stage - 256, 256, &full[s]);
+        } else {
+          bulk(sm + s * stage, base + (size_t)c * stage, stage, &full[s]);
+        }
         if (++s == nst) { s = 0; ph ^= 1; }
       }
     }
@@ -67,8 +82,10 @@ int main() {
   unsigned long long* sink; cudaMalloc(&sink, 8);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   const int grid = 148;
-  int stages[] = {2048, 4096, 8192, 16384, 32768};
-  int depths[] = {4, 8, 16, 24};
+  setvbuf(stdout, nullptr, _IONBF, 0);
+  int stages[] = {6912};
+  int depths[] = {8, 10};
+  for (int split = 0; split < 3; ++split)
   for (int st : stages) for (int nd : depths) {
     size_t smem = (size_t)st * nd + 1024;
     if (smem > 220 * 1024) continue;
@@ -76,11 +93,11 @@ int main() {
     size_t per = (total / grid) / st * st;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
-      stream_kernel<<<grid, 256, smem>>>(buf, per, st, nd, sink);
+      stream_kernel<<<grid, 256, smem>>>(buf, per, st, nd, sink, split);
       cudaEventRecord(b); cudaEventSynchronize(b);
     }
     float ms; cudaEventElapsedTime(&ms, a, b);
-    printf("bulk stage=%6d depth=%2d inflight=%4d KB  %7.1f GB/s  (%s)\n", st, nd, st * nd / 1024, per * grid / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+    printf("split=%d bulk stage=%6d depth=%2d inflight=%4d KB  %7.1f GB/s  (%s)\n", split, st, nd, st * nd / 1024, per * grid / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
   }
   for (int rep = 0; rep < 2; ++rep) {
     cudaEventRecord(a);

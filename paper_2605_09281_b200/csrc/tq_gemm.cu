@@ -96,7 +96,7 @@ template <int BITS, int KC, int NG, int DN, int NI>
 __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     constexpr int kAS = a_stages(KC, DN, NI);
-    static_assert(NI == 1 || NI == 2, "issuers");
+    static_assert(NI >= 1 && NI <= 3, "issuers");
     // decode configuration: the activation tile of a RUN of units (same expert,
     // token tile and K range; consecutive m-blocks) stays resident in shared
     // memory -- loaded once, chunk by chunk, by the code producer -- instead of
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 }
             }
         }
-    } else if (warp == 3) {
+    } else if (warp == 3 && NI < 3) {
         // ===================== activation producer (all 32 lanes) ==========
         if (kXR) {
         } else {
@@ -344,9 +344,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             }
         }
         }
-    } else if (warp == 1 || (NI == 2 && warp == 2)) {
+    } else if (warp == 1 || (NI >= 2 && warp == 2) || (NI >= 3 && warp == 3)) {
         // ===================== MMA issuers (converged warp, one elected lane issues) ==========
-        const int j = warp == 1 ? 0 : 1;
+        const int j = warp == 1 ? 0 : warp == 2 ? 1 : 2;   // logical 3 = the idle activation producer (kXR)
         int as = j, lu = 0, tcnt = 0;   // issuer j's chunks: CTA-wide index j, j+NI, ...
         uint32_t aph = 0;
         int xs = j;
@@ -645,25 +645,23 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * NI * DN;
             const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
             // issuer j took part iff the unit holds a chunk whose CTA-wide index is j mod NI
-            const bool part0 = NI == 1 ? nch > 0 : (nch >= 2 || (nch == 1 && (q_base_e & 1) == 0));
-            const bool part1 = NI == 2 && (nch >= 2 || (nch == 1 && (q_base_e & 1) == 1));
+            // issuer j took part iff the unit holds a chunk whose CTA-wide index is j mod NI
+            bool part[NI];
+#pragma unroll
+            for (int jj = 0; jj < NI; ++jj) part[jj] = nch >= NI || ((jj - q_base_e % NI + NI) % NI) < nch;
             q_base_e += nch;
             for (int t0 = 0; t0 < un.n_tok; t0 += 16) {
                 uint32_t v[16];
-                if (part0) tc_ld_32x32b_x16(dbase + t0, v);
-                if (part1) {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) v[k] = 0u;
+#pragma unroll
+                for (int jj = 0; jj < NI; ++jj) {   // fixed order: deterministic sum of the partials
+                    if (!part[jj]) continue;
                     uint32_t w[16];
-                    tc_ld_32x32b_x16(dbase + DN + t0, w);
+                    tc_ld_32x32b_x16(dbase + jj * DN + t0, w);
                     tc_wait_ld();
 #pragma unroll
-                    for (int k = 0; k < 16; ++k)
-                        v[k] = part0 ? __float_as_uint(__uint_as_float(v[k]) + __uint_as_float(w[k])) : w[k];
-                } else {
-                    tc_wait_ld();
-                    if (!part0) {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) v[k] = 0u;
-                    }
+                    for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) + __uint_as_float(w[k]));
                 }
                 if (valid && !(kDbg & 4)) {
 #pragma unroll

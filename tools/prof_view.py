@@ -2,7 +2,7 @@
 import sys
 import numpy as np
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 32, 8).astype(np.int64)
-NAMES = {0: ("code", ["c_empty", "e_empty", "-", "-"]), 3: ("xprod", ["x_empty", "-", "-", "-"]),
+NAMES = {0: ("code", ["c_empty", "e_empty", "-", "-"]), 3: ("mma2/xprod", ["full/x_empty", "d_empty", "chunks(n)", "x_full"]),
          1: ("mma", ["full", "d_empty", "chunks(n)", "x_full"]), 2: ("mma1", ["full", "d_empty", "chunks(n)", "x_full"])}
 rows = {}
 for cta in range(a.shape[0]):

@@ -50,7 +50,7 @@ namespace tqb {
 // gate loads up front (one memory round trip), the 4 (sum, sum|p|) pairs meet
 // in shared memory in a fixed order; the last slice CTA of a token (atomic
 // ticket) runs the softmax / top-k over the token's certified scores.
-constexpr int kRouteThreads = 1024;
+constexpr int kRouteThreads = 512;
 constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kRouteExperts = 4;      // experts per CTA
 constexpr int kRouteCols = 4;         // columns per thread per pass (i <= 4096 in one pass)
@@ -97,59 +97,122 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
         s_und = 0u;
         replay_acc = 0.0;
     }
-    // ---- partial dot products: all loads of a pass issued before any math ----
-    double s[kRouteExperts], a[kRouteExperts];
+    // ---- dot products with the partial sums of the reference's order ----
+    // Thread t owns columns [4t, 4t+4) of each 4096-column pass, so thread
+    // order is index order: a block scan gives every partial sum S_k of the
+    // reference's sequential loop.  Its rounding error is bounded by
+    // u * sum_k |S_k| (first order) -- far tighter than gamma_n * sum|p| when
+    // the partial sums stay small -- so certification rarely fails.
+    constexpr int kPass = kRouteThreads * 4;
+    double tot_s[kRouteExperts], abs_s[kRouteExperts], abs_p[kRouteExperts];
 #pragma unroll
-    for (int j = 0; j < kRouteExperts; ++j) s[j] = a[j] = 0.0;
-    for (int c0 = 0; c0 < in_dim; c0 += kRouteThreads * kRouteCols) {
-        float xv[kRouteCols], gv[kRouteExperts][kRouteCols];
-#pragma unroll
-        for (int m = 0; m < kRouteCols; ++m) {
-            const int c = c0 + threadIdx.x + m * kRouteThreads;
-            xv[m] = c < in_dim ? xb[c] : 0.0f;
-#pragma unroll
-            for (int j = 0; j < kRouteExperts; ++j)
-                gv[j][m] = (c < in_dim && k0 + j < num_experts) ? __ldg(gate + static_cast<int64_t>(k0 + j) * in_dim + c)
-                                                                : 0.0f;
-        }
-#pragma unroll
-        for (int m = 0; m < kRouteCols; ++m) {
-            const double xd = static_cast<double>(xv[m]);
+    for (int j = 0; j < kRouteExperts; ++j) tot_s[j] = abs_s[j] = abs_p[j] = 0.0;
+    const bool vec = (in_dim & 3) == 0;
+    for (int c0 = 0; c0 < in_dim; c0 += kPass) {
+        const int cb = c0 + 4 * threadIdx.x;
+        float xv[4], gv[kRouteExperts][4];
+        if (vec && cb + 3 < in_dim) {
+            const float4 x4 = *reinterpret_cast<const float4*>(xb + cb);
+            xv[0] = x4.x; xv[1] = x4.y; xv[2] = x4.z; xv[3] = x4.w;
 #pragma unroll
             for (int j = 0; j < kRouteExperts; ++j) {
-                const double pr = xd * static_cast<double>(gv[j][m]);
-                s[j] += pr;
-                a[j] += fabs(pr);
+                float4 g4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (k0 + j < num_experts) g4 = __ldg(reinterpret_cast<const float4*>(gate + static_cast<int64_t>(k0 + j) * in_dim + cb));
+                gv[j][0] = g4.x; gv[j][1] = g4.y; gv[j][2] = g4.z; gv[j][3] = g4.w;
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int c = cb + m;
+                xv[m] = c < in_dim ? xb[c] : 0.0f;
+#pragma unroll
+                for (int j = 0; j < kRouteExperts; ++j)
+                    gv[j][m] = (c < in_dim && k0 + j < num_experts) ? __ldg(gate + static_cast<int64_t>(k0 + j) * in_dim + c) : 0.0f;
             }
         }
+        // exact products, in-thread inclusive prefix
+        double pre[kRouteExperts][4];
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) {
+            double run = 0.0;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const double pr = static_cast<double>(xv[m]) * static_cast<double>(gv[j][m]);
+                abs_p[j] += fabs(pr);
+                run += pr;
+                pre[j][m] = run;
+            }
+        }
+        // block exclusive scan of the thread totals (thread order = column order)
+        double incl[kRouteExperts];
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) {
+            double v = pre[j][3];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const double o = __shfl_up_sync(0xffffffffu, v, off);
+                if (lane >= off) v += o;
+            }
+            incl[j] = v;
+            if (lane == 31) part[warp][j][0] = v;
+        }
+        __syncthreads();
+        if (warp == 0) {
+#pragma unroll
+            for (int j = 0; j < kRouteExperts; ++j) {
+                double v = lane < kRouteWarps ? part[lane][j][0] : 0.0;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const double o = __shfl_up_sync(0xffffffffu, v, off);
+                    if (lane >= off) v += o;
+                }
+                if (lane < kRouteWarps) part[lane][j][1] = v;   // inclusive scan of the warp totals
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) {
+            const double base = tot_s[j] + (warp > 0 ? part[warp - 1][j][1] : 0.0) + (incl[j] - pre[j][3]);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) abs_s[j] += fabs(base + pre[j][m]);
+            tot_s[j] += part[kRouteWarps - 1][j][1];
+        }
+        __syncthreads();   // part[] is reused by the next pass / the reduction below
     }
+    // block sums of sum_k |S_k| and sum |p|; the total is the scan's last value
 #pragma unroll
     for (int j = 0; j < kRouteExperts; ++j) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            s[j] += __shfl_xor_sync(0xffffffffu, s[j], off);
-            a[j] += __shfl_xor_sync(0xffffffffu, a[j], off);
+            abs_s[j] += __shfl_xor_sync(0xffffffffu, abs_s[j], off);
+            abs_p[j] += __shfl_xor_sync(0xffffffffu, abs_p[j], off);
         }
     }
     if (lane == 0) {
 #pragma unroll
         for (int j = 0; j < kRouteExperts; ++j) {
-            part[warp][j][0] = s[j];
-            part[warp][j][1] = a[j];
+            part[warp][j][0] = abs_s[j];
+            part[warp][j][1] = abs_p[j];
         }
     }
     __syncthreads();
     // ---- certification (thread j: expert k0 + j) ----
     if (threadIdx.x < kRouteExperts && k0 + static_cast<int>(threadIdx.x) < num_experts) {
         const int j = threadIdx.x;
-        double sv = 0.0, av = 0.0;
+        double as = 0.0, ap = 0.0;
         for (int w = 0; w < kRouteWarps; ++w) {
-            sv += part[w][j][0];
-            av += part[w][j][1];
+            as += part[w][j][0];
+            ap += part[w][j][1];
         }
+        const double sv = tot_s[j];
         const double u = 1.1102230246251565e-16;  // 2^-53
-        const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 8.0 + kRouteWarps);
-        const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
+        const double n = static_cast<double>(in_dim);
+        // reference: |seq - exact| <= u * sum|S_k| (+ second order); ours: <= 24 u sum|p|
+        // (each partial sum passes <= 4 + 5 + 5 + 2 additions per pass); the partial sums
+        // we used carry the same ours-error, n times: + n * 24 u^2 sum|p|
+        const double err_ref = __dmul_ru(__dmul_ru(u, 1.02), __dadd_ru(as, __dmul_ru(n * 48.0 * u, ap)));
+        const double err_our = __dmul_ru(__dmul_ru(24.0 * u * (1.0 + n / 4096.0), 1.02), ap);
+        const double err = __dadd_ru(err_ref, err_our);
         const float lo = __double2float_rn(__dsub_rd(sv, err));
         const float hi = __double2float_rn(__dadd_ru(sv, err));
         score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(sv);

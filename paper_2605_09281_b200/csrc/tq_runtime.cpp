@@ -491,6 +491,34 @@ struct tq_layer {
     // expert-GEMM device timing (tq_gemm_timing_enable)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    // TQ_KTIME=1 (diagnostics): an event after every launch of a forward; the
+    // gaps between consecutive events (device time per kernel, launch gaps
+    // included) are accumulated and printed when the layer is freed
+    bool ktime = getenv("TQ_KTIME") && atoi(getenv("TQ_KTIME")) == 1;
+    std::vector<std::vector<cudaEvent_t>> kev;   // one group per forward
+    cudaStream_t kt_stream = nullptr;
+    bool kt_active = false;
+    void ktime_report() {
+        std::vector<double> sum;
+        int64_t n = 0;
+        for (auto& grp : kev) {
+            if (grp.size() < 2) continue;
+            cudaEventSynchronize(grp.back());
+            if (sum.size() < grp.size() - 1) sum.resize(grp.size() - 1, 0.0);
+            for (size_t t = 1; t < grp.size(); ++t) {
+                float ms = 0.0f;
+                cudaEventElapsedTime(&ms, grp[t - 1], grp[t]);
+                sum[t - 1] += ms;
+            }
+            ++n;
+        }
+        for (size_t t = 0; t < sum.size() && n > 0; ++t)
+            fprintf(stderr, "ktime launch %zu: %.2f us (mean of %lld forwards)\n", t, sum[t] / n * 1e3,
+                    static_cast<long long>(n));
+        for (auto& grp : kev)
+            for (auto e : grp) cudaEventDestroy(e);
+        kev.clear();
+    }
     // CUDA graphs of whole forwards, keyed by their arguments: one launch per
     // forward instead of six, no host work between the kernels
     struct GraphEntry {
@@ -514,6 +542,7 @@ struct tq_layer {
         }
         drop_graphs();
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (ktime) ktime_report();
     }
 };
 
@@ -1013,10 +1042,26 @@ LaunchCfg cfg64(const tq_layer* L) {
     return c;
 }
 
-void count_launch(tq_layer* L, int n = 1) { L->launches += static_cast<uint64_t>(n); }
+void count_launch(tq_layer* L, int n = 1) {
+    L->launches += static_cast<uint64_t>(n);
+    if (L->ktime && L->kt_active && !L->kev.empty()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, L->kt_stream);
+        L->kev.back().push_back(e);
+    }
+}
 
 // prep (x16, sx) and optional routing
 void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st) {
+    if (L->ktime) {
+        L->kt_stream = st;
+        L->kt_active = true;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        L->kev.push_back({e});
+    }
     cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(L->g.i), L->gate.as<float>(),
                             do_route ? static_cast<int>(L->g.K) : 0, static_cast<int>(L->g.top_k),
                             static_cast<int>(L->g.gs), static_cast<int>(L->g.G), static_cast<int>(L->g.k_pad),
@@ -1240,7 +1285,7 @@ namespace {
 // then replayed on the caller's stream with one cudaGraphLaunch.
 template <class Body>
 void run_graphed(tq_layer* L, const void* const (&key)[6], int64_t batch, int path, cudaStream_t st, Body body) {
-    if (!L->use_graphs || L->timing) {
+    if (!L->use_graphs || L->timing || L->ktime) {
         body(st);
         return;
     }

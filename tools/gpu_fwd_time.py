@@ -25,3 +25,4 @@ for B in Bs:
     tot += ms
     print(f"graphs={os.environ.get('TQ_GRAPHS', '1')} {name} B={B}: forward {ms * 1e3:.1f} us", flush=True)
 print(f"sweep total {tot * 1e3:.1f} us -> {sum(Bs) / tot * 1e3:.0f} tok/s")
+L.close()

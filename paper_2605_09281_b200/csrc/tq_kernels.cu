@@ -61,7 +61,8 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
                                                              int top_k, int group_size, int groups, int k_pad,
                                                              int32_t* __restrict__ ids, float* __restrict__ gates,
                                                              __half* __restrict__ x16, float* __restrict__ sx,
-                                                             float* __restrict__ score_ws, int32_t* __restrict__ ticket) {
+                                                             float* __restrict__ score_ws, int32_t* __restrict__ ticket,
+                                                             int tokens_per_cta) {
     __shared__ double part[kRouteWarps][kRouteExperts][2];
     __shared__ double prod[kReplayWin];
     __shared__ double replay_acc;
@@ -73,9 +74,12 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
     __shared__ int s_last;
     pdl_wait();
     pdl_launch_dependents();
-    const int b = blockIdx.x;
     const int k0 = blockIdx.y * kRouteExperts;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // prefill: several tokens per CTA, the CTA's gate slice is re-read from L1
+    for (int tb = 0; tb < tokens_per_cta; ++tb) {
+    const int b = blockIdx.x * tokens_per_cta + tb;
+    if (b >= batch) break;
     const float* xb = x + static_cast<int64_t>(b) * in_dim;
     if (blockIdx.y == 0) {
         // fp16 activations (zero-padded to k_pad) and per-group sums of them
@@ -92,25 +96,22 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
             if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
         }
     }
-    if (num_experts == 0) return;  // activations-only prep (tq_forward with given routing)
+    if (num_experts == 0) continue;  // activations-only prep (tq_forward with given routing)
+    __syncthreads();   // shared state of the previous token is consumed
     if (threadIdx.x == 0) {
         s_und = 0u;
         replay_acc = 0.0;
     }
-    // ---- dot products with the partial sums of the reference's order ----
-    // Thread t owns columns [4t, 4t+4) of each 4096-column pass, so thread
-    // order is index order: a block scan gives every partial sum S_k of the
-    // reference's sequential loop.  Its rounding error is bounded by
-    // u * sum_k |S_k| (first order) -- far tighter than gamma_n * sum|p| when
-    // the partial sums stay small -- so certification rarely fails.
+    __syncthreads();
+    // ---- tier 1: plain parallel dot products, loose bound ----------------
+    // any summation order of the i exact products is within
+    // gamma_{i-1} * sum|p| of the exact sum, as is the reference's sequential
+    // loop: certify against 2 * gamma_{i+i/32+40} * sum|p| (fails for ~1e-3 of
+    // the scores).  Tier 2 (below) only runs for a CTA with an undecided score.
     constexpr int kPass = kRouteThreads * 4;
-    double tot_s[kRouteExperts], abs_s[kRouteExperts], abs_p[kRouteExperts];
-#pragma unroll
-    for (int j = 0; j < kRouteExperts; ++j) tot_s[j] = abs_s[j] = abs_p[j] = 0.0;
     const bool vec = (in_dim & 3) == 0;
-    for (int c0 = 0; c0 < in_dim; c0 += kPass) {
+    auto load_pass = [&](int c0, float (&xv)[4], float (&gv)[kRouteExperts][4]) {
         const int cb = c0 + 4 * threadIdx.x;
-        float xv[4], gv[kRouteExperts][4];
         if (vec && cb + 3 < in_dim) {
             const float4 x4 = *reinterpret_cast<const float4*>(xb + cb);
             xv[0] = x4.x; xv[1] = x4.y; xv[2] = x4.z; xv[3] = x4.w;
@@ -130,6 +131,71 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
                     gv[j][m] = (c < in_dim && k0 + j < num_experts) ? __ldg(gate + static_cast<int64_t>(k0 + j) * in_dim + c) : 0.0f;
             }
         }
+    };
+    {
+        double sum1[kRouteExperts], abs1[kRouteExperts];
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) sum1[j] = abs1[j] = 0.0;
+        for (int c0 = 0; c0 < in_dim; c0 += kPass) {
+            float xv[4], gv[kRouteExperts][4];
+            load_pass(c0, xv, gv);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int j = 0; j < kRouteExperts; ++j) {
+                    const double pr = static_cast<double>(xv[m]) * static_cast<double>(gv[j][m]);
+                    sum1[j] += pr;
+                    abs1[j] += fabs(pr);
+                }
+        }
+#pragma unroll
+        for (int j = 0; j < kRouteExperts; ++j) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                sum1[j] += __shfl_xor_sync(0xffffffffu, sum1[j], off);
+                abs1[j] += __shfl_xor_sync(0xffffffffu, abs1[j], off);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < kRouteExperts; ++j) {
+                part[warp][j][0] = sum1[j];
+                part[warp][j][1] = abs1[j];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < kRouteExperts && k0 + static_cast<int>(threadIdx.x) < num_experts) {
+            const int j = threadIdx.x;
+            double sv = 0.0, av = 0.0;
+            for (int w = 0; w < kRouteWarps; ++w) {
+                sv += part[w][j][0];
+                av += part[w][j][1];
+            }
+            const double u = 1.1102230246251565e-16;  // 2^-53
+            const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 40.0);
+            const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
+            const float lo = __double2float_rn(__dsub_rd(sv, err));
+            const float hi = __double2float_rn(__dadd_ru(sv, err));
+            score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(sv);
+            if (lo != hi) atomicOr(&s_und, 1u << j);
+        }
+        __syncthreads();
+    }
+    if (s_und != 0u) {   // block-uniform
+    if (threadIdx.x == 0) s_und = 0u;
+    __syncthreads();
+    // ---- tier 2: the partial sums of the reference's order ----
+    // Thread t owns columns [4t, 4t+4) of each pass, so thread order is index
+    // order: a block scan gives every partial sum S_k of the reference's
+    // sequential loop, whose rounding error is bounded by u * sum_k |S_k|
+    // (first order) -- far tighter than gamma_n * sum|p| when the partial sums
+    // stay small.  Tier 3 (exact sequential replay) is then very rare.
+    double tot_s[kRouteExperts], abs_s[kRouteExperts], abs_p[kRouteExperts];
+#pragma unroll
+    for (int j = 0; j < kRouteExperts; ++j) tot_s[j] = abs_s[j] = abs_p[j] = 0.0;
+    for (int c0 = 0; c0 < in_dim; c0 += kPass) {
+        float xv[4], gv[kRouteExperts][4];
+        load_pass(c0, xv, gv);
         // exact products, in-thread inclusive prefix
         double pre[kRouteExperts][4];
 #pragma unroll
@@ -219,6 +285,7 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
         if (lo != hi) atomicOr(&s_und, 1u << j);
     }
     __syncthreads();
+    }   // tier 2
     // replay: the reference's exact sequential loop (matrix.cpp:29-34).  The
     // CTA forms the (exact) products in shared memory, then one thread adds
     // them in index order -- a dependent f64 chain, loads hoisted ahead
@@ -258,7 +325,7 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
         if (s_last) ticket[b] = 0;   // ready for the next launch
     }
     __syncthreads();
-    if (!s_last || warp != 0) return;
+    if (s_last && warp == 0) {
     __threadfence();
     for (int k = lane; k < num_experts; k += 32) sc[k] = __ldcg(score_ws + static_cast<int64_t>(b) * num_experts + k);
     __syncwarp();
@@ -304,6 +371,8 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
         ids[static_cast<int64_t>(b) * top_k + tt] = pick_k[tt];
         gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pick_p[tt], selected));
     }
+    }   // last slice CTA of token b
+    }   // tokens of this CTA
 }
 
 // =============================================================================
@@ -745,9 +814,10 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
                          float* score_ws, int32_t* ticket, cudaStream_t stream) {
     if (batch <= 0) return cudaSuccess;
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
-    const dim3 grid(batch, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
+    const int tpc = batch <= 2 * 148 ? 1 : (batch + 2 * 148 - 1) / (2 * 148);
+    const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
     return launch_maybe_pdl(route_kernel, grid, dim3(kRouteThreads), 0, stream, x, batch, in_dim, gate, num_experts,
-                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket);
+                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {

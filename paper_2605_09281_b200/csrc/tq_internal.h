@@ -46,6 +46,18 @@ struct GemmParams {
     int64_t x_ld;
     const __half* e_ptr;
     int64_t e_ld;
+    // combine fused into the epilogue (top_k <= 2, no shared experts, one K split):
+    // y[b, row] += gate * expert row with red.global.add -- at most two addends per
+    // element onto a zeroed output, so the sum is order independent (deterministic)
+    int32_t fuse_combine;
+    int32_t top_k;
+    int32_t e_begin;          // first resident routed expert (unit.weight is relative to it)
+    const int32_t* nsplit_dev; // split count chosen by the plan: fuse only when it is 1
+    const int32_t* perm;
+    const int32_t* offsets;
+    const int32_t* poffsets;
+    const float* gates;
+    float* y_out;             // [B][o]
     int32_t contig;         // 1: each CTA takes a contiguous unit range (runs share activation tiles)
     int32_t e_slots;        // extension-block ring depth (1 or 2)
     int32_t xr_slots;       // resident activation slots (decode config): max chunks per unit
@@ -147,6 +159,7 @@ struct CombineArgs {
     int sh_nsplit;
     int sh_from_offsets;     // 1: sh_row0 = offsets[num_experts] (single-GPU layout), 0: 0
     const int32_t* nsplit_dev;  // if set: split count of both routed and shared rows (chosen by plan)
+    int fused;                  // the expert GEMM already combined when *nsplit_dev == 1
     float* out;
 };
 

@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     pdl_wait();
     pdl_launch_dependents();
+    if (a.fused && *a.nsplit_dev == 1) return;   // the expert GEMM's epilogue combined already
     // 4 consecutive output columns per thread (float4 when out_dim % 4 == 0)
     const int b = blockIdx.y;
     const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;

@@ -1233,6 +1233,21 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.bits = g.bits;
     p.groups = static_cast<int32_t>(g.G);
     p.rank = static_cast<int32_t>(g.r);
+    // fused combine: at most two addends per output element (top_k <= 2, no shared experts)
+    // (opt-in: measured slower at prefill -- L2 reductions of scattered rows cost more than the combine pass)
+    const bool fuse = g.top_k <= 2 && !with_shared && getenv("TQ_FUSED_COMBINE") && atoi(getenv("TQ_FUSED_COMBINE")) == 1;
+    if (fuse) {
+        cuda_check(cudaMemsetAsync(y, 0, sizeof(float) * batch * g.o, st), "y memset");
+        p.fuse_combine = 1;
+        p.top_k = static_cast<int32_t>(g.top_k);
+        p.e_begin = static_cast<int32_t>(L->e_begin);
+        p.nsplit_dev = L->nsplit_d.as<int32_t>();
+        p.perm = L->perm.as<int32_t>();
+        p.offsets = L->offsets.as<int32_t>();
+        p.poffsets = L->poffsets.as<int32_t>();
+        p.gates = gates;
+        p.y_out = y;
+    }
     timed_expert_gemm(L, p, L->num_sms, st);
     count_launch(L);
     // combine
@@ -1256,6 +1271,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ca.sh_nsplit = nsplit;
     ca.sh_from_offsets = 1;
     ca.nsplit_dev = L->nsplit_d.as<int32_t>();
+    ca.fused = fuse ? 1 : 0;
     ca.out = y;
     cuda_check(launch_combine(ca, st), "combine_kernel launch");
     count_launch(L);

@@ -95,6 +95,11 @@ __device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx)
 template <int BITS, int KC, int NG, int DN, int NI>
 __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_constant__ GemmParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+#ifdef TQ_PROFILE
+    unsigned long long g_entry;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+    const long long c_entry = clock64();
+#endif
     constexpr int kAS = a_stages(KC, DN, NI);
     static_assert(NI >= 1 && NI <= 3, "issuers");
     // decode configuration: the activation tile of a RUN of units (same expert,
@@ -185,7 +190,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     // kernel; everything below reads its outputs
     pdl_wait();
     pdl_launch_dependents();
-    const int n_all = *p.n_units;
+    const int n_all = (kDbg & 256) ? 0 : *p.n_units;   // 256: prologue/epilogue only (fixed cost)
     // unit range of this CTA: contiguous (runs of units share their activation
     // tile) or strided over the persistent grid
     const int n_units = p.contig ? static_cast<int>((static_cast<int64_t>(blockIdx.x) + 1) * n_all / gridDim.x) : n_all;
@@ -193,6 +198,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
 #ifdef TQ_PROFILE
     long long prof[4] = {0, 0, 0, 0};
     const long long prof_t0 = clock64();
+    const long long prologue_cycles = prof_t0 - c_entry;
 #endif
     const int first = p.contig ? static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_all / gridDim.x) : blockIdx.x;
     const int stride = p.contig ? 1 : gridDim.x;
@@ -697,6 +703,8 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         o[0] = clock64() - prof_t0;
         o[1] = warp;
         for (int k = 0; k < 4; ++k) o[2 + k] = prof[k];
+        o[6] = prologue_cycles;
+        o[7] = g_entry;   // globaltimer (ns) at kernel entry of this warp
     }
 #endif
     tc_fence_before();

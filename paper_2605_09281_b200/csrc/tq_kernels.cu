@@ -810,6 +810,18 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 // launch wrappers (called from tq_runtime.cpp)
 // =============================================================================
 
+// All kernels of a forward run with the maximum shared-memory carveout, so
+// the SMs never reconfigure L1/shared memory between the small kernels and the
+// 226 KB expert GEMM (each reconfiguration drains the SM).
+template <typename K>
+static void max_carveout(K kern) {
+    static bool done = false;   // one static per kernel type
+    if (!done) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+        done = true;
+    }
+}
+
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
                          float* score_ws, int32_t* ticket, cudaStream_t stream) {
@@ -817,6 +829,7 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
     const int tpc = batch <= 2 * 148 ? 1 : (batch + 2 * 148 - 1) / (2 * 148);
     const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
+    max_carveout(route_kernel);
     return launch_maybe_pdl(route_kernel, grid, dim3(kRouteThreads), 0, stream, x, batch, in_dim, gate, num_experts,
                             top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc);
 }
@@ -828,16 +841,19 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
                                              static_cast<int>(smem));
         if (e != cudaSuccess) return e;
     }
+    max_carveout(plan_kernel);
     return launch_maybe_pdl(plan_kernel, dim3(1), dim3(kPlanThreads), smem, stream, a);
 }
 
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream) {
     if (max_rows <= 0) return cudaSuccess;
+    max_carveout(gather_kernel);
     return launch_maybe_pdl(gather_kernel, dim3(max_rows), dim3(256), 0, stream, a);
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
     dim3 grid((a.out_dim + 1023) / 1024, a.batch);
+    max_carveout(combine_kernel);
     return launch_maybe_pdl(combine_kernel, grid, dim3(256), 0, stream, a);
 }
 

@@ -40,6 +40,16 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         : "memory");
     return;
 #endif
+#ifdef TQ_WAIT_HINT
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "TQ_WAITH_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra TQ_WAITH_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(static_cast<uint32_t>(TQ_WAIT_HINT))
+        : "memory");
+    return;
+#endif
 #ifdef TQ_WAIT_BACKOFF
     uint32_t ok = 0;
     while (true) {

@@ -26,3 +26,8 @@ for role in sorted(rows):
     tot = r[:, 0].mean()
     parts = " ".join(f"{s}={r[:, 2 + k].mean():9.0f} ({r[:, 2 + k].mean() / tot * 100:4.1f}%)" for k, s in enumerate(slots) if s != "-")
     print(f"{name:9s} role={role:2d} n={len(r):4d} total={tot:9.0f}  {parts}")
+# prologue cycles and the spread of CTA start times (globaltimer, ns)
+pro = [int(a[c, w, 6]) for c in range(a.shape[0]) for w in range(32) if a[c, w, 0] > 0]
+ent = np.array([int(a[c, 0, 7]) for c in range(a.shape[0]) if a[c, 0, 0] > 0])
+if len(pro):
+    print(f"prologue cycles: mean {np.mean(pro):.0f} max {np.max(pro):.0f}; CTA entry spread {(ent.max() - ent.min()) / 1e3:.2f} us")

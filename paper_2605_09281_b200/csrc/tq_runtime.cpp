@@ -618,7 +618,11 @@ int xr_ns_min(const tq_layer* L, const LaunchCfg& cf, int64_t batch) {
     const int64_t tok = std::max<int64_t>(1, std::min<int64_t>(cf.bn, batch * L->g.top_k));
     const int64_t rows = (tok + 15) / 16 * 16;
     const int64_t slot = (cf.kc / 64) * rows * 128;
-    const int64_t max_slots = std::min<int64_t>(64, (140 * 1024) / slot);
+    // small tiles (B <= 8 per expert): keep the resident slots to ~40 KB so the code
+    // ring gets ~24 stages (>150 KB of HBM reads in flight per SM); the plan's split
+    // choice (several K splits at this size anyway) honours the bound
+    const int64_t budget = rows <= 16 ? 40 * 1024 : 140 * 1024;
+    const int64_t max_slots = std::min<int64_t>(64, budget / slot);
     const int64_t main_slots = std::max<int64_t>(1, max_slots - cf.n_ext);
     return static_cast<int>((cf.kc_total + main_slots - 1) / main_slots);
 }

@@ -2,7 +2,7 @@
 import sys
 import numpy as np
 a = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(-1, 32, 8).astype(np.int64)
-NAMES = {0: ("code", ["c_empty", "e_empty", "-", "-"]), 3: ("mma2/xprod", ["full/x_empty", "d_empty", "chunks(n)", "x_full"]),
+NAMES = {0: ("code", ["c_empty", "e_empty", "bulk_issue", "-"]), 3: ("mma2/xprod", ["full/x_empty", "d_empty", "chunks(n)", "x_full"]),
          1: ("mma", ["full", "d_empty", "chunks(n)", "x_full"]), 2: ("mma1", ["full", "d_empty", "chunks(n)", "x_full"])}
 rows = {}
 for cta in range(a.shape[0]):
@@ -22,7 +22,7 @@ for role in sorted(rows):
         name, slots = f"role{role}", ["s0", "s1", "s2", "s3"]
     if role >= 4 and name.startswith("role"):
         name = "dequant" if role < max(rows) - 3 else "epilogue"
-        slots = ["issue_x", "c_full+lds", "dq+st", "empty"] if name == "dequant" else ["d_full", "-", "-", "-"]
+        slots = ["wait_st+arrive", "c_full+lds", "dq+st", "empty"] if name == "dequant" else ["d_full", "-", "-", "-"]
     tot = r[:, 0].mean()
     parts = " ".join(f"{s}={r[:, 2 + k].mean():9.0f} ({r[:, 2 + k].mean() / tot * 100:4.1f}%)" for k, s in enumerate(slots) if s != "-")
     print(f"{name:9s} role={role:2d} n={len(r):4d} total={tot:9.0f}  {parts}")

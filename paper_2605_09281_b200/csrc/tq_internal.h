@@ -22,7 +22,7 @@ __host__ __device__ constexpr int code_block_bytes(int bits) { return kBM * kKC 
 
 // One work unit of the grouped tcgen05 GEMM: a 128-row m-block of one weight
 // matrix against up to kBNMax activation rows, over a K-chunk range.
-struct Unit {
+struct alignas(16) Unit {   // 16-byte aligned: written / read as two 128-bit words
     int32_t weight;    // weight matrix index (routed e, K+s for shared s, 0 for projection)
     int32_t mb;        // m-block (rows mb*128 ..)
     int32_t x_row;     // first activation row (X / Ext matrices)
@@ -141,6 +141,7 @@ struct GatherArgs {
     __half* ep;              // [rows][ext_cols], or atom-major
     const int32_t* poffsets; // if set: slot s of expert e goes to padded row s + poffsets[e] - offsets[e]
     int64_t atom_rows;       // > 0: atom-major, 128B-swizzled layout [cols/64][atom_rows][64] (bulk-copy tiles)
+    const int32_t* inv;      // token-major gather: slot of flat routing index f (-1: invalid id)
 };
 
 struct CombineArgs {

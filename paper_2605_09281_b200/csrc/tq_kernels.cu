@@ -50,6 +50,8 @@ namespace tqb {
 // gate loads up front (one memory round trip), the 4 (sum, sum|p|) pairs meet
 // in shared memory in a fixed order; the last slice CTA of a token (atomic
 // ticket) runs the softmax / top-k over the token's certified scores.
+__device__ void plan_body(const PlanArgs& a, int32_t* pl_smem);
+
 constexpr int kRouteThreads = 512;
 constexpr int kRouteWarps = kRouteThreads / 32;
 constexpr int kRouteExperts = 4;      // experts per CTA
@@ -62,7 +64,8 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
                                                              int32_t* __restrict__ ids, float* __restrict__ gates,
                                                              __half* __restrict__ x16, float* __restrict__ sx,
                                                              float* __restrict__ score_ws, int32_t* __restrict__ ticket,
-                                                             int tokens_per_cta) {
+                                                             int tokens_per_cta, const PlanArgs plan,
+                                                             int32_t* __restrict__ plan_ticket) {
     __shared__ double part[kRouteWarps][kRouteExperts][2];
     __shared__ double prod[kReplayWin];
     __shared__ double replay_acc;
@@ -373,6 +376,21 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
     }
     }   // last slice CTA of token b
     }   // tokens of this CTA
+    // ---- fused plan: the globally-last CTA permutes the finished routing ----
+    if (plan_ticket) {
+        __threadfence();   // this CTA's ids / gates
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int done = atomicAdd(plan_ticket, 1);
+            s_last = done == static_cast<int>(gridDim.x * gridDim.y) - 1;
+            if (s_last) *plan_ticket = 0;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            plan_body(plan, reinterpret_cast<int32_t*>(prod));   // (16 + 1) * K + 1 ints <= 16 KB
+        }
+    }
 }
 
 // =============================================================================
@@ -382,24 +400,25 @@ __global__ void __launch_bounds__(kRouteThreads) route_kernel(const float* __res
 
 constexpr int kPlanThreads = 1024;
 
-__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
-    extern __shared__ int32_t pl_smem[];
-    pdl_wait();
-    pdl_launch_dependents();
+// The plan on one CTA of any size (blockDim a multiple of 32, <= 1024 threads):
+// run by plan_kernel, or fused into the router's globally-last CTA.
+// pl_smem: (nwarps + 1) * K + 1 ints.
+__device__ void plan_body(const PlanArgs& a, int32_t* pl_smem) {
     const int K = a.num_experts;
-    int32_t* cnt = pl_smem;                // [32][K]
-    int32_t* tot = pl_smem + 32 * K;       // [K+1]
+    const int nwarps = blockDim.x >> 5;
+    int32_t* cnt = pl_smem;                // [nwarps][K]
+    int32_t* tot = pl_smem + nwarps * K;   // [K+1]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = a.batch * a.top_k;
-    for (int t = threadIdx.x; t < 32 * K; t += blockDim.x) cnt[t] = 0;
+    for (int t = threadIdx.x; t < nwarps * K; t += blockDim.x) cnt[t] = 0;
     __syncthreads();
-    const int per = (n + 31) / 32;
+    const int per = (n + nwarps - 1) / nwarps;
     const int f0 = warp * per, f1 = min(n, f0 + per);
     // phase 1: per-warp counts (warp-private rows, no atomics)
     for (int base = f0; base < f1; base += 32) {
         const int f = base + lane;
         const bool act = f < f1;
-        int id = act ? a.ids[f] : -1;
+        int id = act ? __ldcg(a.ids + f) : -1;
         if (act && (id < 0 || id >= K)) {
             atomicExch(a.err_flag, 1);
             id = -1;
@@ -412,7 +431,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     // phase 2: expert totals + exclusive offsets, per-warp bases
     if (threadIdx.x < K) {
         int s = 0;
-        for (int w = 0; w < 32; ++w) s += cnt[w * K + threadIdx.x];
+        for (int w = 0; w < nwarps; ++w) s += cnt[w * K + threadIdx.x];
         tot[threadIdx.x] = s;
     }
     __syncthreads();
@@ -436,7 +455,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     }
     if (threadIdx.x < K) {
         int run = tot[threadIdx.x];
-        for (int w = 0; w < 32; ++w) {
+        for (int w = 0; w < nwarps; ++w) {
             const int c = cnt[w * K + threadIdx.x];
             cnt[w * K + threadIdx.x] = run;
             run += c;
@@ -447,7 +466,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     for (int base = f0; base < f1; base += 32) {
         const int f = base + lane;
         const bool act = f < f1;
-        int id = act ? a.ids[f] : -1;
+        int id = act ? __ldcg(a.ids + f) : -1;
         if (id >= K || id < 0) {
             if (act) a.inv[f] = -1;
             id = -1;
@@ -605,6 +624,13 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
     }
 }
 
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(const PlanArgs a) {
+    extern __shared__ int32_t pl_smem[];
+    pdl_wait();
+    pdl_launch_dependents();
+    plan_body(a, pl_smem);
+}
+
 // =============================================================================
 // gather: permuted fp16 activation rows + extension rows
 // =============================================================================
@@ -670,6 +696,107 @@ __global__ void __launch_bounds__(256) gather_kernel(const GatherArgs a) {
 // =============================================================================
 
 
+// Token-major gather (the forward path): CTA b reads token b's fp16 activation
+// row once and writes it to each of its top_k expert slots (+ the shared-expert
+// row), with the extension rows.  The projection partials Z are reduced with
+// the split index spread over threads (independent loads, fixed order).
+constexpr int kGatherThreads = 256;
+constexpr int kGatherMaxDest = 65;   // top_k <= 64, + shared
+
+__global__ void __launch_bounds__(kGatherThreads) gather_tokens_kernel(const GatherArgs a) {
+    extern __shared__ float s_z[];             // [top_k][rank]
+    __shared__ float s_part[kGatherThreads];
+    __shared__ int64_t s_row[kGatherMaxDest];  // destination row (-1: none)
+    __shared__ int s_e[kGatherMaxDest];
+    pdl_wait();
+    pdl_launch_dependents();
+    const int b = blockIdx.x;
+    const int nr = a.num_experts > 0 ? a.top_k : 0;
+    const int nd = nr + (a.with_shared ? 1 : 0);
+    if (threadIdx.x < nd) {
+        int64_t prow = -1;
+        int e = -1;
+        if (static_cast<int>(threadIdx.x) < nr) {
+            const int f = b * nr + threadIdx.x;
+            const int pos = a.inv[f];
+            e = a.ids[f];
+            if (pos >= 0) prow = a.poffsets ? pos + a.poffsets[e] - a.offsets[e] : pos;
+            else e = -1;
+        } else {
+            prow = (a.poffsets ? a.poffsets[a.num_experts] : a.offsets[a.num_experts]) + b;
+        }
+        s_row[threadIdx.x] = prow;
+        s_e[threadIdx.x] = e;
+    }
+    __syncthreads();
+    // Z of each routed destination: sum over the projection's K splits
+    const int pairs = a.use_z ? nr * a.rank : 0;
+    if (pairs > 0) {
+        const int ns = a.proj_nsplit;
+        const int G = pairs >= kGatherThreads ? 1 : min(ns, kGatherThreads / pairs);
+        const int per = kGatherThreads / G;
+        for (int p0 = 0; p0 < pairs; p0 += per) {
+            const int pi = threadIdx.x % per, g = threadIdx.x / per, pair = p0 + pi;
+            float acc = 0.0f;
+            if (pair < pairs && g < G) {
+                const int d = pair / a.rank, j = pair % a.rank, e = s_e[d];
+                if (e >= 0) {
+                    const float* zb = a.zpart + static_cast<int64_t>(b) * a.zcols + a.pm_of[e] * a.rank + j;
+#pragma unroll 4
+                    for (int sp = g; sp < ns; sp += G) acc += zb[sp * a.zsplit_stride];
+                }
+            }
+            s_part[threadIdx.x] = acc;
+            __syncthreads();
+            if (static_cast<int>(threadIdx.x) < per && p0 + static_cast<int>(threadIdx.x) < pairs) {
+                float z = 0.0f;
+                for (int q = 0; q < G; ++q) z += s_part[q * per + threadIdx.x];
+                s_z[p0 + threadIdx.x] = z;
+            }
+            __syncthreads();
+        }
+    }
+    auto dst_piece = [&](__half* base, int cols, int64_t prow, int t) -> int4* {
+        if (a.atom_rows > 0) {
+            const int at = t >> 3, ch = t & 7;
+            return reinterpret_cast<int4*>(base + ((static_cast<int64_t>(at) * a.atom_rows + prow) * 64 +
+                                                   ((ch ^ static_cast<int>(prow & 7)) << 3)));
+        }
+        return reinterpret_cast<int4*>(base + prow * cols) + t;
+    };
+    // activation row, read once, written to every destination
+    const int4* src = reinterpret_cast<const int4*>(a.x16 + static_cast<int64_t>(b) * a.k_pad);
+    for (int t = threadIdx.x; t < a.k_pad / 8; t += kGatherThreads) {
+        const int4 v = src[t];
+        for (int d = 0; d < nd; ++d)
+            if (s_row[d] >= 0) *dst_piece(a.xp, a.k_pad, s_row[d], t) = v;
+    }
+    // extension rows: [Sx | zscale * Z * rowscale | 0]
+    const int n8 = a.ext_cols / 8;
+    for (int idx = threadIdx.x; idx < nd * n8; idx += kGatherThreads) {
+        const int d = idx / n8, t = idx % n8;
+        const int64_t prow = s_row[d];
+        if (prow < 0) continue;
+        const int e = s_e[d];
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int col = t * 8 + q;
+            float v = 0.0f;
+            if (col < a.groups) {
+                if (a.use_sx) v = a.sx[static_cast<int64_t>(b) * a.groups + col];
+            } else if (col < a.groups + a.rank) {
+                if (pairs > 0 && e >= 0) {
+                    const int j = col - a.groups;
+                    v = s_z[d * a.rank + j] * a.rowscale[a.pm_of[e] * a.rank + j] * a.zscale[e];
+                }
+            }
+            h[q] = __float2half_rn(v);
+        }
+        *dst_piece(a.ep, a.ext_cols, prow, t) = *reinterpret_cast<const int4*>(h);
+    }
+}
+
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     pdl_wait();
     pdl_launch_dependents();
@@ -702,6 +829,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
                 pos += a.poffsets[e] - a.offsets[e];
             }
             float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll 8
             for (int sp = 0; sp < ns; ++sp)
                 load4(a.y + sp * a.split_stride + static_cast<int64_t>(pos) * a.out_dim + c0, v);
             const float g = a.gates[f];
@@ -824,14 +952,18 @@ static void max_carveout(K kern) {
 
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
-                         float* score_ws, int32_t* ticket, cudaStream_t stream) {
+                         float* score_ws, int32_t* ticket, const PlanArgs* plan, int32_t* plan_ticket,
+                         cudaStream_t stream) {
     if (batch <= 0) return cudaSuccess;
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
+    if (plan && num_experts <= 0) return cudaErrorInvalidValue;
+    const PlanArgs pa = plan ? *plan : PlanArgs{};
     const int tpc = batch <= 2 * 148 ? 1 : (batch + 2 * 148 - 1) / (2 * 148);
     const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
     max_carveout(route_kernel);
     return launch_maybe_pdl(route_kernel, grid, dim3(kRouteThreads), 0, stream, x, batch, in_dim, gate, num_experts,
-                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc);
+                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
+                            plan ? plan_ticket : nullptr);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
@@ -852,9 +984,24 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
-    dim3 grid((a.out_dim + 1023) / 1024, a.batch);
+    // small batches: narrow CTAs so the split partials are read by many SMs
+    const int threads = a.batch <= 16 ? 64 : 256;
+    dim3 grid((a.out_dim + 4 * threads - 1) / (4 * threads), a.batch);
     max_carveout(combine_kernel);
-    return launch_maybe_pdl(combine_kernel, grid, dim3(256), 0, stream, a);
+    return launch_maybe_pdl(combine_kernel, grid, dim3(threads), 0, stream, a);
+}
+
+cudaError_t launch_gather_tokens(const GatherArgs& a, cudaStream_t stream) {
+    if (a.batch <= 0) return cudaSuccess;
+    if (a.top_k + 1 > kGatherMaxDest) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(float) * static_cast<size_t>(a.use_z ? a.top_k * a.rank : 0);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(gather_tokens_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+    }
+    max_carveout(gather_tokens_kernel);
+    return launch_maybe_pdl(gather_tokens_kernel, dim3(a.batch), dim3(kGatherThreads), smem, stream, a);
 }
 
 cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,

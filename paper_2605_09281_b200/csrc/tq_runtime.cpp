@@ -34,9 +34,11 @@ namespace tqb {
 cudaError_t launch_gemm(const GemmParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
-                         float* score_ws, int32_t* ticket, cudaStream_t stream);
+                         float* score_ws, int32_t* ticket, const PlanArgs* plan, int32_t* plan_ticket,
+                         cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream);
+cudaError_t launch_gather_tokens(const GatherArgs& a, cudaStream_t stream);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
 cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,
                           int32_t* err_flag, cudaStream_t stream);
@@ -670,8 +672,8 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     L->x16.alloc(sizeof(__half) * cap * g.k_pad);
     L->sx.alloc(sizeof(float) * cap * std::max<int64_t>(1, g.G));
     L->route_ws.alloc(sizeof(float) * cap * g.K);
-    L->route_ticket.alloc(sizeof(int32_t) * cap);
-    cuda_check(cudaMemset(L->route_ticket.p, 0, sizeof(int32_t) * cap), "cudaMemset");
+    L->route_ticket.alloc(sizeof(int32_t) * (cap + 1));   // + the fused plan's grid ticket
+    cuda_check(cudaMemset(L->route_ticket.p, 0, sizeof(int32_t) * (cap + 1)), "cudaMemset");
     L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
     L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
     L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
@@ -1056,8 +1058,21 @@ void count_launch(tq_layer* L, int n = 1) {
     }
 }
 
-// prep (x16, sx) and optional routing
-void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st) {
+// the plan fused into the router's last CTA (TQ_FUSE_PLAN=1; off by default:
+// measured slower, the plan's unit loop wants the full 1024-thread CTA)
+static bool fuse_plan(const tq_layer* L) {
+    (void)L;
+    static const bool on = [] {
+        const char* e = std::getenv("TQ_FUSE_PLAN");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+// prep (x16, sx) and optional routing; with `plan` the router's last CTA also
+// runs the plan (permutation + work units) on the routing it just produced
+void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st,
+               const PlanArgs* plan = nullptr) {
     if (L->ktime) {
         L->kt_stream = st;
         L->kt_active = true;
@@ -1070,7 +1085,8 @@ void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaSt
                             do_route ? static_cast<int>(L->g.K) : 0, static_cast<int>(L->g.top_k),
                             static_cast<int>(L->g.gs), static_cast<int>(L->g.G), static_cast<int>(L->g.k_pad),
                             L->ids.as<int32_t>(), L->gates.as<float>(), L->x16.as<__half>(), L->sx.as<float>(),
-                            L->route_ws.as<float>(), L->route_ticket.as<int32_t>(), st),
+                            L->route_ws.as<float>(), L->route_ticket.as<int32_t>(), do_route ? plan : nullptr,
+                            L->route_ticket.as<int32_t>() + L->cap, st),
                "route_kernel launch");
     count_launch(L);
 }
@@ -1092,9 +1108,8 @@ static void timed_expert_gemm(tq_layer* L, const GemmParams& p, int grid, cudaSt
     }
 }
 
-void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
-                 int path, cudaStream_t st) {
-    (void)x;
+// the plan of one forward: permutation of `ids` and the GEMM work units
+PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path) {
     const Geometry& g = L->g;
     const bool use_lotile = path != TQ_PATH_QMOE;
     const bool use_qmoe = path != TQ_PATH_LOTILE;
@@ -1105,7 +1120,6 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     const int nsplit = use_qmoe ? main_nsplit(L, batch) : 1;
     const int pns = proj_nsplit(L, batch);
     const bool with_shared = use_qmoe && g.S > 0;
-    // plan
     PlanArgs pa{};
     pa.ids = ids;
     pa.batch = static_cast<int>(batch);
@@ -1146,8 +1160,27 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     pa.proj_units = L->punits.as<Unit>();
     pa.n_proj_units = L->n_punits.as<int32_t>();
     pa.err_flag = L->err_flag.as<int32_t>();
-    cuda_check(launch_plan(pa, st), "plan_kernel launch");
-    count_launch(L);
+    return pa;
+}
+
+// plan_done: the router already ran the plan (run_route with make_plan_args)
+void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
+                 int path, cudaStream_t st, bool plan_done = false) {
+    (void)x;
+    const Geometry& g = L->g;
+    const bool use_lotile = path != TQ_PATH_QMOE;
+    const bool use_qmoe = path != TQ_PATH_LOTILE;
+    const LaunchCfg cf = cfg_for(L, batch);
+    const LaunchCfg cfp = proj_cfg(L, batch);
+    const bool xr = cf.dn == 32;
+    const int ns_min = use_qmoe ? xr_ns_min(L, cf, batch) : 1;
+    const int pns = proj_nsplit(L, batch);
+    const bool with_shared = use_qmoe && g.S > 0;
+    const PlanArgs pa = make_plan_args(L, batch, ids, path);
+    if (!plan_done) {
+        cuda_check(launch_plan(pa, st), "plan_kernel launch");
+        count_launch(L);
+    }
     const int64_t atom_rows = rows_for(L, L->cap);   // capacity rows of xperm / extperm / ypart
     // projection pass: Z = P . x for every token (dense fp16 weights)
     if (use_lotile && L->proj_mb > 0) {
@@ -1205,7 +1238,8 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ga.ep = L->extperm.as<__half>();
     ga.poffsets = L->poffsets.as<int32_t>();
     ga.atom_rows = atom_rows;
-    cuda_check(launch_gather(ga, static_cast<int>(compact_rows(L, batch)), st), "gather_kernel launch");
+    ga.inv = L->inv.as<int32_t>();
+    cuda_check(launch_gather_tokens(ga, st), "gather_tokens_kernel launch");
     count_launch(L);
     // fused expert pass
     GemmParams p = base_params(L, cf, batch);
@@ -1258,7 +1292,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     CombineArgs ca{};
     ca.y = L->ypart.as<float>();
     ca.split_stride = rows_for(L, batch) * g.o;
-    ca.nsplit = nsplit;
+    ca.nsplit = pa.nsplit;
     ca.inv = L->inv.as<int32_t>();
     ca.gates = gates;
     ca.offsets = L->offsets.as<int32_t>();
@@ -1272,7 +1306,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ca.use_routed = 1;
     ca.ysh = L->ypart.as<float>();
     ca.sh_split_stride = ca.split_stride;
-    ca.sh_nsplit = nsplit;
+    ca.sh_nsplit = pa.nsplit;
     ca.sh_from_offsets = 1;
     ca.nsplit_dev = L->nsplit_d.as<int32_t>();
     ca.fused = fuse ? 1 : 0;
@@ -1477,8 +1511,9 @@ tq_status tq_forward_routed(tq_layer* L, const float* x, int64_t batch, float* y
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const void* const key[6] = {x, nullptr, nullptr, y, ids, gates};
         run_graphed(L, key, batch, path + 16, st, [&](cudaStream_t s2) {
-            run_route(L, x, batch, true, s2);
-            run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2);
+            const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
+            run_route(L, x, batch, true, s2, fuse_plan(L) ? &pa : nullptr);
+            run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2, fuse_plan(L));
             if (ids)
                 cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
                                            s2),
@@ -1501,9 +1536,10 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
         cudaStream_t st = nullptr;
         auto body = [&](cudaStream_t s2) {
             cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, s2), "x H2D");
-            run_route(L, L->xin.as<float>(), batch, true, s2);
+            const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
+            run_route(L, L->xin.as<float>(), batch, true, s2, fuse_plan(L) ? &pa : nullptr);
             run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(), L->yout.as<float>(),
-                        path, s2);
+                        path, s2, fuse_plan(L));
             cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, s2),
                        "y D2H");
         };
@@ -1633,7 +1669,7 @@ tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const floa
         cuda_check(cudaMemsetAsync(ticket.p, 0, sizeof(int32_t) * batch, st), "cudaMemsetAsync");
         cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(in_dim), gate,
                                 static_cast<int>(num_experts), static_cast<int>(top_k), 1, 0, 0, ids, gates, nullptr,
-                                nullptr, ws.as<float>(), ticket.as<int32_t>(), st),
+                                nullptr, ws.as<float>(), ticket.as<int32_t>(), nullptr, nullptr, st),
                    "route_kernel launch");
         cuda_check(cudaStreamSynchronize(st), "stream sync");   // workspace lifetime
     });

@@ -1,5 +1,5 @@
 import sys, numpy as np
-t = np.fromfile(sys.argv[1], dtype=np.uint64).reshape(8, 4096).astype(np.int64)
+t = np.fromfile(sys.argv[1], dtype=np.uint64)[:8 * 4096].reshape(8, 4096).astype(np.int64)
 names = ["codeIssue", "xIssue", "mma_afull", "mma_xfull", "dq_cfull", "dq_computed", "dq_aempty", "dq_st"]
 n = [int((t[s] > 0).sum()) for s in range(8)]
 t0 = min(int(t[s][t[s] > 0].min()) for s in range(8) if n[s])

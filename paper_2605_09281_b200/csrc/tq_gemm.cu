@@ -54,6 +54,8 @@ __host__ __device__ constexpr int code_stage_bytes(int bits, int kc) {
 // extension blocks of one (weight, m-block): n_ext64 dense fp16 128 x 64 blocks
 __host__ __device__ inline int ext_slot_bytes(int n_ext64) { return n_ext64 * code_block_bytes(kDenseBits); }
 
+constexpr int kHdrBytes = 2048;   // barrier header region
+constexpr int kUnitCache = 64;    // work units staged in shared memory per CTA
 struct SharedHdr {
     // one ring for the MMA operands: stage s = A columns in TMEM + an activation
     // tile in smem; full = 4 dequant warps + the activation producer (with its
@@ -67,6 +69,8 @@ struct SharedHdr {
     uint64_t e_full[2], e_empty[2];
     uint32_t tmem_base;
 };
+
+static_assert(sizeof(SharedHdr) <= kHdrBytes, "barrier header");
 
 __device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx) {
 #ifdef TQ_TRACE
@@ -147,6 +151,8 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                    : (wid == kRoleBase ? 2 : wid == kRoleBase + 1 ? 0 : wid == kRoleBase + 2 ? 3 : 1);
 #ifdef TQ_EXPERIMENT
     const int kDbg = p.debug;   // experiment builds: runtime skip flags (TQ_DEBUG)
+#elif defined(TQ_DBG_CONST)
+    constexpr int kDbg = TQ_DBG_CONST;   // compile-time skip flags (ablation builds)
 #else
     constexpr int kDbg = 0;     // production: every debug branch folds away
 #endif
@@ -202,6 +208,21 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
 #endif
     const int first = p.contig ? static_cast<int>(static_cast<int64_t>(blockIdx.x) * n_all / gridDim.x) : blockIdx.x;
     const int stride = p.contig ? 1 : gridDim.x;
+    // this CTA's work units, staged in shared memory once: every role walks the
+    // same list (a dependent global load per unit per role otherwise)
+    Unit* s_units = reinterpret_cast<Unit*>(reinterpret_cast<uint8_t*>(hdr) + kHdrBytes);
+    {
+        const int n_mine = first < n_units ? (n_units - first + stride - 1) / stride : 0;
+        const int n_cache = n_mine < kUnitCache ? n_mine : kUnitCache;
+        for (int i = threadIdx.x; i < 2 * n_cache; i += blockDim.x)
+            reinterpret_cast<int4*>(s_units)[i] =
+                reinterpret_cast<const int4*>(p.units + first + static_cast<int64_t>(i >> 1) * stride)[i & 1];
+        __syncthreads();
+    }
+    auto unit_at = [&](int u) -> Unit {
+        const int k = stride == 1 ? u - first : (u - first) / stride;
+        return k < kUnitCache ? s_units[k] : p.units[u];
+    };
     // resident activation slots (kXR): slot c holds chunk c of the current run
     const int xr_slot_bytes = kAtoms * x_atom_bytes;
     auto same_run = [](const Unit& a, const Unit& b) {
@@ -217,11 +238,12 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             uint32_t cph = 0, eph = 0;
             uint64_t xm = 0;   // kXR: per-slot count (mod 2) of runs that have used the slot
             Unit prev{};
-            Unit nxt = first < n_units ? p.units[first] : Unit{};
+            Unit nxt = first < n_units ? unit_at(first) : Unit{};
             for (int u = first; u < n_units; u += stride) {
                 const Unit un = nxt;
-                if (u + stride < n_units) nxt = p.units[u + stride];
+                if (u + stride < n_units) nxt = unit_at(u + stride);
                 const bool run_start = u == first || !same_run(prev, un);
+                if (kXR && lane == 0) trace_ev(p, 1, u - first);
                 prev = un;
                 const int nmain = un.kc_end - un.kc_begin;
                 const int64_t wm = static_cast<int64_t>(un.weight) * (p.o_pad / kBM) + un.mb;  // (w, mb) slab
@@ -246,29 +268,57 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     }
                     __syncwarp();
                 };
-                for (int c = 0; c < nmain; ++c) {
-                    const int kc = un.kc_begin + c;
-                    if (kXR && run_start) load_x(c);
+                // per-chunk issue path kept short: pointers advance incrementally, the
+                // activation loads of a run's first unit take a separate loop
+                const uint8_t* csrc = wbase + static_cast<int64_t>(un.kc_begin) * kCBytes;
+                uint8_t* cdst = smem + c_off + cs * kCStage;
+                const __half* sbase = p.scales + wm * p.groups * kBM;
+                int e0 = un.kc_begin * KC;
+                auto issue_codes = [&]() {
+#ifdef TQ_TRACE_PROD
+                    if (lane == 0) trace_ev(p, 5, tcnt);
+#endif
                     TQ_TIMED(0, mbar_wait_sleep(&hdr->c_empty[cs], cph ^ 1u));
-                    uint8_t* st = smem + c_off + cs * kCStage;
-                    const uint8_t* src = wbase + static_cast<int64_t>(kc) * kCBytes;
+#ifdef TQ_TRACE_PROD
+                    if (lane == 0) trace_ev(p, 6, tcnt);
+#endif
                     if (kDbg & 128) {
                         if (lane == 0) mbar_arrive(&hdr->c_full[cs]);
                     } else if constexpr (BITS == kDenseBits) {
-                        bulk_copy2_elect(&hdr->c_full[cs], st, src, kCBytes, st, src, 0u);
+                        bulk_copy2_elect(&hdr->c_full[cs], cdst, csrc, kCBytes, cdst, csrc, 0u);
                     } else {
-                        const int e0 = kc * KC;
-                        const int g0 = gshift >= 0 ? e0 >> gshift : e0 / p.group_size;
-                        const int glast = gshift >= 0 ? (e0 + KC - 1) >> gshift : (e0 + KC - 1) / p.group_size;
+                        int g0, glast;
+                        if (gshift >= 0) {
+                            g0 = e0 >> gshift;
+                            glast = (e0 + KC - 1) >> gshift;
+                        } else {
+                            g0 = e0 / p.group_size;
+                            glast = (e0 + KC - 1) / p.group_size;
+                        }
                         const int g1 = min(p.groups - 1, glast);
-                        const uint32_t sbytes = static_cast<uint32_t>(g1 - g0 + 1) * kBM * 2;
-                        bulk_copy2_elect(&hdr->c_full[cs], st, src, kCBytes, st + kCBytes,
-                                         p.scales + (wm * p.groups + g0) * kBM, sbytes);
+                        bulk_copy2_elect(&hdr->c_full[cs], cdst, csrc, kCBytes, cdst + kCBytes, sbase + g0 * kBM,
+                                         static_cast<uint32_t>(g1 - g0 + 1) * kBM * 2);
                     }
                     if (lane == 0) trace_ev(p, 0, tcnt);
                     ++tcnt;
-                    if (++cs == c_stages) { cs = 0; cph ^= 1u; }
+                    csrc += kCBytes;
+                    e0 += KC;
+                    cdst += kCStage;
+                    if (++cs == c_stages) {
+                        cs = 0;
+                        cph ^= 1u;
+                        cdst = smem + c_off;
+                    }
+                };
+                if (kXR && run_start) {
+                    for (int c = 0; c < nmain; ++c) {
+                        load_x(c);
+                        issue_codes();
+                    }
+                } else {
+                    for (int c = 0; c < nmain; ++c) issue_codes();
                 }
+                if (kXR && lane == 0) trace_ev(p, 3, u - first);
                 if (kXR && run_start)
                     for (int c = nmain; c < nmain + un.n_ext; ++c) load_x(c);
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
@@ -288,10 +338,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         // the packed-code bulk copies in the SM's copy engine; large tiles: TMA
         int xs = 0, tcnt = 0;
         uint32_t xph = 0;
-        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        Unit nxt = first < n_units ? unit_at(first) : Unit{};
         for (int u = first; u < n_units; u += stride) {
             const Unit un = nxt;
-            if (u + stride < n_units) nxt = p.units[u + stride];
+            if (u + stride < n_units) nxt = unit_at(u + stride);
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
             const bool small = un.n_tok <= 8;   // a few rows: LSU; 16-row granules and up: TMA
@@ -359,10 +409,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         uint32_t xph = 0;
         int c_next = j;
         uint64_t xm = 0;   // kXR: per-slot count (mod 2) of completed runs that used the slot
-        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        Unit nxt = first < n_units ? unit_at(first) : Unit{};
         for (int u = first; u < n_units; u += stride, ++lu) {
             const Unit un = nxt;
-            if (u + stride < n_units) nxt = p.units[u + stride];
+            if (u + stride < n_units) nxt = unit_at(u + stride);
             const bool run_end = u + stride >= n_units || !same_run(un, nxt);
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
@@ -476,7 +526,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             xs_n += NG;
             if (xs_n >= x_stages) { xs_n -= x_stages; xph_n ^= 1; }
         };
-        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        Unit nxt = first < n_units ? unit_at(first) : Unit{};
         if (kGX && first < n_units) {
             const int nch0 = (nxt.kc_end - nxt.kc_begin) + nxt.n_ext;
             if (grp < nch0) issue_x(nxt, grp);
@@ -485,7 +535,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         }
         for (int u = first; u < n_units; u += stride) {
             const Unit un = nxt;
-            if (u + stride < n_units) nxt = p.units[u + stride];
+            if (u + stride < n_units) nxt = unit_at(u + stride);
             const bool has_nxt = u + stride < n_units;
             const int nmain = un.kc_end - un.kc_begin;
             const int nch = nmain + un.n_ext;
@@ -557,7 +607,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                             prof[1] += clock64() - tcf0;
 #endif
                             TQ_TIMED(3, mbar_wait(&hdr->empty[as], aph ^ 1u));
+#ifndef TQ_TRACE_PROD
                             if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+#endif
                             tc_fence_after();
 #ifdef TQ_PROFILE
                             const long long tdq0 = clock64();
@@ -587,7 +639,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                         TQ_TIMED(0, mbar_wait(&hdr->e_full[es], eph));
                         const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
                         TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
+#ifndef TQ_TRACE_PROD
                         if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
+#endif
                         tc_fence_after();
 #pragma unroll
                         for (int s = 0; s < kSW; ++s) {
@@ -612,7 +666,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&hdr->full[as]);
+#ifndef TQ_TRACE_PROD
                     if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
+#endif
                     if (lane == 0 && grp == 0) trace_ev(p, 7, q * 1024 + tcnt);   // per-warp skew of group 0
                     ++tcnt;
                 }
@@ -632,13 +688,13 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         const bool fuse = p.fuse_combine && *p.nsplit_dev == 1;
         int lu = 0;
         int q_base_e = 0;       // CTA-wide chunk index of the unit's first chunk
-        Unit nxt = first < n_units ? p.units[first] : Unit{};
+        Unit nxt = first < n_units ? unit_at(first) : Unit{};
         float nscale = first < n_units ? p.w_outscale[nxt.weight] : 1.0f;
         for (int u = first; u < n_units; u += stride, ++lu) {
             const Unit un = nxt;
             const float oscale = nscale;
             if (u + stride < n_units) {
-                nxt = p.units[u + stride];
+                nxt = unit_at(u + stride);
                 nscale = p.w_outscale[nxt.weight];
             }
             const int ds = lu & 1;
@@ -731,7 +787,7 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     const int x_stage = (kc / kKC) * rows * 128;
     const int c_stage = code_stage_bytes(p.bits, kc);
     if (p.e_slots != 1) p.e_slots = 2;
-    const int fixed = 2048 + p.e_slots * ext_slot_bytes(p.n_ext64);
+    const int fixed = kHdrBytes + kUnitCache * static_cast<int>(sizeof(Unit)) + p.e_slots * ext_slot_bytes(p.n_ext64);
     const int ni = (kc == 128 && dn <= 64) ? 2 : 1;
     const int as_n = a_stages(kc, dn, ni);
     int cs, xs;
@@ -758,7 +814,8 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     p.group_shift = -1;
     for (int s = 0; s < 16; ++s)
         if ((1 << s) == p.group_size) p.group_shift = s;
-    const int smem = 1024 + xs * x_stage + cs * c_stage + p.e_slots * ext_slot_bytes(p.n_ext64) + 2048;
+    const int smem = 1024 + xs * x_stage + cs * c_stage + p.e_slots * ext_slot_bytes(p.n_ext64) + kHdrBytes +
+                     kUnitCache * static_cast<int>(sizeof(Unit));
     static const int dbg = getenv("TQ_DEBUG") ? atoi(getenv("TQ_DEBUG")) : 0;
     p.debug = dbg;
     static unsigned long long* trace_buf = nullptr;

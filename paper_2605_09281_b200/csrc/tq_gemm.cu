@@ -138,6 +138,15 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const uint32_t c_off = x_off + x_stages * x_stage_bytes;
     const uint32_t e_off = c_off + c_stages * kCStage;
     SharedHdr* hdr = reinterpret_cast<SharedHdr*>(smem + e_off + p.e_slots * ext_bytes);
+#ifdef TQ_WAIT_TRAP
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("TQ_WAIT_TRAP layout: hdr 0x%x (full +0, empty +%d, x_full +%d, x_empty +%d, c_full +%d, c_empty +%d, "
+               "d_full +%d, d_empty +%d, e_full +%d, e_empty +%d) kAS %d xs %d cs %d\n",
+               smem_u32(hdr), (int)offsetof(SharedHdr, empty), (int)offsetof(SharedHdr, x_full),
+               (int)offsetof(SharedHdr, x_empty), (int)offsetof(SharedHdr, c_full), (int)offsetof(SharedHdr, c_empty),
+               (int)offsetof(SharedHdr, d_full), (int)offsetof(SharedHdr, d_empty), (int)offsetof(SharedHdr, e_full),
+               (int)offsetof(SharedHdr, e_empty), kAS, x_stages, c_stages);
+#endif
 
     // Role layout: the scheduler arbitrates highest-warp-id first, so the
     // latency-critical single-thread roles sit at the top:

@@ -50,6 +50,30 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         : "memory");
     return;
 #endif
+#ifdef TQ_WAIT_TRAP
+    // diagnostics: a wait that has not completed after ~2 s reports the barrier
+    // (shared-memory offset, parity, CTA, warp) and gives up
+    {
+        const long long t0 = clock64();
+        uint32_t ok = 0;
+        while (true) {
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\t"
+                "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, P1;\n}"
+                : "=r"(ok)
+                : "r"(smem_u32(bar)), "r"(parity)
+                : "memory");
+            if (ok) return;
+            if (clock64() - t0 > 4000000000ll) {
+                if ((threadIdx.x & 31) == 0)
+                    printf("TQ_WAIT_TRAP cta %d warp %d bar smem 0x%x parity %u\n", blockIdx.x, threadIdx.x >> 5,
+                           smem_u32(bar), parity);
+                return;   // give up: the kernel runs to completion (garbage) so the report is flushed
+            }
+        }
+    }
+#endif
 #ifdef TQ_WAIT_BACKOFF
     uint32_t ok = 0;
     while (true) {
@@ -76,6 +100,10 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 // Same with a suspend-time hint: for roles that wait long (epilogue), so their
 // polling does not steal issue slots from the dequant warps.
 static __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#ifdef TQ_WAIT_TRAP
+    mbar_wait(bar, parity);
+    return;
+#endif
     asm volatile(
         "{\n\t.reg .pred P1;\n"
         "TQ_WAITS_%=:\n\t"

@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         }
         for (int s = 0; s < x_stages; ++s) {
             mbar_init(&hdr->x_full[s], 1);
-            mbar_init(&hdr->x_empty[s], 1);   // kXR: committed by the issuer of the run's last chunk c
+            mbar_init(&hdr->x_empty[s], kXR ? NI : 1);   // kXR: one commit per issuer at the run's end
         }
         for (int s = 0; s < c_stages; ++s) {
             mbar_init(&hdr->c_full[s], 1);
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 }
                 tc_commit_elect(&hdr->empty[as]);
                 if (!kXR) tc_commit_elect(&hdr->x_empty[xs]);
-                else if (run_end) tc_commit_elect(&hdr->x_empty[c]);   // the run's last use of slot c
+
 #ifdef TQ_PROFILE
                 prof[2] += 1;   // chunks
 #endif
@@ -476,7 +476,13 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             if (c_first < nch) tc_commit_elect(&hdr->d_full[ds]);
             else if (lane == 0) mbar_arrive(&hdr->d_full[ds]);
             c_next = c - nch;
-            if (kXR && run_end) xm ^= (nch >= 64 ? ~0ull : ((1ull << nch) - 1ull));
+            if (kXR && run_end) {
+                // every issuer releases every slot of the run: a commit covers only the
+                // committing thread's MMAs, and with an odd chunk count per unit both
+                // issuers have read each slot
+                for (int cc = 0; cc < nch; ++cc) tc_commit_elect(&hdr->x_empty[cc]);
+                xm ^= (nch >= 64 ? ~0ull : ((1ull << nch) - 1ull));
+            }
         }
     } else if (warp >= 4 && warp < kEpi0) {
         // ===================== dequant groups =====================
@@ -775,6 +781,17 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+#ifdef TQ_PROFILE
+    if (threadIdx.x == 0 && p.trace) {
+        // row 31: per-CTA summary (word 0 stays 0 so per-warp views skip it)
+        unsigned long long* o = p.trace + (static_cast<size_t>(blockIdx.x) * 32 + 31) * 8;
+        unsigned long long g_exit;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+        o[0] = 0;
+        o[1] = static_cast<unsigned long long>(first < n_units ? (n_units - first + stride - 1) / stride : 0);
+        o[7] = g_exit;
+    }
+#endif
     if (warp == 2) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols)
                      : "memory");

@@ -615,8 +615,18 @@ LaunchCfg proj_cfg(const tq_layer* L, int64_t batch) {
 
 // decode configuration (dn == 32): resident activation slots of kc-wide chunks
 // must fit ~140 KB of shared memory -> lower bound on the split-K count
+// experiments: TQ_NS_FORCE=<n> pins the decode K-split count
+static int ns_force() {
+    static const int v = [] {
+        const char* e = std::getenv("TQ_NS_FORCE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+
 int xr_ns_min(const tq_layer* L, const LaunchCfg& cf, int64_t batch) {
     if (cf.dn != 32) return 1;
+    if (ns_force() > 0) return static_cast<int>(std::min<int64_t>(ns_force(), std::max<int64_t>(1, cf.kc_total / 2)));
     const int64_t tok = std::max<int64_t>(1, std::min<int64_t>(cf.bn, batch * L->g.top_k));
     const int64_t rows = (tok + 15) / 16 * 16;
     const int64_t slot = (cf.kc / 64) * rows * 128;
@@ -640,6 +650,7 @@ int main_nsplit(const tq_layer* L, int64_t batch) {
     int64_t ns = (16 * L->num_sms + base - 1) / base;
     ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 2));
     ns = std::max<int64_t>(1, std::min<int64_t>(ns, 16));
+    if (ns_force() > 0 && cfg_for(L, batch).dn == 32) return xr_ns_min(L, cfg_for(L, batch), batch);
     return static_cast<int>(std::max<int64_t>(ns, xr_ns_min(L, cfg_for(L, batch), batch)));
 }
 

@@ -31,3 +31,11 @@ pro = [int(a[c, w, 6]) for c in range(a.shape[0]) for w in range(32) if a[c, w, 
 ent = np.array([int(a[c, 0, 7]) for c in range(a.shape[0]) if a[c, 0, 0] > 0])
 if len(pro):
     print(f"prologue cycles: mean {np.mean(pro):.0f} max {np.max(pro):.0f}; CTA entry spread {(ent.max() - ent.min()) / 1e3:.2f} us")
+
+# per-CTA spans (row 31: units, exit globaltimer)
+ex = np.array([int(a[c, 31, 7]) for c in range(a.shape[0]) if a[c, 31, 7] > 0])
+if len(ex) and len(ent):
+    units = np.array([int(a[c, 31, 1]) for c in range(a.shape[0]) if a[c, 31, 7] > 0])
+    dur = (ex - ent[:len(ex)]) / 1e3
+    print(f"CTA span us: min {dur.min():.2f} median {np.median(dur):.2f} max {dur.max():.2f}; kernel span {(ex.max() - ent.min()) / 1e3:.2f} us; "
+          f"units/CTA min {units.min()} max {units.max()}; slowest CTAs {np.argsort(-dur)[:5].tolist()} units {units[np.argsort(-dur)[:5]].tolist()}")

@@ -252,7 +252,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 const Unit un = nxt;
                 if (u + stride < n_units) nxt = unit_at(u + stride);
                 const bool run_start = u == first || !same_run(prev, un);
+#ifndef TQ_TRACE_UNIT
                 if (kXR && lane == 0) trace_ev(p, 1, u - first);
+#endif
                 prev = un;
                 const int nmain = un.kc_end - un.kc_begin;
                 const int64_t wm = static_cast<int64_t>(un.weight) * (p.o_pad / kBM) + un.mb;  // (w, mb) slab
@@ -327,7 +329,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                 } else {
                     for (int c = 0; c < nmain; ++c) issue_codes();
                 }
+#ifndef TQ_TRACE_UNIT
                 if (kXR && lane == 0) trace_ev(p, 3, u - first);
+#endif
                 if (kXR && run_start)
                     for (int c = nmain; c < nmain + un.n_ext; ++c) load_x(c);
                 if (un.n_ext > 0 && p.n_ext64 > 0) {
@@ -435,6 +439,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             // epilogue to release this accumulator buffer before it arrives on
             // d_full[ds], so its arrival cannot fall into an older phase
             TQ_TIMED(1, mbar_wait(&hdr->d_empty[ds], dph ^ 1u));
+#ifdef TQ_TRACE_UNIT
+            if (lane == 0) trace_ev(p, j == 0 ? 1 : 7, lu);
+#endif
             tc_fence_after();
             const int c_first = c;
             for (; c < nch; c += NI) {
@@ -475,6 +482,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             // this issuer's part of unit u is accumulated (or it had no chunk in it)
             if (c_first < nch) tc_commit_elect(&hdr->d_full[ds]);
             else if (lane == 0) mbar_arrive(&hdr->d_full[ds]);
+#ifdef TQ_TRACE_UNIT
+            if (lane == 0 && j == 0) trace_ev(p, 3, lu);
+#endif
             c_next = c - nch;
             if (kXR && run_end) {
                 // every issuer releases every slot of the run: a commit covers only the
@@ -622,7 +632,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                             prof[1] += clock64() - tcf0;
 #endif
                             TQ_TIMED(3, mbar_wait(&hdr->empty[as], aph ^ 1u));
-#ifndef TQ_TRACE_PROD
+#if !defined(TQ_TRACE_PROD) && !defined(TQ_TRACE_UNIT)
                             if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
 #endif
                             tc_fence_after();
@@ -654,7 +664,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                         TQ_TIMED(0, mbar_wait(&hdr->e_full[es], eph));
                         const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
                         TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
-#ifndef TQ_TRACE_PROD
+#if !defined(TQ_TRACE_PROD) && !defined(TQ_TRACE_UNIT)
                         if (tr) trace_ev(p, 5, grp * 1024 + tcnt);
 #endif
                         tc_fence_after();
@@ -681,10 +691,12 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&hdr->full[as]);
-#ifndef TQ_TRACE_PROD
+#if !defined(TQ_TRACE_PROD) && !defined(TQ_TRACE_UNIT)
                     if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
 #endif
+#ifndef TQ_TRACE_UNIT
                     if (lane == 0 && grp == 0) trace_ev(p, 7, q * 1024 + tcnt);   // per-warp skew of group 0
+#endif
                     ++tcnt;
                 }
                 as += NG;
@@ -719,6 +731,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             float* out = p.y + static_cast<int64_t>(un.split) * p.y_split_stride +
                          static_cast<int64_t>(un.y_row) * p.ldy + row;
             TQ_TIMED(0, mbar_wait_sleep(&hdr->d_full[ds], dph));
+#ifdef TQ_TRACE_UNIT
+            if (lane == 0 && q == 0) trace_ev(p, 5, lu);
+#endif
             tc_fence_after();
             const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * NI * DN;
             const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
@@ -765,6 +780,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&hdr->d_empty[ds]);
+#ifdef TQ_TRACE_UNIT
+            if (lane == 0 && q == 0) trace_ev(p, 6, lu);
+#endif
         }
     }
 

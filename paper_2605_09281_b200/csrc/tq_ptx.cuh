@@ -100,7 +100,7 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 // Same with a suspend-time hint: for roles that wait long (epilogue), so their
 // polling does not steal issue slots from the dequant warps.
 static __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-#ifdef TQ_WAIT_TRAP
+#if defined(TQ_WAIT_TRAP) || defined(TQ_NO_SLEEP)
     mbar_wait(bar, parity);
     return;
 #endif

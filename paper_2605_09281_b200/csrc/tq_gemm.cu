@@ -72,9 +72,16 @@ struct SharedHdr {
 
 static_assert(sizeof(SharedHdr) <= kHdrBytes, "barrier header");
 
+// TQ_TRACE_ID builds: record identities instead of times (debugging the chunk accounting)
+__device__ __forceinline__ void trace_id(const GemmParams& p, int slot, int idx, unsigned long long v) {
+#ifdef TQ_TRACE_ID
+    if ((p.debug & 8) && static_cast<int>(blockIdx.x) == (p.debug >> 16) && idx < 4096) p.trace[slot * 4096 + idx] = v;
+#endif
+}
+
 __device__ __forceinline__ void trace_ev(const GemmParams& p, int slot, int idx) {
-#ifdef TQ_TRACE
-    if ((p.debug & 8) && blockIdx.x == 0 && idx < 4096) p.trace[slot * 4096 + idx] = clock64();
+#if defined(TQ_TRACE) && !defined(TQ_TRACE_ID)
+    if ((p.debug & 8) && static_cast<int>(blockIdx.x) == (p.debug >> 16) && idx < 4096) p.trace[slot * 4096 + idx] = clock64();
 #endif
 }
 
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     const uint32_t c_off = x_off + x_stages * x_stage_bytes;
     const uint32_t e_off = c_off + c_stages * kCStage;
     SharedHdr* hdr = reinterpret_cast<SharedHdr*>(smem + e_off + p.e_slots * ext_bytes);
-#ifdef TQ_WAIT_TRAP
+#ifdef TQ_WAIT_TRAP_LAYOUT
     if (blockIdx.x == 0 && threadIdx.x == 0)
         printf("TQ_WAIT_TRAP layout: hdr 0x%x (full +0, empty +%d, x_full +%d, x_empty +%d, c_full +%d, c_empty +%d, "
                "d_full +%d, d_empty +%d, e_full +%d, e_empty +%d) kAS %d xs %d cs %d\n",
@@ -338,6 +345,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     TQ_TIMED(1, mbar_wait_sleep(&hdr->e_empty[es], eph ^ 1u));
                     uint8_t* dst = smem + e_off + es * ext_bytes;
                     bulk_copy2_elect(&hdr->e_full[es], dst, p.ext_blocks + wm * ext_bytes, ext_bytes, dst, dst, 0u);
+                    if (lane == 0) trace_id(p, 1, u - first, (static_cast<unsigned long long>(es) << 8) | eph | (static_cast<unsigned long long>(un.n_ext) << 16) | (static_cast<unsigned long long>(nmain) << 24));
                     if (++es == p.e_slots) { es = 0; eph ^= 1u; }
                 }
             }
@@ -691,6 +699,11 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&hdr->full[as]);
+                    if (lane == 0 && q == 0)
+                        trace_id(p, 4 + (grp & 3), tcnt,
+                                 (static_cast<unsigned long long>(u - first) << 40) | (static_cast<unsigned long long>(c) << 24) |
+                                     (static_cast<unsigned long long>(nmain) << 8) | (main_chunk ? 1ull : 0ull) |
+                                     (static_cast<unsigned long long>(as) << 16) | (static_cast<unsigned long long>(es) << 4));
 #if !defined(TQ_TRACE_PROD) && !defined(TQ_TRACE_UNIT)
                     if (tr) trace_ev(p, 6, grp * 1024 + tcnt);
 #endif

@@ -54,8 +54,16 @@ static __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
     // diagnostics: a wait that has not completed after ~2 s reports the barrier
     // (shared-memory offset, parity, CTA, warp) and gives up
     {
-        const long long t0 = clock64();
         uint32_t ok = 0;
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, P1;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;   // the common case costs what the production wait costs
+        const long long t0 = clock64();
         while (true) {
             asm volatile(
                 "{\n\t.reg .pred P1;\n\t"

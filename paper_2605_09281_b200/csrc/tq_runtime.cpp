@@ -648,7 +648,9 @@ int main_nsplit(const tq_layer* L, int64_t batch) {
     const int64_t active = std::max<int64_t>(1, std::min<int64_t>(local, batch * L->g.top_k) + L->g.S);
     const int64_t base = active * L->g.mb_count;
     int64_t ns = (16 * L->num_sms + base - 1) / base;
-    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / 2));
+    // >= 4 main chunks per unit on the decode path (units of 2 chunks expose an
+    // intermittent hang under forced 16-way splits -- see DESIGN.md, known issues)
+    ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / (cfg_for(L, batch).dn == 32 ? 4 : 2)));
     ns = std::max<int64_t>(1, std::min<int64_t>(ns, 16));
     if (ns_force() > 0 && cfg_for(L, batch).dn == 32) return xr_ns_min(L, cfg_for(L, batch), batch);
     return static_cast<int>(std::max<int64_t>(ns, xr_ns_min(L, cfg_for(L, batch), batch)));

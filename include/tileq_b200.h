@@ -16,6 +16,11 @@
  *   tq_unpack_codes    <- unpack_codes(bytes, bits, count)      include/tileq/codec.hpp:68, src/codec.cpp:168-195
  *   tq_launch_count    <- dispatch_count()                      include/tileq/infer.hpp:37-38 (GPU analogue:
  *                                                               kernel launches per forward, constant in B)
+ *   tq_layout_forward  <- bench()'s layouts: lotile_forward / baseline_1d_forward /
+ *                         baseline_elementwise_forward / dequantize-all
+ *                                                               include/tileq/infer.hpp:77-131, src/infer.cpp:187-426
+ *   tq_dequantize_experts <- dequantize(residual) for every resident expert
+ *                                                               include/tileq/quant.hpp, src/quant.cpp:285-323
  *
  * Status codes mirror the reference error taxonomy (include/tileq/errors.hpp:13-50)
  * with the same triggering conditions; the message (tq_last_error, thread
@@ -166,6 +171,33 @@ tq_status tq_gemm_time_get(tq_layer* layer, double* ms_total, int64_t* launches)
  * of dispatch_count(), infer.hpp:37-38). */
 uint64_t tq_launch_count(const tq_layer* layer);
 void tq_reset_launch_count(tq_layer* layer);
+
+/* ---- comparison layouts (the paper's bench, infer.cpp:345-426) --------- */
+
+/* The bench layouts (BenchLayout, infer.hpp:113). */
+typedef enum {
+    TQ_LAYOUT_FUSED_2D = 0,     /* lotile_forward: the engine's fused low-rank path        */
+    TQ_LAYOUT_SHARED_1D = 1,    /* baseline_1d_forward on shared_1d_from_tiled_representative */
+    TQ_LAYOUT_ELEMENT_WISE = 2, /* baseline_elementwise_forward on elementwise_factors_from_tiled */
+    TQ_LAYOUT_DEQUANT_ONLY = 3  /* dequantize() every resident routed expert                 */
+} tq_layout;
+
+/* Prepare a layout's factors / buffers once, outside any timed region, as
+ * bench() does (infer.cpp:381-387).  tq_layout_forward prepares on first use. */
+tq_status tq_layout_prepare(tq_layer* layer, int layout);
+
+/* One call of a layout on a GIVEN routing: x [dev] f32 batch x in_dim, ids
+ * [dev] int32 / gates [dev] f32 batch x top_k, y [dev] f32 batch x out_dim
+ * (ignored by DEQUANT_ONLY).  *dispatches [host, may be NULL] receives the
+ * reference-style dispatch count of the call (matrix multiplies:
+ * fused 2, 1D 1 + B*top_k, element-wise 2*B*top_k, dequant 0; the kernel
+ * launches are in tq_launch_count). */
+tq_status tq_layout_forward(tq_layer* layer, int layout, const float* x, int64_t batch, const int32_t* ids,
+                            const float* gates, float* y, int64_t* dispatches, void* stream);
+
+/* Every resident routed expert's residual, dequantized: out [dev] fp16
+ * [n_experts][out_dim][in_dim] (the DEQUANT_ONLY layout's work). */
+tq_status tq_dequantize_experts(tq_layer* layer, uint16_t* out, void* stream);
 
 /* ---- expert-parallel stages (EP host orchestration in Python calls these
  * around its NCCL all-to-all exchange) ------------- */

@@ -284,6 +284,8 @@ class RefLib:
         L.tq_ref_f32_to_f16.argtypes = [_p, _i64, _p]
         L.tq_ref_dequantize.argtypes = [_p, _i64, _p, C.c_char_p, C.c_int]
         L.tq_ref_reconstruct.argtypes = [_p, _i64, _p, C.c_char_p, C.c_int]
+        L.tq_ref_layout.argtypes = [_p, C.c_int, _p, _i64, _p, _p, _p, _p, C.c_char_p, C.c_int]
+        L.tq_ref_bench.argtypes = [_p, C.c_int, _p, _i64, _i64, _i64, C.c_uint64, _p, C.c_char_p, C.c_int]
         L.tq_ref_make_artifact.argtypes = [C.c_char_p] + [_i64] * 8 + [C.c_int, _i64, C.c_int, _i64,
                                            C.c_double, C.c_double, _i64, C.c_uint64, C.c_int,
                                            C.c_char_p, C.c_int]
@@ -369,6 +371,31 @@ class RefLayer:
         self.ref._check(self.ref.lib.tq_ref_forward(self.h, _ptr(x), B, mode, threads, _ptr(y),
                                                     _ptr(ids), _ptr(gates), buf, 1024), buf)
         return y, ids, gates
+
+    LAYOUTS = ("fused_2d", "shared_1d", "element_wise", "dequant_only")
+
+    def layout(self, layout: str, x, ids, gates):
+        """The paper's comparison layouts on a given routing (infer.cpp:187-339):
+        returns (y, dispatch_count); dequant_only returns (None, count)."""
+        x = np.ascontiguousarray(x, np.float32)
+        ids = np.ascontiguousarray(ids, np.int64)
+        gates = np.ascontiguousarray(gates, np.float32)
+        B = x.shape[0]
+        y = np.zeros((B, self.o), np.float32)
+        disp = np.zeros(1, np.int64)
+        buf = C.create_string_buffer(1024)
+        self.ref._check(self.ref.lib.tq_ref_layout(self.h, self.LAYOUTS.index(layout), _ptr(x), B, _ptr(ids),
+                                                   _ptr(gates), _ptr(y), _ptr(disp), buf, 1024), buf)
+        return (None if layout == "dequant_only" else y), int(disp[0])
+
+    def bench(self, layout: str, batches, repeats=5, warmup=1, seed=1):
+        """The reference's bench() (infer.cpp:371-426): {batch: (median_ns, p10_ns, p90_ns, dispatches)}."""
+        bs = np.ascontiguousarray(batches, np.int64)
+        out = np.zeros(4 * len(bs), np.float64)
+        buf = C.create_string_buffer(1024)
+        self.ref._check(self.ref.lib.tq_ref_bench(self.h, self.LAYOUTS.index(layout), _ptr(bs), len(bs), repeats,
+                                                  warmup, C.c_uint64(seed), _ptr(out), buf, 1024), buf)
+        return {int(b): tuple(out[4 * t:4 * t + 4]) for t, b in enumerate(bs)}
 
     def dequantize(self, e):
         out = np.zeros((self.o, self.i), np.float32)

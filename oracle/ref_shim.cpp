@@ -305,4 +305,70 @@ int tq_ref_make_artifact(const char* dir, std::int64_t num_experts, std::int64_t
     });
 }
 
+// The comparison layouts of the paper's bench (infer.cpp:187-426) on a GIVEN
+// routing: layout 0 fused_2d = lotile_forward, 1 shared_1d =
+// baseline_1d_forward on shared_1d_from_tiled_representative, 2 element_wise =
+// baseline_elementwise_forward on elementwise_factors_from_tiled, 3
+// dequant_only = dequantize every routed expert, as bench() does (y untouched).  The
+// factors are prepared outside the measured call, as bench() does
+// (infer.cpp:381-387); *dispatches receives dispatch_count() of the call.
+int tq_ref_layout(void* hv, int layout, const float* x, std::int64_t batch, const std::int64_t* ids,
+                  const float* gates, float* y, std::int64_t* dispatches, char* errbuf, int errlen) {
+    auto* h = static_cast<RefHandle*>(hv);
+    return guarded(errbuf, errlen, [&] {
+        const TileQLayer& layer = h->art.layer;
+        const std::size_t k = layer.spec.top_k;
+        const std::int64_t in_dim = static_cast<std::int64_t>(layer.spec.in_dim);
+        DenseMatrix xm = wrap(x, batch, in_dim);
+        RoutingDecision routing;
+        routing.batch = static_cast<std::size_t>(batch);
+        routing.top_k = k;
+        routing.expert_ids.resize(static_cast<std::size_t>(batch) * k);
+        routing.gates = DenseMatrix(static_cast<std::size_t>(batch), k);
+        for (std::size_t f = 0; f < routing.expert_ids.size(); ++f) {
+            routing.expert_ids[f] = static_cast<std::size_t>(ids[f]);
+            routing.gates.data[f] = gates[f];
+        }
+        std::vector<LowRankFactor> ew;
+        Shared1DFactors sd;
+        if (layout == 1) sd = shared_1d_from_tiled_representative(layer.tiled);
+        if (layout == 2) ew = elementwise_factors_from_tiled(layer.tiled);
+        reset_dispatch_count();
+        DenseMatrix out;
+        if (layout == 0) out = lotile_forward(xm, layer.tiled, routing);
+        else if (layout == 1) out = baseline_1d_forward(xm, sd, routing);
+        else if (layout == 2) out = baseline_elementwise_forward(xm, ew, routing);
+        else if (layout == 3) {
+            for (const QuantizedExpert& q : layer.quantized) (void)dequantize(q);
+        } else {
+            throw ParamError("unknown layout " + std::to_string(layout));
+        }
+        if (dispatches) *dispatches = static_cast<std::int64_t>(dispatch_count());
+        if (layout != 3) copy_out(out, y);
+    });
+}
+
+// The reference's own bench() (infer.cpp:371-426) for one layout: per batch,
+// median / p10 / p90 wall ns and the dispatch count (out: 4 doubles per batch).
+int tq_ref_bench(void* hv, int layout, const std::int64_t* batches, std::int64_t nb, std::int64_t repeats,
+                 std::int64_t warmup, std::uint64_t seed, double* out, char* errbuf, int errlen) {
+    auto* h = static_cast<RefHandle*>(hv);
+    return guarded(errbuf, errlen, [&] {
+        std::vector<std::size_t> bs;
+        for (std::int64_t t = 0; t < nb; ++t) bs.push_back(static_cast<std::size_t>(batches[t]));
+        const BenchLayout lay = layout == 0 ? BenchLayout::fused_2d
+                              : layout == 1 ? BenchLayout::shared_1d
+                              : layout == 2 ? BenchLayout::element_wise
+                                            : BenchLayout::dequant_only;
+        const auto reps = bench(lay, h->art.layer, bs, static_cast<std::size_t>(repeats),
+                                static_cast<std::size_t>(warmup), 1, seed);
+        for (std::size_t t = 0; t < reps.size(); ++t) {
+            out[4 * t + 0] = reps[t].median_ns();
+            out[4 * t + 1] = reps[t].p10_ns();
+            out[4 * t + 2] = reps[t].p90_ns();
+            out[4 * t + 3] = static_cast<double>(reps[t].dispatches);
+        }
+    });
+}
+
 } // extern "C"

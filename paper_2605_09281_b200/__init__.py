@@ -118,6 +118,9 @@ def lib() -> C.CDLL:
     L.tq_ep_combine.argtypes = [p, p, i64, p, p, p, p, i32, p]
     L.tq_gemm_timing_enable.argtypes = [p, i32]
     L.tq_gemm_time_get.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64)]
+    L.tq_layout_prepare.argtypes = [p, i32]
+    L.tq_layout_forward.argtypes = [p, i32, p, i64, p, p, p, C.POINTER(i64), p]
+    L.tq_dequantize_experts.argtypes = [p, p, p]
     L.tq_ep_xrow_elems.restype = i64
     L.tq_ep_xrow_elems.argtypes = [p]
     L.tq_ep_extrow_elems.restype = i64
@@ -239,6 +242,40 @@ class Layer:
             check(lib().tq_forward(self._h, x.data_ptr(), B, ids32.data_ptr(), g.data_ptr(), y.data_ptr(),
                                    _PATHS[path], st))
         return y
+
+    # the paper's bench layouts (infer.cpp:345-426), in BenchLayout order
+    LAYOUTS = ("fused_2d", "shared_1d", "element_wise", "dequant_only")
+
+    def layout_prepare(self, layout: str):
+        """Build a comparison layout's factors once (outside timed regions)."""
+        check(lib().tq_layout_prepare(self._h, self.LAYOUTS.index(layout)))
+
+    def layout_forward(self, layout: str, x, ids, gates, out=None):
+        """One call of a bench layout on a given routing (device tensors):
+        fused_2d = lotile_forward, shared_1d = baseline_1d_forward,
+        element_wise = baseline_elementwise_forward, dequant_only = dequantize
+        every resident expert.  Returns (y or None, dispatch count)."""
+        torch = _torch()
+        self._check_x(x)
+        B = x.shape[0]
+        ids32 = ids.to(torch.int32).contiguous()
+        if ids32.shape != (B, self.top_k):
+            raise ShapeError(f"routing batch {ids32.shape[0]} vs input batch {B}")
+        g = gates.to(torch.float32).contiguous()
+        y = out if out is not None else torch.empty((B, self.out_dim), dtype=torch.float32, device=x.device)
+        disp = C.c_int64(0)
+        check(lib().tq_layout_forward(self._h, self.LAYOUTS.index(layout), x.data_ptr(), B, ids32.data_ptr(),
+                                      g.data_ptr(), y.data_ptr(), C.byref(disp), _stream_ptr(x.device)))
+        return (None if layout == "dequant_only" else y), int(disp.value)
+
+    def dequantize_experts(self):
+        """fp16 [n_experts, out_dim, in_dim]: every resident expert's residual
+        dequantized (quant.cpp:285-323) from the engine's repacked layout."""
+        torch = _torch()
+        n = self.info["expert_end"] - self.info["expert_begin"]
+        out = torch.empty((n, self.out_dim, self.in_dim), dtype=torch.float16, device=f"cuda:{self.device}")
+        check(lib().tq_dequantize_experts(self._h, out.data_ptr(), _stream_ptr(out.device)))
+        return out
 
     def forward_routed(self, x, path: str = "full"):
         """(y, ids int32, gates) in one call."""

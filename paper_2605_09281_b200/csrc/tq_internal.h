@@ -144,6 +144,19 @@ struct GatherArgs {
     const int32_t* inv;      // token-major gather: slot of flat routing index f (-1: invalid id)
 };
 
+// dequant_only comparison layout (tq_layouts.cu)
+struct DequantAllArgs {
+    const uint8_t* codes;      // repacked code blocks [w][mb][kb64]
+    int64_t weight_stride;     // bytes per weight
+    const uint16_t* scales;    // [w][mb][G][128] prescaled fp16
+    const uint8_t* ext_blocks; // [w][mb] n_ext64 dense blocks; columns [0, G) = -zero * s'
+    int64_t ext_bytes;         // bytes per (w, mb)
+    const float* w_outscale;   // 2^-k per weight
+    __half* out;               // [w][o][i] fp16
+    int64_t o, i;
+    int n_weights, mb_count, kb_total, groups, group_size;
+};
+
 struct CombineArgs {
     const float* y;          // split buffers [nsplit][rows][o]
     int64_t split_stride;

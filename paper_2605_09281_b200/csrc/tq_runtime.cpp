@@ -40,6 +40,11 @@ cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream);
 cudaError_t launch_gather_tokens(const GatherArgs& a, cudaStream_t stream);
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream);
+cudaError_t launch_lr_right(const float* A, int64_t a_ld, int rows, const float* x, int64_t x_ld, int tokens, int n,
+                            const float* scale, float* mid, int64_t mid_ld, cudaStream_t stream);
+cudaError_t launch_lr_left(const float* U, int o, int r, const float* mid, const float* gate, float* acc,
+                           cudaStream_t stream);
+cudaError_t launch_dequant_all(const DequantAllArgs& a, int bits, cudaStream_t stream);
 cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,
                           int32_t* err_flag, cudaStream_t stream);
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
@@ -489,6 +494,15 @@ struct tq_layer {
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
     std::atomic<uint64_t> launches{0};
+    // comparison layouts (infer.cpp:187-339): decoded factors kept on the host
+    // (decode_block_i8, codec.cpp:122-129) and device copies built on demand
+    struct {
+        int64_t M = 0, N = 0, R = 0;
+        std::vector<float> U, V, sigma, scaling;   // M x o x r, N x r x i, r, K x i
+        std::vector<uint16_t> placement;           // K x 2 (p, q)
+    } lay;
+    DBuf lay_U, lay_right, lay_proj1d, lay_sigma, lay_dq;
+    bool lay_ready[4] = {false, false, false, false};
     int num_sms = 148;
     // expert-GEMM device timing (tq_gemm_timing_enable)
     bool timing = false;
@@ -806,6 +820,27 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     std::vector<float> uabs(M), vabs(N);
     std::memcpy(uabs.data(), uabs_b.data(), uabs_b.size());
     std::memcpy(vabs.data(), vabs_b.data(), vabs_b.size());
+    {
+        // host copies for the comparison layouts: value = float(code) * (absmax / 127.0f)
+        L->lay.M = static_cast<int64_t>(M);
+        L->lay.N = static_cast<int64_t>(N);
+        L->lay.R = static_cast<int64_t>(R);
+        L->lay.U.resize(M * O * R);
+        for (size_t pb = 0; pb < M; ++pb) {
+            const float sc = uabs[pb] / 127.0f;
+            for (size_t t = 0; t < O * R; ++t)
+                L->lay.U[pb * O * R + t] = static_cast<float>(static_cast<int8_t>(u_b[pb * O * R + t])) * sc;
+        }
+        L->lay.V.resize(N * R * I);
+        for (size_t qb = 0; qb < N; ++qb) {
+            const float sc = vabs[qb] / 127.0f;
+            for (size_t t = 0; t < R * I; ++t)
+                L->lay.V[qb * R * I + t] = static_cast<float>(static_cast<int8_t>(v_b[qb * R * I + t])) * sc;
+        }
+        L->lay.sigma = sigma;
+        L->lay.scaling = scaling;
+        L->lay.placement = placement;
+    }
 
     // residual experts
     if (e_end < 0 || e_end > g.K) e_end = g.K;
@@ -1582,6 +1617,155 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
                        "gates D2H");
         cuda_check(cudaStreamSynchronize(st), "stream sync");
         for (size_t t = 0; t < hid.size(); ++t) ids[t] = hid[t];
+    });
+}
+
+// ---------------------------------------------------------------------------
+// comparison layouts (the paper's bench: infer.cpp:187-339, 345-426)
+// ---------------------------------------------------------------------------
+
+static void layout_prepare(tq_layer* L, int layout) {
+    if (layout < 0 || layout > 3) fail(TQ_ERR_PARAM, "unknown layout " + std::to_string(layout));
+    if (L->lay_ready[layout]) return;
+    const Geometry& g = L->g;
+    const int64_t O = g.o, I = g.i, R = L->lay.R;
+    if ((layout == 1 || layout == 2) && !L->lay_U.p) L->lay_U.upload(L->lay.U.data(), sizeof(float) * L->lay.U.size());
+    if (layout == 1) {
+        // shared_1d_from_tiled_representative (infer.cpp:320-335): P = sigma * V_0, U_p(k) per expert
+        std::vector<float> P(static_cast<size_t>(R * I));
+        for (int64_t j = 0; j < R; ++j)
+            for (int64_t c = 0; c < I; ++c)
+                P[j * I + c] = static_cast<float>(static_cast<double>(L->lay.sigma[j]) * L->lay.V[j * I + c]);
+        L->lay_proj1d.upload(P.data(), sizeof(float) * P.size());
+    } else if (layout == 2) {
+        // elementwise_factors_from_tiled (infer.cpp:271-289): right_k = V_q(k) / s_k, sigma at the product
+        const int64_t nloc = L->e_end - L->e_begin;
+        std::vector<float> right(static_cast<size_t>(nloc * R * I));
+        for (int64_t k = 0; k < nloc; ++k) {
+            const int64_t e = L->e_begin + k;
+            const int64_t q = L->lay.placement[2 * e + 1];
+            const float* v = L->lay.V.data() + q * R * I;
+            const float* sk = L->lay.scaling.data() + e * I;
+            for (int64_t j = 0; j < R; ++j)
+                for (int64_t c = 0; c < I; ++c)
+                    right[(k * R + j) * I + c] = static_cast<float>(static_cast<double>(v[j * I + c]) / sk[c]);
+        }
+        L->lay_right.upload(right.data(), sizeof(float) * right.size());
+        L->lay_sigma.upload(L->lay.sigma.data(), sizeof(float) * L->lay.sigma.size());
+    } else if (layout == 3) {
+        L->lay_dq.alloc(sizeof(uint16_t) * static_cast<size_t>((L->e_end - L->e_begin) * O * I));
+    }
+    (void)O;
+    L->lay_ready[layout] = true;
+}
+
+static void launch_dequant_experts(tq_layer* L, uint16_t* out, cudaStream_t st) {
+    const Geometry& g = L->g;
+    DequantAllArgs a{};
+    a.codes = L->codes.as<uint8_t>();
+    a.weight_stride = L->weight_stride;
+    a.scales = L->scales.as<uint16_t>();
+    a.ext_blocks = L->ext_blocks.as<uint8_t>();
+    a.ext_bytes = g.n_ext * code_block_bytes(kDenseBits);
+    a.w_outscale = L->w_outscale.as<float>();
+    a.out = reinterpret_cast<__half*>(out);
+    a.o = g.o;
+    a.i = g.i;
+    a.n_weights = static_cast<int>(L->e_end - L->e_begin);
+    a.mb_count = static_cast<int>(g.mb_count);
+    a.kb_total = static_cast<int>(g.k_pad / kKC);
+    a.groups = static_cast<int>(g.G);
+    a.group_size = static_cast<int>(g.gs);
+    cuda_check(launch_dequant_all(a, g.bits, st), "dequant_all_kernel launch");
+    count_launch(L);
+}
+
+tq_status tq_layout_prepare(tq_layer* L, int layout) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        layout_prepare(L, layout);
+    });
+}
+
+tq_status tq_layout_forward(tq_layer* L, int layout, const float* x, int64_t batch, const int32_t* ids,
+                            const float* gates, float* y, int64_t* dispatches, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        check_batch(L, batch);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        layout_prepare(L, layout);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const Geometry& g = L->g;
+        const int64_t k = g.top_k, O = g.o, I = g.i, R = L->lay.R;
+        int64_t disp = 0;
+        if (layout == TQ_LAYOUT_FUSED_2D) {
+            if (batch > 0) {
+                run_route(L, x, batch, false, st);
+                run_experts(L, x, batch, ids, gates, y, TQ_PATH_LOTILE, st);
+            }
+            disp = 2;   // the two fused products (infer.cpp:120,173)
+        } else if (layout == TQ_LAYOUT_DEQUANT_ONLY) {
+            launch_dequant_experts(L, L->lay_dq.as<uint16_t>(), st);
+        } else {
+            // host-orchestrated per-(token, expert) dispatches, as the reference loops
+            std::vector<int32_t> h_ids(static_cast<size_t>(batch * k));
+            if (batch > 0) {
+                cuda_check(cudaMemcpyAsync(h_ids.data(), ids, sizeof(int32_t) * h_ids.size(), cudaMemcpyDeviceToHost, st),
+                           "ids D2H");
+                cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+                cuda_check(cudaMemsetAsync(y, 0, sizeof(float) * batch * O, st), "y memset");
+            }
+            for (int32_t e : h_ids)
+                if (e < L->e_begin || e >= L->e_end)
+                    fail(TQ_ERR_PARAM, std::string(layout == 1 ? "1d" : "elementwise") + " baseline: expert id " +
+                                           std::to_string(e) + " out of range");
+            float* mid = L->zpart.as<float>();   // B*top_k x r scratch (>= cap * proj_rows floats)
+            if (static_cast<int64_t>(L->zpart_cap_floats) < batch * k * R)
+                fail(TQ_ERR_SIZE, "layout scratch too small: reserve a larger batch");
+            if (layout == TQ_LAYOUT_SHARED_1D) {
+                cuda_check(launch_lr_right(L->lay_proj1d.as<float>(), I, static_cast<int>(R), x, I,
+                                           static_cast<int>(batch), static_cast<int>(I), nullptr, mid, R, st),
+                           "shared projection launch");
+                count_launch(L);
+                disp = 1;
+                for (int64_t b = 0; b < batch; ++b)
+                    for (int64_t t = 0; t < k; ++t) {
+                        const int64_t f = b * k + t;
+                        const int64_t p = L->lay.placement[2 * h_ids[f]];
+                        cuda_check(launch_lr_left(L->lay_U.as<float>() + p * O * R, static_cast<int>(O),
+                                                  static_cast<int>(R), mid + b * R, gates + f, y + b * O, st),
+                                   "output multiply launch");
+                        count_launch(L);
+                        ++disp;
+                    }
+            } else {
+                for (int64_t b = 0; b < batch; ++b)
+                    for (int64_t t = 0; t < k; ++t) {
+                        const int64_t f = b * k + t;
+                        const int64_t e = h_ids[f];
+                        const int64_t p = L->lay.placement[2 * e];
+                        cuda_check(launch_lr_right(L->lay_right.as<float>() + (e - L->e_begin) * R * I, I,
+                                                   static_cast<int>(R), x + b * I, I, 1, static_cast<int>(I),
+                                                   L->lay_sigma.as<float>(), mid + f * R, R, st),
+                                   "right-factor multiply launch");
+                        cuda_check(launch_lr_left(L->lay_U.as<float>() + p * O * R, static_cast<int>(O),
+                                                  static_cast<int>(R), mid + f * R, gates + f, y + b * O, st),
+                                   "left-factor multiply launch");
+                        count_launch(L, 2);
+                        disp += 2;
+                    }
+            }
+        }
+        if (dispatches) *dispatches = disp;
+    });
+}
+
+tq_status tq_dequantize_experts(tq_layer* L, uint16_t* out, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        launch_dequant_experts(L, out, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -230,3 +230,35 @@ def test_bench_reference_arm_contract(tmp_path):
             assert k in line
         assert line["e2e"]["h2d_bytes_per_step"] == 0
         assert line["cpu_baseline"]["kind"] == "reference"
+
+
+# ---------------------------------------------------------------------------
+# the paper's bench layouts: reference fixtures
+# ---------------------------------------------------------------------------
+
+def test_layout_fixtures_follow_the_dispatch_contract(golden):
+    """tests/golden/layouts.npz (reference outputs): dispatch counts are the
+    reference's contract -- fused 2, 1D 1 + B*k, element-wise 2*B*k, dequant 0
+    (test_infer.cpp:204-231) -- and element-wise equals the fused 2D result
+    (same factors, different association; both f64 in the reference)."""
+    lay = dict(np.load(os.path.join(GOLD, "layouts.npz")))
+    for name in ART_NAMES:
+        k = golden[f"{name}/ids7"].shape[1]
+        for B in (7, 33):
+            assert int(lay[f"{name}/fused_2d{B}_dispatches"]) == 2
+            assert int(lay[f"{name}/shared_1d{B}_dispatches"]) == 1 + B * k
+            assert int(lay[f"{name}/element_wise{B}_dispatches"]) == 2 * B * k
+            assert int(lay[f"{name}/dequant_only{B}_dispatches"]) == 0
+            assert rel_frob(lay[f"{name}/element_wise{B}"], lay[f"{name}/fused_2d{B}"]) <= 1e-5
+            assert rel_frob(lay[f"{name}/fused_2d{B}"], golden[f"{name}/lotile{B}"]) <= 1e-6
+
+
+def test_layout_fixtures_reproduce_with_reference(ref, golden):
+    """The committed layout fixtures are what the reference computes today."""
+    lay = dict(np.load(os.path.join(GOLD, "layouts.npz")))
+    R = ref.load(os.path.join(GOLD, "folded_b3"))
+    x, ids, gates = golden["folded_b3/x7"], golden["folded_b3/ids7"], golden["folded_b3/gates7"]
+    for layout in ("shared_1d", "element_wise"):
+        y, d = R.layout(layout, x, ids, gates)
+        np.testing.assert_array_equal(y, lay[f"folded_b3/{layout}7"])
+        assert d == int(lay[f"folded_b3/{layout}7_dispatches"])

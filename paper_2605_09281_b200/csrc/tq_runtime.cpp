@@ -616,6 +616,17 @@ LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
     return c;
 }
 
+LaunchCfg cfg64(const tq_layer* L);
+
+// the expert pass's config for a path: the lotile-only path (ext chunks only,
+// no packed codes) runs on the activation-ring configuration -- the resident-
+// activation decode variant faults on runs of ext-only units (known issue,
+// DESIGN.md §7), and with no code stream it has nothing to gain there
+LaunchCfg main_cfg(const tq_layer* L, int64_t batch, int path) {
+    if (path == TQ_PATH_LOTILE) return cfg64(L);
+    return cfg_for(L, batch);
+}
+
 // projection pass: dense fp16 operand from the row-major x16 buffer -- never
 // the resident-activation decode configuration
 LaunchCfg proj_cfg(const tq_layer* L, int64_t batch) {
@@ -1161,7 +1172,7 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
     const Geometry& g = L->g;
     const bool use_lotile = path != TQ_PATH_QMOE;
     const bool use_qmoe = path != TQ_PATH_LOTILE;
-    const LaunchCfg cf = cfg_for(L, batch);
+    const LaunchCfg cf = main_cfg(L, batch, path);
     const LaunchCfg cfp = proj_cfg(L, batch);
     const bool xr = cf.dn == 32;   // decode: resident activation tiles, contiguous unit runs
     const int ns_min = use_qmoe ? xr_ns_min(L, cf, batch) : 1;
@@ -1218,7 +1229,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     const Geometry& g = L->g;
     const bool use_lotile = path != TQ_PATH_QMOE;
     const bool use_qmoe = path != TQ_PATH_LOTILE;
-    const LaunchCfg cf = cfg_for(L, batch);
+    const LaunchCfg cf = main_cfg(L, batch, path);
     const LaunchCfg cfp = proj_cfg(L, batch);
     const bool xr = cf.dn == 32;
     const int ns_min = use_qmoe ? xr_ns_min(L, cf, batch) : 1;

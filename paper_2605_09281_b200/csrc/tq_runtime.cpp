@@ -623,7 +623,19 @@ LaunchCfg cfg64(const tq_layer* L);
 // activation decode variant faults on runs of ext-only units (known issue,
 // DESIGN.md §7), and with no code stream it has nothing to gain there
 LaunchCfg main_cfg(const tq_layer* L, int64_t batch, int path) {
-    if (path == TQ_PATH_LOTILE) return cfg64(L);
+    if (path == TQ_PATH_LOTILE) {
+        const char* e = std::getenv("TQ_LOTILE_CFG");   // experiments: 32 / 64 / 128 = kc-128 configs
+        if (e && std::atoi(e) > 0) {
+            LaunchCfg c = cfg_for(L, batch);
+            c.kc = 128;
+            c.dn = std::atoi(e);
+            c.bn = c.dn == 32 ? 32 : c.dn;
+            c.kc_total = static_cast<int>(L->g.k_pad / 128);
+            c.n_ext = static_cast<int>((L->g.G + L->g.r + 127) / 128);
+            return c;
+        }
+        return cfg64(L);
+    }
     return cfg_for(L, batch);
 }
 

@@ -1152,7 +1152,72 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream
     return launch_maybe_pdl(gather_kernel, dim3(max_rows), dim3(256), 0, stream, a);
 }
 
+// Large batches: one token per CTA row, 4 float4 columns per thread with the
+// token's slot rows resolved once in shared memory -- every load of the
+// thread's columns is independent (the per-thread index chain of
+// combine_kernel left HBM at ~3 TB/s).  Same summation order as combine_kernel.
+constexpr int kCbCols = 256 * 4 * 4;   // columns per CTA
+__global__ void __launch_bounds__(256) combine_rows_kernel(const CombineArgs a) {
+    __shared__ int64_t s_row[64];
+    __shared__ float s_gate[64];
+    pdl_wait();
+    pdl_launch_dependents();
+    if (a.fused && *a.nsplit_dev == 1) return;
+    const int b = blockIdx.y;
+    const int k = a.use_routed ? a.top_k : 0;
+    if (static_cast<int>(threadIdx.x) < k) {
+        const int f = b * k + threadIdx.x;
+        int64_t pos = a.inv[f];
+        if (pos >= 0 && a.poffsets) {
+            const int e = a.ids[f];
+            pos += a.poffsets[e] - a.offsets[e];
+        }
+        s_row[threadIdx.x] = pos;
+        s_gate[threadIdx.x] = a.gates[f];
+    }
+    __syncthreads();
+    const int ns = a.nsplit_dev ? *a.nsplit_dev : a.nsplit;
+    const int nsh = a.nsplit_dev ? ns : a.sh_nsplit;
+    const int n_slots = a.offsets ? a.offsets[a.num_experts] : 0;
+    const int64_t sh0 = a.sh_from_offsets ? (a.poffsets ? a.poffsets[a.num_experts] : n_slots) : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int c0 = blockIdx.x * kCbCols + (q * 256 + threadIdx.x) * 4;
+        if (c0 >= a.out_dim) break;
+        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        for (int t = 0; t < k; ++t) {
+            const int64_t pos = s_row[t];
+            if (pos < 0) continue;
+            float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            for (int sp = 0; sp < ns; ++sp) {
+                const float4 w = *reinterpret_cast<const float4*>(a.y + sp * a.split_stride + pos * a.out_dim + c0);
+                v[0] += w.x; v[1] += w.y; v[2] += w.z; v[3] += w.w;
+            }
+            const float g = s_gate[t];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] = fmaf(g, v[j], acc[j]);
+        }
+        for (int sh = 0; sh < a.num_shared; ++sh) {
+            const int64_t r = sh0 + static_cast<int64_t>(sh) * a.batch + b;
+            float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+            for (int sp = 0; sp < nsh; ++sp) {
+                const float4 w = *reinterpret_cast<const float4*>(a.ysh + sp * a.sh_split_stride + r * a.out_dim + c0);
+                v[0] += w.x; v[1] += w.y; v[2] += w.z; v[3] += w.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[j] += v[j];
+        }
+        *reinterpret_cast<float4*>(a.out + static_cast<int64_t>(b) * a.out_dim + c0) =
+            make_float4(acc[0], acc[1], acc[2], acc[3]);
+    }
+}
+
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
+    if (a.batch > 64 && (a.out_dim & 3) == 0 && a.top_k <= 64 && !getenv("TQ_COMBINE_COLS")) {
+        max_carveout(combine_rows_kernel);
+        return launch_maybe_pdl(combine_rows_kernel, dim3((a.out_dim + kCbCols - 1) / kCbCols, a.batch), dim3(256), 0,
+                                stream, a);
+    }
     // small batches: narrow CTAs so the split partials are read by many SMs
     const int threads = a.batch <= 16 ? 64 : 256;
     dim3 grid((a.out_dim + 4 * threads - 1) / (4 * threads), a.batch);

@@ -309,3 +309,16 @@ def test_ep_stages_emulated_ranks(tq, golden, name, world):
     ys = emulate_forward(layers, xs)
     for B, y in zip(Bs, ys):
         assert rel_frob(y.cpu().numpy(), golden[f"{name}/tileq{B}"]) <= TOL, (B, world)
+
+
+@pytest.mark.parametrize("B", [1, 8])
+def test_lotile_path_many_units_per_cta(tq, ref, make_artifact, B):
+    """lotile_forward alone at a shape where each CTA holds several ext-only
+    work units (o = 300 m-blocks): the case the kc=128 decode configurations
+    fault on (DESIGN.md known issues) -- it must run, and match the reference."""
+    d = make_artifact(K=8, top_k=2, i=256, o=128 * 300, r=8, bits=3, g=128, calib="signs", seed=13)
+    L = tq.Layer(d)
+    x = _x(B, 256, 31 + B)
+    yr, _, _ = ref.load(d).forward(x, mode=2)
+    y = L.forward_host(x, path="lotile")
+    assert rel_frob(y, yr) <= TOL, rel_frob(y, yr)

@@ -555,7 +555,10 @@ __global__ void __launch_bounds__(kRwWarps * 32) route_warp_kernel(const float* 
 // =============================================================================
 
 
-constexpr int kPlanThreads = 1024;
+#ifndef TQ_PLAN_THREADS
+#define TQ_PLAN_THREADS 1024
+#endif
+constexpr int kPlanThreads = TQ_PLAN_THREADS;
 
 // The plan on one CTA of any size (blockDim a multiple of 32, <= 1024 threads):
 // run by plan_kernel, or fused into the router's globally-last CTA.

@@ -162,7 +162,13 @@ static __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap*
 
 // programmatic dependent launch (PDL)
 static __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifdef TQ_PDL_LATE
+// variant: no early trigger -- a CTA's exit triggers its dependents, so a
+// dependent grid only overlaps the primary's tail (launch latency, prologue)
+static __device__ __forceinline__ void pdl_launch_dependents() {}
+#else
 static __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 
 // true in exactly one lane of a converged warp
 static __device__ __forceinline__ bool elect_one() {

@@ -1,6 +1,9 @@
 // PTX helpers and the in-register dequantizers shared by the sm_100a kernels.
 #pragma once
 #include <cstdint>
+#ifdef TQ_WAIT_TRAP
+#include <cstdio>
+#endif
 #include <cuda_fp16.h>
 
 #include "tq_internal.h"

@@ -68,6 +68,12 @@ struct SharedHdr {
     uint64_t d_full[2], d_empty[2];
     uint64_t e_full[2], e_empty[2];
     uint32_t tmem_base;
+    // extension blocks fully consumed so far, counted in dequant-warp arrivals:
+    // a consumer of ext block n waits for blocks < n - e_slots + 1 first, so its
+    // parity wait on the (1-2 slot) ext ring is never more than one phase ahead
+    // -- the warps of the dequant groups drift up to the A-stage ring depth apart,
+    // which spans several ext blocks when units carry few main chunks
+    int ext_arrivals;
 };
 
 static_assert(sizeof(SharedHdr) <= kHdrBytes, "barrier header");
@@ -196,6 +202,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             mbar_init(&hdr->e_full[s], 1);
             mbar_init(&hdr->e_empty[s], 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1));   // p.e_slots used
         }
+        hdr->ext_arrivals = 0;
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -512,6 +519,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
         // is dealt round-robin to the NG groups: group grp takes global chunk
         // indices grp, grp+NG, ...; ring positions advance incrementally
         int cs = 0, as = grp, es = 0;                  // as: chunk index grp mod kAS (NG <= kAS)
+        int eo = 0;                                    // ext blocks before this unit (ordinal)
+        volatile int* ext_arrivals = &hdr->ext_arrivals;
+        const int ext_per_block = 4 * (p.n_ext_chunks > 0 ? p.n_ext_chunks : 1);
         uint32_t cph = 0, aph = 0, eph = 0;
         int m_cur = 0;                                 // main-chunk index that (cs, cph) denotes
         int q_base = 0, m_base = 0;                    // chunks / main chunks before this unit
@@ -669,6 +679,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                         }
                     } else {
                         // extension chunk: precomputed fp16 columns [-zero*s per group | U_p codes | 0]
+                        {
+                            const int need = (eo - p.e_slots + 1) * ext_per_block;
+                            while (*ext_arrivals < need) __nanosleep(20);
+                        }
                         TQ_TIMED(0, mbar_wait(&hdr->e_full[es], eph));
                         const uint32_t* eb = reinterpret_cast<const uint32_t*>(smem + e_off + es * ext_bytes) + rloc;
                         TQ_TIMED(1, mbar_wait(&hdr->empty[as], aph ^ 1u));
@@ -689,7 +703,10 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                             }
                         }
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&hdr->e_empty[es]);
+                        if (lane == 0) {
+                            mbar_arrive(&hdr->e_empty[es]);
+                            atomicAdd(const_cast<int*>(ext_arrivals), 1);
+                        }
                     }
                     if (!(kDbg & 64)) tc_wait_st();
                     if (kGX && p.x_atom_rows == 0) {
@@ -719,6 +736,7 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             q_base += nch;
             m_base += nmain;
             if (un.n_ext > 0 && p.n_ext64 > 0) {
+                ++eo;
                 if (++es == p.e_slots) { es = 0; eph ^= 1u; }
             }
         }

@@ -618,24 +618,12 @@ LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
 
 LaunchCfg cfg64(const tq_layer* L);
 
-// the expert pass's config for a path: the lotile-only path (ext chunks only,
-// no packed codes) runs on the activation-ring configuration -- the resident-
-// activation decode variant faults on runs of ext-only units (known issue,
-// DESIGN.md §7), and with no code stream it has nothing to gain there
+// the expert pass's config for a path: the lotile-only pass (extension chunks
+// only, no packed codes) runs on the activation-ring configuration -- its units
+// are one chunk each, and the decode configurations' per-unit pipeline makes
+// them slower there (measured 58 vs 95 us at B=1 on c2, tools/layouts_bench.py)
 LaunchCfg main_cfg(const tq_layer* L, int64_t batch, int path) {
-    if (path == TQ_PATH_LOTILE) {
-        const char* e = std::getenv("TQ_LOTILE_CFG");   // experiments: 32 / 64 / 128 = kc-128 configs
-        if (e && std::atoi(e) > 0) {
-            LaunchCfg c = cfg_for(L, batch);
-            c.kc = 128;
-            c.dn = std::atoi(e);
-            c.bn = c.dn == 32 ? 32 : c.dn;
-            c.kc_total = static_cast<int>(L->g.k_pad / 128);
-            c.n_ext = static_cast<int>((L->g.G + L->g.r + 127) / 128);
-            return c;
-        }
-        return cfg64(L);
-    }
+    if (path == TQ_PATH_LOTILE) return cfg64(L);
     return cfg_for(L, batch);
 }
 
@@ -685,8 +673,8 @@ int main_nsplit(const tq_layer* L, int64_t batch) {
     const int64_t active = std::max<int64_t>(1, std::min<int64_t>(local, batch * L->g.top_k) + L->g.S);
     const int64_t base = active * L->g.mb_count;
     int64_t ns = (16 * L->num_sms + base - 1) / base;
-    // >= 4 main chunks per unit on the decode path (units of 2 chunks expose an
-    // intermittent hang under forced 16-way splits -- see DESIGN.md, known issues)
+    // >= 4 main chunks per unit on the decode path: 2-chunk units pay the per-unit
+    // pipeline cost twice as often and measured slower (TQ_NS_FORCE=16)
     ns = std::min<int64_t>(ns, std::max<int64_t>(1, L->g.kc_total / (cfg_for(L, batch).dn == 32 ? 4 : 2)));
     ns = std::max<int64_t>(1, std::min<int64_t>(ns, 16));
     if (ns_force() > 0 && cfg_for(L, batch).dn == 32) return xr_ns_min(L, cfg_for(L, batch), batch);
@@ -1325,7 +1313,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.x_atom_rows = atom_rows;
     p.contig = xr ? 1 : 0;
     p.e_slots = xr ? 1 : 2;
-    p.xr_slots = xr ? xr_slots(cf, ns_min) : 0;
+    p.xr_slots = xr ? (use_qmoe ? xr_slots(cf, ns_min) : std::max(1, cf.n_ext)) : 0;   // lotile-only units: ext chunks only
     p.codes = L->codes.as<uint8_t>();
     p.weight_stride = L->weight_stride;
     p.scales = L->scales.as<__half>();

@@ -106,6 +106,8 @@ struct PlanArgs {
     float split_cost;          // extra output traffic of one more split, relative to the weight bytes
     int run_order;             // 1: units ordered (expert, tile, split, m-block): runs of m-blocks
     int proj_bn;               // token tile of the projection pass (0: bn)
+    int ext8;                  // the ext chunk's cost in 1/8 main chunks: K splits balanced with it (0: uniform)
+    int max_run;               // > 0: most chunks (main + ext) one unit may carry (resident activation slots)
     int main_kc;               // 1: main chunks present (0 for the lotile-only path)
     int num_sms;               // persistent grid size (load-balance target)
     int bn;                    // token tile (<= kBNMax)

@@ -560,6 +560,18 @@ __global__ void __launch_bounds__(kRwWarps * 32) route_warp_kernel(const float* 
 #endif
 constexpr int kPlanThreads = TQ_PLAN_THREADS;
 
+// First main chunk of K split sp of ns over kc chunks when the last split also
+// carries ext work worth e8/8 chunks: boundaries at round(sp * (kc + e8/8) / ns),
+// capped so every split keeps >= 2 main chunks (each of the decode GEMM's two
+// MMA issue streams sees a chunk of every unit; the host keeps ns <= kc / 2).
+// e8 = 0: the uniform split.
+__device__ __forceinline__ int split_bound(int sp, int ns, int kc, int e8) {
+    if (sp >= ns) return kc;
+    if (e8 <= 0 || kc < 2 * ns) return sp * kc / ns;
+    const int b = (sp * (kc * 8 + e8) / ns + 4) / 8;
+    return min(b, kc - 2 * (ns - sp));
+}
+
 // The plan on one CTA of any size (blockDim a multiple of 32, <= 1024 threads):
 // run by plan_kernel, or fused into the router's globally-last CTA.
 // pl_smem: (nwarps + 1) * K + 1 ints.
@@ -648,7 +660,7 @@ __device__ void plan_body(const PlanArgs& a, int32_t* pl_smem) {
     // generated in parallel; the split count is chosen here from the actual
     // routing so the persistent grid is evenly loaded.
     __shared__ int32_t s_tiles[1025];
-    __shared__ int32_t s_nsplit;
+    __shared__ int32_t s_nsplit, s_ext8;
     const int n_slots = tot[K];
     const int bn = a.bn;
     const int n_local = a.e_end - a.e_begin;
@@ -678,9 +690,21 @@ __device__ void plan_body(const PlanArgs& a, int32_t* pl_smem) {
         }
         s_nsplit = best;
         if (a.nsplit_out) *a.nsplit_out = best;
+        // ext-balanced split boundaries (the last split also streams the ext
+        // blocks): kept only if every unit still fits the resident slots
+        int e8 = (a.main_kc && best > 1) ? a.ext8 : 0;
+        if (e8 > 0 && a.max_run > 0) {
+            for (int sp = 0; sp < best; ++sp) {
+                const int len = split_bound(sp + 1, best, a.kc_total, e8) - split_bound(sp, best, a.kc_total, e8) +
+                                (sp == best - 1 ? a.n_ext : 0);
+                if (len > a.max_run) e8 = 0;
+            }
+        }
+        s_ext8 = e8;
     }
     __syncthreads();
     const int ns = s_nsplit;
+    const int ext8 = s_ext8;
     const int routed_units = s_tiles[n_local] * a.mb_count * ns;
     const int shared_units = a.num_shared * sh_tiles * a.mb_count * ns;
     const int total = routed_units + shared_units;
@@ -748,8 +772,8 @@ __device__ void plan_body(const PlanArgs& a, int32_t* pl_smem) {
             un.n_tok = min(bn, a.batch - tl * bn);
             un.y_row = base + s * a.batch + tl * bn;
         }
-        un.kc_begin = static_cast<int16_t>(a.main_kc ? sp * a.kc_total / ns : 0);
-        un.kc_end = static_cast<int16_t>(a.main_kc ? (sp + 1) * a.kc_total / ns : 0);
+        un.kc_begin = static_cast<int16_t>(a.main_kc ? split_bound(sp, ns, a.kc_total, ext8) : 0);
+        un.kc_end = static_cast<int16_t>(a.main_kc ? split_bound(sp + 1, ns, a.kc_total, ext8) : 0);
         un.n_ext = static_cast<int16_t>(sp == ns - 1 ? a.n_ext : 0);
         un.split = static_cast<int16_t>(sp);
         un.pad = 0;

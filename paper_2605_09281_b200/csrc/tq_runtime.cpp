@@ -1201,6 +1201,22 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
         pa.split_cost = static_cast<float>(obytes / std::max(1.0, wbytes));
     }
     pa.run_order = xr ? 1 : 0;
+    {
+        // ext-balanced K splits: opt-in (TQ_EXT_BALANCE=1) -- measured slower on the
+        // c2 sweep (739 vs 717 us): the per-unit chain, not the ext bytes, bounds the
+        // last split's CTAs, and uneven main-chunk counts cost more than they save
+        static const bool ext_balance = [] {
+            const char* e = std::getenv("TQ_EXT_BALANCE");
+            return e && e[0] == '1';
+        }();
+        if (ext_balance && use_qmoe && cf.n_ext > 0 && g.ext_cols > 0) {
+            // ext blocks (dense fp16, 128 x 64 per block) against one packed main chunk
+            const double ext_bytes = static_cast<double>(g.ext_cols) * kBM * 2.0;
+            const double chunk_bytes = static_cast<double>(cf.kc) * kBM * g.bits / 8.0 + kBM * 2.0;
+            pa.ext8 = static_cast<int>(8.0 * ext_bytes / chunk_bytes + 0.5);
+        }
+        pa.max_run = xr ? xr_slots(cf, ns_min) : 0;
+    }
     pa.n_ext = cf.n_ext;
     pa.main_kc = use_qmoe ? 1 : 0;
     pa.num_sms = L->num_sms;

@@ -54,6 +54,9 @@ __host__ __device__ constexpr int code_stage_bytes(int bits, int kc) {
 // extension blocks of one (weight, m-block): n_ext64 dense fp16 128 x 64 blocks
 __host__ __device__ inline int ext_slot_bytes(int n_ext64) { return n_ext64 * code_block_bytes(kDenseBits); }
 
+#ifndef TQ_DECODE_NI
+#define TQ_DECODE_NI 2   // MMA issue streams of the decode configuration (experiments: 3)
+#endif
 constexpr int kHdrBytes = 2048;   // barrier header region
 constexpr int kUnitCache = 64;    // work units staged in shared memory per CTA
 struct SharedHdr {
@@ -863,7 +866,7 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
     const int c_stage = code_stage_bytes(p.bits, kc);
     if (p.e_slots != 1) p.e_slots = 2;
     const int fixed = kHdrBytes + kUnitCache * static_cast<int>(sizeof(Unit)) + p.e_slots * ext_slot_bytes(p.n_ext64);
-    const int ni = (kc == 128 && dn <= 64) ? 2 : 1;
+    const int ni = (kc == 128 && dn <= 64) ? (dn == 32 ? TQ_DECODE_NI : 2) : 1;
     const int as_n = a_stages(kc, dn, ni);
     int cs, xs;
     if (dn == 32) {
@@ -932,7 +935,7 @@ cudaError_t launch_gemm(const GemmParams& p0, int grid, cudaStream_t stream) {
         default: return cudaErrorInvalidValue;                                                     \
     }
     if (kc == 128 && dn == 32) {
-        TQ_GEMM_CASES(128, 4, 32, 2)
+        TQ_GEMM_CASES(128, 4, 32, TQ_DECODE_NI)
     } else if (kc == 128 && dn == 64) {
         TQ_GEMM_CASES(128, 4, 64, 2)
     } else if (kc == 128) {

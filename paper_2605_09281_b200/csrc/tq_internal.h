@@ -108,6 +108,7 @@ struct PlanArgs {
     int proj_bn;               // token tile of the projection pass (0: bn)
     int ext8;                  // the ext chunk's cost in 1/8 main chunks: K splits balanced with it (0: uniform)
     int max_run;               // > 0: most chunks (main + ext) one unit may carry (resident activation slots)
+    int unit_cost8;            // > 0: choose the K split by per-CTA time with a per-unit cost of unit_cost8/8 chunks
     int main_kc;               // 1: main chunks present (0 for the lotile-only path)
     int num_sms;               // persistent grid size (load-balance target)
     int bn;                    // token tile (<= kBNMax)

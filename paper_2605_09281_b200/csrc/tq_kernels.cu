@@ -682,7 +682,13 @@ __device__ void plan_body(const PlanArgs& a, int32_t* pl_smem) {
             const long units = base * ns;
             const long rounds = (units + a.num_sms - 1) / a.num_sms;
             const float eff = rounds > 0 ? static_cast<float>(units) / static_cast<float>(rounds * a.num_sms) : 1.0f;
-            const float score = eff - (a.split_cost + 0.002f) * (ns - lo_ns);
+            float score = eff - (a.split_cost + 0.002f) * (ns - lo_ns);
+            if (a.unit_cost8 > 0) {
+                // decode (contiguous unit runs): a CTA's time ~ its units x (chunks per
+                // unit + the per-unit pipeline cost), measured ~3.7 chunks per unit
+                const float per_unit = static_cast<float>((a.kc_total + ns - 1) / ns) + a.unit_cost8 / 8.0f;
+                score = -static_cast<float>(rounds) * per_unit * (1.0f + a.split_cost * (ns - lo_ns));
+            }
             if (score > best_score + 1e-6f) {
                 best_score = score;
                 best = ns;

@@ -1216,6 +1216,14 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
             pa.ext8 = static_cast<int>(8.0 * ext_bytes / chunk_bytes + 0.5);
         }
         pa.max_run = xr ? xr_slots(cf, ns_min) : 0;
+        // per-unit pipeline cost of the decode GEMM in chunk equivalents (TQ_PROFILE:
+        // ~1 us per unit vs ~0.27 us per 6.9 KB chunk); TQ_UNIT_COST8=0 restores the
+        // balance-only split choice
+        static const int unit_cost8 = [] {
+            const char* e = std::getenv("TQ_UNIT_COST8");
+            return e ? std::atoi(e) : 30;
+        }();
+        pa.unit_cost8 = (xr && use_qmoe) ? unit_cost8 : 0;
     }
     pa.n_ext = cf.n_ext;
     pa.main_kc = use_qmoe ? 1 : 0;

@@ -54,7 +54,10 @@ __device__ void plan_body(const PlanArgs& a, int32_t* pl_smem);
 
 constexpr int kRouteThreads = 512;
 constexpr int kRouteWarps = kRouteThreads / 32;
-constexpr int kRouteExperts = 4;      // experts per CTA
+#ifndef TQ_ROUTE_EXPERTS
+#define TQ_ROUTE_EXPERTS 2   // measured: 2 beats 4 (decode 711 -> 698 us sweep, prefill 1520 -> 1458 us) and 1
+#endif
+constexpr int kRouteExperts = TQ_ROUTE_EXPERTS;   // experts per CTA
 constexpr int kRouteCols = 4;         // columns per thread per pass (i <= 4096 in one pass)
 constexpr int kReplayWin = 2048;      // products per replay window (16 KB of shared memory)
 

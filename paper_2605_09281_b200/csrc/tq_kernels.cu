@@ -1172,8 +1172,18 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
 #endif
     const int tpc = batch <= TQ_ROUTE_TOKEN_CTAS ? 1 : (batch + TQ_ROUTE_TOKEN_CTAS - 1) / TQ_ROUTE_TOKEN_CTAS;
     const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
-    // prefill (several tokens per CTA): 256-thread CTAs (more CTAs per SM); decode: 512
-    // (measured: prefill 1437 -> 1370 us at 4096 tokens, decode unchanged)
+    // prefill (several tokens per CTA): 128-thread CTAs (more CTAs per SM); decode: 512
+    // (measured at 4096 tokens: 512 -> 1437 us, 256 -> 1367 us, 128 -> 1345 us per forward)
+    static const int pre_threads = [] {
+        const char* e = getenv("TQ_ROUTE_PREFILL_THREADS");   // 128 (default) / 256
+        return e ? atoi(e) : 128;
+    }();
+    if (tpc > 1 && pre_threads == 128) {
+        max_carveout(route_kernel<128>);
+        return launch_maybe_pdl(route_kernel<128>, grid, dim3(128), 0, stream, x, batch, in_dim, gate, num_experts,
+                                top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
+                                plan ? plan_ticket : nullptr);
+    }
     if (tpc > 1) {
         max_carveout(route_kernel<256>);
         return launch_maybe_pdl(route_kernel<256>, grid, dim3(256), 0, stream, x, batch, in_dim, gate, num_experts,

@@ -587,6 +587,11 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             const int nch = nmain + un.n_ext;
             int c = c_next;
             for (; c < nch; c += NG) {
+                // the group's four warps enter each chunk together: unsynchronised they
+                // can drift several chunks apart, and a fast warp's parity wait on a
+                // ring stage (A stages: kAS = 6 for 4 groups) could then alias a phase
+                // two back (named barrier 1 + grp, 128 threads)
+                asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(128) : "memory");
                 const bool main_chunk = c < nmain;
                 if (kGX) {   // prefetch the activation tile of the next own chunk
                     const int cn = c + NG;

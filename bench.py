@@ -192,7 +192,7 @@ def make_tokens(B: int, i: int, seed: int) -> np.ndarray:
 def artifact_for(config: str, rank: int, world: int) -> str:
     from paper_2605_09281_b200 import synth
     root = os.environ.get("TILEQ_ARTIFACT_ROOT", "/tmp/tileq_artifacts")
-    path = os.path.join(root, f"{config}_folded_s0")
+    path = synth.config_path(config, root)
     if rank == 0:
         synth.ensure_config(config, root=root)
     if world > 1:
@@ -432,6 +432,8 @@ def bench_tileq(args, rank, world, local_rank):
             "per_batch": per_b, "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_forward": launches / max(1, args.steps * len(batches)),
             "gemm_launches_per_forward": launches_per_fwd, "clocks": clk, "clock_settle_steps": settle}
+    if os.environ.get("TQ_BENCH_RETRY"):
+        line["retry_after_fault"] = os.environ["TQ_BENCH_RETRY"]
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, art, geo)
     print(json.dumps(line), flush=True)
@@ -535,7 +537,21 @@ def main():
             dist.destroy_process_group()
     if args.impl == "reference":
         return bench_reference(args, 0, 1)
-    return bench_tileq(args, 0, 1, local_rank)
+    try:
+        return bench_tileq(args, 0, 1, local_rank)
+    except Exception as e:   # noqa: BLE001
+        # An intermittent device fault of the decode GEMM ("known
+        # issue") poisons the CUDA context; re-run the bench ONCE in a fresh
+        # process and record the fault in its JSON line (never silently).
+        msg = f"{type(e).__name__}: {str(e).splitlines()[0] if str(e) else ''}"
+        if "CUDA" not in msg and "cuda" not in msg:
+            raise
+        if os.environ.get("TQ_BENCH_RETRY"):
+            raise
+        print(f"bench: device fault ({msg}); re-running once in a fresh process", file=sys.stderr, flush=True)
+        import subprocess
+        env = dict(os.environ, TQ_BENCH_RETRY=msg[:200])
+        return subprocess.run([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env).returncode
 
 
 if __name__ == "__main__":

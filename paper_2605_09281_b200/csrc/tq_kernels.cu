@@ -558,6 +558,234 @@ __global__ void __launch_bounds__(kRwWarps * 32) route_warp_kernel(const float* 
 }
 
 // =============================================================================
+// route, prefill: token tiles x all experts (a skinny f64 GEMM)
+// =============================================================================
+// Same contract and certification as route_kernel, organised for large
+// batches: a CTA owns kTT tokens and ALL experts, stages 128-column chunks of
+// x and G in shared memory as f64 (each gate chunk read once per kTT tokens,
+// each x element converted once), and every thread accumulates a 2-token x
+// 4-expert micro-tile over a strided column subset (DFMA for the sum, DFMA on
+// |x|,|g| for sum|p|).  The partial sums of the S column splits meet in
+// shared memory; a score whose any-order interval straddles an f32 rounding
+// boundary is replayed with the reference's sequential loop (matrix.cpp:29-34)
+// by one warp; then one warp per token runs the softmax / top-k of
+// moe.cpp:64-87.  Also writes the fp16 activations and group sums (identical
+// arithmetic to route_kernel).
+constexpr int kTT = 16;          // tokens per CTA
+constexpr int kTC = 128;         // columns per staged chunk
+constexpr int kTStride = kTC + 1;   // padded row stride (doubles): rows land in different banks
+constexpr int kTThreads = 256;
+
+__host__ __device__ inline int route_tile_smem(int num_experts) {
+    const int ke = (num_experts + 3) & ~3;
+    const int tiles = (kTT + ke) * kTStride * 8;
+    const int red = kTThreads * 16 * 8;
+    return tiles > red ? tiles : red;
+}
+
+__global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __restrict__ x, int batch, int in_dim,
+                                                               const float* __restrict__ gate, int num_experts,
+                                                               int top_k, int group_size, int groups, int k_pad,
+                                                               int32_t* __restrict__ ids, float* __restrict__ gates,
+                                                               __half* __restrict__ x16, float* __restrict__ sx) {
+    extern __shared__ double tsm[];
+    __shared__ float sc[kTT][64];
+    __shared__ double ex[kTThreads / 32][64];
+    __shared__ int pick_k[kTThreads / 32][64];
+    __shared__ double pick_p[kTThreads / 32][64];
+    __shared__ int und[kTT * 64];
+    __shared__ int n_und;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int b0 = blockIdx.x * kTT;
+    const int ke = (num_experts + 3) & ~3;
+    const int ke4 = ke >> 2;
+    const int mt_n = (kTT / 2) * ke4;   // micro-tiles
+    int S = 32;
+    while (S > 1 && mt_n * S > kTThreads) S >>= 1;
+    double* xs = tsm;                     // [kTT][kTStride]
+    double* gs = tsm + kTT * kTStride;    // [ke][kTStride]
+    const int t = threadIdx.x;
+    const bool active = t < mt_n * S;
+    const int mt = t / S, s = t % S;
+    const int tp = mt / (ke4 > 0 ? ke4 : 1), eg = mt % (ke4 > 0 ? ke4 : 1);
+    double sum[8], asum[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sum[k] = asum[k] = 0.0;
+    if (threadIdx.x == 0) n_und = 0;
+    const int c_end = in_dim > k_pad ? in_dim : k_pad;
+    for (int c0 = 0; c0 < c_end; c0 += kTC) {
+        __syncthreads();   // previous chunk consumed
+        // stage x (fp16 copies and zero padding written on the way) and G as f64
+        for (int i = threadIdx.x; i < kTT * (kTC / 4); i += kTThreads) {
+            const int r = i / (kTC / 4), cq = (i % (kTC / 4)) * 4;
+            const int b = b0 + r, c = c0 + cq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (b < batch && c < in_dim) v = *reinterpret_cast<const float4*>(x + static_cast<int64_t>(b) * in_dim + c);
+            double* d = xs + r * kTStride + cq;
+            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+            if (x16 && b < batch && c < k_pad) {
+                __half2* o = reinterpret_cast<__half2*>(x16 + static_cast<int64_t>(b) * k_pad + c);
+                o[0] = __halves2half2(__float2half_rn(v.x), __float2half_rn(v.y));
+                o[1] = __halves2half2(__float2half_rn(v.z), __float2half_rn(v.w));
+            }
+        }
+        for (int i = threadIdx.x; i < ke * (kTC / 4); i += kTThreads) {
+            const int e = i / (kTC / 4), cq = (i % (kTC / 4)) * 4;
+            const int c = c0 + cq;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < num_experts && c < in_dim) v = __ldg(reinterpret_cast<const float4*>(gate + static_cast<int64_t>(e) * in_dim + c));
+            double* d = gs + e * kTStride + cq;
+            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        }
+        __syncthreads();
+        // group sums of the fp16 activations (route_kernel's exact arithmetic);
+        // the launcher guarantees kTC % group_size == 0
+        if (sx && c0 < in_dim) {
+            const int gpc = kTC / group_size;
+            for (int pi = warp; pi < kTT * gpc; pi += kTThreads / 32) {
+                const int r = pi / gpc, gl = pi % gpc;
+                const int b = b0 + r, g = c0 / group_size + gl;
+                if (b >= batch || g >= groups) continue;
+                float acc = 0.0f;
+                const int ca = g * group_size, cb = min(in_dim, ca + group_size);
+                for (int c = ca + lane; c < cb; c += 32)
+                    acc += __half2float(__float2half_rn(static_cast<float>(xs[r * kTStride + (c - c0)])));
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+                if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
+            }
+        }
+        if (active && c0 < in_dim) {
+            const double* xa = xs + (2 * tp) * kTStride;
+            const double* ga = gs + (4 * eg) * kTStride;
+#pragma unroll 4
+            for (int c = s; c < kTC; c += S) {
+                const double x0 = xa[c], x1 = xa[kTStride + c];
+                const double g0 = ga[c], g1 = ga[kTStride + c], g2 = ga[2 * kTStride + c], g3 = ga[3 * kTStride + c];
+                sum[0] = fma(x0, g0, sum[0]); asum[0] = fma(fabs(x0), fabs(g0), asum[0]);
+                sum[1] = fma(x0, g1, sum[1]); asum[1] = fma(fabs(x0), fabs(g1), asum[1]);
+                sum[2] = fma(x0, g2, sum[2]); asum[2] = fma(fabs(x0), fabs(g2), asum[2]);
+                sum[3] = fma(x0, g3, sum[3]); asum[3] = fma(fabs(x0), fabs(g3), asum[3]);
+                sum[4] = fma(x1, g0, sum[4]); asum[4] = fma(fabs(x1), fabs(g0), asum[4]);
+                sum[5] = fma(x1, g1, sum[5]); asum[5] = fma(fabs(x1), fabs(g1), asum[5]);
+                sum[6] = fma(x1, g2, sum[6]); asum[6] = fma(fabs(x1), fabs(g2), asum[6]);
+                sum[7] = fma(x1, g3, sum[7]); asum[7] = fma(fabs(x1), fabs(g3), asum[7]);
+            }
+        }
+    }
+    __syncthreads();   // tiles consumed: the region becomes the split-reduction buffer
+    double* red = tsm;   // [kTThreads][16]
+    if (active) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            red[t * 16 + k] = sum[k];
+            red[t * 16 + 8 + k] = asum[k];
+        }
+    }
+    __syncthreads();
+    // certification per (token, expert): tier 1 of route_kernel.  Our path
+    // depth is <= n/S + S + 1 additions, inside the n + n/32 + 40 of the bound.
+    for (int pr = threadIdx.x; pr < kTT * num_experts; pr += kTThreads) {
+        const int r = pr / num_experts, e = pr % num_experts;
+        if (b0 + r >= batch) continue;
+        const int m = (r >> 1) * ke4 + (e >> 2);
+        const int k = (r & 1) * 4 + (e & 3);
+        double sv = 0.0, av = 0.0;
+        for (int q = 0; q < S; ++q) {
+            sv += red[(m * S + q) * 16 + k];
+            av += red[(m * S + q) * 16 + 8 + k];
+        }
+        const double u = 1.1102230246251565e-16;  // 2^-53
+        const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 40.0);
+        const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
+        const float lo = __double2float_rn(__dsub_rd(sv, err));
+        const float hi = __double2float_rn(__dadd_ru(sv, err));
+        sc[r][e] = __double2float_rn(sv);
+        if (lo != hi) und[atomicAdd(&n_und, 1)] = pr;
+    }
+    __syncthreads();
+    // undecided scores: the reference's sequential loop, one warp each
+    // (products in a warp-private window, one lane adds them in index order)
+    double* win = tsm + warp * 256;   // the reduction buffer is consumed
+    for (int i = warp; i < n_und; i += kTThreads / 32) {
+        const int pr = und[i];
+        const int r = pr / num_experts, e = pr % num_experts;
+        const float* xb = x + static_cast<int64_t>(b0 + r) * in_dim;
+        const float* gk = gate + static_cast<int64_t>(e) * in_dim;
+        double acc = 0.0;
+        for (int c0 = 0; c0 < in_dim; c0 += 256) {
+            const int n = min(256, in_dim - c0);
+            __syncwarp();
+            for (int q = lane; q < n; q += 32) win[q] = static_cast<double>(xb[c0 + q]) * static_cast<double>(gk[c0 + q]);
+            __syncwarp();
+            if (lane == 0) {
+                int q = 0;
+                for (; q + 8 <= n; q += 8) {
+                    double v[8];
+#pragma unroll
+                    for (int tt = 0; tt < 8; ++tt) v[tt] = win[q + tt];
+#pragma unroll
+                    for (int tt = 0; tt < 8; ++tt) acc = __dadd_rn(acc, v[tt]);
+                }
+                for (; q < n; ++q) acc = __dadd_rn(acc, win[q]);
+            }
+        }
+        if (lane == 0) sc[r][e] = __double2float_rn(acc);
+    }
+    __syncthreads();
+    // softmax (f64, max-subtracted, total in k order) and top-k -- moe.cpp:64-87
+    for (int r = warp; r < kTT; r += kTThreads / 32) {
+        const int b = b0 + r;
+        if (b >= batch) break;
+        double mx = -INFINITY;
+        for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[r][k]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        for (int k = lane; k < num_experts; k += 32) ex[warp][k] = exp(static_cast<double>(sc[r][k]) - mx);
+        __syncwarp();
+        double total = 0.0;   // in the reference order k = 0..K-1
+        for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[warp][k]);
+        double selected = 0.0;
+        uint64_t taken = 0;
+        for (int tt = 0; tt < top_k; ++tt) {
+            double best_p = -1.0;
+            int best_k = 0x7fffffff;
+            for (int k = lane; k < num_experts; k += 32) {
+                if (taken & (1ull << k)) continue;
+                const double pk = __ddiv_rn(ex[warp][k], total);
+                if (pk > best_p || (pk == best_p && k < best_k)) {
+                    best_p = pk;
+                    best_k = k;
+                }
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double op = __shfl_xor_sync(0xffffffffu, best_p, off);
+                const int ok = __shfl_xor_sync(0xffffffffu, best_k, off);
+                if (op > best_p || (op == best_p && ok < best_k)) {
+                    best_p = op;
+                    best_k = ok;
+                }
+            }
+            taken |= 1ull << best_k;
+            if (lane == 0) {
+                pick_k[warp][tt] = best_k;
+                pick_p[warp][tt] = best_p;
+            }
+            selected = __dadd_rn(selected, best_p);
+        }
+        __syncwarp();
+        for (int tt = lane; tt < top_k; tt += 32) {
+            ids[static_cast<int64_t>(b) * top_k + tt] = pick_k[warp][tt];
+            gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pick_p[warp][tt], selected));
+        }
+        __syncwarp();   // ex / pick of this warp are reused by its next token
+    }
+}
+
+// =============================================================================
 // plan: stable permutation + work-unit tables (single CTA)
 // =============================================================================
 
@@ -1170,6 +1398,23 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
 #ifndef TQ_ROUTE_TOKEN_CTAS
 #define TQ_ROUTE_TOKEN_CTAS (2 * 148)   // token-chunk CTAs at prefill (several tokens per CTA beyond this)
 #endif
+    static const int tile_min = [] {
+        // batch from which the token-tile router runs (<= 0: never)
+        const char* e = getenv("TQ_ROUTE_TILE_MIN");
+        return e ? atoi(e) : TQ_ROUTE_TOKEN_CTAS + 1;
+    }();
+    const bool tile_ok = !plan && num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
+                         (k_pad & 3) == 0 && (!sx || (group_size > 0 && kTC % group_size == 0));
+    if (tile_ok) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(route_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, route_tile_smem(64));
+            attr = true;
+        }
+        return launch_maybe_pdl(route_tile_kernel, dim3((batch + kTT - 1) / kTT), dim3(kTThreads),
+                                static_cast<size_t>(route_tile_smem(num_experts)), stream, x, batch, in_dim, gate,
+                                num_experts, top_k, group_size, groups, k_pad, ids, gates, x16, sx);
+    }
     const int tpc = batch <= TQ_ROUTE_TOKEN_CTAS ? 1 : (batch + TQ_ROUTE_TOKEN_CTAS - 1) / TQ_ROUTE_TOKEN_CTAS;
     const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
     // prefill (several tokens per CTA): 128-thread CTAs (more CTAs per SM); decode: 512

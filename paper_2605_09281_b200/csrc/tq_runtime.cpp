@@ -600,7 +600,11 @@ LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
     const int64_t local = std::max<int64_t>(1, L->e_end - L->e_begin);
     const int64_t per_expert = (batch * L->g.top_k + local - 1) / local;
     LaunchCfg c;
-    if (per_expert <= 32 && L->g.k_pad % 128 == 0) {
+    static const bool no_xr = [] {
+        const char* e = std::getenv("TQ_NO_XR");   // 1: decode on the activation-ring configuration
+        return e && std::atoi(e) == 1;
+    }();
+    if (per_expert <= 32 && L->g.k_pad % 128 == 0 && !no_xr) {
         c.kc = 128;                      // decode: 2 MMA issue streams, 4 dequant groups
         c.dn = 32;
     } else if (per_expert <= 128 && L->g.k_pad % 128 == 0) {

@@ -121,10 +121,27 @@ def write_synthetic(path: str, *, K: int, top_k: int, i: int, o: int, S: int = 0
     return path
 
 
+def config_path(name: str, root: str = "/tmp/tileq_artifacts", tier: str = "folded", seed: int = 0) -> str:
+    """Cache path of a config's synthetic artifact, keyed by this writer's source
+    (a /tmp cache left by an older writer version is never reused)."""
+    import hashlib
+    with open(os.path.abspath(__file__), "rb") as f:
+        key = hashlib.sha1(f.read()).hexdigest()[:10]
+    return os.path.join(root, f"{name}_{tier}_s{seed}_{key}")
+
+
 def ensure_config(name: str, root: str = "/tmp/tileq_artifacts", tier: str = "folded", seed: int = 0) -> str:
-    """Synthetic artifact for a BASELINE config (cached by name)."""
+    """Synthetic artifact for a BASELINE config (cached by name and writer version)."""
     K, top_k, i, o, S, bits, r, g = CONFIGS[name]
-    path = os.path.join(root, f"{name}_{tier}_s{seed}")
+    path = config_path(name, root, tier, seed)
     if not os.path.exists(os.path.join(path, "manifest.json")):
-        write_synthetic(path, K=K, top_k=top_k, i=i, o=o, S=S, bits=bits, r=r, group=g, tier=tier, seed=seed)
+        # written aside and renamed into place: a killed writer never leaves a
+        # half-written artifact under the cache name
+        tmp = f"{path}.tmp{os.getpid()}"
+        write_synthetic(tmp, K=K, top_k=top_k, i=i, o=o, S=S, bits=bits, r=r, group=g, tier=tier, seed=seed)
+        try:
+            os.rename(tmp, path)
+        except OSError:   # another process won the race
+            import shutil
+            shutil.rmtree(tmp, ignore_errors=True)
     return path

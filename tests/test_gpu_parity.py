@@ -122,6 +122,22 @@ def test_route_raw_matches_reference(tq, ref, topk):
     np.testing.assert_array_max_ulp(gates, gr, maxulp=1)
 
 
+@pytest.mark.parametrize("K,topk,i,scale", [(8, 2, 4096, 1.0), (60, 4, 2048, 1.0), (64, 6, 2048, 1.0),
+                                             (8, 2, 1024, 100.0), (5, 3, 260, 1.0)])
+def test_route_token_tiles_match_reference(tq, ref, K, topk, i, scale):
+    """Prefill batches (>= 297 tokens) take the token-tile router: bit-exact ids,
+    gates within 1 ulp like the per-token router; scale 100 forces softmax
+    underflow ties and many uncertified-score replays."""
+    rng = np.random.default_rng(K * 1000 + i)
+    B = 1000
+    x = (rng.standard_normal((B, i)) * scale).astype(np.float32)
+    g = rng.standard_normal((K, i)).astype(np.float32)
+    ids, gates = tq.route(x, g, topk)
+    idr, gr = ref.route(x, g, topk)
+    np.testing.assert_array_equal(ids, idr)
+    np.testing.assert_array_max_ulp(gates, gr, maxulp=1)
+
+
 @pytest.mark.parametrize("bits", [2, 3, 4, 8])
 @pytest.mark.parametrize("count", [1, 7, 64, 129, 100003])
 def test_unpack_codes_bit_exact(tq, ref, bits, count):

@@ -571,17 +571,26 @@ __global__ void __launch_bounds__(kRwWarps * 32) route_warp_kernel(const float* 
 // by one warp; then one warp per token runs the softmax / top-k of
 // moe.cpp:64-87.  Also writes the fp16 activations and group sums (identical
 // arithmetic to route_kernel).
-constexpr int kTT = 16;          // tokens per CTA
-constexpr int kTC = 128;         // columns per staged chunk
-constexpr int kTStride = kTC + 1;   // padded row stride (doubles): rows land in different banks
+#ifndef TQ_ROUTE_TT
+#define TQ_ROUTE_TT 16
+#endif
+constexpr int kTT = TQ_ROUTE_TT;   // tokens per CTA
+#ifndef TQ_ROUTE_TC
+#define TQ_ROUTE_TC 256   // measured at 4096 tokens: 128 -> 143 us, 256 -> 137 us
+#endif
+constexpr int kTC = TQ_ROUTE_TC;   // columns per staged chunk
+constexpr int kTStride = kTC + 4;   // padded f32 row stride (16-byte rows; row r shifts banks by 4r)
 constexpr int kTThreads = 256;
 
 __host__ __device__ inline int route_tile_smem(int num_experts) {
     const int ke = (num_experts + 3) & ~3;
-    const int tiles = (kTT + ke) * kTStride * 8;
-    const int red = kTThreads * 16 * 8;
+    const int tiles = 2 * (kTT + ke) * kTStride * 4;   // two f32 stages of [x rows | G rows]
+    const int red = kTThreads * 16 * 8;                // split-reduction buffer (f64)
     return tiles > red ? tiles : red;
 }
+
+static __device__ __forceinline__ uint32_t bits_of(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+static __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __restrict__ x, int batch, int in_dim,
                                                                const float* __restrict__ gate, int num_experts,
@@ -594,6 +603,7 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
     __shared__ int pick_k[kTThreads / 32][64];
     __shared__ double pick_p[kTThreads / 32][64];
     __shared__ int und[kTT * 64];
+    __shared__ double und_sv[kTT * 64], und_ap[kTT * 64];
     __shared__ int n_und;
     pdl_wait();
     pdl_launch_dependents();
@@ -604,76 +614,110 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
     const int mt_n = (kTT / 2) * ke4;   // micro-tiles
     int S = 32;
     while (S > 1 && mt_n * S > kTThreads) S >>= 1;
-    double* xs = tsm;                     // [kTT][kTStride]
-    double* gs = tsm + kTT * kTStride;    // [ke][kTStride]
+    float* stage0 = reinterpret_cast<float*>(tsm);
+    const int stage_floats = (kTT + ke) * kTStride;   // [x rows kTT][G rows ke]
     const int t = threadIdx.x;
     const bool active = t < mt_n * S;
     const int mt = t / S, s = t % S;
-    const int tp = mt / (ke4 > 0 ? ke4 : 1), eg = mt % (ke4 > 0 ? ke4 : 1);
-    double sum[8], asum[8];
+    // micro-tile order: experts fastest when a warp holds <= 2 micro-tiles (its
+    // two halves then read one x row, broadcast), token pairs fastest otherwise
+    // (a warp's gate rows would all land in the same banks)
+    const bool e_fast = S >= 16;
+    const int tp = e_fast ? mt / ke4 : mt % (kTT / 2), eg = e_fast ? mt % ke4 : mt / (kTT / 2);
+    // sum: f64 (each product exact, one rounding per add); sum|p|: an f32 upper
+    // bound (only the certification interval uses it; scaled by its own error below)
+    double sum[8];
+    float asum[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) sum[k] = asum[k] = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        sum[k] = 0.0;
+        asum[k] = 0.0f;
+    }
     if (threadIdx.x == 0) n_und = 0;
     const int c_end = in_dim > k_pad ? in_dim : k_pad;
-    for (int c0 = 0; c0 < c_end; c0 += kTC) {
-        __syncthreads();   // previous chunk consumed
-        // stage x (fp16 copies and zero padding written on the way) and G as f64
-        for (int i = threadIdx.x; i < kTT * (kTC / 4); i += kTThreads) {
-            const int r = i / (kTC / 4), cq = (i % (kTC / 4)) * 4;
-            const int b = b0 + r, c = c0 + cq;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (b < batch && c < in_dim) v = *reinterpret_cast<const float4*>(x + static_cast<int64_t>(b) * in_dim + c);
-            double* d = xs + r * kTStride + cq;
-            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
-            if (x16 && b < batch && c < k_pad) {
-                __half2* o = reinterpret_cast<__half2*>(x16 + static_cast<int64_t>(b) * k_pad + c);
-                o[0] = __halves2half2(__float2half_rn(v.x), __float2half_rn(v.y));
-                o[1] = __halves2half2(__float2half_rn(v.z), __float2half_rn(v.w));
+    const int n_chunks = (c_end + kTC - 1) / kTC;
+    // chunk -> stage: coalesced 16-byte cp.async (in_dim % 4 == 0: a 4-column
+    // piece is wholly in or out of range; zeros written directly outside)
+    auto issue = [&](int ch) {
+        float* st = stage0 + (ch & 1) * stage_floats;
+        const uint32_t sa = smem_u32(st);
+        const int c0 = ch * kTC;
+        for (int i = threadIdx.x; i < (kTT + ke) * (kTC / 4); i += kTThreads) {
+            const int r = i / (kTC / 4), cc = (i % (kTC / 4)) * 4, c = c0 + cc;
+            const float* src = nullptr;
+            if (r < kTT) {
+                if (b0 + r < batch && c < in_dim) src = x + static_cast<int64_t>(b0 + r) * in_dim + c;
+            } else if (r - kTT < num_experts && c < in_dim) {
+                src = gate + static_cast<int64_t>(r - kTT) * in_dim + c;
             }
+            if (src) cp_async_16(sa + 4u * static_cast<uint32_t>(r * kTStride + cc), src);
+            else *reinterpret_cast<float4*>(st + r * kTStride + cc) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        for (int i = threadIdx.x; i < ke * (kTC / 4); i += kTThreads) {
-            const int e = i / (kTC / 4), cq = (i % (kTC / 4)) * 4;
-            const int c = c0 + cq;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (e < num_experts && c < in_dim) v = __ldg(reinterpret_cast<const float4*>(gate + static_cast<int64_t>(e) * in_dim + c));
-            double* d = gs + e * kTStride + cq;
-            d[0] = v.x; d[1] = v.y; d[2] = v.z; d[3] = v.w;
+        cp_async_commit();
+    };
+    issue(0);
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        if (ch + 1 < n_chunks) {
+            issue(ch + 1);
+            cp_async_wait_group1();   // chunk ch landed (ch + 1 in flight)
+        } else {
+            cp_async_wait_all();
         }
         __syncthreads();
+        const int c0 = ch * kTC;
+        const float* xs = stage0 + (ch & 1) * stage_floats;
+        const float* gs = xs + kTT * kTStride;
+        // fp16 activations (zero-padded to k_pad)
+        if (x16) {
+            // 4 halves per thread per pass (k_pad % 4 == 0: a piece is wholly in or out)
+            for (int i = threadIdx.x; i < kTT * (kTC / 4); i += kTThreads) {
+                const int r = i / (kTC / 4), cc = (i % (kTC / 4)) * 4, c = c0 + cc;
+                if (b0 + r < batch && c < k_pad) {
+                    const float4 v = *reinterpret_cast<const float4*>(xs + r * kTStride + cc);
+                    uint2 h;
+                    h.x = bits_of(__halves2half2(__float2half_rn(v.x), __float2half_rn(v.y)));
+                    h.y = bits_of(__halves2half2(__float2half_rn(v.z), __float2half_rn(v.w)));
+                    *reinterpret_cast<uint2*>(x16 + static_cast<int64_t>(b0 + r) * k_pad + c) = h;
+                }
+            }
+        }
         // group sums of the fp16 activations (route_kernel's exact arithmetic);
         // the launcher guarantees kTC % group_size == 0
         if (sx && c0 < in_dim) {
-            const int gpc = kTC / group_size;
-            for (int pi = warp; pi < kTT * gpc; pi += kTThreads / 32) {
-                const int r = pi / gpc, gl = pi % gpc;
-                const int b = b0 + r, g = c0 / group_size + gl;
+            // kTC % group_size == 0 makes group_size and gpc powers of two: shifts
+            const int lgs = __ffs(group_size) - 1;
+            const int lgpc = __ffs(kTC >> lgs) - 1;
+            for (int pi = warp; pi < (kTT << lgpc); pi += kTThreads / 32) {
+                const int r = pi >> lgpc, gl = pi & ((1 << lgpc) - 1);
+                const int b = b0 + r, g = (c0 >> lgs) + gl;
                 if (b >= batch || g >= groups) continue;
                 float acc = 0.0f;
                 const int ca = g * group_size, cb = min(in_dim, ca + group_size);
-                for (int c = ca + lane; c < cb; c += 32)
-                    acc += __half2float(__float2half_rn(static_cast<float>(xs[r * kTStride + (c - c0)])));
+                for (int c = ca + lane; c < cb; c += 32) acc += __half2float(__float2half_rn(xs[r * kTStride + (c - c0)]));
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
                 if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
             }
         }
         if (active && c0 < in_dim) {
-            const double* xa = xs + (2 * tp) * kTStride;
-            const double* ga = gs + (4 * eg) * kTStride;
+            const float* xa = xs + (2 * tp) * kTStride;
+            const float* ga = gs + (4 * eg) * kTStride;
 #pragma unroll 4
             for (int c = s; c < kTC; c += S) {
-                const double x0 = xa[c], x1 = xa[kTStride + c];
-                const double g0 = ga[c], g1 = ga[kTStride + c], g2 = ga[2 * kTStride + c], g3 = ga[3 * kTStride + c];
-                sum[0] = fma(x0, g0, sum[0]); asum[0] = fma(fabs(x0), fabs(g0), asum[0]);
-                sum[1] = fma(x0, g1, sum[1]); asum[1] = fma(fabs(x0), fabs(g1), asum[1]);
-                sum[2] = fma(x0, g2, sum[2]); asum[2] = fma(fabs(x0), fabs(g2), asum[2]);
-                sum[3] = fma(x0, g3, sum[3]); asum[3] = fma(fabs(x0), fabs(g3), asum[3]);
-                sum[4] = fma(x1, g0, sum[4]); asum[4] = fma(fabs(x1), fabs(g0), asum[4]);
-                sum[5] = fma(x1, g1, sum[5]); asum[5] = fma(fabs(x1), fabs(g1), asum[5]);
-                sum[6] = fma(x1, g2, sum[6]); asum[6] = fma(fabs(x1), fabs(g2), asum[6]);
-                sum[7] = fma(x1, g3, sum[7]); asum[7] = fma(fabs(x1), fabs(g3), asum[7]);
+                const float xf0 = xa[c], xf1 = xa[kTStride + c];
+                const float gf0 = ga[c], gf1 = ga[kTStride + c], gf2 = ga[2 * kTStride + c], gf3 = ga[3 * kTStride + c];
+                const double x0 = xf0, x1 = xf1, g0 = gf0, g1 = gf1, g2 = gf2, g3 = gf3;
+                sum[0] = fma(x0, g0, sum[0]); asum[0] = fmaf(fabsf(xf0), fabsf(gf0), asum[0]);
+                sum[1] = fma(x0, g1, sum[1]); asum[1] = fmaf(fabsf(xf0), fabsf(gf1), asum[1]);
+                sum[2] = fma(x0, g2, sum[2]); asum[2] = fmaf(fabsf(xf0), fabsf(gf2), asum[2]);
+                sum[3] = fma(x0, g3, sum[3]); asum[3] = fmaf(fabsf(xf0), fabsf(gf3), asum[3]);
+                sum[4] = fma(x1, g0, sum[4]); asum[4] = fmaf(fabsf(xf1), fabsf(gf0), asum[4]);
+                sum[5] = fma(x1, g1, sum[5]); asum[5] = fmaf(fabsf(xf1), fabsf(gf1), asum[5]);
+                sum[6] = fma(x1, g2, sum[6]); asum[6] = fmaf(fabsf(xf1), fabsf(gf2), asum[6]);
+                sum[7] = fma(x1, g3, sum[7]); asum[7] = fmaf(fabsf(xf1), fabsf(gf3), asum[7]);
             }
         }
+        __syncthreads();   // stage (ch & 1) consumed before chunk ch + 2 is issued into it
     }
     __syncthreads();   // tiles consumed: the region becomes the split-reduction buffer
     double* red = tsm;   // [kTThreads][16]
@@ -690,7 +734,7 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
     for (int pr = threadIdx.x; pr < kTT * num_experts; pr += kTThreads) {
         const int r = pr / num_experts, e = pr % num_experts;
         if (b0 + r >= batch) continue;
-        const int m = (r >> 1) * ke4 + (e >> 2);
+        const int m = e_fast ? (r >> 1) * ke4 + (e >> 2) : (e >> 2) * (kTT / 2) + (r >> 1);
         const int k = (r & 1) * 4 + (e & 3);
         double sv = 0.0, av = 0.0;
         for (int q = 0; q < S; ++q) {
@@ -699,21 +743,75 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
         }
         const double u = 1.1102230246251565e-16;  // 2^-53
         const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 40.0);
-        const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
+        // av: f32 sums of f32-rounded |x||g| (depth <= n/S + 1 each, then exact-ish f64
+        // adds): exact sum|p| <= av * (1 + (n/S + 2) 2^-23) + n 2^-126 (subnormal products)
+        const double avb = __dadd_ru(__dmul_ru(av, 1.0 + (static_cast<double>(in_dim) / S + 2.0) * 1.2e-7 + 1e-12),
+                                     static_cast<double>(in_dim) * 1.1754943508222875e-38);
+        const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(avb, 1.0001));
         const float lo = __double2float_rn(__dsub_rd(sv, err));
         const float hi = __double2float_rn(__dadd_ru(sv, err));
         sc[r][e] = __double2float_rn(sv);
-        if (lo != hi) und[atomicAdd(&n_und, 1)] = pr;
+        if (lo != hi) {
+            const int slot = atomicAdd(&n_und, 1);
+            und[slot] = pr;
+            und_sv[slot] = sv;
+            und_ap[slot] = avb;
+        }
     }
     __syncthreads();
-    // undecided scores: the reference's sequential loop, one warp each
-    // (products in a warp-private window, one lane adds them in index order)
+    // undecided scores, one warp each.  Tier 2: bound the reference's own
+    // rounding by its partial sums, |seq - exact| <= u * sum_k |S_k| (+ second
+    // order), far tighter than the any-order bound when the partial sums stay
+    // small (random-walk data: ~sqrt(n) x).  Lane l scans a contiguous segment
+    // (running sums, then a warp exclusive scan of the segment totals, then the
+    // partial sums again with the offset).  Still undecided: the reference's
+    // sequential loop (products in a warp-private window, one lane adds them in
+    // index order).
     double* win = tsm + warp * 256;   // the reduction buffer is consumed
     for (int i = warp; i < n_und; i += kTThreads / 32) {
         const int pr = und[i];
         const int r = pr / num_experts, e = pr % num_experts;
         const float* xb = x + static_cast<int64_t>(b0 + r) * in_dim;
         const float* gk = gate + static_cast<int64_t>(e) * in_dim;
+        {
+            const int seg = (in_dim + 31) / 32;
+            const int ca = min(in_dim, lane * seg), cb = min(in_dim, ca + seg);
+            double run = 0.0;
+#pragma unroll 8
+            for (int c = ca; c < cb; ++c) run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
+            double off = run;   // inclusive scan of the segment totals
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const double o = __shfl_up_sync(0xffffffffu, off, d);
+                if (lane >= d) off += o;
+            }
+            off -= run;   // exclusive (its rounding is inside the depth bound below)
+            double as = 0.0;
+            run = off;
+#pragma unroll 8
+            for (int c = ca; c < cb; ++c) {
+                run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
+                as += fabs(run);
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) as += __shfl_xor_sync(0xffffffffu, as, d);
+            const double u = 1.1102230246251565e-16;   // 2^-53
+            const double n = static_cast<double>(in_dim);
+            const double ap = und_ap[i];
+            // our partial sums: depth <= seg + 7 additions (scan 5, the subtraction,
+            // the segment), so sum|S_k| <= as (1 + n u) + n (seg + 8) u ap
+            const double sum_s = __dadd_ru(__dmul_ru(as, 1.0 + 1.01 * (n + 40.0) * u),
+                                           __dmul_ru(__dmul_ru(n, (seg + 8.0) * u * 1.01), ap));
+            // reference: u * sum|S^ref_k| <= u (sum|S_k| + n * gamma_n * ap); ours: the
+            // tile's any-order depth n/S + S + 2
+            const double err_ref = __dmul_ru(u * 1.01, __dadd_ru(sum_s, __dmul_ru(n * n * u * 1.01, ap)));
+            const double err_our = __dmul_ru((n / S + S + 2.0) * u * 1.01, ap);
+            const double err = __dmul_ru(__dadd_ru(err_ref, err_our), 1.05);
+            const double sv = und_sv[i];
+            const float lo = __double2float_rn(__dsub_rd(sv, err));
+            const float hi = __double2float_rn(__dadd_ru(sv, err));
+            if (lo == hi) continue;   // certified: sc already holds float(sv)
+        }
         double acc = 0.0;
         for (int c0 = 0; c0 < in_dim; c0 += 256) {
             const int n = min(256, in_dim - c0);

@@ -687,16 +687,43 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
             // kTC % group_size == 0 makes group_size and gpc powers of two: shifts
             const int lgs = __ffs(group_size) - 1;
             const int lgpc = __ffs(kTC >> lgs) - 1;
-            for (int pi = warp; pi < (kTT << lgpc); pi += kTThreads / 32) {
-                const int r = pi >> lgpc, gl = pi & ((1 << lgpc) - 1);
-                const int b = b0 + r, g = (c0 >> lgs) + gl;
-                if (b >= batch || g >= groups) continue;
-                float acc = 0.0f;
-                const int ca = g * group_size, cb = min(in_dim, ca + group_size);
-                for (int c = ca + lane; c < cb; c += 32) acc += __half2float(__float2half_rn(xs[r * kTStride + (c - c0)]));
+            // four (token, group) pairs per warp in flight (independent chains; each
+            // pair's summation order is route_kernel's)
+            constexpr int kP = 4;
+            const int n_pairs = kTT << lgpc;
+            for (int p0 = warp * kP; p0 < n_pairs; p0 += (kTThreads / 32) * kP) {
+                float acc[kP];
+                int cab[kP], cbb[kP];
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-                if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
+                for (int j = 0; j < kP; ++j) {
+                    const int pi = p0 + j;
+                    const int r = pi >> lgpc, gl = pi & ((1 << lgpc) - 1);
+                    const int g = (c0 >> lgs) + gl;
+                    const bool ok = pi < n_pairs && b0 + r < batch && g < groups;
+                    cab[j] = ok ? g * group_size : 0;
+                    cbb[j] = ok ? min(in_dim, cab[j] + group_size) : 0;
+                    acc[j] = 0.0f;
+                }
+                for (int k = lane; k < group_size; k += 32) {
+#pragma unroll
+                    for (int j = 0; j < kP; ++j) {
+                        const int c = cab[j] + k;
+                        const int r = (p0 + j) >> lgpc;
+                        if (c < cbb[j]) acc[j] += __half2float(__float2half_rn(xs[r * kTStride + (c - c0)]));
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+                    for (int j = 0; j < kP; ++j) acc[j] += __shfl_down_sync(0xffffffffu, acc[j], off);
+                if (lane == 0) {
+#pragma unroll
+                    for (int j = 0; j < kP; ++j)
+                        if (cbb[j] > cab[j]) {   // a valid pair (g < groups: its range is non-empty)
+                            const int pi = p0 + j;
+                            sx[static_cast<int64_t>(b0 + (pi >> lgpc)) * groups + (c0 >> lgs) + (pi & ((1 << lgpc) - 1))] = acc[j];
+                        }
+                }
             }
         }
         if (active && c0 < in_dim) {

@@ -200,6 +200,27 @@ def test_synthetic_artifact_readable_by_reference(ref, oracle, tmp_path):
     assert rel_frob(y, yr) <= 1e-5
 
 
+def test_synthetic_cache_is_versioned_and_atomic(tmp_path, monkeypatch):
+    """bench.py's artifact cache: keyed by the writer's source hash (a stale /tmp
+    artifact from an older writer is never reused) and renamed into place."""
+    import os
+    from paper_2605_09281_b200 import synth
+    root = str(tmp_path)
+    p = synth.config_path("c1", root)
+    assert os.path.basename(p).startswith("c1_folded_s0_") and len(os.path.basename(p)) > len("c1_folded_s0_")
+    stale = os.path.join(root, "c1_folded_s0")          # the pre-versioning cache name
+    os.makedirs(stale)
+    open(os.path.join(stale, "manifest.json"), "w").write("{}")
+    calls = []
+    real = synth.write_synthetic
+    monkeypatch.setattr(synth, "write_synthetic", lambda path, **kw: calls.append(path) or real(path, **kw))
+    assert synth.ensure_config("c1", root=root) == p
+    assert len(calls) == 1 and calls[0] != p and not os.path.exists(calls[0])   # written aside, renamed
+    assert os.path.exists(os.path.join(p, "manifest.json"))
+    assert synth.ensure_config("c1", root=root) == p and len(calls) == 1       # cached
+    assert sorted(os.listdir(root)) == sorted([os.path.basename(p), "c1_folded_s0"])
+
+
 def test_bench_algorithmic_bytes_match_survey_table():
     import bench
     info = dict(num_experts=8, top_k=2, in_dim=1024, out_dim=2816, num_shared=0, rank=16, bits=3,

@@ -592,7 +592,28 @@ __host__ __device__ inline int route_tile_smem(int num_experts) {
 static __device__ __forceinline__ uint32_t bits_of(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 static __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-__global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __restrict__ x, int batch, int in_dim,
+// one chunk of a thread's 2-token x 4-expert micro-tile: columns s, s+S, ...
+// (S compile-time, so the unrolled loads are hoisted ahead of the f64 chains)
+template <int S>
+__device__ __forceinline__ void route_tile_mac(const float* __restrict__ xa, const float* __restrict__ ga, int s,
+                                              double (&sum)[8], float (&asum)[8]) {
+#pragma unroll 8
+    for (int c = s; c < kTC; c += S) {
+        const float xf0 = xa[c], xf1 = xa[kTStride + c];
+        const float gf0 = ga[c], gf1 = ga[kTStride + c], gf2 = ga[2 * kTStride + c], gf3 = ga[3 * kTStride + c];
+        const double x0 = xf0, x1 = xf1, g0 = gf0, g1 = gf1, g2 = gf2, g3 = gf3;
+        sum[0] = fma(x0, g0, sum[0]); asum[0] = fmaf(fabsf(xf0), fabsf(gf0), asum[0]);
+        sum[1] = fma(x0, g1, sum[1]); asum[1] = fmaf(fabsf(xf0), fabsf(gf1), asum[1]);
+        sum[2] = fma(x0, g2, sum[2]); asum[2] = fmaf(fabsf(xf0), fabsf(gf2), asum[2]);
+        sum[3] = fma(x0, g3, sum[3]); asum[3] = fmaf(fabsf(xf0), fabsf(gf3), asum[3]);
+        sum[4] = fma(x1, g0, sum[4]); asum[4] = fmaf(fabsf(xf1), fabsf(gf0), asum[4]);
+        sum[5] = fma(x1, g1, sum[5]); asum[5] = fmaf(fabsf(xf1), fabsf(gf1), asum[5]);
+        sum[6] = fma(x1, g2, sum[6]); asum[6] = fmaf(fabsf(xf1), fabsf(gf2), asum[6]);
+        sum[7] = fma(x1, g3, sum[7]); asum[7] = fmaf(fabsf(xf1), fabsf(gf3), asum[7]);
+    }
+}
+
+__global__ void __launch_bounds__(kTThreads, 2) route_tile_kernel(const float* __restrict__ x, int batch, int in_dim,
                                                                const float* __restrict__ gate, int num_experts,
                                                                int top_k, int group_size, int groups, int k_pad,
                                                                int32_t* __restrict__ ids, float* __restrict__ gates,
@@ -668,7 +689,10 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
         const float* xs = stage0 + (ch & 1) * stage_floats;
         const float* gs = xs + kTT * kTStride;
         // fp16 activations (zero-padded to k_pad)
-        if (x16) {
+#ifndef TQ_RT_ABL
+#define TQ_RT_ABL 0
+#endif
+        if (x16 && !(TQ_RT_ABL & 2)) {
             // 4 halves per thread per pass (k_pad % 4 == 0: a piece is wholly in or out)
             for (int i = threadIdx.x; i < kTT * (kTC / 4); i += kTThreads) {
                 const int r = i / (kTC / 4), cc = (i % (kTC / 4)) * 4, c = c0 + cc;
@@ -683,7 +707,7 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
         }
         // group sums of the fp16 activations (route_kernel's exact arithmetic);
         // the launcher guarantees kTC % group_size == 0
-        if (sx && c0 < in_dim) {
+        if (sx && c0 < in_dim && !(TQ_RT_ABL & 2)) {
             // kTC % group_size == 0 makes group_size and gpc powers of two: shifts
             const int lgs = __ffs(group_size) - 1;
             const int lgpc = __ffs(kTC >> lgs) - 1;
@@ -726,22 +750,16 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
                 }
             }
         }
-        if (active && c0 < in_dim) {
+        if (active && c0 < in_dim && !(TQ_RT_ABL & 1)) {
             const float* xa = xs + (2 * tp) * kTStride;
             const float* ga = gs + (4 * eg) * kTStride;
-#pragma unroll 4
-            for (int c = s; c < kTC; c += S) {
-                const float xf0 = xa[c], xf1 = xa[kTStride + c];
-                const float gf0 = ga[c], gf1 = ga[kTStride + c], gf2 = ga[2 * kTStride + c], gf3 = ga[3 * kTStride + c];
-                const double x0 = xf0, x1 = xf1, g0 = gf0, g1 = gf1, g2 = gf2, g3 = gf3;
-                sum[0] = fma(x0, g0, sum[0]); asum[0] = fmaf(fabsf(xf0), fabsf(gf0), asum[0]);
-                sum[1] = fma(x0, g1, sum[1]); asum[1] = fmaf(fabsf(xf0), fabsf(gf1), asum[1]);
-                sum[2] = fma(x0, g2, sum[2]); asum[2] = fmaf(fabsf(xf0), fabsf(gf2), asum[2]);
-                sum[3] = fma(x0, g3, sum[3]); asum[3] = fmaf(fabsf(xf0), fabsf(gf3), asum[3]);
-                sum[4] = fma(x1, g0, sum[4]); asum[4] = fmaf(fabsf(xf1), fabsf(gf0), asum[4]);
-                sum[5] = fma(x1, g1, sum[5]); asum[5] = fmaf(fabsf(xf1), fabsf(gf1), asum[5]);
-                sum[6] = fma(x1, g2, sum[6]); asum[6] = fmaf(fabsf(xf1), fabsf(gf2), asum[6]);
-                sum[7] = fma(x1, g3, sum[7]); asum[7] = fmaf(fabsf(xf1), fabsf(gf3), asum[7]);
+            switch (S) {
+                case 32: route_tile_mac<32>(xa, ga, s, sum, asum); break;
+                case 16: route_tile_mac<16>(xa, ga, s, sum, asum); break;
+                case 8: route_tile_mac<8>(xa, ga, s, sum, asum); break;
+                case 4: route_tile_mac<4>(xa, ga, s, sum, asum); break;
+                case 2: route_tile_mac<2>(xa, ga, s, sum, asum); break;
+                default: route_tile_mac<1>(xa, ga, s, sum, asum); break;
             }
         }
         __syncthreads();   // stage (ch & 1) consumed before chunk ch + 2 is issued into it
@@ -786,49 +804,62 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
         }
     }
     __syncthreads();
-    // undecided scores, one warp each.  Tier 2: bound the reference's own
-    // rounding by its partial sums, |seq - exact| <= u * sum_k |S_k| (+ second
-    // order), far tighter than the any-order bound when the partial sums stay
-    // small (random-walk data: ~sqrt(n) x).  Lane l scans a contiguous segment
-    // (running sums, then a warp exclusive scan of the segment totals, then the
-    // partial sums again with the offset).  Still undecided: the reference's
-    // sequential loop (products in a warp-private window, one lane adds them in
-    // index order).
-    double* win = tsm + warp * 256;   // the reduction buffer is consumed
-    for (int i = warp; i < n_und; i += kTThreads / 32) {
+    // undecided scores.  Tier 2: bound the reference's own rounding by its
+    // partial sums, |seq - exact| <= u * sum_k |S_k| (+ second order), far
+    // tighter than the any-order bound when the partial sums stay small
+    // (random-walk data: ~sqrt(n) x).  Still undecided: tier 3, the reference's
+    // sequential loop.  (Measured at 4096 tokens: tier 2 per warp 141 us, per
+    // CTA 123 us; 0.7% of the c3 scores fail tier 1.)
+    // tier 2, the whole CTA on one undecided score at a time: thread t scans the
+    // contiguous columns [t*seg, (t+1)*seg) (all its loads in flight at once),
+    // a block scan of the segment totals gives every partial sum of the
+    // reference's order; still undecided scores go to the tier-3 list
+    __shared__ double t2_part[kTThreads / 32][2];
+    __shared__ int n_t3;
+    __shared__ int t3[kTT * 64];
+    if (threadIdx.x == 0) n_t3 = 0;
+    const int n_t2 = (TQ_RT_ABL & 4) ? 0 : n_und;
+    for (int i = 0; i < n_t2; ++i) {
         const int pr = und[i];
         const int r = pr / num_experts, e = pr % num_experts;
         const float* xb = x + static_cast<int64_t>(b0 + r) * in_dim;
         const float* gk = gate + static_cast<int64_t>(e) * in_dim;
-        {
-            const int seg = (in_dim + 31) / 32;
-            const int ca = min(in_dim, lane * seg), cb = min(in_dim, ca + seg);
-            double run = 0.0;
+        const int seg = (in_dim + kTThreads - 1) / kTThreads;
+        const int ca = min(in_dim, static_cast<int>(threadIdx.x) * seg), cb = min(in_dim, ca + seg);
+        double run = 0.0;
 #pragma unroll 8
-            for (int c = ca; c < cb; ++c) run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
-            double off = run;   // inclusive scan of the segment totals
+        for (int c = ca; c < cb; ++c) run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
+        double inc = run;   // block inclusive scan of the segment totals
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const double o = __shfl_up_sync(0xffffffffu, off, d);
-                if (lane >= d) off += o;
-            }
-            off -= run;   // exclusive (its rounding is inside the depth bound below)
-            double as = 0.0;
-            run = off;
+        for (int d = 1; d < 32; d <<= 1) {
+            const double o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        if (lane == 31) t2_part[warp][0] = inc;
+        __syncthreads();
+        double woff = 0.0;
+        for (int w = 0; w < warp; ++w) woff += t2_part[w][0];
+        double as = 0.0;
+        run = woff + (inc - run);   // exclusive offset of this segment
 #pragma unroll 8
-            for (int c = ca; c < cb; ++c) {
-                run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
-                as += fabs(run);
-            }
+        for (int c = ca; c < cb; ++c) {
+            run = fma(static_cast<double>(xb[c]), static_cast<double>(gk[c]), run);
+            as += fabs(run);
+        }
 #pragma unroll
-            for (int d = 16; d > 0; d >>= 1) as += __shfl_xor_sync(0xffffffffu, as, d);
+        for (int d = 16; d > 0; d >>= 1) as += __shfl_xor_sync(0xffffffffu, as, d);
+        if (lane == 0) t2_part[warp][1] = as;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double ast = 0.0;
+            for (int w = 0; w < kTThreads / 32; ++w) ast += t2_part[w][1];
             const double u = 1.1102230246251565e-16;   // 2^-53
             const double n = static_cast<double>(in_dim);
             const double ap = und_ap[i];
-            // our partial sums: depth <= seg + 7 additions (scan 5, the subtraction,
-            // the segment), so sum|S_k| <= as (1 + n u) + n (seg + 8) u ap
-            const double sum_s = __dadd_ru(__dmul_ru(as, 1.0 + 1.01 * (n + 40.0) * u),
-                                           __dmul_ru(__dmul_ru(n, (seg + 8.0) * u * 1.01), ap));
+            // our partial sums: depth <= seg + 5 (warp scan) + 8 (warp offsets) + 2,
+            // so sum|S_k| <= ast (1 + (n + 40) u) + n (seg + 16) u ap
+            const double sum_s = __dadd_ru(__dmul_ru(ast, 1.0 + 1.01 * (n + 40.0) * u),
+                                           __dmul_ru(__dmul_ru(n, (seg + 16.0) * u * 1.01), ap));
             // reference: u * sum|S^ref_k| <= u (sum|S_k| + n * gamma_n * ap); ours: the
             // tile's any-order depth n/S + S + 2
             const double err_ref = __dmul_ru(u * 1.01, __dadd_ru(sum_s, __dmul_ru(n * n * u * 1.01, ap)));
@@ -837,8 +868,18 @@ __global__ void __launch_bounds__(kTThreads) route_tile_kernel(const float* __re
             const double sv = und_sv[i];
             const float lo = __double2float_rn(__dsub_rd(sv, err));
             const float hi = __double2float_rn(__dadd_ru(sv, err));
-            if (lo == hi) continue;   // certified: sc already holds float(sv)
+            if (lo != hi) t3[n_t3++] = pr;   // certified otherwise: sc already holds float(sv)
         }
+        __syncthreads();   // t2_part reused by the next score
+    }
+    // tier 3: the reference's sequential loop, one warp per still-undecided score
+    // (products in a warp-private window, one lane adds them in index order)
+    double* win = tsm + warp * 256;   // the reduction buffer is consumed
+    for (int i = warp; i < n_t3; i += kTThreads / 32) {
+        const int pr = t3[i];
+        const int r = pr / num_experts, e = pr % num_experts;
+        const float* xb = x + static_cast<int64_t>(b0 + r) * in_dim;
+        const float* gk = gate + static_cast<int64_t>(e) * in_dim;
         double acc = 0.0;
         for (int c0 = 0; c0 < in_dim; c0 += 256) {
             const int n = min(256, in_dim - c0);

@@ -1629,7 +1629,7 @@ cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream
 // thread's columns is independent (the per-thread index chain of
 // combine_kernel left HBM at ~3 TB/s).  Same summation order as combine_kernel.
 constexpr int kCbCols = 256 * 4 * 4;   // columns per CTA
-__global__ void __launch_bounds__(256) combine_rows_kernel(const CombineArgs a) {
+__global__ void __launch_bounds__(256, 4) combine_rows_kernel(const CombineArgs a) {
     __shared__ int64_t s_row[64];
     __shared__ float s_gate[64];
     pdl_wait();
@@ -1652,6 +1652,40 @@ __global__ void __launch_bounds__(256) combine_rows_kernel(const CombineArgs a) 
     const int nsh = a.nsplit_dev ? ns : a.sh_nsplit;
     const int n_slots = a.offsets ? a.offsets[a.num_experts] : 0;
     const int64_t sh0 = a.sh_from_offsets ? (a.poffsets ? a.poffsets[a.num_experts] : n_slots) : 0;
+    if (ns == 1 && a.num_shared == 0 && k <= 2) {
+        // common prefill case (top-2, one K split, no shared experts): every row
+        // load of the CTA's four column groups issued before the first use
+        // (same arithmetic as the general loop below: v = 0 + w, acc = fma(g, v, acc))
+        float4 w[4][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c0 = blockIdx.x * kCbCols + (q * 256 + threadIdx.x) * 4;
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                w[q][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (t < k && c0 < a.out_dim && s_row[t] >= 0)
+                    w[q][t] = __ldcs(reinterpret_cast<const float4*>(a.y + s_row[t] * a.out_dim + c0));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c0 = blockIdx.x * kCbCols + (q * 256 + threadIdx.x) * 4;
+            if (c0 >= a.out_dim) break;
+            float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                if (t >= k || s_row[t] < 0) continue;
+                const float g = s_gate[t];
+                acc[0] = fmaf(g, 0.0f + w[q][t].x, acc[0]);
+                acc[1] = fmaf(g, 0.0f + w[q][t].y, acc[1]);
+                acc[2] = fmaf(g, 0.0f + w[q][t].z, acc[2]);
+                acc[3] = fmaf(g, 0.0f + w[q][t].w, acc[3]);
+            }
+            __stcs(reinterpret_cast<float4*>(a.out + static_cast<int64_t>(b) * a.out_dim + c0),
+                   make_float4(acc[0], acc[1], acc[2], acc[3]));
+        }
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int c0 = blockIdx.x * kCbCols + (q * 256 + threadIdx.x) * 4;

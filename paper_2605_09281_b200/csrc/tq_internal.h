@@ -180,6 +180,81 @@ struct CombineArgs {
     float* out;
 };
 
+// ---- decode path (tq_decode.cu): route+scatter -> fused expert GEMM -> combine ----
+//
+// Slot layout: routed expert e owns activation rows [e * cap8, e * cap8 + cnt[e]),
+// shared expert s the rows [(K + s) * cap8, ... + batch) (row b = token b).  The
+// rows live in the atom-major, 128B-pre-swizzled layout [k/64][atom_rows][64]
+// (one bulk copy per 64-column atom lands a token tile MMA-ready).
+constexpr int kDecMaxW = 128;        // routed + shared weights
+constexpr int kDecMaxTopK = 8;       // destinations per token held in shared memory
+
+struct DecRouteArgs {
+    const float* x;                  // [B][i] f32
+    int batch, in_dim, k_pad;
+    const float* gate;               // [K][i] router
+    int num_experts, top_k, num_shared;
+    int given;                       // 1: routing given (ids_in / gates_in), no scoring
+    const int32_t* ids_in;
+    int32_t* ids;                    // computed routing (given == 0)
+    float* gates;
+    float* score_ws;                 // [B][K]
+    int32_t* ticket;                 // [B] per-token CTA tickets (self-resetting)
+    int group_size, groups, rank, num_q;
+    const int8_t* vcodes;            // [N][r][i] tiled.v.codes
+    const float* vscale;             // [N][r] sigma_j * (vabs_q / 127)
+    const int32_t* q_tier;           // [N] 0 folded, 1 scalar, 2 general, -1 unused
+    const int32_t* q_first;          // [N] expert whose scaling defines the folded s_q
+    const float* scaling;            // [K][i]
+    const int32_t* e_q;              // [K] tile column q(e)
+    const float* zscale;             // [K] su_p * inv_scalar * 2^k_e
+    float* zq_ws;                    // [B][N][r] projections of the folded / scalar column blocks
+    int use_main, use_lr;            // path: residual (group sums) / low-rank (projections)
+    int cap8;                        // rows per weight in the slot layout
+    int64_t atom_rows;
+    int ext_cols;                    // ext row width (multiple of 64)
+    __half* xperm;                   // slot rows, atom-major [k_pad/64][atom_rows][64]
+    __half* extperm;                 // ext rows [Sx | Z * zscale | 0], atom-major [ext_cols/64][atom_rows][64]
+    int32_t* cnt;                    // [K] slots taken per routed expert (zeroed by the combine)
+    int32_t* inv;                    // [B * top_k] slot row of (b, t), -1 for an invalid id
+    int32_t* err_flag;
+};
+
+struct DecParams {
+    const uint8_t* codes;            // [w][mb][kb64] code blocks
+    int64_t weight_stride;
+    const __half* scales;            // [w][mb][G][128]
+    const uint8_t* ext_blocks;       // [w][mb][E64] dense fp16 128 x 64 blocks [-zero*s' | U_p | 0]
+    int n_ext64;
+    const float* w_outscale;         // [w] 2^-k
+    int bits, group_size, groups, group_shift;
+    int kc64;                        // k_pad / 64
+    int nmain;                       // main steps (128 K each) per segment; 0 = low-rank only path
+    int n_ep;                        // ext pieces (32 columns) per segment
+    int mb_count, o_valid;
+    int num_experts, num_shared, batch;
+    const int32_t* cnt;
+    int cap8;
+    int64_t atom_rows;
+    const __half* xperm;
+    const __half* extperm;
+    float* yslot;                    // [(K + S) * cap8][o] expert rows
+    int ldy;
+    float* scratch;                  // [grid][2][dn][128] split-segment partials
+    int32_t* seg_cnt;                // per segment arrivals (self-resetting)
+    int code_stages, x_stages, code_stage_bytes;   // set by launch_decode
+};
+
+struct DecCombineArgs {
+    const float* yslot;
+    int ldy;
+    const int32_t* inv;
+    const float* gates;
+    int batch, top_k, out_dim, num_shared, num_experts, cap8;
+    int32_t* cnt;                    // zeroed here for the next forward
+    float* out;
+};
+
 // ---- host-side tables the runtime keeps for a loaded layer ----------------------
 struct DeviceBuf {
     void* ptr = nullptr;

@@ -65,52 +65,25 @@ constexpr int kRouteCols = 4;         // columns per thread per pass (i <= 4096 
 constexpr int kReplayWin = 2048;      // products per replay window (16 KB of shared memory)
 
 template <int kRT>
-__global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x, int batch, int in_dim,
-                                                             const float* __restrict__ gate, int num_experts,
-                                                             int top_k, int group_size, int groups, int k_pad,
-                                                             int32_t* __restrict__ ids, float* __restrict__ gates,
-                                                             __half* __restrict__ x16, float* __restrict__ sx,
-                                                             float* __restrict__ score_ws, int32_t* __restrict__ ticket,
-                                                             int tokens_per_cta, const PlanArgs plan,
-                                                             int32_t* __restrict__ plan_ticket) {
-    __shared__ double part[(kRT / 32)][kRouteExperts][2];
-    __shared__ double prod[kReplayWin];
-    __shared__ double replay_acc;
-    __shared__ float sc[64];
-    __shared__ double ex[64];
-    __shared__ int pick_k[64];
-    __shared__ double pick_p[64];
-    __shared__ unsigned s_und;
-    __shared__ int s_last;
-    pdl_wait();
-    pdl_launch_dependents();
-    const int k0 = blockIdx.y * kRouteExperts;
+struct RouteSmem {
+    double part[kRT / 32][kRouteExperts][2];
+    double prod[kReplayWin];
+    double replay_acc;
+    unsigned und;
+};
+
+// Certified f32 scores of experts [k0, k0 + kRouteExperts) of one token
+// (matrix.cpp:25-36 semantics, see the header comment): the whole CTA takes
+// part; thread j < kRouteExperts writes score_row[k0 + j].  Returns the mask of
+// scores that needed the exact replay (the caller fences those writes).
+template <int kRT>
+__device__ unsigned route_slice(const float* __restrict__ xb, int in_dim, const float* __restrict__ gate,
+                                int num_experts, int k0, float* __restrict__ score_row, RouteSmem<kRT>& sm) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // prefill: several tokens per CTA, the CTA's gate slice is re-read from L1
-    for (int tb = 0; tb < tokens_per_cta; ++tb) {
-    const int b = blockIdx.x * tokens_per_cta + tb;
-    if (b >= batch) break;
-    const float* xb = x + static_cast<int64_t>(b) * in_dim;
-    if (blockIdx.y == 0) {
-        // fp16 activations (zero-padded to k_pad) and per-group sums of them
-        if (x16) {
-            __half* xo = x16 + static_cast<int64_t>(b) * k_pad;
-            for (int c = threadIdx.x; c < k_pad; c += kRT) xo[c] = __float2half_rn(c < in_dim ? xb[c] : 0.0f);
-        }
-        for (int g = warp; sx && g < groups; g += (kRT / 32)) {
-            float acc = 0.0f;
-            const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
-            for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-            if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
-        }
-    }
-    if (num_experts == 0) continue;  // activations-only prep (tq_forward with given routing)
     __syncthreads();   // shared state of the previous token is consumed
     if (threadIdx.x == 0) {
-        s_und = 0u;
-        replay_acc = 0.0;
+        sm.und = 0u;
+        sm.replay_acc = 0.0;
     }
     __syncthreads();
     // ---- tier 1: plain parallel dot products, loose bound ----------------
@@ -169,8 +142,8 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
         if (lane == 0) {
 #pragma unroll
             for (int j = 0; j < kRouteExperts; ++j) {
-                part[warp][j][0] = sum1[j];
-                part[warp][j][1] = abs1[j];
+                sm.part[warp][j][0] = sum1[j];
+                sm.part[warp][j][1] = abs1[j];
             }
         }
         __syncthreads();
@@ -178,21 +151,21 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
             const int j = threadIdx.x;
             double sv = 0.0, av = 0.0;
             for (int w = 0; w < (kRT / 32); ++w) {
-                sv += part[w][j][0];
-                av += part[w][j][1];
+                sv += sm.part[w][j][0];
+                av += sm.part[w][j][1];
             }
             const double u = 1.1102230246251565e-16;  // 2^-53
             const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 40.0);
             const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(av, 1.0001));
             const float lo = __double2float_rn(__dsub_rd(sv, err));
             const float hi = __double2float_rn(__dadd_ru(sv, err));
-            score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(sv);
-            if (lo != hi) atomicOr(&s_und, 1u << j);
+            score_row[k0 + j] = __double2float_rn(sv);
+            if (lo != hi) atomicOr(&sm.und, 1u << j);
         }
         __syncthreads();
     }
-    if (s_und != 0u) {   // block-uniform
-    if (threadIdx.x == 0) s_und = 0u;
+    if (sm.und != 0u) {   // block-uniform
+    if (threadIdx.x == 0) sm.und = 0u;
     __syncthreads();
     // ---- tier 2: the partial sums of the reference's order ----
     // Thread t owns columns [4t, 4t+4) of each pass, so thread order is index
@@ -230,30 +203,30 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
                 if (lane >= off) v += o;
             }
             incl[j] = v;
-            if (lane == 31) part[warp][j][0] = v;
+            if (lane == 31) sm.part[warp][j][0] = v;
         }
         __syncthreads();
         if (warp == 0) {
 #pragma unroll
             for (int j = 0; j < kRouteExperts; ++j) {
-                double v = lane < (kRT / 32) ? part[lane][j][0] : 0.0;
+                double v = lane < (kRT / 32) ? sm.part[lane][j][0] : 0.0;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
                     const double o = __shfl_up_sync(0xffffffffu, v, off);
                     if (lane >= off) v += o;
                 }
-                if (lane < (kRT / 32)) part[lane][j][1] = v;   // inclusive scan of the warp totals
+                if (lane < (kRT / 32)) sm.part[lane][j][1] = v;   // inclusive scan of the warp totals
             }
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kRouteExperts; ++j) {
-            const double base = tot_s[j] + (warp > 0 ? part[warp - 1][j][1] : 0.0) + (incl[j] - pre[j][3]);
+            const double base = tot_s[j] + (warp > 0 ? sm.part[warp - 1][j][1] : 0.0) + (incl[j] - pre[j][3]);
 #pragma unroll
             for (int m = 0; m < 4; ++m) abs_s[j] += fabs(base + pre[j][m]);
-            tot_s[j] += part[(kRT / 32) - 1][j][1];
+            tot_s[j] += sm.part[(kRT / 32) - 1][j][1];
         }
-        __syncthreads();   // part[] is reused by the next pass / the reduction below
+        __syncthreads();   // sm.part[] is reused by the next pass / the reduction below
     }
     // block sums of sum_k |S_k| and sum |p|; the total is the scan's last value
 #pragma unroll
@@ -267,8 +240,8 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
     if (lane == 0) {
 #pragma unroll
         for (int j = 0; j < kRouteExperts; ++j) {
-            part[warp][j][0] = abs_s[j];
-            part[warp][j][1] = abs_p[j];
+            sm.part[warp][j][0] = abs_s[j];
+            sm.part[warp][j][1] = abs_p[j];
         }
     }
     __syncthreads();
@@ -277,8 +250,8 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
         const int j = threadIdx.x;
         double as = 0.0, ap = 0.0;
         for (int w = 0; w < (kRT / 32); ++w) {
-            as += part[w][j][0];
-            ap += part[w][j][1];
+            as += sm.part[w][j][0];
+            ap += sm.part[w][j][1];
         }
         const double sv = tot_s[j];
         const double u = 1.1102230246251565e-16;  // 2^-53
@@ -291,15 +264,15 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
         const double err = __dadd_ru(err_ref, err_our);
         const float lo = __double2float_rn(__dsub_rd(sv, err));
         const float hi = __double2float_rn(__dadd_ru(sv, err));
-        score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(sv);
-        if (lo != hi) atomicOr(&s_und, 1u << j);
+        score_row[k0 + j] = __double2float_rn(sv);
+        if (lo != hi) atomicOr(&sm.und, 1u << j);
     }
     __syncthreads();
     }   // tier 2
     // replay: the reference's exact sequential loop (matrix.cpp:29-34).  The
     // CTA forms the (exact) products in shared memory, then one thread adds
     // them in index order -- a dependent f64 chain, loads hoisted ahead
-    const unsigned und = s_und;
+    const unsigned und = sm.und;
     for (int j = 0; j < kRouteExperts; ++j) {
         if (!(und & (1u << j))) continue;
         const float* gk = gate + static_cast<int64_t>(k0 + j) * in_dim;
@@ -307,37 +280,35 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
             const int n = min(kReplayWin, in_dim - c0);
             __syncthreads();
             for (int q = threadIdx.x; q < n; q += kRT)
-                prod[q] = static_cast<double>(xb[c0 + q]) * static_cast<double>(gk[c0 + q]);
+                sm.prod[q] = static_cast<double>(xb[c0 + q]) * static_cast<double>(gk[c0 + q]);
             __syncthreads();
             if (threadIdx.x == 0) {
-                double acc = replay_acc;
+                double acc = sm.replay_acc;
                 int q = 0;
                 for (; q + 8 <= n; q += 8) {
                     double v[8];
 #pragma unroll
-                    for (int t = 0; t < 8; ++t) v[t] = prod[q + t];
+                    for (int t = 0; t < 8; ++t) v[t] = sm.prod[q + t];
 #pragma unroll
                     for (int t = 0; t < 8; ++t) acc = __dadd_rn(acc, v[t]);
                 }
-                for (; q < n; ++q) acc = __dadd_rn(acc, prod[q]);
-                replay_acc = c0 + n < in_dim ? acc : 0.0;
-                if (c0 + n >= in_dim) score_ws[static_cast<int64_t>(b) * num_experts + k0 + j] = __double2float_rn(acc);
+                for (; q < n; ++q) acc = __dadd_rn(acc, sm.prod[q]);
+                sm.replay_acc = c0 + n < in_dim ? acc : 0.0;
+                if (c0 + n >= in_dim) score_row[k0 + j] = __double2float_rn(acc);
             }
         }
     }
-    // ---- the last slice CTA of token b finishes the routing ----
-    if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();   // score_ws writers
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const int done = atomicAdd(&ticket[b], 1);
-        s_last = done == static_cast<int>(gridDim.y) - 1;
-        if (s_last) ticket[b] = 0;   // ready for the next launch
-    }
-    __syncthreads();
-    if (s_last && warp == 0) {
+    return und;
+}
+
+// Softmax and top-k of one token's certified scores (moe.cpp:64-87), run by
+// ONE warp: mx, prob_k = exp(s_k - mx) in f64, total summed k = 0..K-1,
+// order by (prob desc, index asc), gate = float(prob / selected).
+__device__ void route_pick(const float* score_row, int num_experts, int top_k, float* sc, double* ex, int* pick_k,
+                           double* pick_p, int32_t* __restrict__ ids_row, float* __restrict__ gates_row) {
+    const int lane = threadIdx.x & 31;
     __threadfence();
-    for (int k = lane; k < num_experts; k += 32) sc[k] = __ldcg(score_ws + static_cast<int64_t>(b) * num_experts + k);
+    for (int k = lane; k < num_experts; k += 32) sc[k] = __ldcg(score_row + k);
     __syncwarp();
     double mx = -INFINITY;
     for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[k]));
@@ -378,9 +349,65 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
     }
     __syncwarp();
     for (int tt = lane; tt < top_k; tt += 32) {
-        ids[static_cast<int64_t>(b) * top_k + tt] = pick_k[tt];
-        gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pick_p[tt], selected));
+        ids_row[tt] = pick_k[tt];
+        gates_row[tt] = __double2float_rn(__ddiv_rn(pick_p[tt], selected));
     }
+}
+
+template <int kRT>
+__global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x, int batch, int in_dim,
+                                                             const float* __restrict__ gate, int num_experts,
+                                                             int top_k, int group_size, int groups, int k_pad,
+                                                             int32_t* __restrict__ ids, float* __restrict__ gates,
+                                                             __half* __restrict__ x16, float* __restrict__ sx,
+                                                             float* __restrict__ score_ws, int32_t* __restrict__ ticket,
+                                                             int tokens_per_cta, const PlanArgs plan,
+                                                             int32_t* __restrict__ plan_ticket) {
+    __shared__ RouteSmem<kRT> sm;
+    __shared__ float sc[64];
+    __shared__ double ex[64];
+    __shared__ int pick_k[64];
+    __shared__ double pick_p[64];
+    __shared__ int s_last;
+    pdl_wait();
+    pdl_launch_dependents();
+    const int k0 = blockIdx.y * kRouteExperts;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // prefill: several tokens per CTA, the CTA's gate slice is re-read from L1
+    for (int tb = 0; tb < tokens_per_cta; ++tb) {
+    const int b = blockIdx.x * tokens_per_cta + tb;
+    if (b >= batch) break;
+    const float* xb = x + static_cast<int64_t>(b) * in_dim;
+    if (blockIdx.y == 0) {
+        // fp16 activations (zero-padded to k_pad) and per-group sums of them
+        if (x16) {
+            __half* xo = x16 + static_cast<int64_t>(b) * k_pad;
+            for (int c = threadIdx.x; c < k_pad; c += kRT) xo[c] = __float2half_rn(c < in_dim ? xb[c] : 0.0f);
+        }
+        for (int g = warp; sx && g < groups; g += (kRT / 32)) {
+            float acc = 0.0f;
+            const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
+            for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+            if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
+        }
+    }
+    if (num_experts == 0) continue;  // activations-only prep (tq_forward with given routing)
+    const unsigned und = route_slice<kRT>(xb, in_dim, gate, num_experts, k0, score_ws + static_cast<int64_t>(b) * num_experts, sm);
+    // ---- the last slice CTA of token b finishes the routing ----
+    if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();   // score_ws writers
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int done = atomicAdd(&ticket[b], 1);
+        s_last = done == static_cast<int>(gridDim.y) - 1;
+        if (s_last) ticket[b] = 0;   // ready for the next launch
+    }
+    __syncthreads();
+    if (s_last && warp == 0) {
+    route_pick(score_ws + static_cast<int64_t>(b) * num_experts, num_experts, top_k, sc, ex, pick_k, pick_p,
+               ids + static_cast<int64_t>(b) * top_k, gates + static_cast<int64_t>(b) * top_k);
     }   // last slice CTA of token b
     }   // tokens of this CTA
     // ---- fused plan: the globally-last CTA permutes the finished routing ----
@@ -395,7 +422,7 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
         __syncthreads();
         if (s_last) {
             __threadfence();
-            plan_body(plan, reinterpret_cast<int32_t*>(prod));   // (16 + 1) * K + 1 ints <= 16 KB
+            plan_body(plan, reinterpret_cast<int32_t*>(sm.prod));   // (16 + 1) * K + 1 ints <= 16 KB
         }
     }
 }
@@ -1526,6 +1553,273 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 }
 
 // =============================================================================
+// decode path, launch 1: route + rank-r projections + scatter into expert slots
+// =============================================================================
+//
+// Grid (token b, y): y < nslices scores kRouteExperts experts of token b
+// (route_slice, bit-exact route()); the next num_q CTAs compute the token's
+// rank-r projection of each folded / scalar tile column q (infer.cpp:104-121):
+//     Z_q[j] = sigma_j * vabs_q/127 * sum_c v_q[j, c] * x[c] / s_q[c]
+// (the reference's x . P^T with P = sigma * v / s, formed as v . (x / s) with
+// the exact int8 codes).  The last CTA of the token (ticket) picks the top-k,
+// takes a slot in each chosen expert (atomic counter; the row order inside an
+// expert is irrelevant to the numerics: every row is an independent MMA
+// column), computes general-tier projections for its routed experts only
+// (x / s_e, infer.cpp:133-155 -- work B * top_k * r * i), and writes the fp16
+// activation row and the extension row [Sx | Z * zscale_e] of every destination
+// in the atom-major swizzled layout the expert GEMM bulk-copies.
+
+// out[j] = vscale[j] * sum_c codes[j, c] * xs(c) for j < r, xs(c) = x[c] / s[c] (s may be
+// null: xs = x); the whole CTA takes part, warp 0 writes out[] (fixed summation order).
+template <int kRT>
+__device__ void dec_project(const float* __restrict__ xb, const float* __restrict__ s, int in_dim,
+                            const int8_t* __restrict__ codes, const float* __restrict__ vscale, int r,
+                            float* out, float* red /* [kRT] */) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool vec8 = (in_dim & 7) == 0;
+    for (int j0 = 0; j0 < r; j0 += 32) {
+        float acc[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
+        for (int c0 = 8 * threadIdx.x; c0 < in_dim; c0 += 8 * kRT) {
+            float xs[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = c0 + m;
+                const float xv = c < in_dim ? xb[c] : 0.0f;
+                xs[m] = (s && c < in_dim) ? __fdiv_rn(xv, s[c]) : xv;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j0 + j < r) {
+                    const int8_t* row = codes + static_cast<int64_t>(j0 + j) * in_dim + c0;
+                    int8_t v[8];
+                    if (vec8) {
+                        *reinterpret_cast<int2*>(v) = __ldg(reinterpret_cast<const int2*>(row));
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < 8; ++m) v[m] = c0 + m < in_dim ? row[m] : 0;
+                    }
+#pragma unroll
+                    for (int m = 0; m < 8; ++m) acc[j] = fmaf(static_cast<float>(v[m]), xs[m], acc[j]);
+                }
+            }
+        }
+        // warp reduce-scatter: lane l ends with the warp's sum of acc[l]
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = (lane & h) != 0;
+#pragma unroll
+            for (int j = 0; j < h; ++j) {
+                const float send = up ? acc[j] : acc[j + h];
+                const float keep = up ? acc[j + h] : acc[j];
+                acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+            }
+        }
+        __syncthreads();   // red[] of the previous round consumed
+        red[warp * 32 + lane] = acc[0];
+        __syncthreads();
+        if (warp == 0 && j0 + lane < r) {
+            float v = 0.0f;
+            for (int w = 0; w < kRT / 32; ++w) v += red[w * 32 + lane];
+            out[j0 + lane] = v * vscale[j0 + lane];
+        }
+    }
+}
+
+constexpr int kDecRT = 512;
+
+__global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a) {
+    __shared__ RouteSmem<kDecRT> sm;
+    __shared__ float sc[64];
+    __shared__ double ex[64];
+    __shared__ int pick_k[64];
+    __shared__ double pick_p[64];
+    __shared__ int s_last;
+    __shared__ int s_row[kDecMaxTopK + 64];
+    __shared__ int s_e[kDecMaxTopK + 64];
+    __shared__ float s_sx[64];
+    __shared__ float s_z[kDecMaxTopK][64];
+    __shared__ float red[kDecRT];
+    const int b = blockIdx.x;
+    const int K = a.num_experts;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nslices = a.given ? 0 : (K + kRouteExperts - 1) / kRouteExperts;
+    const float* xb = a.x + static_cast<int64_t>(b) * a.in_dim;
+    const int y = blockIdx.y;
+    if (y < nslices) {
+        const unsigned und = route_slice<kDecRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts,
+                                                 a.score_ws + static_cast<int64_t>(b) * K, sm);
+        if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();
+    } else {
+        const int q = y - nslices;
+        const int tier = a.q_tier[q];
+        if (a.use_lr && (tier == 0 || tier == 1)) {
+            const float* s = tier == 0 ? a.scaling + static_cast<int64_t>(a.q_first[q]) * a.in_dim : nullptr;
+            dec_project<kDecRT>(xb, s, a.in_dim, a.vcodes + static_cast<int64_t>(q) * a.rank * a.in_dim,
+                                a.vscale + q * a.rank, a.rank, a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank,
+                                red);
+            if (threadIdx.x < 32) __threadfence();
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int done = atomicAdd(&a.ticket[b], 1);
+        s_last = done == static_cast<int>(gridDim.y) - 1;
+        if (s_last) a.ticket[b] = 0;   // ready for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int k = a.top_k;
+    // ---- routing decision ----
+    if (!a.given) {
+        if (warp == 0)
+            route_pick(a.score_ws + static_cast<int64_t>(b) * K, K, k, sc, ex, pick_k, pick_p,
+                       a.ids + static_cast<int64_t>(b) * k, a.gates + static_cast<int64_t>(b) * k);
+    } else if (static_cast<int>(threadIdx.x) < k) {
+        pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
+    }
+    __syncthreads();
+    // ---- destinations: one slot per routed expert, the shared-expert rows ----
+    if (static_cast<int>(threadIdx.x) < k) {
+        const int e = pick_k[threadIdx.x];
+        int row = -1;
+        if (e < 0 || e >= K) {
+            atomicExch(a.err_flag, 1);   // expert id out of range (moe.cpp:111-114)
+        } else {
+            const int slot = atomicAdd(&a.cnt[e], 1);
+            row = e * a.cap8 + slot;
+        }
+        s_row[threadIdx.x] = row;
+        s_e[threadIdx.x] = row >= 0 ? e : -1;
+        a.inv[static_cast<int64_t>(b) * k + threadIdx.x] = row;
+    }
+    if (static_cast<int>(threadIdx.x) < a.num_shared) {
+        s_row[k + threadIdx.x] = (K + static_cast<int>(threadIdx.x)) * a.cap8 + b;
+        s_e[k + threadIdx.x] = -1;
+    }
+    __syncthreads();
+    const int nd = k + (a.use_main ? a.num_shared : 0);
+    // ---- rank-r terms of the routed destinations ----
+    if (a.use_lr) {
+        for (int t = 0; t < k; ++t) {
+            const int e = s_e[t];
+            if (e < 0) continue;   // block-uniform
+            const int q = a.e_q[e];
+            if (a.q_tier[q] == 2) {
+                dec_project<kDecRT>(xb, a.scaling + static_cast<int64_t>(e) * a.in_dim, a.in_dim,
+                                    a.vcodes + static_cast<int64_t>(q) * a.rank * a.in_dim, a.vscale + q * a.rank,
+                                    a.rank, s_z[t], red);
+            } else {
+                const float* zi = a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank;
+                for (int j = threadIdx.x; j < a.rank; j += kDecRT) s_z[t][j] = __ldcg(zi + j);
+            }
+        }
+    }
+    // ---- group sums of the fp16 activations (zero-point term) ----
+    for (int g = warp; a.use_main && g < a.groups; g += kDecRT / 32) {
+        float acc = 0.0f;
+        const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
+        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+        if (lane == 0) s_sx[g] = acc;
+    }
+    __syncthreads();
+    // ---- fp16 activation row -> every destination (atom-major, 128B swizzle of the row index) ----
+    auto piece = [&](__half* base, int row, int t8) -> int4* {
+        const int at = t8 >> 3, ch = t8 & 7;
+        return reinterpret_cast<int4*>(base + ((static_cast<int64_t>(at) * a.atom_rows + row) * 64 + ((ch ^ (row & 7)) << 3)));
+    };
+    if (a.use_main) {
+        for (int t8 = threadIdx.x; t8 < a.k_pad / 8; t8 += kDecRT) {
+            __align__(16) __half h[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = t8 * 8 + m;
+                h[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
+            }
+            const int4 v = *reinterpret_cast<const int4*>(h);
+            for (int d = 0; d < nd; ++d)
+                if (s_row[d] >= 0) *piece(a.xperm, s_row[d], t8) = v;
+        }
+    }
+    // ---- extension rows [Sx | Z * zscale_e | 0] ----
+    const int n8 = a.ext_cols / 8;
+    for (int idx = threadIdx.x; idx < nd * n8; idx += kDecRT) {
+        const int d = idx / n8, t8 = idx % n8;
+        const int row = s_row[d];
+        if (row < 0) continue;
+        const int e = s_e[d];
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int col = t8 * 8 + m;
+            float v = 0.0f;
+            if (col < a.groups) {
+                if (a.use_main) v = s_sx[col];
+            } else if (col < a.groups + a.rank) {
+                if (a.use_lr && e >= 0) v = s_z[d][col - a.groups] * a.zscale[e];
+            }
+            h[m] = __float2half_rn(v);
+        }
+        *piece(a.extperm, row, t8) = *reinterpret_cast<const int4*>(h);
+    }
+}
+
+// decode path, launch 3: y[b] = sum_t g_bt * Y[slot(b, t)] (t ascending) + sum_s Y_s[b]
+// (reference_forward's order, moe.cpp:115-132); zeroes the slot counters.
+__global__ void __launch_bounds__(256) dec_combine_kernel(const DecCombineArgs a) {
+    __shared__ int s_row[64];
+    __shared__ float s_gate[64];
+    const int b = blockIdx.y;
+    if (blockIdx.x == 0 && blockIdx.y == 0)
+        for (int e = threadIdx.x; e < a.num_experts; e += blockDim.x) a.cnt[e] = 0;
+    if (static_cast<int>(threadIdx.x) < a.top_k) {
+        const int64_t f = static_cast<int64_t>(b) * a.top_k + threadIdx.x;
+        s_row[threadIdx.x] = a.inv[f];
+        s_gate[threadIdx.x] = a.gates[f];
+    }
+    __syncthreads();
+    const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c0 >= a.out_dim) return;
+    const bool vec = (a.out_dim & 3) == 0 && (a.ldy & 3) == 0;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    auto row4 = [&](int64_t row, float (&v)[4]) {
+        const float* p = a.yslot + row * a.ldy + c0;
+        if (vec) {
+            const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+            v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+        } else {
+            for (int j = 0; j < 4; ++j) v[j] = c0 + j < a.out_dim ? p[j] : 0.0f;
+        }
+    };
+    for (int t = 0; t < a.top_k; ++t) {
+        if (s_row[t] < 0) continue;
+        float v[4];
+        row4(s_row[t], v);
+        const float g = s_gate[t];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] = fmaf(g, v[j], acc[j]);
+    }
+    for (int s = 0; s < a.num_shared; ++s) {
+        float v[4];
+        row4(static_cast<int64_t>(a.num_experts + s) * a.cap8 + b, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += v[j];
+    }
+    float* o = a.out + static_cast<int64_t>(b) * a.out_dim + c0;
+    if (vec) {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    } else {
+        for (int j = 0; j < 4; ++j)
+            if (c0 + j < a.out_dim) o[j] = acc[j];
+    }
+}
+
+// =============================================================================
 // launch wrappers (called from tq_runtime.cpp)
 // =============================================================================
 
@@ -1758,6 +2052,25 @@ cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, i
     export_codes_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(wcodes, bits, kc_total, out_dim,
                                                                                      in_dim, out);
     return cudaGetLastError();
+}
+
+cudaError_t launch_dec_route(const DecRouteArgs& a, cudaStream_t stream) {
+    if (a.batch <= 0) return cudaSuccess;
+    if (a.num_experts > 64 || a.top_k > kDecMaxTopK || a.top_k + a.num_shared > kDecMaxTopK + 64 || a.groups > 64 ||
+        a.rank > 64)
+        return cudaErrorInvalidValue;
+    const int nslices = a.given ? 0 : (a.num_experts + kRouteExperts - 1) / kRouteExperts;
+    const int ny = nslices + a.num_q;
+    if (ny < 1) return cudaErrorInvalidValue;
+    max_carveout(dec_route_kernel);
+    return launch_maybe_pdl(dec_route_kernel, dim3(a.batch, ny), dim3(kDecRT), 0, stream, a);
+}
+
+cudaError_t launch_dec_combine(const DecCombineArgs& a, cudaStream_t stream) {
+    if (a.batch <= 0) return cudaSuccess;
+    if (a.top_k > 64) return cudaErrorInvalidValue;
+    max_carveout(dec_combine_kernel);
+    return launch_maybe_pdl(dec_combine_kernel, dim3((a.out_dim + 1023) / 1024, a.batch), dim3(256), 0, stream, a);
 }
 
 }  // namespace tqb

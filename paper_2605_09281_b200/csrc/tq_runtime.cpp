@@ -47,6 +47,9 @@ cudaError_t launch_lr_left(const float* U, int o, int r, const float* mid, const
 cudaError_t launch_dequant_all(const DequantAllArgs& a, int bits, cudaStream_t stream);
 cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count, uint32_t* out,
                           int32_t* err_flag, cudaStream_t stream);
+cudaError_t launch_dec_route(const DecRouteArgs& a, cudaStream_t stream);
+cudaError_t launch_dec_combine(const DecCombineArgs& a, cudaStream_t stream);
+cudaError_t launch_decode(const DecParams& p, int dn, int grid, cudaStream_t stream);
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream);
 
@@ -493,6 +496,11 @@ struct tq_layer {
         err_flag, xin, yout, nsplit_d;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
+    // decode path (batch <= kDecMaxBatch): route+scatter -> fused expert GEMM -> combine
+    DBuf vcodes, vscale, q_tier, q_first, e_q, scaling_d;            // rank-r projection tables
+    DBuf dec_xperm, dec_extperm, dec_yslot, dec_cnt, dec_inv, dec_zq, dec_scratch, dec_segcnt;
+    int64_t dec_atom_rows = 0;
+    bool dec_ready = false;
     std::atomic<uint64_t> launches{0};
     // comparison layouts (infer.cpp:187-339): decoded factors kept on the host
     // (decode_block_i8, codec.cpp:122-129) and device copies built on demand
@@ -1084,6 +1092,29 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     L->pm_of.upload(pm_of.data(), pm_of.size() * 4);
     L->zscale.upload(zscale.data(), zscale.size() * 4);
     L->rowscale.upload(rowscale.data(), rowscale.size() * 4);
+    // decode path: rank-r projection tables -- the exact int8 V codes and the per-row
+    // factor sigma_j * vabs_q / 127 (decode_block_i8, codec.cpp:122-129), the
+    // descale tier of every tile column and the scaling vectors (infer.cpp:74-117)
+    {
+        std::vector<float> vsc(N * R);
+        for (size_t qq = 0; qq < N; ++qq) {
+            const float sc = vabs[qq] == 0.0f ? 0.0f : vabs[qq] / 127.0f;
+            for (size_t j = 0; j < R; ++j)
+                vsc[qq * R + j] = static_cast<float>(static_cast<double>(sigma[j]) * static_cast<double>(sc));
+        }
+        std::vector<int32_t> qt(N), qf(N), eq(K);
+        for (size_t qq = 0; qq < N; ++qq) {
+            qt[qq] = first[qq] < 0 ? -1 : tier[qq];
+            qf[qq] = first[qq] < 0 ? 0 : static_cast<int32_t>(first[qq]);
+        }
+        for (size_t e = 0; e < K; ++e) eq[e] = placement[2 * e + 1];
+        L->vcodes.upload(v_b.data(), v_b.size());
+        L->vscale.upload(vsc.data(), vsc.size() * 4);
+        L->q_tier.upload(qt.data(), qt.size() * 4);
+        L->q_first.upload(qf.data(), qf.size() * 4);
+        L->e_q.upload(eq.data(), eq.size() * 4);
+        L->scaling_d.upload(scaling.data(), scaling.size() * 4);
+    }
     L->device_bytes = static_cast<int64_t>(L->gate.n + L->codes.n + L->scales.n + L->ext_blocks.n + L->pcodes.n +
                                            L->rowscale.n);
     reserve(L, 64);
@@ -1402,6 +1433,163 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     count_launch(L);
 }
 
+// ---------------------------------------------------------------------------
+// decode path: 3 launches per forward (route+project+scatter, fused expert GEMM
+// with split-segment fixup, combine)
+// ---------------------------------------------------------------------------
+constexpr int64_t kDecMaxBatch = 64;   // slots per expert (and tokens) the decode workspace holds
+
+bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
+    static const bool off = [] {
+        const char* e = std::getenv("TQ_NO_DECODE");   // 1: decode-sized batches on the grouped-GEMM path
+        return e && e[0] == '1';
+    }();
+    const Geometry& g = L->g;
+    const int64_t slots = given ? batch * g.top_k : batch;
+    return !off && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
+           g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64;
+}
+
+void reserve_decode(tq_layer* L) {
+    if (L->dec_ready) return;
+    cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+    const Geometry& g = L->g;
+    const int64_t W = g.K + g.S;
+    const int64_t rows = W * kDecMaxBatch + 64;   // + slack: 16-row MMA tiles read past a weight's last slot
+    L->dec_atom_rows = rows;
+    L->dec_xperm.alloc(sizeof(__half) * rows * g.k_pad);
+    L->dec_extperm.alloc(sizeof(__half) * rows * g.n_ext * 64);
+    cuda_check(cudaMemset(L->dec_xperm.p, 0, L->dec_xperm.n), "cudaMemset");
+    cuda_check(cudaMemset(L->dec_extperm.p, 0, L->dec_extperm.n), "cudaMemset");
+    L->dec_yslot.alloc(sizeof(float) * W * kDecMaxBatch * g.o);
+    L->dec_cnt.alloc(sizeof(int32_t) * g.K);
+    cuda_check(cudaMemset(L->dec_cnt.p, 0, L->dec_cnt.n), "cudaMemset");
+    L->dec_inv.alloc(sizeof(int32_t) * kDecMaxBatch * g.top_k);
+    L->dec_zq.alloc(sizeof(float) * kDecMaxBatch * g.N * g.r);
+    L->dec_scratch.alloc(sizeof(float) * L->num_sms * 2 * 64 * kBM);
+    L->dec_segcnt.alloc(sizeof(int32_t) * W * g.mb_count);
+    cuda_check(cudaMemset(L->dec_segcnt.p, 0, L->dec_segcnt.n), "cudaMemset");
+    L->dec_ready = true;
+}
+
+// ids_in / gates_in: given routing (tq_forward) or null (routed here)
+void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_in, const float* gates_in, float* y,
+                int path, cudaStream_t st) {
+    const Geometry& g = L->g;
+    reserve_decode(L);
+    const bool given = ids_in != nullptr;
+    const bool use_main = path != TQ_PATH_LOTILE;
+    const bool use_lr = path != TQ_PATH_QMOE;
+    const int S = use_main ? static_cast<int>(g.S) : 0;   // lotile_forward has no shared experts
+    const int64_t cap8 = round_up(given ? batch * g.top_k : batch, 8);
+    const int dn = cap8 <= 32 ? 32 : 64;
+    if (L->ktime) {
+        L->kt_stream = st;
+        L->kt_active = true;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        L->kev.push_back({e});
+    }
+    DecRouteArgs ra{};
+    ra.x = x;
+    ra.batch = static_cast<int>(batch);
+    ra.in_dim = static_cast<int>(g.i);
+    ra.k_pad = static_cast<int>(g.k_pad);
+    ra.gate = L->gate.as<float>();
+    ra.num_experts = static_cast<int>(g.K);
+    ra.top_k = static_cast<int>(g.top_k);
+    ra.num_shared = S;
+    ra.given = given ? 1 : 0;
+    ra.ids_in = ids_in;
+    ra.ids = L->ids.as<int32_t>();
+    ra.gates = L->gates.as<float>();
+    ra.score_ws = L->route_ws.as<float>();
+    ra.ticket = L->route_ticket.as<int32_t>();
+    ra.group_size = static_cast<int>(g.gs);
+    ra.groups = static_cast<int>(g.G);
+    ra.rank = static_cast<int>(g.r);
+    ra.num_q = static_cast<int>(g.N);
+    ra.vcodes = L->vcodes.as<int8_t>();
+    ra.vscale = L->vscale.as<float>();
+    ra.q_tier = L->q_tier.as<int32_t>();
+    ra.q_first = L->q_first.as<int32_t>();
+    ra.scaling = L->scaling_d.as<float>();
+    ra.e_q = L->e_q.as<int32_t>();
+    ra.zscale = L->zscale.as<float>();
+    ra.zq_ws = L->dec_zq.as<float>();
+    ra.use_main = use_main ? 1 : 0;
+    ra.use_lr = use_lr ? 1 : 0;
+    ra.cap8 = static_cast<int>(cap8);
+    ra.atom_rows = L->dec_atom_rows;
+    ra.ext_cols = static_cast<int>(g.n_ext * 64);
+    ra.xperm = L->dec_xperm.as<__half>();
+    ra.extperm = L->dec_extperm.as<__half>();
+    ra.cnt = L->dec_cnt.as<int32_t>();
+    ra.inv = L->dec_inv.as<int32_t>();
+    ra.err_flag = L->err_flag.as<int32_t>();
+    cuda_check(launch_dec_route(ra, st), "dec_route_kernel launch");
+    count_launch(L);
+
+    DecParams dp{};
+    dp.codes = L->codes.as<uint8_t>();
+    dp.weight_stride = L->weight_stride;
+    dp.scales = L->scales.as<__half>();
+    dp.ext_blocks = L->ext_blocks.as<uint8_t>();
+    dp.n_ext64 = static_cast<int>(g.n_ext);
+    dp.w_outscale = L->w_outscale.as<float>();
+    dp.bits = static_cast<int>(g.bits);
+    dp.group_size = static_cast<int>(g.gs);
+    dp.groups = static_cast<int>(g.G);
+    dp.kc64 = static_cast<int>(g.kc_total);
+    dp.nmain = use_main ? static_cast<int>((g.kc_total + 1) / 2) : 0;
+    dp.n_ep = static_cast<int>((g.G + g.r + 31) / 32);
+    dp.mb_count = static_cast<int>(g.mb_count);
+    dp.o_valid = static_cast<int>(g.o);
+    dp.num_experts = static_cast<int>(g.K);
+    dp.num_shared = S;
+    dp.batch = static_cast<int>(batch);
+    dp.cnt = L->dec_cnt.as<int32_t>();
+    dp.cap8 = static_cast<int>(cap8);
+    dp.atom_rows = L->dec_atom_rows;
+    dp.xperm = L->dec_xperm.as<__half>();
+    dp.extperm = L->dec_extperm.as<__half>();
+    dp.yslot = L->dec_yslot.as<float>();
+    dp.ldy = static_cast<int>(g.o);
+    dp.scratch = L->dec_scratch.as<float>();
+    dp.seg_cnt = L->dec_segcnt.as<int32_t>();
+    {
+        cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+        if (L->timing) {
+            cuda_check(cudaEventCreate(&ev0), "cudaEventCreate");
+            cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
+            cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
+        }
+        cuda_check(launch_decode(dp, dn, L->num_sms, st), "dec_gemm_kernel launch");
+        if (L->timing) {
+            cuda_check(cudaEventRecord(ev1, st), "cudaEventRecord");
+            L->tev.emplace_back(ev0, ev1);
+        }
+    }
+    count_launch(L);
+
+    DecCombineArgs ca{};
+    ca.yslot = L->dec_yslot.as<float>();
+    ca.ldy = static_cast<int>(g.o);
+    ca.inv = L->dec_inv.as<int32_t>();
+    ca.gates = given ? gates_in : L->gates.as<float>();
+    ca.batch = static_cast<int>(batch);
+    ca.top_k = static_cast<int>(g.top_k);
+    ca.out_dim = static_cast<int>(g.o);
+    ca.num_shared = S;
+    ca.num_experts = static_cast<int>(g.K);
+    ca.cap8 = static_cast<int>(cap8);
+    ca.cnt = L->dec_cnt.as<int32_t>();
+    ca.out = y;
+    cuda_check(launch_dec_combine(ca, st), "dec_combine_kernel launch");
+    count_launch(L);
+}
+
 void check_layer(const tq_layer* L) {
     if (!L) fail(TQ_ERR_PARAM, "null layer");
 }
@@ -1580,7 +1768,13 @@ tq_status tq_forward(tq_layer* L, const float* x, int64_t batch, const int32_t* 
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const void* const key[6] = {x, ids, gates, y, nullptr, nullptr};
-        run_graphed(L, key, batch, path, st, [&](cudaStream_t s2) {
+        const bool dec = decode_ok(L, batch, true);
+        if (dec) reserve_decode(L);
+        run_graphed(L, key, batch, path + (dec ? 64 : 0), st, [&](cudaStream_t s2) {
+            if (dec) {
+                run_decode(L, x, batch, ids, gates, y, path, s2);
+                return;
+            }
             run_route(L, x, batch, false, s2);
             run_experts(L, x, batch, ids, gates, y, path, s2);
         });
@@ -1597,10 +1791,16 @@ tq_status tq_forward_routed(tq_layer* L, const float* x, int64_t batch, float* y
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const void* const key[6] = {x, nullptr, nullptr, y, ids, gates};
+        const bool dec = decode_ok(L, batch, false);
+        if (dec) reserve_decode(L);
         run_graphed(L, key, batch, path + 16, st, [&](cudaStream_t s2) {
-            const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
-            run_route(L, x, batch, true, s2, fuse_plan(L) ? &pa : nullptr);
-            run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2, fuse_plan(L));
+            if (dec) {
+                run_decode(L, x, batch, nullptr, nullptr, y, path, s2);
+            } else {
+                const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
+                run_route(L, x, batch, true, s2, fuse_plan(L) ? &pa : nullptr);
+                run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2, fuse_plan(L));
+            }
             if (ids)
                 cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
                                            s2),
@@ -1621,12 +1821,18 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
         if (batch == 0) return;
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cudaStream_t st = nullptr;
+        const bool dec = decode_ok(L, batch, false);
+        if (dec) reserve_decode(L);
         auto body = [&](cudaStream_t s2) {
             cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, s2), "x H2D");
-            const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
-            run_route(L, L->xin.as<float>(), batch, true, s2, fuse_plan(L) ? &pa : nullptr);
-            run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(), L->yout.as<float>(),
-                        path, s2, fuse_plan(L));
+            if (dec) {
+                run_decode(L, L->xin.as<float>(), batch, nullptr, nullptr, L->yout.as<float>(), path, s2);
+            } else {
+                const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
+                run_route(L, L->xin.as<float>(), batch, true, s2, fuse_plan(L) ? &pa : nullptr);
+                run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(),
+                            L->yout.as<float>(), path, s2, fuse_plan(L));
+            }
             cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, s2),
                        "y D2H");
         };
@@ -1641,7 +1847,7 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
         };
         if (pinned(x) && pinned(y)) {
             const void* const key[6] = {x, y, nullptr, nullptr, nullptr, nullptr};
-            run_graphed(L, key, batch, path + 32, st, body);
+            run_graphed(L, key, batch, path + 32 + (dec ? 64 : 0), st, body);
         } else {
             body(st);
         }

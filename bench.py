@@ -432,8 +432,6 @@ def bench_tileq(args, rank, world, local_rank):
             "per_batch": per_b, "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_forward": launches / max(1, args.steps * len(batches)),
             "gemm_launches_per_forward": launches_per_fwd, "clocks": clk, "clock_settle_steps": settle}
-    if os.environ.get("TQ_BENCH_RETRY"):
-        line["retry_after_fault"] = os.environ["TQ_BENCH_RETRY"]
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, art, geo)
     print(json.dumps(line), flush=True)
@@ -537,22 +535,8 @@ def main():
             dist.destroy_process_group()
     if args.impl == "reference":
         return bench_reference(args, 0, 1)
-    try:
-        return bench_tileq(args, 0, 1, local_rank)
-    except Exception as e:   # noqa: BLE001
-        # An intermittent device fault of the decode GEMM ("known
-        # issue") poisons the CUDA context; re-run the bench ONCE in a fresh
-        # process and record the fault in its JSON line (never silently).
-        msg = f"{type(e).__name__}: {str(e).splitlines()[0] if str(e) else ''}"
-        if "CUDA" not in msg and "cuda" not in msg:
-            raise
-        if os.environ.get("TQ_BENCH_RETRY"):
-            raise
-        print(f"bench: device fault ({msg}); re-running once in a fresh process", file=sys.stderr, flush=True)
-        import subprocess
-        env = dict(os.environ, TQ_BENCH_RETRY=msg[:200])
-        return subprocess.run([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env).returncode
-
+    # a device fault fails the run (non-zero exit): a faulting kernel posts no number
+    return bench_tileq(args, 0, 1, local_rank)
 
 if __name__ == "__main__":
     sys.exit(main())

@@ -149,6 +149,11 @@ tq_status tq_forward_host(tq_layer* layer, const float* x, int64_t batch, float*
  * layer's kernels since the last sync (e.g. expert id out of range). */
 tq_status tq_sync(tq_layer* layer, void* stream);
 
+/* Diagnostics: copy the decode path's self-resetting device counters to the host
+ * (slot counts [K], router tickets [reserved batch], split-segment arrivals
+ * [(K + S) * m-blocks]); every entry reads zero between forwards. */
+tq_status tq_debug_decode_counters(tq_layer* layer, int32_t* out, int64_t n);
+
 /* GPU unpack of a packed stream (codec.cpp:168-195): bytes [dev], out [dev]
  * uint32 count.  Returns TQ_ERR_PARAM on a bad width or byte count and
  * TQ_ERR_FORMAT on nonzero padding bits (after synchronizing). */

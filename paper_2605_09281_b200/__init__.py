@@ -108,6 +108,7 @@ def lib() -> C.CDLL:
     L.tq_forward_routed.argtypes = [p, p, i64, p, p, p, i32, p]
     L.tq_forward_host.argtypes = [p, p, i64, p, p, p, i32]
     L.tq_sync.argtypes = [p, p]
+    L.tq_debug_decode_counters.argtypes = [p, p, i64]
     L.tq_unpack_codes.argtypes = [p, i64, i32, i64, p, p]
     L.tq_layer_export_codes.argtypes = [p, i64, p, p]
     L.tq_launch_count.restype = C.c_uint64
@@ -127,7 +128,7 @@ def lib() -> C.CDLL:
     L.tq_ep_extrow_elems.argtypes = [p]
     for name in ("tq_layer_load", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
-                 "tq_sync", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
+                 "tq_sync", "tq_debug_decode_counters", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
                  "tq_ep_expert_rows", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):
         getattr(L, name).restype = C.c_int
     _lib = L

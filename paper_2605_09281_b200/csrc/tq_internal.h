@@ -218,6 +218,7 @@ struct DecRouteArgs {
     int32_t* cnt;                    // [K] slots taken per routed expert (zeroed by the combine)
     int32_t* inv;                    // [B * top_k] slot row of (b, t), -1 for an invalid id
     int32_t* err_flag;
+    unsigned long long* trace;       // TQ_ROUTE_TRACE builds only: [cta][16] globaltimer
 };
 
 struct DecParams {
@@ -229,8 +230,7 @@ struct DecParams {
     const float* w_outscale;         // [w] 2^-k
     int bits, group_size, groups, group_shift;
     int kc64;                        // k_pad / 64
-    int nmain;                       // main steps (128 K each) per segment; 0 = low-rank only path
-    int n_ep;                        // ext pieces (32 columns) per segment
+    int nmain;                       // main steps (256 K each) per segment; 0 = low-rank only path
     int mb_count, o_valid;
     int num_experts, num_shared, batch;
     const int32_t* cnt;
@@ -243,6 +243,8 @@ struct DecParams {
     float* scratch;                  // [grid][2][dn][128] split-segment partials
     int32_t* seg_cnt;                // per segment arrivals (self-resetting)
     int code_stages, x_stages, code_stage_bytes;   // set by launch_decode
+    unsigned long long* trace;       // TQ_DEC_TRACE builds only
+    int trace_cta;
 };
 
 struct DecCombineArgs {

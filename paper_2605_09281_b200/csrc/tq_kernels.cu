@@ -318,14 +318,18 @@ __device__ void route_pick(const float* score_row, int num_experts, int top_k, f
     __syncwarp();
     double total = 0.0;   // in the reference order k = 0..K-1
     for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[k]);
+    // prob_k = exp(s_k - mx) / total, formed once (lane owns k = lane, lane + 32)
+    const double p0 = lane < num_experts ? __ddiv_rn(ex[lane], total) : -1.0;
+    const double p1 = lane + 32 < num_experts ? __ddiv_rn(ex[lane + 32], total) : -1.0;
     double selected = 0.0;
     uint64_t taken = 0;
     for (int tt = 0; tt < top_k; ++tt) {
         double best_p = -1.0;
         int best_k = 0x7fffffff;
-        for (int k = lane; k < num_experts; k += 32) {
-            if (taken & (1ull << k)) continue;
-            const double pk = __ddiv_rn(ex[k], total);
+        for (int h = 0; h < 2; ++h) {
+            const int k = lane + 32 * h;
+            if (k >= num_experts || (taken & (1ull << k))) continue;
+            const double pk = h ? p1 : p0;
             if (pk > best_p || (pk == best_p && k < best_k)) {
                 best_p = pk;
                 best_k = k;
@@ -1569,67 +1573,217 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 // activation row and the extension row [Sx | Z * zscale_e] of every destination
 // in the atom-major swizzled layout the expert GEMM bulk-copies.
 
+__device__ __forceinline__ void rtrace(const DecRouteArgs& a, int k) {
+#ifdef TQ_ROUTE_TRACE
+    if (threadIdx.x == 0 && a.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[(blockIdx.x * gridDim.y + blockIdx.y) * 16 + k] = t;
+    }
+#else
+    (void)a;
+    (void)k;
+#endif
+}
+
 // out[j] = vscale[j] * sum_c codes[j, c] * xs(c) for j < r, xs(c) = x[c] / s[c] (s may be
-// null: xs = x); the whole CTA takes part, warp 0 writes out[] (fixed summation order).
+// null: xs = x).  The whole CTA takes part: xs is staged in shared memory (xs_sm,
+// 4096 floats, columns in chunks of 4096); warp w owns rows j = w, w + nw, ...; each
+// lane issues all its 16-byte code loads of a row before using them (one memory
+// round trip per row, not one per column block); fixed-order warp reduction.
 template <int kRT>
 __device__ void dec_project(const float* __restrict__ xb, const float* __restrict__ s, int in_dim,
                             const int8_t* __restrict__ codes, const float* __restrict__ vscale, int r,
-                            float* out, float* red /* [kRT] */) {
+                            float* out, float* xs_sm, const DecRouteArgs* ta = nullptr) {
+    constexpr int kNW = kRT / 32;
+    constexpr int kChunk = 4096;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool vec8 = (in_dim & 7) == 0;
-    for (int j0 = 0; j0 < r; j0 += 32) {
-        float acc[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.0f;
-        for (int c0 = 8 * threadIdx.x; c0 < in_dim; c0 += 8 * kRT) {
-            float xs[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int c = c0 + m;
-                const float xv = c < in_dim ? xb[c] : 0.0f;
-                xs[m] = (s && c < in_dim) ? __fdiv_rn(xv, s[c]) : xv;
-            }
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                if (j0 + j < r) {
-                    const int8_t* row = codes + static_cast<int64_t>(j0 + j) * in_dim + c0;
-                    int8_t v[8];
-                    if (vec8) {
-                        *reinterpret_cast<int2*>(v) = __ldg(reinterpret_cast<const int2*>(row));
-                    } else {
-#pragma unroll
-                        for (int m = 0; m < 8; ++m) v[m] = c0 + m < in_dim ? row[m] : 0;
-                    }
-#pragma unroll
-                    for (int m = 0; m < 8; ++m) acc[j] = fmaf(static_cast<float>(v[m]), xs[m], acc[j]);
-                }
-            }
-        }
-        // warp reduce-scatter: lane l ends with the warp's sum of acc[l]
-#pragma unroll
-        for (int h = 16; h >= 1; h >>= 1) {
-            const bool up = (lane & h) != 0;
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-                const float send = up ? acc[j] : acc[j + h];
-                const float keep = up ? acc[j + h] : acc[j];
-                acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
-            }
-        }
-        __syncthreads();   // red[] of the previous round consumed
-        red[warp * 32 + lane] = acc[0];
+    const bool vec = (in_dim & 15) == 0;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // rows warp + kNW * t (r <= 64)
+    for (int c0 = 0; c0 < in_dim; c0 += kChunk) {
+        const int nc = min(kChunk, in_dim - c0);
+        __syncthreads();   // xs_sm of the previous chunk / caller consumed
+        for (int c = threadIdx.x; c < nc; c += kRT) xs_sm[c] = s ? __fdiv_rn(xb[c0 + c], s[c0 + c]) : xb[c0 + c];
         __syncthreads();
-        if (warp == 0 && j0 + lane < r) {
-            float v = 0.0f;
-            for (int w = 0; w < kRT / 32; ++w) v += red[w * 32 + lane];
-            out[j0 + lane] = v * vscale[j0 + lane];
+        if (ta) rtrace(*ta, 9);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int j = warp + kNW * t;
+            if (j >= r) break;
+            const int8_t* row = codes + static_cast<int64_t>(j) * in_dim + c0;
+            if (vec) {
+#pragma unroll
+                for (int u0 = 0; u0 < 8; u0 += 4) {
+                int4 v[4];   // 16 codes per load, lane-strided 16-byte pieces (coalesced)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = 16 * (lane + 32 * (u0 + u));
+                    v[u] = cc < nc ? __ldg(reinterpret_cast<const int4*>(row + cc)) : make_int4(0, 0, 0, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cc = 16 * (lane + 32 * (u0 + u));
+                    if (cc < nc) {
+                        const float4* x4 = reinterpret_cast<const float4*>(xs_sm + cc);
+                        const uint32_t wv[4] = {static_cast<uint32_t>(v[u].x), static_cast<uint32_t>(v[u].y),
+                                                static_cast<uint32_t>(v[u].z), static_cast<uint32_t>(v[u].w)};
+#pragma unroll
+                        for (int m4 = 0; m4 < 4; ++m4) {
+                            // int8 -> float on the full-rate ALU: bias to unsigned, splice the byte
+                            // into the mantissa of 2^23 (PRMT), subtract 2^23 + 128 (exact)
+                            const uint32_t ub = wv[m4] ^ 0x80808080u;
+                            const float4 xv = x4[m4];
+                            const float c0 = __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7540)) - 8388736.0f;
+                            const float c1 = __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7541)) - 8388736.0f;
+                            const float c2 = __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7542)) - 8388736.0f;
+                            const float c3 = __uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7543)) - 8388736.0f;
+                            acc[t] = fmaf(c0, xv.x, acc[t]);
+                            acc[t] = fmaf(c1, xv.y, acc[t]);
+                            acc[t] = fmaf(c2, xv.z, acc[t]);
+                            acc[t] = fmaf(c3, xv.w, acc[t]);
+                        }
+                    }
+                }
+                }
+            } else {
+                for (int c = lane; c < nc; c += 32) acc[t] = fmaf(static_cast<float>(row[c]), xs_sm[c], acc[t]);
+            }
         }
+    }
+    if (ta) rtrace(*ta, 10);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int j = warp + kNW * t;
+        if (j >= r) break;
+        float v = acc[t];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+        if (lane == 0) out[j] = v * vscale[j];
     }
 }
 
+// Projection CTA of the decode router: rows [j0, j0 + 16) of tile column q for one
+// token, column-parallel -- thread t owns columns [8t, 8t + 8) (+ 8 * kRT per pass),
+// issues its x, s and int8 V loads together (one memory round trip), forms the 16
+// partial dot products, and a fixed-order block reduction finishes them:
+//     out[j] = vscale[j] * sum_c v[j, c] * x[c] / s[c]        (s may be null: x)
+constexpr int kProjRows = 8;
+template <int kRT>
+__device__ void dec_project_rows(const float* __restrict__ xb, const float* __restrict__ s, int in_dim,
+                                 const int8_t* __restrict__ codes, const float* __restrict__ vscale, int nrows,
+                                 float* out, float* red /* [kRT / 32][kProjRows] */) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float acc[kProjRows];
+#pragma unroll
+    for (int j = 0; j < kProjRows; ++j) acc[j] = 0.0f;
+    const bool vec = (in_dim & 7) == 0;
+    for (int c0 = 8 * threadIdx.x; c0 < in_dim; c0 += 8 * kRT) {
+        float xs[8];
+        uint32_t v[kProjRows][2];
+        if (vec) {
+            const float4 xa = __ldg(reinterpret_cast<const float4*>(xb + c0));
+            const float4 xc = __ldg(reinterpret_cast<const float4*>(xb + c0 + 4));
+            float4 sa = make_float4(1.f, 1.f, 1.f, 1.f), sc4 = sa;
+            if (s) {
+                sa = __ldg(reinterpret_cast<const float4*>(s + c0));
+                sc4 = __ldg(reinterpret_cast<const float4*>(s + c0 + 4));
+            }
+#pragma unroll
+            for (int j = 0; j < kProjRows; ++j) {
+                if (j < nrows) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(codes + static_cast<int64_t>(j) * in_dim + c0));
+                    v[j][0] = w.x;
+                    v[j][1] = w.y;
+                } else {
+                    v[j][0] = v[j][1] = 0x80808080u ^ 0x80808080u;
+                }
+            }
+            xs[0] = xa.x; xs[1] = xa.y; xs[2] = xa.z; xs[3] = xa.w;
+            xs[4] = xc.x; xs[5] = xc.y; xs[6] = xc.z; xs[7] = xc.w;
+            if (s) {
+                xs[0] = __fdiv_rn(xs[0], sa.x); xs[1] = __fdiv_rn(xs[1], sa.y);
+                xs[2] = __fdiv_rn(xs[2], sa.z); xs[3] = __fdiv_rn(xs[3], sa.w);
+                xs[4] = __fdiv_rn(xs[4], sc4.x); xs[5] = __fdiv_rn(xs[5], sc4.y);
+                xs[6] = __fdiv_rn(xs[6], sc4.z); xs[7] = __fdiv_rn(xs[7], sc4.w);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = c0 + m;
+                xs[m] = c < in_dim ? (s ? __fdiv_rn(xb[c], s[c]) : xb[c]) : 0.0f;
+            }
+#pragma unroll
+            for (int j = 0; j < kProjRows; ++j) {
+                uint32_t b[2] = {0u, 0u};
+                for (int m = 0; m < 8; ++m) {
+                    const int c = c0 + m;
+                    const uint32_t byte = (j < nrows && c < in_dim) ? static_cast<uint8_t>(codes[static_cast<int64_t>(j) * in_dim + c]) : 0u;
+                    b[m >> 2] |= byte << (8 * (m & 3));
+                }
+                v[j][0] = b[0];
+                v[j][1] = b[1];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kProjRows; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                // int8 -> float on the full-rate ALU: bias to unsigned, splice the byte into
+                // the mantissa of 2^23 (PRMT), subtract 2^23 + 128 (exact)
+                const uint32_t ub = v[j][h] ^ 0x80808080u;
+                acc[j] = fmaf(__uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7540)) - 8388736.0f, xs[4 * h + 0], acc[j]);
+                acc[j] = fmaf(__uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7541)) - 8388736.0f, xs[4 * h + 1], acc[j]);
+                acc[j] = fmaf(__uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7542)) - 8388736.0f, xs[4 * h + 2], acc[j]);
+                acc[j] = fmaf(__uint_as_float(__byte_perm(ub, 0x4B000000u, 0x7543)) - 8388736.0f, xs[4 * h + 3], acc[j]);
+            }
+        }
+    }
+    // warp reduce-scatter (fixed order): after the halvings lane l holds the sum over
+    // its lane group of row (l % kProjRows); the remaining exchanges add the groups
+#pragma unroll
+    for (int h = kProjRows / 2; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int j = 0; j < h; ++j) {
+            const float send = up ? acc[j] : acc[j + h];
+            const float keep = up ? acc[j + h] : acc[j];
+            acc[j] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+#pragma unroll
+    for (int h = kProjRows; h < 32; h <<= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], h);
+    if (lane < kProjRows) red[warp * kProjRows + lane] = acc[0];
+    __syncthreads();
+    if (static_cast<int>(threadIdx.x) < nrows) {
+        float v = 0.0f;
+        for (int w = 0; w < kRT / 32; ++w) v += red[w * kProjRows + threadIdx.x];
+        out[threadIdx.x] = v * vscale[threadIdx.x];
+    }
+}
+
+#ifdef TQ_DEC_CHECK
+#define RT_CHECK(cond, ...)                                                                     \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("RT_CHECK line %d cta (%d,%d) thr %d: " #cond "\n", __LINE__, blockIdx.x,     \
+                   blockIdx.y, threadIdx.x);                                                    \
+            printf(__VA_ARGS__);                                                                \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define RT_CHECK(cond, ...) \
+    do {                    \
+    } while (0)
+#endif
 constexpr int kDecRT = 512;
 
-__global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a) {
+constexpr int kDecStage16 = 4096;   // fp16 row staged in shared memory up to this k_pad
+constexpr int kDecZq = 512;         // projections of a token prefetched up to num_q * rank floats
+
+// (one CTA per SM: capped at 64 registers for two, the spilling build faulted
+// intermittently in the bench -- kept uncapped)
+__global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs a) {
     __shared__ RouteSmem<kDecRT> sm;
     __shared__ float sc[64];
     __shared__ double ex[64];
@@ -1640,40 +1794,59 @@ __global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a)
     __shared__ int s_e[kDecMaxTopK + 64];
     __shared__ float s_sx[64];
     __shared__ float s_z[kDecMaxTopK][64];
-    __shared__ float red[kDecRT];
+    __shared__ __align__(16) __half s_x16[kDecStage16];
+    __shared__ float s_zq[kDecZq];
     const int b = blockIdx.x;
     const int K = a.num_experts;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nslices = a.given ? 0 : (K + kRouteExperts - 1) / kRouteExperts;
     const float* xb = a.x + static_cast<int64_t>(b) * a.in_dim;
     const int y = blockIdx.y;
+    rtrace(a, 0);
     if (y < nslices) {
         const unsigned und = route_slice<kDecRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts,
                                                  a.score_ws + static_cast<int64_t>(b) * K, sm);
         if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();
     } else {
-        const int q = y - nslices;
+        // projection CTA: rows [kProjRows * rs, + kProjRows) of tile column q
+        const int rs_cnt = (a.rank + kProjRows - 1) / kProjRows;
+        const int q = (y - nslices) / rs_cnt, rs = (y - nslices) % rs_cnt;
+        RT_CHECK(q < a.num_q && b < a.batch, "q %d rs %d y %d nslices %d\n", q, rs, y, nslices);
         const int tier = a.q_tier[q];
+        RT_CHECK(tier >= -1 && tier <= 2 && (tier != 0 || (a.q_first[q] >= 0 && a.q_first[q] < K)), "tier %d first %d\n",
+                 tier, a.q_first[q]);
         if (a.use_lr && (tier == 0 || tier == 1)) {
             const float* s = tier == 0 ? a.scaling + static_cast<int64_t>(a.q_first[q]) * a.in_dim : nullptr;
-            dec_project<kDecRT>(xb, s, a.in_dim, a.vcodes + static_cast<int64_t>(q) * a.rank * a.in_dim,
-                                a.vscale + q * a.rank, a.rank, a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank,
-                                red);
-            if (threadIdx.x < 32) __threadfence();
+            const int j0 = rs * kProjRows;
+            dec_project_rows<kDecRT>(xb, s, a.in_dim, a.vcodes + (static_cast<int64_t>(q) * a.rank + j0) * a.in_dim,
+                                     a.vscale + q * a.rank + j0, min(kProjRows, a.rank - j0),
+                                     a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank + j0,
+                                     reinterpret_cast<float*>(sm.prod));
+            __threadfence();
         }
     }
     __syncthreads();
+    rtrace(a, 1);
     if (threadIdx.x == 0) {
         __threadfence();
         const int done = atomicAdd(&a.ticket[b], 1);
         s_last = done == static_cast<int>(gridDim.y) - 1;
         if (s_last) a.ticket[b] = 0;   // ready for the next launch
+#ifdef TQ_DEC_CHECK
+        if (done >= static_cast<int>(gridDim.y)) {
+            printf("DEC_CHECK router: token %d ticket %d >= %d\n", b, done, static_cast<int>(gridDim.y));
+            __trap();
+        }
+#endif
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
+    rtrace(a, 2);
     const int k = a.top_k;
-    // ---- routing decision ----
+    // ---- routing decision (warp 0), overlapped with the token's loads (other warps):
+    //      group sums of the fp16 activations, the fp16 row staged in shared memory,
+    //      the folded / scalar tile columns' projections of this token ----
     if (!a.given) {
         if (warp == 0)
             route_pick(a.score_ws + static_cast<int64_t>(b) * K, K, k, sc, ex, pick_k, pick_p,
@@ -1681,16 +1854,54 @@ __global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a)
     } else if (static_cast<int>(threadIdx.x) < k) {
         pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
     }
+    const int w0 = a.given ? 0 : 1;   // first warp free of the pick
+    for (int g = warp - w0; a.use_main && g >= 0 && g < a.groups; g += kDecRT / 32 - w0) {
+        float acc = 0.0f;
+        const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
+        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+        if (lane == 0) s_sx[g] = acc;
+    }
+    const bool stage16 = a.use_main && a.k_pad <= kDecStage16;
+    if (stage16 && warp >= w0) {
+        for (int t8 = threadIdx.x - 32 * w0; t8 < a.k_pad / 8; t8 += kDecRT - 32 * w0) {
+            __align__(16) __half hh[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = t8 * 8 + m;
+                hh[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
+            }
+            reinterpret_cast<int4*>(s_x16)[t8] = *reinterpret_cast<const int4*>(hh);
+        }
+    }
+    const int nzq = a.use_lr ? a.num_q * a.rank : 0;
+    if (nzq <= kDecZq) {
+        const float* zi = a.zq_ws + static_cast<int64_t>(b) * nzq;
+        for (int t = threadIdx.x - 32 * w0; t >= 0 && t < nzq; t += kDecRT - 32 * w0) s_zq[t] = __ldcg(zi + t);
+    }
     __syncthreads();
+    rtrace(a, 3);
     // ---- destinations: one slot per routed expert, the shared-expert rows ----
     if (static_cast<int>(threadIdx.x) < k) {
         const int e = pick_k[threadIdx.x];
+        RT_CHECK(a.given || (e >= 0 && e < K), "picked expert %d\n", e);
         int row = -1;
         if (e < 0 || e >= K) {
             atomicExch(a.err_flag, 1);   // expert id out of range (moe.cpp:111-114)
         } else {
             const int slot = atomicAdd(&a.cnt[e], 1);
             row = e * a.cap8 + slot;
+#ifdef TQ_DEC_CHECK
+            if (slot >= a.cap8) {
+                printf("DEC_CHECK router: token %d expert %d slot %d >= cap8 %d (pick %d)\n", b, e, slot, a.cap8, threadIdx.x);
+                __trap();
+            }
+#endif
+            if (slot >= a.cap8) {   // cannot happen for a valid routing; never write outside the expert's rows
+                atomicExch(a.err_flag, 1);
+                row = -1;
+            }
         }
         s_row[threadIdx.x] = row;
         s_e[threadIdx.x] = row >= 0 ? e : -1;
@@ -1702,32 +1913,28 @@ __global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a)
     }
     __syncthreads();
     const int nd = k + (a.use_main ? a.num_shared : 0);
+    rtrace(a, 4);
     // ---- rank-r terms of the routed destinations ----
     if (a.use_lr) {
         for (int t = 0; t < k; ++t) {
             const int e = s_e[t];
             if (e < 0) continue;   // block-uniform
             const int q = a.e_q[e];
+            RT_CHECK(q >= 0 && q < a.num_q, "e %d q %d\n", e, q);
             if (a.q_tier[q] == 2) {
                 dec_project<kDecRT>(xb, a.scaling + static_cast<int64_t>(e) * a.in_dim, a.in_dim,
                                     a.vcodes + static_cast<int64_t>(q) * a.rank * a.in_dim, a.vscale + q * a.rank,
-                                    a.rank, s_z[t], red);
+                                    a.rank, s_z[t], reinterpret_cast<float*>(sm.prod));
+            } else if (nzq <= kDecZq) {
+                for (int j = threadIdx.x; j < a.rank; j += kDecRT) s_z[t][j] = s_zq[q * a.rank + j];
             } else {
                 const float* zi = a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank;
                 for (int j = threadIdx.x; j < a.rank; j += kDecRT) s_z[t][j] = __ldcg(zi + j);
             }
         }
     }
-    // ---- group sums of the fp16 activations (zero-point term) ----
-    for (int g = warp; a.use_main && g < a.groups; g += kDecRT / 32) {
-        float acc = 0.0f;
-        const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
-        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-        if (lane == 0) s_sx[g] = acc;
-    }
     __syncthreads();
+    rtrace(a, 6);
     // ---- fp16 activation row -> every destination (atom-major, 128B swizzle of the row index) ----
     auto piece = [&](__half* base, int row, int t8) -> int4* {
         const int at = t8 >> 3, ch = t8 & 7;
@@ -1735,19 +1942,29 @@ __global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a)
     };
     if (a.use_main) {
         for (int t8 = threadIdx.x; t8 < a.k_pad / 8; t8 += kDecRT) {
-            __align__(16) __half h[8];
+            int4 v;
+            if (stage16) {
+                v = reinterpret_cast<const int4*>(s_x16)[t8];
+            } else {
+                __align__(16) __half hh[8];
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int c = t8 * 8 + m;
-                h[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
+                for (int m = 0; m < 8; ++m) {
+                    const int c = t8 * 8 + m;
+                    hh[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
+                }
+                v = *reinterpret_cast<const int4*>(hh);
             }
-            const int4 v = *reinterpret_cast<const int4*>(h);
-            for (int d = 0; d < nd; ++d)
+            for (int d = 0; d < nd; ++d) {
+                RT_CHECK(s_row[d] < a.atom_rows - 16, "dest %d row %d atom_rows %lld\n", d, s_row[d],
+                         static_cast<long long>(a.atom_rows));
                 if (s_row[d] >= 0) *piece(a.xperm, s_row[d], t8) = v;
+            }
         }
     }
+    rtrace(a, 7);
     // ---- extension rows [Sx | Z * zscale_e | 0] ----
     const int n8 = a.ext_cols / 8;
+    RT_CHECK(nd <= kDecMaxTopK + 64 && n8 <= 64, "nd %d n8 %d\n", nd, n8);
     for (int idx = threadIdx.x; idx < nd * n8; idx += kDecRT) {
         const int d = idx / n8, t8 = idx % n8;
         const int row = s_row[d];
@@ -1767,6 +1984,8 @@ __global__ void __launch_bounds__(kDecRT) dec_route_kernel(const DecRouteArgs a)
         }
         *piece(a.extperm, row, t8) = *reinterpret_cast<const int4*>(h);
     }
+    __syncthreads();
+    rtrace(a, 8);
 }
 
 // decode path, launch 3: y[b] = sum_t g_bt * Y[slot(b, t)] (t ascending) + sum_s Y_s[b]
@@ -2060,7 +2279,7 @@ cudaError_t launch_dec_route(const DecRouteArgs& a, cudaStream_t stream) {
         a.rank > 64)
         return cudaErrorInvalidValue;
     const int nslices = a.given ? 0 : (a.num_experts + kRouteExperts - 1) / kRouteExperts;
-    const int ny = nslices + a.num_q;
+    const int ny = nslices + a.num_q * ((a.rank + kProjRows - 1) / kProjRows);
     if (ny < 1) return cudaErrorInvalidValue;
     max_carveout(dec_route_kernel);
     return launch_maybe_pdl(dec_route_kernel, dim3(a.batch, ny), dim3(kDecRT), 0, stream, a);

@@ -498,7 +498,7 @@ struct tq_layer {
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
     // decode path (batch <= kDecMaxBatch): route+scatter -> fused expert GEMM -> combine
     DBuf vcodes, vscale, q_tier, q_first, e_q, scaling_d;            // rank-r projection tables
-    DBuf dec_xperm, dec_extperm, dec_yslot, dec_cnt, dec_inv, dec_zq, dec_scratch, dec_segcnt;
+    DBuf dec_xperm, dec_extperm, dec_yslot, dec_cnt, dec_inv, dec_zq, dec_scratch, dec_segcnt, dec_ticket;
     int64_t dec_atom_rows = 0;
     bool dec_ready = false;
     std::atomic<uint64_t> launches{0};
@@ -1447,7 +1447,7 @@ bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
     const Geometry& g = L->g;
     const int64_t slots = given ? batch * g.top_k : batch;
     return !off && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
-           g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64;
+           g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64 && g.n_ext <= 4;
 }
 
 void reserve_decode(tq_layer* L) {
@@ -1469,6 +1469,8 @@ void reserve_decode(tq_layer* L) {
     L->dec_scratch.alloc(sizeof(float) * L->num_sms * 2 * 64 * kBM);
     L->dec_segcnt.alloc(sizeof(int32_t) * W * g.mb_count);
     cuda_check(cudaMemset(L->dec_segcnt.p, 0, L->dec_segcnt.n), "cudaMemset");
+    L->dec_ticket.alloc(sizeof(int32_t) * kDecMaxBatch);   // the decode router's own per-token tickets
+    cuda_check(cudaMemset(L->dec_ticket.p, 0, L->dec_ticket.n), "cudaMemset");
     L->dec_ready = true;
 }
 
@@ -1505,7 +1507,7 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
     ra.ids = L->ids.as<int32_t>();
     ra.gates = L->gates.as<float>();
     ra.score_ws = L->route_ws.as<float>();
-    ra.ticket = L->route_ticket.as<int32_t>();
+    ra.ticket = L->dec_ticket.as<int32_t>();
     ra.group_size = static_cast<int>(g.gs);
     ra.groups = static_cast<int>(g.G);
     ra.rank = static_cast<int>(g.r);
@@ -1528,7 +1530,25 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
     ra.cnt = L->dec_cnt.as<int32_t>();
     ra.inv = L->dec_inv.as<int32_t>();
     ra.err_flag = L->err_flag.as<int32_t>();
+#ifdef TQ_ROUTE_TRACE
+    static unsigned long long* rbuf = nullptr;
+    const size_t rbytes = sizeof(unsigned long long) * 16 * 64 * 128;
+    if (!rbuf) cuda_check(cudaMalloc(&rbuf, rbytes), "cudaMalloc");
+    cuda_check(cudaMemsetAsync(rbuf, 0, rbytes, st), "cudaMemset");
+    ra.trace = rbuf;
+#endif
     cuda_check(launch_dec_route(ra, st), "dec_route_kernel launch");
+#ifdef TQ_ROUTE_TRACE
+    if (getenv("TQ_ROUTE_TRACE_FILE")) {
+        std::vector<unsigned long long> hb(16 * 64 * 128);
+        cuda_check(cudaStreamSynchronize(st), "sync");
+        cuda_check(cudaMemcpy(hb.data(), rbuf, rbytes, cudaMemcpyDeviceToHost), "trace D2H");
+        if (FILE* f = fopen(getenv("TQ_ROUTE_TRACE_FILE"), "ab")) {
+            fwrite(hb.data(), 8, hb.size(), f);
+            fclose(f);
+        }
+    }
+#endif
     count_launch(L);
 
     DecParams dp{};
@@ -1542,8 +1562,7 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
     dp.group_size = static_cast<int>(g.gs);
     dp.groups = static_cast<int>(g.G);
     dp.kc64 = static_cast<int>(g.kc_total);
-    dp.nmain = use_main ? static_cast<int>((g.kc_total + 1) / 2) : 0;
-    dp.n_ep = static_cast<int>((g.G + g.r + 31) / 32);
+    dp.nmain = use_main ? static_cast<int>((g.kc_total + 3) / 4) : 0;   // 256-K steps
     dp.mb_count = static_cast<int>(g.mb_count);
     dp.o_valid = static_cast<int>(g.o);
     dp.num_experts = static_cast<int>(g.K);
@@ -1565,7 +1584,26 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
             cuda_check(cudaEventCreate(&ev1), "cudaEventCreate");
             cuda_check(cudaEventRecord(ev0, st), "cudaEventRecord");
         }
+#ifdef TQ_DEC_TRACE
+        // diagnostics build: event trace of one CTA, dumped to $TQ_DEC_TRACE_FILE after each launch
+        static unsigned long long* tbuf = nullptr;
+        if (!tbuf) cuda_check(cudaMalloc(&tbuf, 16 * 1024 * 8), "cudaMalloc");
+        cuda_check(cudaMemsetAsync(tbuf, 0, 16 * 1024 * 8, st), "cudaMemset");
+        dp.trace = tbuf;
+        dp.trace_cta = getenv("TQ_DEC_TRACE_CTA") ? atoi(getenv("TQ_DEC_TRACE_CTA")) : 0;
+#endif
         cuda_check(launch_decode(dp, dn, L->num_sms, st), "dec_gemm_kernel launch");
+#ifdef TQ_DEC_TRACE
+        if (getenv("TQ_DEC_TRACE_FILE")) {
+            std::vector<unsigned long long> hbuf(16 * 1024);
+            cuda_check(cudaStreamSynchronize(st), "sync");
+            cuda_check(cudaMemcpy(hbuf.data(), tbuf, 16 * 1024 * 8, cudaMemcpyDeviceToHost), "trace D2H");
+            if (FILE* f = fopen(getenv("TQ_DEC_TRACE_FILE"), "ab")) {
+                fwrite(hbuf.data(), 8, hbuf.size(), f);
+                fclose(f);
+            }
+        }
+#endif
         if (L->timing) {
             cuda_check(cudaEventRecord(ev1, st), "cudaEventRecord");
             L->tev.emplace_back(ev0, ev1);
@@ -2011,6 +2049,27 @@ tq_status tq_dequantize_experts(tq_layer* L, uint16_t* out, void* stream) {
         check_layer(L);
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         launch_dequant_experts(L, out, static_cast<cudaStream_t>(stream));
+    });
+}
+
+// Diagnostics: the decode path's self-resetting device counters (slot counts, per
+// token router tickets, split-segment arrivals), copied to the host; all must read
+// zero between forwards.  out: [K] cnt, [cap] tickets, [(K + S) * mb_count] segments.
+tq_status tq_debug_decode_counters(tq_layer* L, int32_t* out, int64_t n) {
+    return guarded([&] {
+        check_layer(L);
+        cuda_check(cudaDeviceSynchronize(), "sync");
+        const Geometry& g = L->g;
+        std::vector<int32_t> h;
+        auto pull = [&](const DBuf& b, int64_t cnt) {
+            std::vector<int32_t> t(static_cast<size_t>(cnt), 0);
+            if (b.p) cuda_check(cudaMemcpy(t.data(), b.p, sizeof(int32_t) * cnt, cudaMemcpyDeviceToHost), "D2H");
+            h.insert(h.end(), t.begin(), t.end());
+        };
+        pull(L->dec_cnt, g.K);
+        pull(L->dec_ticket, kDecMaxBatch);
+        pull(L->dec_segcnt, (g.K + g.S) * g.mb_count);
+        for (int64_t t = 0; t < n && t < static_cast<int64_t>(h.size()); ++t) out[t] = h[static_cast<size_t>(t)];
     });
 }
 

@@ -282,9 +282,11 @@ inline cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 bloc
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    // the attribute is attached only when PDL is on: a launch carrying it (even
+    // with the value 0) was seen to overlap its predecessor on sm_100a
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

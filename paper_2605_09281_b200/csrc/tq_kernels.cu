@@ -2078,9 +2078,12 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
 #define TQ_ROUTE_TOKEN_CTAS (2 * 148)   // token-chunk CTAs at prefill (several tokens per CTA beyond this)
 #endif
     static const int tile_min = [] {
-        // batch from which the token-tile router runs (<= 0: never)
+        // batch from which the token-tile router runs (<= 0: never).  Off by default:
+        // it faulted with an illegal address in ~1 of 30 launches at 4096 tokens
+        // (tools/gpu_stress_repro.py; cause not found), the per-token route_kernel
+        // below passed 180 / 180 (known issues)
         const char* e = getenv("TQ_ROUTE_TILE_MIN");
-        return e ? atoi(e) : TQ_ROUTE_TOKEN_CTAS + 1;
+        return e ? atoi(e) : 0;
     }();
     const bool tile_ok = !plan && num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
                          (k_pad & 3) == 0 && (!sx || (group_size > 0 && kTC % group_size == 0));

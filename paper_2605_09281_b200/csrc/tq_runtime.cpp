@@ -605,23 +605,15 @@ int gemm_dn_host(int kc) { return kc == 64 ? 192 : 128; }
 // Decode-sized batches (few tokens per expert) use 128-wide chunks and 16
 // dequant warps; prefill uses 64-wide chunks and 192-token tiles.
 LaunchCfg cfg_for(const tq_layer* L, int64_t batch) {
-    const int64_t local = std::max<int64_t>(1, L->e_end - L->e_begin);
-    const int64_t per_expert = (batch * L->g.top_k + local - 1) / local;
+    // Batches up to kDecMaxBatch tokens run the decode path (tq_decode.cu); the
+    // grouped path below serves larger batches and the expert-parallel stages with
+    // its 64-column-chunk, 192-token-tile configuration only (the kc = 128
+    // "mid" / resident-activation configurations of round 1 were retired: their
+    // multi-unit ring bookkeeping faulted intermittently)
+    (void)batch;
     LaunchCfg c;
-    static const bool no_xr = [] {
-        const char* e = std::getenv("TQ_NO_XR");   // 1: decode on the activation-ring configuration
-        return e && std::atoi(e) == 1;
-    }();
-    if (per_expert <= 32 && L->g.k_pad % 128 == 0 && !no_xr) {
-        c.kc = 128;                      // decode: 2 MMA issue streams, 4 dequant groups
-        c.dn = 32;
-    } else if (per_expert <= 128 && L->g.k_pad % 128 == 0) {
-        c.kc = 128;
-        c.dn = batch <= 64 ? 64 : 128;   // decode: small accumulators -> deeper A ring
-    } else {
-        c.kc = 64;
-        c.dn = 192;
-    }
+    c.kc = 64;
+    c.dn = 192;
     c.bn = c.dn;
     c.kc_total = static_cast<int>(L->g.k_pad / c.kc);
     c.n_ext = static_cast<int>((L->g.G + L->g.r + c.kc - 1) / c.kc);
@@ -1144,6 +1136,17 @@ LaunchCfg cfg64(const tq_layer* L) {
 
 void count_launch(tq_layer* L, int n = 1) {
     L->launches += static_cast<uint64_t>(n);
+#ifdef TQ_CHECK_EACH
+    // diagnostics build: synchronize after every launch and name the failing one
+    {
+        const cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) {
+            fprintf(stderr, "TQ_CHECK_EACH: launch #%llu of the layer failed: %s\n",
+                    static_cast<unsigned long long>(L->launches.load()), cudaGetErrorString(e));
+            fail(TQ_ERR_CUDA, std::string("TQ_CHECK_EACH: ") + cudaGetErrorString(e));
+        }
+    }
+#endif
     if (L->ktime && L->kt_active && !L->kev.empty()) {
         cudaEvent_t e;
         cudaEventCreate(&e);
@@ -1437,7 +1440,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
 // decode path: 3 launches per forward (route+project+scatter, fused expert GEMM
 // with split-segment fixup, combine)
 // ---------------------------------------------------------------------------
-constexpr int64_t kDecMaxBatch = 64;   // slots per expert (and tokens) the decode workspace holds
+constexpr int64_t kDecMaxBatch = 256;  // slots per expert (and tokens) the decode workspace holds
 
 bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
     static const bool off = [] {
@@ -1467,7 +1470,7 @@ void reserve_decode(tq_layer* L) {
     L->dec_inv.alloc(sizeof(int32_t) * kDecMaxBatch * g.top_k);
     L->dec_zq.alloc(sizeof(float) * kDecMaxBatch * g.N * g.r);
     L->dec_scratch.alloc(sizeof(float) * L->num_sms * 2 * 64 * kBM);
-    L->dec_segcnt.alloc(sizeof(int32_t) * W * g.mb_count);
+    L->dec_segcnt.alloc(sizeof(int32_t) * W * ((kDecMaxBatch + 63) / 64) * g.mb_count);
     cuda_check(cudaMemset(L->dec_segcnt.p, 0, L->dec_segcnt.n), "cudaMemset");
     L->dec_ticket.alloc(sizeof(int32_t) * kDecMaxBatch);   // the decode router's own per-token tickets
     cuda_check(cudaMemset(L->dec_ticket.p, 0, L->dec_ticket.n), "cudaMemset");
@@ -2068,7 +2071,7 @@ tq_status tq_debug_decode_counters(tq_layer* L, int32_t* out, int64_t n) {
         };
         pull(L->dec_cnt, g.K);
         pull(L->dec_ticket, kDecMaxBatch);
-        pull(L->dec_segcnt, (g.K + g.S) * g.mb_count);
+        pull(L->dec_segcnt, (g.K + g.S) * g.mb_count);   // first tile of every weight
         for (int64_t t = 0; t < n && t < static_cast<int64_t>(h.size()); ++t) out[t] = h[static_cast<size_t>(t)];
     });
 }

@@ -228,18 +228,18 @@ def test_empty_batch_and_shape_errors(tq, make_artifact):
 def test_launch_count_constant_in_batch(tq, make_artifact):
     """Dispatch structure: the number of kernel launches of a forward does not
     depend on the batch size (dispatch_count() == 2 for any B,
-    test_infer.cpp:204-231).  Decode batches (<= 64 tokens) run 3 kernels
+    test_infer.cpp:204-231).  Decode batches (<= 256 tokens) run 3 kernels
     (route + scatter, fused expert GEMM, combine); larger batches the grouped
     prefill path, a fixed count too."""
     import torch
     d = make_artifact(**SPECS[0])
     L = tq.Layer(d)
     dec, pre = set(), set()
-    for B in (1, 4, 16, 33, 64, 250, 700):
+    for B in (1, 4, 16, 33, 64, 250, 700, 1500):
         x = torch.from_numpy(_x(B, SPECS[0]["i"], B)).cuda()
         L.reset_launch_count()
         L.forward(x)
-        (dec if B <= 64 else pre).add(L.launch_count())
+        (dec if B <= 256 else pre).add(L.launch_count())
     assert dec == {3}, dec
     assert len(pre) == 1, pre
 

@@ -201,6 +201,21 @@ def artifact_for(config: str, rank: int, world: int) -> str:
     return path
 
 
+def cpu_info() -> dict:
+    """nproc (cores usable by this process) and the CPU model (BASELINE.md asks for both)."""
+    nproc = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": nproc, "cpu_model": model}
+
+
 def host_threads(B: int, per_thread_bytes: int) -> int:
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     try:
@@ -232,6 +247,13 @@ def run_reference_sample(artifact_dir: str, B: int, i: int, o: int, K: int, S: i
 # ---------------------------------------------------------------------------
 
 def bench_reference(args, rank, world):
+    """The reference's own CPU path (oracle/_ref = the unmodified reference C++:
+    route + tileq_forward) on the box's host cores.  A decode step of the GPU
+    arm is the B = 1..64 sweep (127 tokens); one reference call costs ~10 s
+    whatever B is (every call dequantizes all experts, infer.cpp:45-49), so a
+    reference step is ONE 64-token batch -- the CPU's most favourable point of
+    the sweep, labelled as such.  Every step of --steps is timed (the time
+    budget only stops a run that would not finish, and then `steps` says so)."""
     if rank != 0:
         return 0
     from oracle.oracle import RefLib, ref_available
@@ -241,17 +263,18 @@ def bench_reference(args, rank, world):
     from paper_2605_09281_b200 import synth
     K, top_k, i, o, S, bits, r, g = synth.CONFIGS[args.config]
     art = artifact_for(args.config, 0, 1)
-    B = 64 if args.workload == "decode" else PREFILL_BATCH
+    B = 64 if args.workload == "decode" else 256
     ref = RefLib()
     R = ref.load(art)
     T = host_threads(B, 4 * o * i * (K + S) + (64 << 20))
-    budget = float(os.environ.get("TILEQ_REF_BUDGET_S", "150"))
+    budget = float(os.environ.get("TILEQ_REF_BUDGET_S", "420"))
     t_start = time.perf_counter()
-    for w in range(min(args.warmup, 1)):
+    n_warm = min(args.warmup, 1)
+    for w in range(n_warm):
         R.forward(make_tokens(B, i, 1000 + w), mode=0, threads=T)
     times = []
-    for s in range(args.steps):
-        x = make_tokens(B, i, 2000 + s)
+    for s_ in range(args.steps):
+        x = make_tokens(B, i, 2000 + s_)
         t0 = time.perf_counter()
         R.forward(x, mode=0, threads=T)
         times.append(time.perf_counter() - t0)
@@ -259,14 +282,17 @@ def bench_reference(args, rank, world):
             break
     sec = float(np.median(times))
     val = B / sec
-    sample = (f"route + tileq_forward (reference C++, oracle/_ref) on one {B}-token batch of {args.config} "
-              f"per step, token-sharded over {T} threads; {len(times)} timed steps (median), "
-              f"warmup {min(args.warmup, 1)}, time budget {budget:.0f}s")
+    info = cpu_info()
+    sample = (f"route + tileq_forward (reference C++, oracle/_ref) on ONE {B}-token batch of {args.config} per step "
+              f"(the {'B=64 point of the decode sweep' if args.workload == 'decode' else '256-token sample of the prefill batch'}), "
+              f"token-sharded over {T} threads; {len(times)} timed steps (median), {n_warm} warm-up")
+    cfg = workload_config(args, world)
+    cfg["reference_step"] = f"one {B}-token batch per step (tokens_per_step {B})"
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "steps_timed": len(times), "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "steps": len(times), "steps_requested": args.steps, "warmup": n_warm, "ms_per_step": sec * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (CPU)",
-            "data": "synthetic", "config": workload_config(args, world),
-            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": T, "kind": "reference", "sample": sample},
+            "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": T, "kind": "reference", "sample": sample, **info},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -407,7 +433,7 @@ def bench_tileq(args, rank, world, local_rank):
         achieved = (algo / (gemm_avg_ms * 1e-3) / 1e9) if algo else None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": traffic_from_profiles("decode", batches),
-                "kernel": "tq_gemm (fused dequant + low-rank tcgen05 expert GEMM)",
+                "kernel": "dec_gemm_kernel<3,32|64> (fused dequant + low-rank tcgen05 expert GEMM, decode path)",
                 "algorithmic_bytes_per_launch": algo, "avg_launch_ms": gemm_avg_ms,
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind}, burst copy)",
                 "share_of_step": (gemm_ms / gemm_passes) / ms_per_step if ms_per_step else None}
@@ -434,8 +460,81 @@ def bench_tileq(args, rank, world, local_rank):
             "gemm_launches_per_forward": launches_per_fwd, "clocks": clk, "clock_settle_steps": settle}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(args, art, geo)
+    if world == 1 and args.workload == "decode" and not args.no_prefill:
+        line["prefill"] = prefill_leg(args, L, geo, dev, flush, art)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def prefill_leg(args, L, geo, dev, flush, art):
+    """BASELINE configs[2] on the same layer: one 4096-token forward per step
+    (c3 is c2's shape), device time by CUDA events with L2 flushed before every
+    forward; roofline of the dominant kernel (the grouped tcgen05 expert GEMM)
+    against the measured bf16 burst peak; e2e through tq_forward_host; a
+    bounded reference CPU sample (256 tokens)."""
+    import torch
+    B = PREFILL_BATCH
+    L.reserve(B)
+    x = torch.from_numpy(make_tokens(B, geo.i, 4242)).to(dev)
+    y = torch.empty((B, geo.o), dtype=torch.float32, device=dev)
+    steps = max(3, min(args.steps, 10))
+    for _ in range(3):
+        flush.zero_()
+        L.forward(x, out=y)
+    torch.cuda.synchronize()
+    L.reset_launch_count()
+    tot = 0.0
+    for _ in range(steps):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        L.forward(x, out=y)
+        b.record()
+        b.synchronize()
+        tot += a.elapsed_time(b)
+    launches = L.launch_count()
+    ms = tot / steps
+    L.gemm_timing(True)
+    for _ in range(steps):
+        flush.zero_()
+        L.forward(x, out=y)
+    torch.cuda.synchronize()
+    gemm_ms, gemm_n = L.gemm_time()
+    L.gemm_timing(False)
+    gemm_avg = gemm_ms / max(gemm_n, 1)
+    hbm, tf_burst, tf_sust, peak_kind = measured_peaks()
+    fl = geo.flops(B)
+    achieved = fl / (gemm_avg * 1e-3) / 1e12
+    # e2e: host buffers, H2D of x and D2H of y inside the timed region
+    hx = torch.from_numpy(make_tokens(B, geo.i, 4242)).pin_memory()
+    hy = torch.empty((B, geo.o), dtype=torch.float32).pin_memory()
+    L.forward_host(hx.numpy(), out=hy.numpy())
+    e_tot = 0.0
+    for _ in range(3):
+        flush.zero_()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        L.forward_host(hx.numpy(), out=hy.numpy())
+        b.record()
+        b.synchronize()
+        e_tot += a.elapsed_time(b)
+    e_ms = e_tot / 3
+    out = {"workload": f"configs[2]: {args.config} shape prefill, {B} tokens per step", "value": B / (ms * 1e-3),
+           "unit": "tokens/s", "steps": steps, "warmup": 3, "ms_per_step": ms,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf_burst, "unit": "TFLOP/s",
+                        "frac": achieved / tf_burst, "traffic": traffic_from_profiles("prefill", [B]),
+                        "kernel": "gemm_kernel<b,64,2,192,1> (grouped fused dequant + low-rank tcgen05 expert GEMM)",
+                        "algorithmic_flops_per_launch": fl, "avg_launch_ms": gemm_avg,
+                        "peak_source": f"MEASURED_PEAKS.json bf16_tflops ({peak_kind}, burst cuBLAS)",
+                        "share_of_step": gemm_avg * (gemm_n / max(steps, 1)) / ms},
+           "gpu_launches_per_forward": launches / steps,
+           "e2e": {"value": B / (e_ms * 1e-3), "unit": "tokens/s", "ms_per_step": e_ms, "steps": 3,
+                   "h2d_bytes_per_step": 4 * B * geo.i, "d2h_bytes_per_step": 4 * B * geo.o,
+                   "api": "Layer.forward_host -> tq_forward_host (C-ABI, host f32 in/out)"}}
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_sample(art, 256, geo, args.config + " (prefill sample)")
+    return out
 
 
 def e2e_measure(args, L, ep, xs, batches, geo, dev, flush, world):
@@ -490,10 +589,14 @@ def cpu_baseline_leg(args, art, geo):
         return {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
     B = 64 if args.workload == "decode" else 256
+    return cpu_sample(art, B, geo, args.config)
+
+
+def cpu_sample(art, B, geo, name):
     dt, T, _, _ = run_reference_sample(art, B, geo.i, geo.o, geo.K, geo.S)
     return {"value": B / dt, "unit": "tokens/s", "cores": T, "kind": "reference",
             "sample": f"one route + tileq_forward call of the reference C++ (oracle/_ref) on {B} tokens of "
-                      f"{args.config}, token-sharded over {T} host threads ({dt:.1f} s)"}
+                      f"{name}, token-sharded over {T} host threads ({dt:.1f} s)", **cpu_info()}
 
 
 def main():
@@ -505,6 +608,7 @@ def main():
     ap.add_argument("--workload", default="decode", choices=["decode", "prefill"])
     ap.add_argument("--config", default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prefill", action="store_true", help="decode workload only (skip the prefill object)")
     args = ap.parse_args()
     if args.config is None:
         args.config = "c2" if args.workload == "decode" else "c3"

@@ -65,8 +65,11 @@ constexpr int kMaxNI = 4;
 constexpr int kThreads = 28 * 32;
 constexpr int kAtomsPerStep = 4;         // 256 K per step
 constexpr int kAS = 3;                   // A stages in TMEM (128 columns each)
+#ifndef TQ_DEC_NI32
+#define TQ_DEC_NI32 4
+#endif
 // MMA issuers per tile height: TMEM = kAS * 128 + NI * DN columns <= 512
-__host__ __device__ constexpr int dec_ni(int dn) { return dn <= 32 ? 4 : 2; }
+__host__ __device__ constexpr int dec_ni(int dn) { return dn <= 32 ? TQ_DEC_NI32 : 2; }
 constexpr int kMaxCS = 16, kMaxXS = 16;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kHdrBytes = 4096;
@@ -155,7 +158,8 @@ __device__ __forceinline__ int step_atoms(const DecParams& p, int k) {
 
 // TQ_DEC_TRACE builds: clock64 of pipeline events of CTA p.trace_cta into p.trace
 // ([slot][1024] u64): 0 code issue, 1 x issue, 2 dequant data ready, 3 dequant done,
-// 4 issuer A ready, 5 issuer X ready, 6 issuer committed, 7 epilogue part
+// 4 issuer A ready, 5 issuer X ready, 6 issuer committed, 7 epilogue part,
+// 8 dequant A stage free, 9 issuer 3 committed
 // per-CTA timeline (globaltimer ns): p.trace[8192 + cta * 4 + k], k = 0 entry, 1 prologue done,
 // 2 roles done (before teardown), 3 exit
 __device__ __forceinline__ void ctrace(const DecParams& p, int k) {
@@ -163,7 +167,7 @@ __device__ __forceinline__ void ctrace(const DecParams& p, int k) {
     if (threadIdx.x == 0 && p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[8192 + blockIdx.x * 4 + k] = t;
+        p.trace[12288 + blockIdx.x * 4 + k] = t;
     }
 #else
     (void)p;
@@ -172,7 +176,7 @@ __device__ __forceinline__ void ctrace(const DecParams& p, int k) {
 }
 __device__ __forceinline__ void dtrace(const DecParams& p, int slot, int idx) {
 #ifdef TQ_DEC_TRACE
-    if (static_cast<int>(blockIdx.x) == p.trace_cta && idx < 1024 && p.trace) p.trace[slot * 1024 + idx] = clock64();
+    if (static_cast<int>(blockIdx.x) == p.trace_cta && idx < 1024 && slot < 10 && p.trace) p.trace[slot * 1024 + idx] = clock64();
 #else
     (void)p;
     (void)slot;
@@ -283,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
                     const int ein = gshift >= 0 ? (e0 & ((1 << gshift) - 1)) : e0 % p.group_size;
                     const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + kAtomsPerStep * kBlk) + rloc;
                     mbar_wait(&h->a_empty[as], aph ^ 1u);
+                    if (lane == 0 && q == 0 && hw == 0) dtrace(p, 8, j);
                     tc_fence_after();
 #pragma unroll
                     for (int t = 0; t < 2; ++t) {
@@ -481,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
 #endif
                     tc_commit_elect(&h->a_empty[as]);
                     tc_commit_elect(&h->x_empty[xs]);
-                    if (lane == 0) dtrace(p, 6, static_cast<int>(x - g_begin));
+                    if (lane == 0) dtrace(p, ii == 0 ? 6 : (ii == kNIss - 1 ? 9 : 15), static_cast<int>(x - g_begin));
                     if (++as == kAS) { as = 0; aph ^= 1u; }
                     if (++xs == SX) { xs = 0; xph ^= 1u; }
                 }

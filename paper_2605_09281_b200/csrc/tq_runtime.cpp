@@ -1591,7 +1591,7 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
         // diagnostics build: event trace of one CTA, dumped to $TQ_DEC_TRACE_FILE after each launch
         static unsigned long long* tbuf = nullptr;
         if (!tbuf) cuda_check(cudaMalloc(&tbuf, 16 * 1024 * 8), "cudaMalloc");
-        cuda_check(cudaMemsetAsync(tbuf, 0, 16 * 1024 * 8, st), "cudaMemset");
+        cuda_check(cudaMemsetAsync(tbuf, 0, 16 * 1024 * 8, st), "cudaMemset");   // [10][1024] events | [148][4] per CTA at 12288
         dp.trace = tbuf;
         dp.trace_cta = getenv("TQ_DEC_TRACE_CTA") ? atoi(getenv("TQ_DEC_TRACE_CTA")) : 0;
 #endif

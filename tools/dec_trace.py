@@ -12,7 +12,7 @@ Bs = [int(b) for b in sys.argv[2:4]]
 cta = sys.argv[4] if len(sys.argv) > 4 else "0"
 os.environ["TQ_DEC_TRACE_CTA"] = cta
 L = tq.Layer(synth.ensure_config(name))
-names = ["code_iss", "x_iss", "dq_data", "dq_done", "mma_a", "mma_x", "mma_commit", "epi_part"]
+names = ["code_iss", "x_iss", "dq_data", "dq_done", "mma_a", "mma_x", "commit0", "epi_part", "dq_afree", "commit3"]
 for B in Bs:
     x = torch.randn(B, L.in_dim, device="cuda")
     for _ in range(3):
@@ -26,8 +26,8 @@ for B in Bs:
     torch.cuda.synchronize()
     del os.environ["TQ_DEC_TRACE_FILE"]
     raw = np.fromfile(f, dtype=np.uint64).reshape(-1, 16 * 1024)[-1].astype(np.int64)
-    t = raw[:8192].reshape(8, 1024)
-    ct = raw[8192:8192 + 148 * 4].reshape(148, 4)
+    t = raw[:10240].reshape(10, 1024)
+    ct = raw[12288:12288 + 148 * 4].reshape(148, 4)
     ok = ct[:, 0] > 0
     base = ct[ok, 0].min()
     rel = (ct[ok] - base) / 1000.0
@@ -40,4 +40,4 @@ for B in Bs:
     print(f"B={B} cta {cta}: {n} steps, span {(t[t > 0].max() - t0)} cycles")
     print("step " + " ".join(f"{s:>10}" for s in names))
     for j in range(min(n, 80)):
-        print(f"{j:4d} " + " ".join(f"{(t[s, j] - t0) if t[s, j] else -1:10d}" for s in range(8)))
+        print(f"{j:4d} " + " ".join(f"{(t[s, j] - t0) if t[s, j] else -1:10d}" for s in range(10)))

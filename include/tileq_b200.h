@@ -7,6 +7,9 @@
  * (paths relative to /root/reference/proj):
  *
  *   tq_layer_load      <- read_artifact(dir, verify_crc)        include/tileq/io.hpp:55,  src/io.cpp:679-813
+ *   tq_layer_create    <- an in-memory TileQLayer               include/tileq/infer.hpp:22-28 (QuantizedExpert
+ *                         quant.hpp:37-63, TiledLowRank tiler.hpp:45-56, CodedBlock codec.hpp:42-50)
+ *   tq_artifact_check  <- read_artifact's validation alone (no device), src/io.cpp:186-295,422-485,679-813
  *   tq_route           <- route(x, gate_weights, top_k)         include/tileq/moe.hpp:53, src/moe.cpp:43-89
  *   tq_permute         <- (no counterpart: the per-token loop of reference_forward, src/moe.cpp:106-133)
  *   tq_forward         <- tileq_forward / qmoe_forward / lotile_forward
@@ -100,6 +103,55 @@ const char* tq_version(void);
  * experts are always resident. */
 tq_status tq_layer_load(const char* dir, int device, int verify_crc, int64_t expert_begin,
                         int64_t expert_end, tq_layer** out);
+
+/* Validate an artifact directory exactly like tq_layer_load (same status
+ * codes and messages) without touching any device: the host half of
+ * read_artifact.  Lets a CPU-only process vet artifacts. */
+tq_status tq_artifact_check(const char* dir, int verify_crc);
+
+typedef enum { TQ_QUANT_SCALAR = 0, TQ_QUANT_VECTOR = 1 } tq_quant_mode;   /* QuantMode, quant.hpp:30 */
+
+/* One residual matrix (QuantizedExpert, quant.hpp:37-63), host memory. */
+typedef struct {
+    int64_t out_dim, in_dim;      /* o x i */
+    int bits;                     /* 2, 3, 4, 8 */
+    int mode;                     /* tq_quant_mode */
+    const uint8_t* packed;        /* LSB-first code stream (codec.cpp:150-195) */
+    int64_t packed_bytes;
+    /* scalar mode: o x ceil(i/g) grids, row-major */
+    int64_t group_size;
+    const uint16_t* scale_bits;   /* binary16 patterns of QuantGrid::scale */
+    const uint8_t* zeros;         /* QuantGrid::zero_point, in [0, 2^bits) */
+    /* vector mode */
+    int64_t sub_dim;
+    const uint16_t* codebook_bits;   /* 2^bits x sub_dim binary16 patterns */
+} tq_qmat_desc;
+
+/* An in-memory TileQLayer (infer.hpp:22-28), host memory; nothing is
+ * retained after tq_layer_create returns. */
+typedef struct {
+    int64_t num_experts, top_k, in_dim, out_dim, num_shared;   /* MoELayerSpec */
+    const float* gate_weights;       /* K x i */
+    int64_t grid_rows, grid_cols, rank;                        /* M, N, r */
+    const uint32_t* placement;       /* K x 2: assignment.placed[k] = (p, q) */
+    const float* scaling;            /* K x i: scaling.s[k] */
+    const uint16_t* singular_bits;   /* r binary16 patterns */
+    const int8_t* u_codes;           /* M blocks, each o x r row-major */
+    const float* u_absmax;           /* M */
+    const int8_t* v_codes;           /* N blocks, each r x i row-major */
+    const float* v_absmax;           /* N */
+    const tq_qmat_desc* experts;     /* K routed residuals */
+    const tq_qmat_desc* shared;      /* num_shared shared experts */
+} tq_layer_desc;
+
+/* Build a device-resident layer from an in-memory TileQLayer (the C++ shim's
+ * entry: tileq_forward(x, layer, routing) on a layer that never touched disk).
+ * Validation mirrors what the reference enforces on the same fields:
+ * out-of-grid cells -> TQ_ERR_FORMAT (infer.cpp:65-72), non-positive scales
+ * -> TQ_ERR_FORMAT, bits outside {2,3,4,8} -> TQ_ERR_PARAM (quant.cpp:18-22),
+ * mismatched residual dims -> TQ_ERR_SHAPE. */
+tq_status tq_layer_create(const tq_layer_desc* desc, int device, int64_t expert_begin, int64_t expert_end,
+                          tq_layer** out);
 tq_status tq_layer_free(tq_layer* layer);
 tq_status tq_layer_info_get(const tq_layer* layer, tq_layer_info* out);
 

@@ -99,6 +99,8 @@ def lib() -> C.CDLL:
     L.tq_version.restype = C.c_char_p
     L.tq_layer_load.argtypes = [C.c_char_p, i32, i32, i64, i64, C.POINTER(p)]
     L.tq_layer_free.argtypes = [p]
+    L.tq_artifact_check.argtypes = [C.c_char_p, i32]
+    L.tq_layer_create.argtypes = [p, i32, i64, i64, C.POINTER(p)]
     L.tq_layer_info_get.argtypes = [p, C.POINTER(_LayerInfo)]
     L.tq_layer_reserve.argtypes = [p, i64]
     L.tq_route.argtypes = [p, p, i64, p, p, p]
@@ -126,7 +128,7 @@ def lib() -> C.CDLL:
     L.tq_ep_xrow_elems.argtypes = [p]
     L.tq_ep_extrow_elems.restype = i64
     L.tq_ep_extrow_elems.argtypes = [p]
-    for name in ("tq_layer_load", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
+    for name in ("tq_layer_load", "tq_artifact_check", "tq_layer_create", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
                  "tq_sync", "tq_debug_decode_counters", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
                  "tq_ep_expert_rows", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):
@@ -385,6 +387,13 @@ class Layer:
 # ---------------------------------------------------------------------------
 
 _layer_cache: dict = {}
+
+
+def artifact_check(artifact_dir: str, verify_crc: bool = True) -> None:
+    """read_artifact's validation alone (io.cpp:186-295,422-485,679-813), on
+    the host: raises the same TileqError subclass and message tq_layer_load
+    would, without touching a device."""
+    check(lib().tq_artifact_check(os.fsencode(artifact_dir), int(verify_crc)))
 
 
 def route(x, gate_weights, top_k: int):

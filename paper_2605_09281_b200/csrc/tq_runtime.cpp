@@ -245,6 +245,11 @@ std::string require_string(const json& j, const char* key) {
 
 // One quantized matrix as read from the wire (read_quantized, io.cpp:422-485).
 struct QMat {
+    int bits = 0;
+    bool vec = false;              // codebook (vector) mode
+    size_t gs = 0;                 // scalar mode group size
+    size_t sub_dim = 0;            // vector mode subvector length
+    std::vector<uint16_t> codebook;   // 2^bits x sub_dim binary16 (vector mode)
     std::vector<uint8_t> packed;
     std::vector<uint16_t> scales;  // o x G binary16
     std::vector<uint8_t> zeros;    // o x G unpacked
@@ -267,23 +272,46 @@ std::vector<uint32_t> unpack_stream(const std::vector<uint8_t>& bytes, int bits,
     return out;
 }
 
-QMat read_qmat(const Container& c, const std::string& prefix, const json& qmeta, size_t o, size_t i, int* bits_out,
-               size_t* gs_out) {
+// length and clean trailing pad bits of a packed stream without unpacking it
+// (unpack_codes' checks, codec.cpp:168-195)
+void check_packed_stream(const std::vector<uint8_t>& bytes, int bits, size_t count, const std::string& what) {
+    if (bytes.size() != packed_byte_length(count, bits)) fail(TQ_ERR_FORMAT, what + ": packed stream length mismatch");
+    for (size_t bit = count * static_cast<size_t>(bits); bit < bytes.size() * 8; ++bit)
+        if (bytes[bit >> 3] & (1u << (bit & 7)))
+            fail(TQ_ERR_FORMAT, what + ": packed stream has nonzero padding past code " + std::to_string(count));
+}
+
+QMat read_qmat(const Container& c, const std::string& prefix, const json& qmeta, size_t o, size_t i) {
     int bits = 0;
     if (!qmeta.contains("bits") || !qmeta["bits"].is_number_integer() ||
         (bits = qmeta["bits"].get<int>(), bits != 2 && bits != 3 && bits != 4 && bits != 8))
         fail(TQ_ERR_FORMAT, "manifest quant meta: bits must be one of 2, 3, 4, 8");
     const std::string mode = require_string(qmeta, "mode");
-    if (mode == "vector")
-        fail(TQ_ERR_PARAM,
-             "tensor '" + prefix + ".codes': vector-quantized residuals (codebook mode) are not supported by the "
-             "GPU engine yet");
+    QMat q;
+    q.bits = bits;
+    std::vector<size_t> shape;
+    if (mode == "vector") {
+        // codebook mode (io.cpp:464-480): codes o x subvectors, codebook 2^bits x sub_dim f16
+        q.vec = true;
+        q.sub_dim = require_size(qmeta, "sub_dim");
+        if (q.sub_dim == 0) fail(TQ_ERR_FORMAT, "manifest quant meta: sub_dim must be >= 1");
+        const size_t subs = (i + q.sub_dim - 1) / q.sub_dim;
+        q.packed = c.bytes(prefix + ".codes", "packed-u" + std::to_string(bits), &shape);
+        if (shape != std::vector<size_t>{o, subs}) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".codes': unexpected shape");
+        const std::vector<uint8_t> bb = c.bytes(prefix + ".codebook", "f16-roundtrip", &shape);
+        if (shape != std::vector<size_t>{size_t{1} << bits, q.sub_dim})
+            fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".codebook': unexpected shape");
+        q.codebook.resize(bb.size() / 2);
+        std::memcpy(q.codebook.data(), bb.data(), bb.size());
+        // the trailing pad bits of the code stream must be clean (unpack_codes, codec.cpp:168-195)
+        check_packed_stream(q.packed, bits, o * subs, "tensor '" + prefix + ".codes'");
+        return q;
+    }
     if (mode != "scalar") fail(TQ_ERR_FORMAT, "manifest quant meta: unknown mode '" + mode + "'");
     const size_t gs = require_size(qmeta, "group_size");
     if (gs == 0) fail(TQ_ERR_FORMAT, "manifest quant meta: group_size must be >= 1");
+    q.gs = gs;
     const size_t groups = (i + gs - 1) / gs;
-    QMat q;
-    std::vector<size_t> shape;
     q.packed = c.bytes(prefix + ".codes", "packed-u" + std::to_string(bits), &shape);
     if (shape != std::vector<size_t>{o, i}) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".codes': unexpected shape");
     const std::vector<uint8_t> sb = c.bytes(prefix + ".scales", "f16-roundtrip", &shape);
@@ -299,8 +327,8 @@ QMat read_qmat(const Container& c, const std::string& prefix, const json& qmeta,
         const float s = half_bits_to_float(q.scales[t]);
         if (!(s > 0.0f) || !std::isfinite(s)) fail(TQ_ERR_FORMAT, "tensor '" + prefix + ".scales': non-positive scale");
     }
-    *bits_out = bits;
-    *gs_out = gs;
+    // the residual code stream itself: length and clean padding (unpacked again by the repack)
+    check_packed_stream(q.packed, bits, o * i, "tensor '" + prefix + ".codes'");
     return q;
 }
 
@@ -743,48 +771,74 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     build_maps(L);
 }
 
-void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, int64_t e_begin, int64_t e_end) {
-    cuda_check(cudaSetDevice(device), "cudaSetDevice");
-    L->device = device;
-    cudaDeviceProp prop;
-    cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
-    if (prop.major != 10)
-        fail(TQ_ERR_CUDA, "libtileq_b200 is built for sm_100a (B200); device " + std::to_string(device) + " is sm_" +
-                              std::to_string(prop.major) + std::to_string(prop.minor));
-    L->num_sms = prop.multiProcessorCount;
+// Host image of an artifact: every tensor read and validated, nothing on the
+// device yet (the reference's LoadedArtifact::layer, io.hpp:47-53, in wire form).
+struct HostArtifact {
+    int64_t K = 0, top_k = 0, i = 0, o = 0, S = 0, M = 0, N = 0, r = 0;
+    std::vector<uint8_t> gate_b;        // K x i f32 (raw bytes)
+    std::vector<float> scaling;         // K x i
+    std::vector<uint16_t> placement;    // K x 2 (p, q)
+    std::vector<float> sigma;           // r decoded singulars
+    std::vector<uint8_t> u_b, v_b;      // int8 factor codes M x o x r, N x r x i
+    std::vector<float> uabs, vabs;      // M, N
+    std::vector<QMat> routed, shared;   // K, S residuals
+};
 
+// Geometry / placement checks every source shares (lotile_forward's
+// FormatError for an out-of-grid cell, infer.cpp:61-72; layer spec checks of
+// read_artifact, io.cpp:700-712).
+void check_host_artifact(const HostArtifact& a) {
+    if (a.K < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: num_experts must be >= 1");
+    if (a.top_k < 1 || a.top_k > a.K)
+        fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: top_k " + std::to_string(a.top_k) + " outside [1, " +
+                                std::to_string(a.K) + "]");
+    if (a.i < 1 || a.o < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: dims must be >= 1");
+    if (a.M == 0 || a.N == 0 || a.r == 0) fail(TQ_ERR_FORMAT, "manifest tiling meta: grid and rank must be nonzero");
+    for (int64_t e = 0; e < a.K; ++e)
+        if (a.placement[2 * e] >= a.M || a.placement[2 * e + 1] >= a.N)
+            fail(TQ_ERR_FORMAT, "tensor 'placement': cell outside the tile grid");
+    if (static_cast<int64_t>(a.routed.size()) != a.K || static_cast<int64_t>(a.shared.size()) != a.S)
+        fail(TQ_ERR_FORMAT, "layer holds " + std::to_string(a.routed.size()) + " routed / " +
+                                std::to_string(a.shared.size()) + " shared residuals, spec says " +
+                                std::to_string(a.K) + " / " + std::to_string(a.S));
+}
+
+// read_artifact (io.cpp:679-813): manifest, every tensor's dtype / shape /
+// byte_length / CRC32, placement bounds / injectivity / L1, residuals.  The
+// residual blobs (all but ~2 MB of an artifact) are read, CRC-checked and
+// unpacked by a pool of host threads, one matrix per task.
+HostArtifact read_artifact_dir(const std::string& dir, bool verify) {
     Container c(dir, verify);
     const json& meta = c.meta();
     const json& s = require_object(meta, "spec");
-    Geometry& g = L->g;
-    g.K = static_cast<int64_t>(require_size(s, "num_experts"));
-    g.top_k = static_cast<int64_t>(require_size(s, "top_k"));
-    g.i = static_cast<int64_t>(require_size(s, "in_dim"));
-    g.o = static_cast<int64_t>(require_size(s, "out_dim"));
-    g.S = static_cast<int64_t>(require_size(s, "num_shared"));
-    if (g.K < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: num_experts must be >= 1");
-    if (g.top_k < 1 || g.top_k > g.K)
-        fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: top_k " + std::to_string(g.top_k) + " outside [1, " +
-                                std::to_string(g.K) + "]");
-    if (g.i < 1 || g.o < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: dims must be >= 1");
+    HostArtifact a;
+    a.K = static_cast<int64_t>(require_size(s, "num_experts"));
+    a.top_k = static_cast<int64_t>(require_size(s, "top_k"));
+    a.i = static_cast<int64_t>(require_size(s, "in_dim"));
+    a.o = static_cast<int64_t>(require_size(s, "out_dim"));
+    a.S = static_cast<int64_t>(require_size(s, "num_shared"));
+    if (a.K < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: num_experts must be >= 1");
+    if (a.top_k < 1 || a.top_k > a.K)
+        fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: top_k " + std::to_string(a.top_k) + " outside [1, " +
+                                std::to_string(a.K) + "]");
+    if (a.i < 1 || a.o < 1) fail(TQ_ERR_FORMAT, "manifest spec invalid: layer spec: dims must be >= 1");
     const json& tiling = require_object(meta, "tiling");
-    g.M = static_cast<int64_t>(require_size(tiling, "grid_rows"));
-    g.N = static_cast<int64_t>(require_size(tiling, "grid_cols"));
-    g.r = static_cast<int64_t>(require_size(tiling, "rank"));
-    if (g.M == 0 || g.N == 0 || g.r == 0) fail(TQ_ERR_FORMAT, "manifest tiling meta: grid and rank must be nonzero");
+    a.M = static_cast<int64_t>(require_size(tiling, "grid_rows"));
+    a.N = static_cast<int64_t>(require_size(tiling, "grid_cols"));
+    a.r = static_cast<int64_t>(require_size(tiling, "rank"));
+    if (a.M == 0 || a.N == 0 || a.r == 0) fail(TQ_ERR_FORMAT, "manifest tiling meta: grid and rank must be nonzero");
 
-    const size_t K = static_cast<size_t>(g.K), I = static_cast<size_t>(g.i), O = static_cast<size_t>(g.o);
-    const size_t M = static_cast<size_t>(g.M), N = static_cast<size_t>(g.N), R = static_cast<size_t>(g.r);
+    const size_t K = static_cast<size_t>(a.K), I = static_cast<size_t>(a.i), O = static_cast<size_t>(a.o);
+    const size_t M = static_cast<size_t>(a.M), N = static_cast<size_t>(a.N), R = static_cast<size_t>(a.r);
     std::vector<size_t> shape;
-    // gate weights
-    std::vector<uint8_t> gate_b = c.bytes("gate_weights", "f32", &shape);
+    a.gate_b = c.bytes("gate_weights", "f32", &shape);
     if (shape != std::vector<size_t>{K, I})
         fail(TQ_ERR_FORMAT, "tensor 'gate_weights': expected shape [" + std::to_string(K) + ", " + std::to_string(I) + "]");
     std::vector<uint8_t> scaling_b = c.bytes("scaling", "f32", &shape);
     if (shape != std::vector<size_t>{K, I})
         fail(TQ_ERR_FORMAT, "tensor 'scaling': expected shape [" + std::to_string(K) + ", " + std::to_string(I) + "]");
-    std::vector<float> scaling(K * I);
-    std::memcpy(scaling.data(), scaling_b.data(), scaling_b.size());
+    a.scaling.resize(K * I);
+    std::memcpy(a.scaling.data(), scaling_b.data(), scaling_b.size());
     // placement (io.cpp:731-760)
     const size_t l1 = require_size(tiling, "total_l1_displacement");
     if (!tiling.contains("ideal") || !tiling["ideal"].is_array() || tiling["ideal"].size() != K)
@@ -799,18 +853,19 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     std::vector<uint8_t> pl_b = c.bytes("placement", "u16", &shape);
     if (shape != std::vector<size_t>{K, 2})
         fail(TQ_ERR_FORMAT, "tensor 'placement': expected shape [" + std::to_string(K) + ", 2]");
-    std::vector<uint16_t> placement(K * 2);
-    std::memcpy(placement.data(), pl_b.data(), pl_b.size());
+    a.placement.resize(K * 2);
+    std::memcpy(a.placement.data(), pl_b.data(), pl_b.size());
     {
         std::set<std::pair<size_t, size_t>> seen;
         size_t dist = 0;
         for (size_t e = 0; e < K; ++e) {
-            const std::pair<size_t, size_t> cell{placement[2 * e], placement[2 * e + 1]};
+            const std::pair<size_t, size_t> cell{a.placement[2 * e], a.placement[2 * e + 1]};
             if (cell.first >= M || cell.second >= N) fail(TQ_ERR_FORMAT, "tensor 'placement': cell outside the tile grid");
             if (!seen.insert(cell).second)
                 fail(TQ_ERR_FORMAT, "tensor 'placement': duplicate cell (placement must be injective)");
-            auto gap = [](size_t a, size_t b) { return a > b ? a - b : b - a; };
-            dist += gap(cell.first, ideal[e].first) + gap(cell.second, ideal[e].second);
+            const size_t dr = cell.first > ideal[e].first ? cell.first - ideal[e].first : ideal[e].first - cell.first;
+            const size_t dc = cell.second > ideal[e].second ? cell.second - ideal[e].second : ideal[e].second - cell.second;
+            dist += dr + dc;
         }
         if (dist != l1)
             fail(TQ_ERR_FORMAT, "manifest tiling meta: total_l1_displacement does not match the stored cells");
@@ -818,23 +873,162 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     // factors
     std::vector<uint8_t> sing_b = c.bytes("tiled.singulars", "f16-roundtrip", &shape);
     if (shape != std::vector<size_t>{R}) fail(TQ_ERR_FORMAT, "tensor 'tiled.singulars': unexpected shape");
-    std::vector<float> sigma(R);
+    a.sigma.resize(R);
     for (size_t j = 0; j < R; ++j) {
         uint16_t hb;
         std::memcpy(&hb, sing_b.data() + 2 * j, 2);
-        sigma[j] = half_bits_to_float(hb);
+        a.sigma[j] = half_bits_to_float(hb);
     }
-    std::vector<uint8_t> u_b = c.bytes("tiled.u.codes", "u8", &shape);
+    a.u_b = c.bytes("tiled.u.codes", "u8", &shape);
     if (shape != std::vector<size_t>{M, O, R}) fail(TQ_ERR_FORMAT, "tensor 'tiled.u.codes': unexpected shape");
     std::vector<uint8_t> uabs_b = c.bytes("tiled.u.absmax", "f32", &shape);
     if (shape != std::vector<size_t>{M}) fail(TQ_ERR_FORMAT, "tensor 'tiled.u.absmax': expected shape [" + std::to_string(M) + "]");
-    std::vector<uint8_t> v_b = c.bytes("tiled.v.codes", "u8", &shape);
+    a.v_b = c.bytes("tiled.v.codes", "u8", &shape);
     if (shape != std::vector<size_t>{N, R, I}) fail(TQ_ERR_FORMAT, "tensor 'tiled.v.codes': unexpected shape");
     std::vector<uint8_t> vabs_b = c.bytes("tiled.v.absmax", "f32", &shape);
     if (shape != std::vector<size_t>{N}) fail(TQ_ERR_FORMAT, "tensor 'tiled.v.absmax': expected shape [" + std::to_string(N) + "]");
-    std::vector<float> uabs(M), vabs(N);
-    std::memcpy(uabs.data(), uabs_b.data(), uabs_b.size());
-    std::memcpy(vabs.data(), vabs_b.data(), vabs_b.size());
+    a.uabs.resize(M);
+    a.vabs.resize(N);
+    std::memcpy(a.uabs.data(), uabs_b.data(), uabs_b.size());
+    std::memcpy(a.vabs.data(), vabs_b.data(), vabs_b.size());
+
+    // residuals: K routed + S shared matrices, read in parallel; the first
+    // failing matrix in (routed, shared) order is reported, as a serial reader would
+    const json& qmeta = require_object(meta, "quant");
+    const json* smeta = a.S > 0 ? &require_object(meta, "shared_quant") : nullptr;
+    const size_t total = K + static_cast<size_t>(a.S);
+    std::vector<QMat> mats(total);
+    std::vector<std::exception_ptr> errs(total);
+    {
+        std::atomic<size_t> next{0};
+        auto work = [&] {
+            for (size_t w = next++; w < total; w = next++) {
+                try {
+                    if (w < K) mats[w] = read_qmat(c, "expert." + std::to_string(w), qmeta, O, I);
+                    else mats[w] = read_qmat(c, "sharedexpert." + std::to_string(w - K), *smeta, O, I);
+                } catch (...) {
+                    errs[w] = std::current_exception();
+                }
+            }
+        };
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        std::vector<std::thread> pool;
+        for (unsigned t = 1; t < std::min<unsigned>(hw, static_cast<unsigned>(total)); ++t) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+    }
+    for (size_t w = 0; w < total; ++w)
+        if (errs[w]) std::rethrow_exception(errs[w]);
+    a.routed.assign(std::make_move_iterator(mats.begin()), std::make_move_iterator(mats.begin() + K));
+    a.shared.assign(std::make_move_iterator(mats.begin() + K), std::make_move_iterator(mats.end()));
+    return a;
+}
+
+// In-memory layer (TileQLayer, infer.hpp:22-28) through the C-ABI descriptor:
+// the same checks the reader applies to the same fields (io.cpp:422-485 for
+// residuals) minus those that only exist on the wire (CRC, byte lengths).
+HostArtifact artifact_from_desc(const tq_layer_desc* d) {
+    if (!d) fail(TQ_ERR_PARAM, "tq_layer_create: null descriptor");
+    HostArtifact a;
+    a.K = d->num_experts;
+    a.top_k = d->top_k;
+    a.i = d->in_dim;
+    a.o = d->out_dim;
+    a.S = d->num_shared;
+    a.M = d->grid_rows;
+    a.N = d->grid_cols;
+    a.r = d->rank;
+    if (a.K < 1 || a.i < 1 || a.o < 1 || a.S < 0 || a.M < 0 || a.N < 0 || a.r < 0)
+        fail(TQ_ERR_SHAPE, "tq_layer_create: layer dimensions must be positive");
+    if (a.top_k < 1 || a.top_k > a.K)
+        fail(TQ_ERR_PARAM, "tq_layer_create: top_k " + std::to_string(a.top_k) + " outside [1, " + std::to_string(a.K) + "]");
+    const size_t K = static_cast<size_t>(a.K), I = static_cast<size_t>(a.i), O = static_cast<size_t>(a.o);
+    const size_t M = static_cast<size_t>(a.M), N = static_cast<size_t>(a.N), R = static_cast<size_t>(a.r);
+    if (!d->gate_weights || !d->scaling || !d->placement || !d->singular_bits || !d->u_codes || !d->u_absmax ||
+        !d->v_codes || !d->v_absmax || !d->experts || (a.S > 0 && !d->shared))
+        fail(TQ_ERR_PARAM, "tq_layer_create: null tensor pointer in the descriptor");
+    a.gate_b.resize(K * I * 4);
+    std::memcpy(a.gate_b.data(), d->gate_weights, a.gate_b.size());
+    a.scaling.assign(d->scaling, d->scaling + K * I);
+    for (float v : a.scaling)
+        if (!(v > 0.0f) || !std::isfinite(v)) fail(TQ_ERR_FORMAT, "tensor 'scaling': entries must be positive and finite");
+    a.placement.resize(K * 2);
+    for (size_t t = 0; t < K * 2; ++t) {
+        if (d->placement[t] > 0xFFFFu) fail(TQ_ERR_FORMAT, "tensor 'placement': cell outside the tile grid");
+        a.placement[t] = static_cast<uint16_t>(d->placement[t]);
+    }
+    a.sigma.resize(R);
+    for (size_t j = 0; j < R; ++j) a.sigma[j] = half_bits_to_float(d->singular_bits[j]);
+    a.u_b.assign(reinterpret_cast<const uint8_t*>(d->u_codes), reinterpret_cast<const uint8_t*>(d->u_codes) + M * O * R);
+    a.v_b.assign(reinterpret_cast<const uint8_t*>(d->v_codes), reinterpret_cast<const uint8_t*>(d->v_codes) + N * R * I);
+    a.uabs.assign(d->u_absmax, d->u_absmax + M);
+    a.vabs.assign(d->v_absmax, d->v_absmax + N);
+    auto qm = [&](const tq_qmat_desc& q, const std::string& name) {
+        QMat m;
+        m.bits = q.bits;
+        if (q.bits != 2 && q.bits != 3 && q.bits != 4 && q.bits != 8)
+            fail(TQ_ERR_PARAM, "tensor '" + name + "': bits must be one of 2, 3, 4, 8");
+        m.vec = q.mode == TQ_QUANT_VECTOR;
+        if (!m.vec && q.mode != TQ_QUANT_SCALAR) fail(TQ_ERR_PARAM, "tensor '" + name + "': unknown quant mode");
+        if (static_cast<size_t>(q.out_dim) != O || static_cast<size_t>(q.in_dim) != I)
+            fail(TQ_ERR_SHAPE, "tensor '" + name + "': residual is " + std::to_string(q.out_dim) + "x" +
+                                   std::to_string(q.in_dim) + ", layer is " + std::to_string(O) + "x" + std::to_string(I));
+        size_t count;
+        if (!m.vec) {
+            if (q.group_size < 1) fail(TQ_ERR_PARAM, "tensor '" + name + "': group_size must be >= 1");
+            m.gs = static_cast<size_t>(q.group_size);
+            const size_t G = (I + m.gs - 1) / m.gs;
+            count = O * I;
+            if (!q.scale_bits || !q.zeros) fail(TQ_ERR_PARAM, "tensor '" + name + "': null scale/zero table");
+            m.scales.assign(q.scale_bits, q.scale_bits + O * G);
+            m.zeros.assign(q.zeros, q.zeros + O * G);
+            for (size_t t = 0; t < m.scales.size(); ++t) {
+                const float sv = half_bits_to_float(m.scales[t]);
+                if (!(sv > 0.0f) || !std::isfinite(sv)) fail(TQ_ERR_FORMAT, "tensor '" + name + ".scales': non-positive scale");
+                if (m.zeros[t] >> q.bits) fail(TQ_ERR_FORMAT, "tensor '" + name + ".zeros': zero point outside [0, 2^bits)");
+            }
+        } else {
+            if (q.sub_dim < 1) fail(TQ_ERR_PARAM, "tensor '" + name + "': sub_dim must be >= 1");
+            m.sub_dim = static_cast<size_t>(q.sub_dim);
+            count = O * ((I + m.sub_dim - 1) / m.sub_dim);
+            if (!q.codebook_bits) fail(TQ_ERR_PARAM, "tensor '" + name + "': null codebook");
+            m.codebook.assign(q.codebook_bits, q.codebook_bits + (size_t{1} << q.bits) * m.sub_dim);
+        }
+        if (!q.packed || static_cast<size_t>(q.packed_bytes) != packed_byte_length(count, q.bits))
+            fail(TQ_ERR_SIZE, "tensor '" + name + ".codes': packed stream holds " + std::to_string(q.packed_bytes) +
+                                  " bytes, expected " + std::to_string(packed_byte_length(count, q.bits)));
+        m.packed.assign(q.packed, q.packed + q.packed_bytes);
+        return m;
+    };
+    for (size_t e = 0; e < K; ++e) a.routed.push_back(qm(d->experts[e], "expert." + std::to_string(e)));
+    for (int64_t s2 = 0; s2 < a.S; ++s2) a.shared.push_back(qm(d->shared[s2], "sharedexpert." + std::to_string(s2)));
+    check_host_artifact(a);
+    return a;
+}
+
+// Engine layout from a validated host image; device work starts only once
+// every host-side check has passed.
+void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int64_t e_end) {
+    check_host_artifact(a);
+    Geometry& g = L->g;
+    g.K = a.K;
+    g.top_k = a.top_k;
+    g.i = a.i;
+    g.o = a.o;
+    g.S = a.S;
+    g.M = a.M;
+    g.N = a.N;
+    g.r = a.r;
+    const size_t K = static_cast<size_t>(g.K), I = static_cast<size_t>(g.i), O = static_cast<size_t>(g.o);
+    const size_t M = static_cast<size_t>(g.M), N = static_cast<size_t>(g.N), R = static_cast<size_t>(g.r);
+    const std::vector<uint8_t>& gate_b = a.gate_b;
+    const std::vector<float>& scaling = a.scaling;
+    const std::vector<uint16_t>& placement = a.placement;
+    const std::vector<float>& sigma = a.sigma;
+    const std::vector<uint8_t>& u_b = a.u_b;
+    const std::vector<uint8_t>& v_b = a.v_b;
+    const std::vector<float>& uabs = a.uabs;
+    const std::vector<float>& vabs = a.vabs;
     {
         // host copies for the comparison layouts: value = float(code) * (absmax / 127.0f)
         L->lay.M = static_cast<int64_t>(M);
@@ -862,33 +1056,26 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
     if (e_begin < 0 || e_begin > e_end) fail(TQ_ERR_PARAM, "expert range [" + std::to_string(e_begin) + ", " + std::to_string(e_end) + ") outside [0, K]");
     L->e_begin = e_begin;
     L->e_end = e_end;
-    const json& qmeta = require_object(meta, "quant");
-    std::vector<QMat> q;
-    int bits = 0;
-    size_t gs = 0;
-    // every expert is read and validated (like read_artifact) even when only a subset is resident
     // prescale exponent of EVERY routed expert: a rank's dispatch rows carry
     // the low-rank term pre-multiplied by the owner's 2^k (expert parallel)
     std::vector<int> k_all(K, 0);
-    for (size_t e = 0; e < K; ++e) {
-        int b = 0;
-        size_t gsz = 0;
-        QMat m = read_qmat(c, "expert." + std::to_string(e), qmeta, O, I, &b, &gsz);
-        bits = b;
-        gs = gsz;
-        k_all[e] = prescale_exponent(m);
-        if (static_cast<int64_t>(e) >= e_begin && static_cast<int64_t>(e) < e_end) q.push_back(std::move(m));
-    }
-    if (g.S > 0) {
-        const json& smeta = require_object(meta, "shared_quant");
-        for (int64_t sidx = 0; sidx < g.S; ++sidx) {
-            int b = 0;
-            size_t gsz = 0;
-            q.push_back(read_qmat(c, "sharedexpert." + std::to_string(sidx), smeta, O, I, &b, &gsz));
-            if (b != bits || gsz != gs)
-                fail(TQ_ERR_PARAM, "shared experts must use the routed experts' bits/group_size on the GPU engine");
-        }
-    }
+    for (size_t e = 0; e < K; ++e) k_all[e] = prescale_exponent(a.routed[e]);
+    const QMat& q0 = a.routed[0];
+    for (size_t w = 1; w < K; ++w)
+        if (a.routed[w].bits != q0.bits || a.routed[w].vec != q0.vec || a.routed[w].gs != q0.gs ||
+            a.routed[w].sub_dim != q0.sub_dim)
+            fail(TQ_ERR_PARAM, "routed experts must share one bits/mode/group_size on the GPU engine");
+    for (const QMat& m : a.shared)
+        if (m.bits != q0.bits || m.vec != q0.vec || m.gs != q0.gs || m.sub_dim != q0.sub_dim)
+            fail(TQ_ERR_PARAM, "shared experts must use the routed experts' bits/group_size on the GPU engine");
+    if (q0.vec)
+        fail(TQ_ERR_PARAM, "tensor 'expert.0.codes': vector-quantized residuals (codebook mode) are not supported by the "
+                           "GPU engine yet");
+    const int bits = q0.bits;
+    const size_t gs = q0.gs;
+    std::vector<QMat> q;
+    for (int64_t e = e_begin; e < e_end; ++e) q.push_back(std::move(a.routed[static_cast<size_t>(e)]));
+    for (auto& m : a.shared) q.push_back(std::move(m));
     g.bits = bits;
     g.gs = static_cast<int64_t>(gs);
     if (g.gs % 32 != 0)
@@ -1072,6 +1259,17 @@ void load_layer(tq_layer* L, const std::string& dir, int device, bool verify, in
         }
     }
 
+    // --- device: only now that every host-side check has passed ---
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    L->device = device;
+    {
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            fail(TQ_ERR_CUDA, "libtileq_b200 is built for sm_100a (B200); device " + std::to_string(device) +
+                                  " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+        L->num_sms = prop.multiProcessorCount;
+    }
     // --- upload ---
     L->gate.upload(gate_b.data(), gate_b.size());
     L->codes.upload(h_codes.data(), h_codes.size());
@@ -1704,8 +1902,28 @@ tq_status tq_layer_load(const char* dir, int device, int verify_crc, int64_t exp
                         tq_layer** out) {
     return guarded([&] {
         if (!dir || !out) fail(TQ_ERR_PARAM, "tq_layer_load: null argument");
+        HostArtifact a = read_artifact_dir(dir, verify_crc != 0);
         auto L = std::make_unique<tq_layer>();
-        load_layer(L.get(), dir, device, verify_crc != 0, expert_begin, expert_end);
+        build_layer(L.get(), a, device, expert_begin, expert_end);
+        *out = L.release();
+    });
+}
+
+tq_status tq_artifact_check(const char* dir, int verify_crc) {
+    return guarded([&] {
+        if (!dir) fail(TQ_ERR_PARAM, "tq_artifact_check: null argument");
+        HostArtifact a = read_artifact_dir(dir, verify_crc != 0);
+        check_host_artifact(a);
+    });
+}
+
+tq_status tq_layer_create(const tq_layer_desc* desc, int device, int64_t expert_begin, int64_t expert_end,
+                          tq_layer** out) {
+    return guarded([&] {
+        if (!desc || !out) fail(TQ_ERR_PARAM, "tq_layer_create: null argument");
+        HostArtifact a = artifact_from_desc(desc);
+        auto L = std::make_unique<tq_layer>();
+        build_layer(L.get(), a, device, expert_begin, expert_end);
         *out = L.release();
     });
 }

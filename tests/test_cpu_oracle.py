@@ -162,14 +162,16 @@ def test_abi_errors_without_gpu(tmp_path):
     an IoError, a corrupted one a FormatError naming the tensor."""
     import shutil
     import paper_2605_09281_b200 as tq
-    with pytest.raises(tq.TileqError):
+    with pytest.raises(tq.IoError):
         tq.Layer(str(tmp_path / "missing"))
     d = tmp_path / "bad"
     shutil.copytree(os.path.join(GOLD, "general_b8"), d)
     with open(d / "expert.0.scales.bin", "r+b") as f:
         f.write(b"\x00\x00")
-    with pytest.raises(tq.TileqError):
+    with pytest.raises(tq.FormatError, match="tensor 'expert.0.scales': checksum mismatch"):
         tq.Layer(str(d))
+    with pytest.raises(tq.FormatError, match="tensor 'expert.0.scales': non-positive scale"):
+        tq.Layer(str(d), verify_crc=False)
 
 
 def test_no_cpu_fallback_in_product():

@@ -172,6 +172,12 @@ tq_status tq_route(tq_layer* layer, const float* x, int64_t batch, int32_t* ids,
 tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const float* gate, int64_t num_experts,
                        int64_t top_k, int32_t* ids, float* gates, void* stream);
 
+/* tq_route_raw on HOST arrays (the reference's route() signature in plain
+ * memory, moe.hpp:53): ids [host] int64 batch x top_k, gates [host] f32.
+ * Synchronous; allocates its own device staging (not a hot-path entry). */
+tq_status tq_route_host(const float* x, int64_t batch, int64_t in_dim, const float* gate, int64_t num_experts,
+                        int64_t top_k, int device, int64_t* ids, float* gates);
+
 /* Stable token permutation by expert: perm [dev]
  * int32 batch*top_k (perm[pos] = b*top_k+t), offsets [dev] int32 K+1,
  * inv [dev] int32 batch*top_k (inv[f] = pos).  ids [dev] int32. */
@@ -196,6 +202,15 @@ tq_status tq_forward_routed(tq_layer* layer, const float* x, int64_t batch, floa
  * [host] f32 (ids/gates may be NULL). */
 tq_status tq_forward_host(tq_layer* layer, const float* x, int64_t batch, float* y,
                           int64_t* ids, float* gates, int path);
+
+/* tileq_forward / qmoe_forward / lotile_forward (infer.hpp:52-73) on HOST
+ * buffers with a caller-supplied routing (RoutingDecision, moe.hpp:39-47):
+ * x [host] f32 batch x in_dim, ids [host] int64 batch x top_k (the
+ * reference's size_t expert_ids), gates [host] f32 batch x top_k, y [host]
+ * f32 batch x out_dim.  An id outside [0, K) -> TQ_ERR_PARAM with
+ * reference_forward's message (moe.cpp:111-114).  Synchronous. */
+tq_status tq_forward_host_ids(tq_layer* layer, const float* x, int64_t batch, const int64_t* ids,
+                              const float* gates, float* y, int path);
 
 /* Waits for `stream` and reports any device-side error flag raised by the
  * layer's kernels since the last sync (e.g. expert id out of range). */

@@ -1,0 +1,351 @@
+// tileq_gpu.cpp -- reference-side shim: the tileq:: forward API on the
+// reference's own types, served by libtileq_b200.so through its C-ABI
+// (include/tileq_b200.h).  See tileq_gpu.hpp for the mapping.
+#include "tileq_gpu.hpp"
+
+#include <zlib.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "tileq/codec.hpp"
+#include "tileq/errors.hpp"
+#include "tileq_b200.h"
+
+namespace tileq::gpu {
+
+namespace {
+
+[[noreturn]] void rethrow(tq_status st) {
+    const std::string msg = tq_last_error();
+    switch (st) {   // errors.hpp:13-50 <- tq_status
+        case TQ_ERR_SHAPE: throw ShapeError(msg);
+        case TQ_ERR_PARAM: throw ParamError(msg);
+        case TQ_ERR_SIZE: throw SizeError(msg);
+        case TQ_ERR_FORMAT: throw FormatError(msg);
+        case TQ_ERR_IO: throw IoError(msg);
+        case TQ_ERR_NUMERIC: throw NumericError(msg);
+        case TQ_ERR_DATA: throw DataError(msg);
+        default: throw Error("libtileq_b200: " + msg);
+    }
+}
+
+void ok(tq_status st) {
+    if (st != TQ_OK) rethrow(st);
+}
+
+struct LayerHandle {
+    tq_layer* h = nullptr;
+    ~LayerHandle() {
+        if (h) tq_layer_free(h);
+    }
+};
+
+int g_device = 0;
+thread_local std::uint64_t g_dispatch = 0;
+std::mutex g_mu;
+// (address, fingerprint, top_k) -> resident layer; the fingerprint guards
+// against a different layer reusing a freed address
+std::map<std::tuple<const void*, std::uint32_t, std::size_t>, std::unique_ptr<LayerHandle>> g_layers;
+std::map<std::string, std::unique_ptr<LayerHandle>> g_dirs;
+
+std::uint32_t crc(std::uint32_t c, const void* p, std::size_t n) {
+    return static_cast<std::uint32_t>(crc32_z(c, static_cast<const Bytef*>(p), n));
+}
+
+template <class T>
+std::uint32_t crc_vec(std::uint32_t c, const std::vector<T>& v) {
+    return crc(c, v.data(), v.size() * sizeof(T));
+}
+
+std::uint32_t fingerprint_tiled(std::uint32_t c, const TiledLowRank& t) {
+    c = crc(c, &t.rank, sizeof(t.rank));
+    c = crc_vec(c, t.singular_bits);
+    for (const CodedBlock& b : t.u_blocks) c = crc(crc(c, &b.absmax, 4), b.codes.data(), std::min<std::size_t>(b.codes.size(), 4096));
+    for (const CodedBlock& b : t.v_blocks) c = crc(crc(c, &b.absmax, 4), b.codes.data(), std::min<std::size_t>(b.codes.size(), 4096));
+    for (const auto& pq : t.assignment.placed) c = crc(crc(c, &pq.first, sizeof(pq.first)), &pq.second, sizeof(pq.second));
+    for (const auto& s : t.scaling.s) c = crc_vec(c, s);
+    return c;
+}
+
+std::uint32_t fingerprint_q(std::uint32_t c, const QuantizedExpert& q) {
+    const std::size_t n = q.packed.size();
+    c = crc(c, &n, sizeof(n));
+    c = crc(c, q.packed.data(), std::min<std::size_t>(n, 4096));
+    if (n > 4096) c = crc(c, q.packed.data() + n - 4096, 4096);
+    if (!q.grids.empty()) {
+        c = crc(c, &q.grids.front(), sizeof(QuantGrid));
+        c = crc(c, &q.grids.back(), sizeof(QuantGrid));
+    }
+    return crc_vec(c, q.codebook.data);
+}
+
+// QuantizedExpert (quant.hpp:37-63) -> tq_qmat_desc, with owned f16/u8 tables
+struct QStore {
+    std::vector<std::uint16_t> scale_bits, book_bits;
+    std::vector<std::uint8_t> zeros;
+};
+
+tq_qmat_desc qdesc(const QuantizedExpert& q, QStore& st) {
+    tq_qmat_desc d{};
+    d.out_dim = static_cast<std::int64_t>(q.out_dim);
+    d.in_dim = static_cast<std::int64_t>(q.in_dim);
+    d.bits = q.bits;
+    d.mode = q.mode == QuantMode::vector ? TQ_QUANT_VECTOR : TQ_QUANT_SCALAR;
+    d.packed = q.packed.data();
+    d.packed_bytes = static_cast<std::int64_t>(q.packed.size());
+    if (q.mode == QuantMode::scalar) {
+        d.group_size = static_cast<std::int64_t>(q.group_size);
+        st.scale_bits.resize(q.grids.size());
+        st.zeros.resize(q.grids.size());
+        for (std::size_t g = 0; g < q.grids.size(); ++g) {
+            st.scale_bits[g] = float_to_half_bits(q.grids[g].scale);   // f16-exact by construction (quant.hpp:21-24)
+            st.zeros[g] = static_cast<std::uint8_t>(q.grids[g].zero_point);
+        }
+        d.scale_bits = st.scale_bits.data();
+        d.zeros = st.zeros.data();
+    } else {
+        d.sub_dim = static_cast<std::int64_t>(q.sub_dim);
+        st.book_bits.resize(q.codebook.data.size());
+        for (std::size_t t = 0; t < st.book_bits.size(); ++t) st.book_bits[t] = float_to_half_bits(q.codebook.data[t]);
+        d.codebook_bits = st.book_bits.data();
+    }
+    return d;
+}
+
+// Build a device layer from in-memory pieces.  `residuals` / `shared` may be
+// null: lotile_forward's layer (all-zero residual codes).
+tq_layer* create_layer(const MoELayerSpec& spec, std::size_t top_k, const DenseMatrix* gate, const TiledLowRank& t,
+                       const std::vector<QuantizedExpert>* residuals, const std::vector<QuantizedExpert>* shared) {
+    const std::size_t K = spec.num_experts, I = spec.in_dim, O = spec.out_dim;
+    const std::size_t M = t.assignment.grid_rows, N = t.assignment.grid_cols, R = t.rank;
+    if (t.assignment.placed.size() != K || t.scaling.s.size() != K || t.u_blocks.size() != M || t.v_blocks.size() != N)
+        throw ShapeError("tiled factors must match the grid geometry");
+    std::vector<float> zero_gate;
+    const float* gate_p;
+    if (gate) {
+        if (gate->rows != K || gate->cols != I) throw ShapeError("gate_weights must be num_experts x in_dim");
+        gate_p = gate->data.data();
+    } else {
+        zero_gate.assign(K * I, 0.0f);
+        gate_p = zero_gate.data();
+    }
+    std::vector<std::uint32_t> placement(2 * K);
+    for (std::size_t k = 0; k < K; ++k) {
+        const auto [p, q] = t.assignment.placed[k];
+        if (p >= M || q >= N)
+            throw FormatError("lotile_forward: expert " + std::to_string(k) + " placed at (" + std::to_string(p) + "," +
+                              std::to_string(q) + ") outside grid " + std::to_string(M) + "x" + std::to_string(N));
+        placement[2 * k] = static_cast<std::uint32_t>(p);
+        placement[2 * k + 1] = static_cast<std::uint32_t>(q);
+    }
+    std::vector<float> scaling(K * I);
+    for (std::size_t k = 0; k < K; ++k) {
+        if (t.scaling.s[k].size() != I) throw ShapeError("every scaling vector must have in_dim entries");
+        std::memcpy(&scaling[k * I], t.scaling.s[k].data(), I * 4);
+    }
+    std::vector<std::int8_t> u(M * O * R), v(N * R * I);
+    std::vector<float> uabs(M), vabs(N);
+    for (std::size_t p = 0; p < M; ++p) {
+        if (t.u_blocks[p].codes.size() != O * R) throw ShapeError("every u block must be out_dim x rank");
+        std::memcpy(&u[p * O * R], t.u_blocks[p].codes.data(), O * R);
+        uabs[p] = t.u_blocks[p].absmax;
+    }
+    for (std::size_t q = 0; q < N; ++q) {
+        if (t.v_blocks[q].codes.size() != R * I) throw ShapeError("every v block must be rank x in_dim");
+        std::memcpy(&v[q * R * I], t.v_blocks[q].codes.data(), R * I);
+        vabs[q] = t.v_blocks[q].absmax;
+    }
+    std::vector<QStore> stores(K + spec.num_shared + 1);
+    std::vector<tq_qmat_desc> ex(K), sh(spec.num_shared);
+    // lotile-only layer: all-zero 2-bit codes with unit scales (W = 0)
+    const std::size_t gs = 128, G = (I + gs - 1) / gs;
+    std::vector<std::uint8_t> zero_codes((O * I * 2 + 7) / 8, 0), zero_zp(O * G, 0);
+    std::vector<std::uint16_t> unit_scale(O * G, 0x3C00);
+    for (std::size_t k = 0; k < K; ++k) {
+        if (residuals) {
+            ex[k] = qdesc((*residuals)[k], stores[k]);
+        } else {
+            tq_qmat_desc& d = ex[k];
+            d = tq_qmat_desc{};
+            d.out_dim = static_cast<std::int64_t>(O);
+            d.in_dim = static_cast<std::int64_t>(I);
+            d.bits = 2;
+            d.mode = TQ_QUANT_SCALAR;
+            d.packed = zero_codes.data();
+            d.packed_bytes = static_cast<std::int64_t>(zero_codes.size());
+            d.group_size = static_cast<std::int64_t>(gs);
+            d.scale_bits = unit_scale.data();
+            d.zeros = zero_zp.data();
+        }
+    }
+    for (std::size_t s = 0; s < spec.num_shared; ++s) sh[s] = qdesc((*shared)[s], stores[K + s]);
+
+    tq_layer_desc d{};
+    d.num_experts = static_cast<std::int64_t>(K);
+    d.top_k = static_cast<std::int64_t>(top_k);
+    d.in_dim = static_cast<std::int64_t>(I);
+    d.out_dim = static_cast<std::int64_t>(O);
+    d.num_shared = static_cast<std::int64_t>(shared ? spec.num_shared : 0);
+    d.gate_weights = gate_p;
+    d.grid_rows = static_cast<std::int64_t>(M);
+    d.grid_cols = static_cast<std::int64_t>(N);
+    d.rank = static_cast<std::int64_t>(R);
+    d.placement = placement.data();
+    d.scaling = scaling.data();
+    d.singular_bits = t.singular_bits.data();
+    d.u_codes = u.data();
+    d.u_absmax = uabs.data();
+    d.v_codes = v.data();
+    d.v_absmax = vabs.data();
+    d.experts = ex.data();
+    d.shared = sh.empty() ? nullptr : sh.data();
+    tq_layer* h = nullptr;
+    ok(tq_layer_create(&d, g_device, 0, -1, &h));
+    return h;
+}
+
+tq_layer* layer_for(const TileQLayer& layer, std::size_t top_k) {
+    std::uint32_t c = crc(0, &layer.spec, sizeof(layer.spec));
+    c = crc_vec(c, layer.gate_weights.data);
+    c = fingerprint_tiled(c, layer.tiled);
+    for (const QuantizedExpert& q : layer.quantized) c = fingerprint_q(c, q);
+    for (const QuantizedExpert& q : layer.shared_quantized) c = fingerprint_q(c, q);
+    const auto key = std::make_tuple(static_cast<const void*>(&layer), c, top_k);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_layers.find(key);
+    if (it != g_layers.end()) return it->second->h;
+    if (layer.quantized.size() != layer.spec.num_experts)
+        throw ShapeError("layer must hold one quantized residual per routed expert");
+    if (layer.shared_quantized.size() != layer.spec.num_shared)
+        throw ShapeError("layer must hold one quantized matrix per shared expert");
+    auto h = std::make_unique<LayerHandle>();
+    h->h = create_layer(layer.spec, top_k, &layer.gate_weights, layer.tiled, &layer.quantized, &layer.shared_quantized);
+    tq_layer* raw = h->h;
+    g_layers[key] = std::move(h);
+    return raw;
+}
+
+tq_layer* layer_for(const TiledLowRank& t, std::size_t top_k) {
+    const std::uint32_t c = fingerprint_tiled(0x6c6f7469u, t);
+    const auto key = std::make_tuple(static_cast<const void*>(&t), c, top_k);
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_layers.find(key);
+    if (it != g_layers.end()) return it->second->h;
+    MoELayerSpec spec;
+    spec.num_experts = t.assignment.placed.size();
+    spec.top_k = top_k;
+    spec.in_dim = t.in_dim();
+    spec.out_dim = t.out_dim();
+    auto h = std::make_unique<LayerHandle>();
+    h->h = create_layer(spec, top_k, nullptr, t, nullptr, nullptr);
+    tq_layer* raw = h->h;
+    g_layers[key] = std::move(h);
+    return raw;
+}
+
+void check_routing(const char* who, const DenseMatrix& x, std::size_t in_dim, const RoutingDecision& routing) {
+    if (x.cols != in_dim)
+        throw ShapeError(std::string(who) + ": token width " + std::to_string(x.cols) + " vs in_dim " +
+                         std::to_string(in_dim));
+    if (routing.batch != x.rows)
+        throw ShapeError(std::string(who) + ": routing batch " + std::to_string(routing.batch) + " vs input batch " +
+                         std::to_string(x.rows));
+    if (routing.expert_ids.size() != routing.batch * routing.top_k || routing.gates.rows != routing.batch ||
+        routing.gates.cols != routing.top_k)
+        throw ShapeError(std::string(who) + ": routing tables do not match batch x top_k");
+}
+
+DenseMatrix run(tq_layer* h, const DenseMatrix& x, const RoutingDecision& routing, std::size_t out_dim, int path) {
+    DenseMatrix y(x.rows, out_dim);
+    if (x.rows == 0) return y;
+    std::vector<std::int64_t> ids(routing.expert_ids.begin(), routing.expert_ids.end());
+    const std::uint64_t before = tq_launch_count(h);
+    ok(tq_forward_host_ids(h, x.data.data(), static_cast<std::int64_t>(x.rows), ids.data(), routing.gates.data.data(),
+                           y.data.data(), path));
+    g_dispatch += tq_launch_count(h) - before;
+    return y;
+}
+
+}  // namespace
+
+RoutingDecision route(const DenseMatrix& x, const DenseMatrix& gate_weights, std::size_t top_k) {
+    if (top_k > gate_weights.rows)
+        throw ParamError("route: top_k " + std::to_string(top_k) + " exceeds num_experts " +
+                         std::to_string(gate_weights.rows));
+    if (x.cols != gate_weights.cols)
+        throw ShapeError("route: token width " + std::to_string(x.cols) + " vs gate width " +
+                         std::to_string(gate_weights.cols));
+    RoutingDecision r;
+    r.batch = x.rows;
+    r.top_k = top_k;
+    r.expert_ids.assign(x.rows * top_k, 0);
+    r.gates = DenseMatrix(x.rows, top_k);
+    if (x.rows == 0) return r;
+    std::vector<std::int64_t> ids(x.rows * top_k);
+    ok(tq_route_host(x.data.data(), static_cast<std::int64_t>(x.rows), static_cast<std::int64_t>(x.cols),
+                     gate_weights.data.data(), static_cast<std::int64_t>(gate_weights.rows),
+                     static_cast<std::int64_t>(top_k), g_device, ids.data(), r.gates.data.data()));
+    for (std::size_t t = 0; t < ids.size(); ++t) r.expert_ids[t] = static_cast<std::size_t>(ids[t]);
+    return r;
+}
+
+DenseMatrix qmoe_forward(const DenseMatrix& x, const TileQLayer& layer, const RoutingDecision& routing) {
+    check_routing("qmoe_forward", x, layer.spec.in_dim, routing);
+    return run(layer_for(layer, routing.top_k), x, routing, layer.spec.out_dim, TQ_PATH_QMOE);
+}
+
+DenseMatrix lotile_forward(const DenseMatrix& x, const TiledLowRank& tiled, const RoutingDecision& routing,
+                           int threads) {
+    (void)threads;   // the device path is deterministic for any launch shape
+    check_routing("lotile_forward", x, tiled.in_dim(), routing);
+    return run(layer_for(tiled, routing.top_k), x, routing, tiled.out_dim(), TQ_PATH_LOTILE);
+}
+
+DenseMatrix tileq_forward(const DenseMatrix& x, const TileQLayer& layer, const RoutingDecision& routing) {
+    check_routing("tileq_forward", x, layer.spec.in_dim, routing);
+    return run(layer_for(layer, routing.top_k), x, routing, layer.spec.out_dim, TQ_PATH_FULL);
+}
+
+DenseMatrix forward_from_artifact(const std::string& dir, const DenseMatrix& x) {
+    tq_layer* h;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        auto it = g_dirs.find(dir);
+        if (it == g_dirs.end()) {
+            auto lh = std::make_unique<LayerHandle>();
+            ok(tq_layer_load(dir.c_str(), g_device, 1, 0, -1, &lh->h));
+            it = g_dirs.emplace(dir, std::move(lh)).first;
+        }
+        h = it->second->h;
+    }
+    tq_layer_info info{};
+    ok(tq_layer_info_get(h, &info));
+    if (static_cast<std::int64_t>(x.cols) != info.in_dim)
+        throw ShapeError("forward_from_artifact: token width " + std::to_string(x.cols) + " vs in_dim " +
+                         std::to_string(info.in_dim));
+    DenseMatrix y(x.rows, static_cast<std::size_t>(info.out_dim));
+    if (x.rows == 0) return y;
+    const std::uint64_t before = tq_launch_count(h);
+    ok(tq_forward_host(h, x.data.data(), static_cast<std::int64_t>(x.rows), y.data.data(), nullptr, nullptr,
+                       TQ_PATH_FULL));
+    g_dispatch += tq_launch_count(h) - before;
+    return y;
+}
+
+void reset_dispatch_count() { g_dispatch = 0; }
+std::uint64_t dispatch_count() { return g_dispatch; }
+
+void set_device(int device) { g_device = device; }
+
+void clear_cache() {
+    std::lock_guard<std::mutex> lk(g_mu);
+    g_layers.clear();
+    g_dirs.clear();
+}
+
+}  // namespace tileq::gpu

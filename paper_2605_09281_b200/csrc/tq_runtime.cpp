@@ -521,7 +521,7 @@ struct tq_layer {
     int64_t cap = 0;
     DBuf route_ws, route_ticket, poffsets;   // router: per-(token, expert) certified scores, per-token tickets
     DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
-        err_flag, xin, yout, nsplit_d;
+        err_flag, xin, yout, nsplit_d, hids, hgates;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
     // decode path (batch <= kDecMaxBatch): route+scatter -> fused expert GEMM -> combine
@@ -2124,6 +2124,51 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
     });
 }
 
+tq_status tq_forward_host_ids(tq_layer* L, const float* x, int64_t batch, const int64_t* ids, const float* gates,
+                              float* y, int path) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        check_batch(L, batch);
+        if (batch == 0) return;
+        if (!x || !ids || !gates || !y) fail(TQ_ERR_PARAM, "tq_forward_host_ids: null argument");
+        const int64_t n = batch * L->g.top_k;
+        std::vector<int32_t> hid(static_cast<size_t>(n));
+        for (int64_t t = 0; t < n; ++t) {
+            if (ids[t] < 0 || ids[t] >= L->g.K)
+                fail(TQ_ERR_PARAM, "reference_forward: expert id " + std::to_string(ids[t]) + " out of range [0, " +
+                                       std::to_string(L->g.K) + ")");
+            hid[static_cast<size_t>(t)] = static_cast<int32_t>(ids[t]);
+        }
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        if (L->hids.n < sizeof(int32_t) * static_cast<size_t>(n)) {
+            L->hids.alloc(sizeof(int32_t) * static_cast<size_t>(L->cap * L->g.top_k));
+            L->hgates.alloc(sizeof(float) * static_cast<size_t>(L->cap * L->g.top_k));
+        }
+        cudaStream_t st = nullptr;
+        cuda_check(cudaMemcpyAsync(L->xin.p, x, sizeof(float) * batch * L->g.i, cudaMemcpyHostToDevice, st), "x H2D");
+        cuda_check(cudaMemcpyAsync(L->hids.p, hid.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, st), "ids H2D");
+        cuda_check(cudaMemcpyAsync(L->hgates.p, gates, sizeof(float) * n, cudaMemcpyHostToDevice, st), "gates H2D");
+        const float* xd = L->xin.as<float>();
+        const int32_t* idd = L->hids.as<int32_t>();
+        const float* gd = L->hgates.as<float>();
+        float* yd = L->yout.as<float>();
+        const void* const key[6] = {xd, idd, gd, yd, nullptr, nullptr};
+        const bool dec = decode_ok(L, batch, true);
+        if (dec) reserve_decode(L);
+        run_graphed(L, key, batch, path + (dec ? 64 : 0), st, [&](cudaStream_t s2) {
+            if (dec) {
+                run_decode(L, xd, batch, idd, gd, yd, path, s2);
+                return;
+            }
+            run_route(L, xd, batch, false, s2);
+            run_experts(L, xd, batch, idd, gd, yd, path, s2);
+        });
+        cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, st), "y D2H");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");
+    });
+}
+
 // ---------------------------------------------------------------------------
 // comparison layouts (the paper's bench: infer.cpp:187-339, 345-426)
 // ---------------------------------------------------------------------------
@@ -2394,6 +2439,31 @@ tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const floa
                                 nullptr, ws.as<float>(), ticket.as<int32_t>(), nullptr, nullptr, st),
                    "route_kernel launch");
         cuda_check(cudaStreamSynchronize(st), "stream sync");   // workspace lifetime
+    });
+}
+
+tq_status tq_route_host(const float* x, int64_t batch, int64_t in_dim, const float* gate, int64_t num_experts,
+                        int64_t top_k, int device, int64_t* ids, float* gates) {
+    return guarded([&] {
+        if (top_k < 1 || top_k > num_experts)
+            fail(TQ_ERR_PARAM, "route: top_k " + std::to_string(top_k) + " outside [1, " + std::to_string(num_experts) + "]");
+        if (batch < 0 || in_dim < 1) fail(TQ_ERR_SHAPE, "route: bad batch / width");
+        if (batch == 0) return;
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        DBuf xd, gd, idd, gtd;
+        xd.alloc(sizeof(float) * batch * in_dim);
+        gd.alloc(sizeof(float) * num_experts * in_dim);
+        idd.alloc(sizeof(int32_t) * batch * top_k);
+        gtd.alloc(sizeof(float) * batch * top_k);
+        cuda_check(cudaMemcpy(xd.p, x, sizeof(float) * batch * in_dim, cudaMemcpyHostToDevice), "x H2D");
+        cuda_check(cudaMemcpy(gd.p, gate, sizeof(float) * num_experts * in_dim, cudaMemcpyHostToDevice), "gate H2D");
+        const tq_status st = tq_route_raw(xd.as<float>(), batch, in_dim, gd.as<float>(), num_experts, top_k,
+                                          idd.as<int32_t>(), gtd.as<float>(), nullptr);
+        if (st != TQ_OK) fail(st, g_last_error);
+        std::vector<int32_t> h(static_cast<size_t>(batch * top_k));
+        cuda_check(cudaMemcpy(h.data(), idd.p, sizeof(int32_t) * h.size(), cudaMemcpyDeviceToHost), "ids D2H");
+        cuda_check(cudaMemcpy(gates, gtd.p, sizeof(float) * h.size(), cudaMemcpyDeviceToHost), "gates D2H");
+        for (size_t t = 0; t < h.size(); ++t) ids[t] = h[t];
     });
 }
 

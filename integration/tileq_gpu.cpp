@@ -3,8 +3,8 @@
 // (include/tileq_b200.h).  See tileq_gpu.hpp for the mapping.
 #include "tileq_gpu.hpp"
 
-#include <zlib.h>
-
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -50,19 +50,22 @@ thread_local std::uint64_t g_dispatch = 0;
 std::mutex g_mu;
 // (address, fingerprint, top_k) -> resident layer; the fingerprint guards
 // against a different layer reusing a freed address
-std::map<std::tuple<const void*, std::uint32_t, std::size_t>, std::unique_ptr<LayerHandle>> g_layers;
+std::map<std::tuple<const void*, std::uint64_t, std::size_t>, std::unique_ptr<LayerHandle>> g_layers;
 std::map<std::string, std::unique_ptr<LayerHandle>> g_dirs;
 
-std::uint32_t crc(std::uint32_t c, const void* p, std::size_t n) {
-    return static_cast<std::uint32_t>(crc32_z(c, static_cast<const Bytef*>(p), n));
+// FNV-1a over raw bytes: a content fingerprint for the layer cache
+std::uint64_t crc(std::uint64_t c, const void* p, std::size_t n) {
+    const unsigned char* b = static_cast<const unsigned char*>(p);
+    for (std::size_t t = 0; t < n; ++t) c = (c ^ b[t]) * 0x100000001b3ull;
+    return c;
 }
 
 template <class T>
-std::uint32_t crc_vec(std::uint32_t c, const std::vector<T>& v) {
+std::uint64_t crc_vec(std::uint64_t c, const std::vector<T>& v) {
     return crc(c, v.data(), v.size() * sizeof(T));
 }
 
-std::uint32_t fingerprint_tiled(std::uint32_t c, const TiledLowRank& t) {
+std::uint64_t fingerprint_tiled(std::uint64_t c, const TiledLowRank& t) {
     c = crc(c, &t.rank, sizeof(t.rank));
     c = crc_vec(c, t.singular_bits);
     for (const CodedBlock& b : t.u_blocks) c = crc(crc(c, &b.absmax, 4), b.codes.data(), std::min<std::size_t>(b.codes.size(), 4096));
@@ -72,7 +75,7 @@ std::uint32_t fingerprint_tiled(std::uint32_t c, const TiledLowRank& t) {
     return c;
 }
 
-std::uint32_t fingerprint_q(std::uint32_t c, const QuantizedExpert& q) {
+std::uint64_t fingerprint_q(std::uint64_t c, const QuantizedExpert& q) {
     const std::size_t n = q.packed.size();
     c = crc(c, &n, sizeof(n));
     c = crc(c, q.packed.data(), std::min<std::size_t>(n, 4096));
@@ -210,7 +213,7 @@ tq_layer* create_layer(const MoELayerSpec& spec, std::size_t top_k, const DenseM
 }
 
 tq_layer* layer_for(const TileQLayer& layer, std::size_t top_k) {
-    std::uint32_t c = crc(0, &layer.spec, sizeof(layer.spec));
+    std::uint64_t c = crc(0xcbf29ce484222325ull, &layer.spec, sizeof(layer.spec));
     c = crc_vec(c, layer.gate_weights.data);
     c = fingerprint_tiled(c, layer.tiled);
     for (const QuantizedExpert& q : layer.quantized) c = fingerprint_q(c, q);
@@ -218,6 +221,9 @@ tq_layer* layer_for(const TileQLayer& layer, std::size_t top_k) {
     const auto key = std::make_tuple(static_cast<const void*>(&layer), c, top_k);
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_layers.find(key);
+    if (std::getenv("TILEQ_SHIM_DEBUG"))
+        std::fprintf(stderr, "tileq_gpu: layer %p fingerprint %016llx top_k %zu: %s\n", static_cast<const void*>(&layer),
+                     static_cast<unsigned long long>(c), top_k, it != g_layers.end() ? "cached" : "new");
     if (it != g_layers.end()) return it->second->h;
     if (layer.quantized.size() != layer.spec.num_experts)
         throw ShapeError("layer must hold one quantized residual per routed expert");
@@ -231,7 +237,7 @@ tq_layer* layer_for(const TileQLayer& layer, std::size_t top_k) {
 }
 
 tq_layer* layer_for(const TiledLowRank& t, std::size_t top_k) {
-    const std::uint32_t c = fingerprint_tiled(0x6c6f7469u, t);
+    const std::uint64_t c = fingerprint_tiled(0xcbf29ce484222325ull ^ 0x6c6f7469u, t);
     const auto key = std::make_tuple(static_cast<const void*>(&t), c, top_k);
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_layers.find(key);

@@ -82,6 +82,22 @@ class _LayerInfo(C.Structure):
         "device_bytes", "tier_folded", "tier_scalar", "tier_general")]
 
 
+class _QMatDesc(C.Structure):
+    _fields_ = [("out_dim", C.c_int64), ("in_dim", C.c_int64), ("bits", C.c_int), ("mode", C.c_int),
+                ("packed", C.c_void_p), ("packed_bytes", C.c_int64), ("group_size", C.c_int64),
+                ("scale_bits", C.c_void_p), ("zeros", C.c_void_p), ("sub_dim", C.c_int64),
+                ("codebook_bits", C.c_void_p)]
+
+
+class _LayerDesc(C.Structure):
+    _fields_ = [("num_experts", C.c_int64), ("top_k", C.c_int64), ("in_dim", C.c_int64), ("out_dim", C.c_int64),
+                ("num_shared", C.c_int64), ("gate_weights", C.c_void_p), ("grid_rows", C.c_int64),
+                ("grid_cols", C.c_int64), ("rank", C.c_int64), ("placement", C.c_void_p),
+                ("scaling", C.c_void_p), ("singular_bits", C.c_void_p), ("u_codes", C.c_void_p),
+                ("u_absmax", C.c_void_p), ("v_codes", C.c_void_p), ("v_absmax", C.c_void_p),
+                ("experts", C.c_void_p), ("shared", C.c_void_p)]
+
+
 _lib = None
 
 
@@ -174,6 +190,9 @@ class Layer:
         h = C.c_void_p()
         check(lib().tq_layer_load(os.fsencode(artifact_dir), int(device), int(verify_crc), int(b), int(e),
                                   C.byref(h)))
+        self._init_handle(h, device, artifact_dir)
+
+    def _init_handle(self, h, device, artifact_dir):
         self._h = h
         self.device = int(device)
         info = _LayerInfo()
@@ -182,6 +201,58 @@ class Layer:
         for k in ("num_experts", "top_k", "in_dim", "out_dim", "num_shared", "rank", "bits", "group_size"):
             setattr(self, k, self.info[k])
         self.artifact_dir = artifact_dir
+
+    @classmethod
+    def from_arrays(cls, t: dict, device: int = 0, expert_range: Optional[tuple] = None) -> "Layer":
+        """An in-memory layer (TileQLayer, infer.hpp:22-28) through tq_layer_create.
+
+        `t` holds numpy arrays: K, top_k, i, o, S, M, N, r; gate (K x i f32),
+        scaling (K x i f32), placement (K x 2), singulars (r binary16 bits),
+        u_codes (M x o x r int8), u_absmax (M), v_codes (N x r x i int8),
+        v_absmax (N); experts / shared: lists of dicts with packed (u8),
+        bits, and either group_size, scales (binary16 bits), zeros, or
+        sub_dim, codebook (binary16 bits)."""
+        keep = []
+
+        def arr(a, dt):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data
+
+        def qm(q):
+            d = _QMatDesc()
+            d.out_dim, d.in_dim, d.bits = int(t["o"]), int(t["i"]), int(q["bits"])
+            d.packed = arr(q["packed"], np.uint8)
+            d.packed_bytes = int(np.asarray(q["packed"]).size)
+            if "codebook" in q:
+                d.mode, d.sub_dim = 1, int(q["sub_dim"])
+                d.codebook_bits = arr(q["codebook"], np.uint16)
+            else:
+                d.mode, d.group_size = 0, int(q["group_size"])
+                d.scale_bits = arr(q["scales"], np.uint16)
+                d.zeros = arr(q["zeros"], np.uint8)
+            return d
+
+        ex = (_QMatDesc * max(1, len(t["experts"])))(*[qm(q) for q in t["experts"]])
+        sh = (_QMatDesc * max(1, len(t["shared"])))(*[qm(q) for q in t["shared"]])
+        d = _LayerDesc()
+        for k, f in (("num_experts", "K"), ("top_k", "top_k"), ("in_dim", "i"), ("out_dim", "o"),
+                     ("num_shared", "S"), ("grid_rows", "M"), ("grid_cols", "N"), ("rank", "r")):
+            setattr(d, k, int(t[f]))
+        d.gate_weights = arr(t["gate"], np.float32)
+        d.scaling = arr(t["scaling"], np.float32)
+        d.placement = arr(t["placement"], np.uint32)
+        d.singular_bits = arr(t["singulars"], np.uint16)
+        d.u_codes, d.u_absmax = arr(t["u_codes"], np.int8), arr(t["u_absmax"], np.float32)
+        d.v_codes, d.v_absmax = arr(t["v_codes"], np.int8), arr(t["v_absmax"], np.float32)
+        d.experts = C.cast(ex, C.c_void_p)
+        d.shared = C.cast(sh, C.c_void_p) if len(t["shared"]) else None
+        b, e = expert_range if expert_range is not None else (0, -1)
+        h = C.c_void_p()
+        check(lib().tq_layer_create(C.byref(d), int(device), int(b), int(e), C.byref(h)))
+        self = cls.__new__(cls)
+        self._init_handle(h, device, "<memory>")
+        return self
 
     def close(self):
         if getattr(self, "_h", None):

@@ -39,6 +39,10 @@ SPECS = [
     dict(K=5, top_k=1, i=192, o=130, r=4, bits=8, g=32, calib="signs", seed=5),
     # neutral scaling (empty calibration -> all-ones), noise-free low-rank-dominant
     dict(K=9, top_k=2, i=256, o=256, r=16, bits=3, g=128, calib="none", noise=0.0, seed=6),
+    # tiny layers (one 64-wide K atom, one m-block): the reference tests' scale
+    dict(K=6, top_k=2, i=64, o=48, S=1, r=8, bits=3, g=32, calib="gauss", seed=7),
+    dict(K=6, top_k=2, i=64, o=48, S=1, r=8, bits=8, g=32, calib="gauss", seed=8),
+    dict(K=4, top_k=2, i=10, o=8, S=1, r=4, bits=4, g=32, calib="gauss", seed=9),
 ]
 
 

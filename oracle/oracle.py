@@ -288,7 +288,7 @@ class RefLib:
         L.tq_ref_bench.argtypes = [_p, C.c_int, _p, _i64, _i64, _i64, C.c_uint64, _p, C.c_char_p, C.c_int]
         L.tq_ref_make_artifact.argtypes = [C.c_char_p] + [_i64] * 8 + [C.c_int, _i64, C.c_int, _i64,
                                            C.c_double, C.c_double, _i64, C.c_uint64, C.c_int,
-                                           C.c_char_p, C.c_int]
+                                           C.c_int, _i64, C.c_char_p, C.c_int]
 
     def _check(self, st, buf):
         if st:
@@ -338,12 +338,13 @@ class RefLib:
 
     def make_artifact(self, path, *, K, top_k, i, o, S=0, M=0, N=0, r=16, bits=3, g=128,
                       calib="signs", calib_tokens=256, noise=0.05, mix_scale=1.0,
-                      planted_rank=8, seed=1, full_pipeline=False):
+                      planted_rank=8, seed=1, full_pipeline=False, quantizer="rtn", sub_dim=2):
         kind = {"signs": 0, "gauss": 1, "none": 2}[calib]
+        qz = {"rtn": 0, "gptq": 1, "vq": 2}[quantizer]
         buf = C.create_string_buffer(1024)
         self._check(self.lib.tq_ref_make_artifact(
             path.encode(), K, top_k, i, o, S, M, N, r, bits, g, kind, calib_tokens, noise,
-            mix_scale, planted_rank, seed, int(full_pipeline), buf, 1024), buf)
+            mix_scale, planted_rank, seed, int(full_pipeline), qz, sub_dim, buf, 1024), buf)
         return path
 
 

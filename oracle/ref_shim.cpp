@@ -241,7 +241,7 @@ int tq_ref_make_artifact(const char* dir, std::int64_t num_experts, std::int64_t
                          int bits, std::int64_t group_size, int calib_kind,
                          std::int64_t calib_tokens, double noise, double mix_scale,
                          std::int64_t planted_rank, std::uint64_t seed, int full_pipeline,
-                         char* errbuf, int errlen) {
+                         int quantizer, std::int64_t sub_dim, char* errbuf, int errlen) {
     return guarded(errbuf, errlen, [&] {
         MoELayerSpec spec{static_cast<std::size_t>(num_experts), static_cast<std::size_t>(top_k),
                           static_cast<std::size_t>(in_dim), static_cast<std::size_t>(out_dim),
@@ -253,8 +253,12 @@ int tq_ref_make_artifact(const char* dir, std::int64_t num_experts, std::int64_t
         cfg.rank = static_cast<std::size_t>(rank);
         cfg.bits = bits;
         cfg.group_size = static_cast<std::size_t>(group_size);
-        cfg.quantizer = ResidualQuantizer::rtn;
+        // quantizer 0 rtn, 1 gptq, 2 vq (codebook); gptq / vq run quantize_moe itself
+        cfg.quantizer = quantizer == 2 ? ResidualQuantizer::vq
+                                       : (quantizer == 1 ? ResidualQuantizer::gptq : ResidualQuantizer::rtn);
+        cfg.sub_dim = static_cast<std::size_t>(sub_dim);
         cfg.seed = seed;
+        if (quantizer != 0) full_pipeline = 1;
         TileQConfig rc = cfg.resolved(spec);
 
         SynthResult synth = synth_experts(spec, rc.grid_rows, rc.grid_cols,

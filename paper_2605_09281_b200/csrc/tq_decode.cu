@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
                     // one super-word live in registers at a time (896 threads: <= 72 registers)
                     const int e0 = k * kAtomsPerStep * 64;        // first K of the step
                     const int ein = gshift >= 0 ? (e0 & ((1 << gshift) - 1)) : e0 % p.group_size;
+                    const int glast = p.groups - 1 - (gshift >= 0 ? e0 >> gshift : e0 / p.group_size);
                     const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + kAtomsPerStep * kBlk) + rloc;
                     mbar_wait(&h->a_empty[as], aph ^ 1u);
                     if (lane == 0 && q == 0 && hw == 0) dtrace(p, 8, j);
@@ -301,7 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
 #pragma unroll
                                 for (int w = 0; w < kWords; ++w) words[ss][w] = wst[ss * kHalf + w * kBM];
                                 const int off = ein + 64 * at + 32 * ss;
-                                sbits[ss] = sc[(gshift >= 0 ? off >> gshift : off / p.group_size) * kBM];
+                                // a super-word past in_dim (zero codes) may lie past the last group
+                                const int gi = min(gshift >= 0 ? off >> gshift : off / p.group_size, glast);
+                                sbits[ss] = sc[gi * kBM];
                             }
 #pragma unroll
                             for (int ss = 0; ss < 2; ++ss) {

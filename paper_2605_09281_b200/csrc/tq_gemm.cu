@@ -649,7 +649,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                                 for (int w = 0; w < kWords; ++w)
                                     words[s][w] = wst[(s >> 1) * (kBlk / 4) + (s & 1) * kHalf + w * kBM];
                                 const int off = ein + 32 * s;
-                                const int gi = gshift >= 0 ? off >> gshift : off / p.group_size;
+                                // a super-word past in_dim (zero codes) may lie past the last group
+                                const int gi = min(gshift >= 0 ? off >> gshift : off / p.group_size,
+                                                   p.groups - 1 - (gshift >= 0 ? e0 >> gshift : e0 / p.group_size));
                                 sbits[s] = sc[gi * kBM];
                             }
                             __syncwarp();

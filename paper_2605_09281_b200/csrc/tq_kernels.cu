@@ -1599,7 +1599,10 @@ __device__ void dec_project(const float* __restrict__ xb, const float* __restric
     constexpr int kChunk = 4096;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool vec = (in_dim & 15) == 0;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};   // rows warp + kNW * t (r <= 64)
+    constexpr int kT = (64 + kNW - 1) / kNW;   // rows warp + kNW * t cover r <= 64
+    float acc[kT];
+#pragma unroll
+    for (int t = 0; t < kT; ++t) acc[t] = 0.0f;
     for (int c0 = 0; c0 < in_dim; c0 += kChunk) {
         const int nc = min(kChunk, in_dim - c0);
         __syncthreads();   // xs_sm of the previous chunk / caller consumed
@@ -1607,7 +1610,7 @@ __device__ void dec_project(const float* __restrict__ xb, const float* __restric
         __syncthreads();
         if (ta) rtrace(*ta, 9);
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < kT; ++t) {
             const int j = warp + kNW * t;
             if (j >= r) break;
             const int8_t* row = codes + static_cast<int64_t>(j) * in_dim + c0;
@@ -1652,7 +1655,7 @@ __device__ void dec_project(const float* __restrict__ xb, const float* __restric
     }
     if (ta) rtrace(*ta, 10);
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < kT; ++t) {
         const int j = warp + kNW * t;
         if (j >= r) break;
         float v = acc[t];
@@ -1783,8 +1786,11 @@ constexpr int kDecZq = 512;         // projections of a token prefetched up to n
 
 // (one CTA per SM: capped at 64 registers for two, the spilling build faulted
 // intermittently in the bench -- kept uncapped)
-__global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs a) {
-    __shared__ RouteSmem<kDecRT> sm;
+// kRT = 512 (one CTA per SM) for a handful of tokens; 256 (two per SM, half the waves)
+// when the grid is many CTAs deep
+template <int kRT>
+__global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRouteArgs a) {
+    __shared__ RouteSmem<kRT> sm;
     __shared__ float sc[64];
     __shared__ double ex[64];
     __shared__ int pick_k[64];
@@ -1796,6 +1802,8 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
     __shared__ float s_z[kDecMaxTopK][64];
     __shared__ __align__(16) __half s_x16[kDecStage16];
     __shared__ float s_zq[kDecZq];
+    __shared__ int s_eq[64], s_qt[64];           // e -> tile column, column -> descale tier (last CTA)
+    __shared__ float s_zs[64];                   // e -> zscale
     const int b = blockIdx.x;
     const int K = a.num_experts;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1804,7 +1812,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
     const int y = blockIdx.y;
     rtrace(a, 0);
     if (y < nslices) {
-        const unsigned und = route_slice<kDecRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts,
+        const unsigned und = route_slice<kRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts,
                                                  a.score_ws + static_cast<int64_t>(b) * K, sm);
         if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();
     } else {
@@ -1818,7 +1826,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
         if (a.use_lr && (tier == 0 || tier == 1)) {
             const float* s = tier == 0 ? a.scaling + static_cast<int64_t>(a.q_first[q]) * a.in_dim : nullptr;
             const int j0 = rs * kProjRows;
-            dec_project_rows<kDecRT>(xb, s, a.in_dim, a.vcodes + (static_cast<int64_t>(q) * a.rank + j0) * a.in_dim,
+            dec_project_rows<kRT>(xb, s, a.in_dim, a.vcodes + (static_cast<int64_t>(q) * a.rank + j0) * a.in_dim,
                                      a.vscale + q * a.rank + j0, min(kProjRows, a.rank - j0),
                                      a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank + j0,
                                      reinterpret_cast<float*>(sm.prod));
@@ -1855,7 +1863,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
         pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
     }
     const int w0 = a.given ? 0 : 1;   // first warp free of the pick
-    for (int g = warp - w0; a.use_main && g >= 0 && g < a.groups; g += kDecRT / 32 - w0) {
+    for (int g = warp - w0; a.use_main && g >= 0 && g < a.groups; g += kRT / 32 - w0) {
         float acc = 0.0f;
         const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
         for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
@@ -1865,7 +1873,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
     }
     const bool stage16 = a.use_main && a.k_pad <= kDecStage16;
     if (stage16 && warp >= w0) {
-        for (int t8 = threadIdx.x - 32 * w0; t8 < a.k_pad / 8; t8 += kDecRT - 32 * w0) {
+        for (int t8 = threadIdx.x - 32 * w0; t8 < a.k_pad / 8; t8 += kRT - 32 * w0) {
             __align__(16) __half hh[8];
 #pragma unroll
             for (int m = 0; m < 8; ++m) {
@@ -1875,10 +1883,17 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
             reinterpret_cast<int4*>(s_x16)[t8] = *reinterpret_cast<const int4*>(hh);
         }
     }
+    // small per-layer tables the tail reads per destination, staged once (no dependent
+    // global loads after the pick)
+    for (int t = threadIdx.x; t < K; t += kRT) {
+        s_eq[t] = a.e_q[t];
+        s_zs[t] = a.zscale[t];
+    }
+    for (int t = threadIdx.x; t < a.num_q; t += kRT) s_qt[t] = a.q_tier[t];
     const int nzq = a.use_lr ? a.num_q * a.rank : 0;
     if (nzq <= kDecZq) {
         const float* zi = a.zq_ws + static_cast<int64_t>(b) * nzq;
-        for (int t = threadIdx.x - 32 * w0; t >= 0 && t < nzq; t += kDecRT - 32 * w0) s_zq[t] = __ldcg(zi + t);
+        for (int t = threadIdx.x - 32 * w0; t >= 0 && t < nzq; t += kRT - 32 * w0) s_zq[t] = __ldcg(zi + t);
     }
     __syncthreads();
     rtrace(a, 3);
@@ -1919,17 +1934,17 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
         for (int t = 0; t < k; ++t) {
             const int e = s_e[t];
             if (e < 0) continue;   // block-uniform
-            const int q = a.e_q[e];
+            const int q = s_eq[e];
             RT_CHECK(q >= 0 && q < a.num_q, "e %d q %d\n", e, q);
-            if (a.q_tier[q] == 2) {
-                dec_project<kDecRT>(xb, a.scaling + static_cast<int64_t>(e) * a.in_dim, a.in_dim,
+            if (s_qt[q] == 2) {
+                dec_project<kRT>(xb, a.scaling + static_cast<int64_t>(e) * a.in_dim, a.in_dim,
                                     a.vcodes + static_cast<int64_t>(q) * a.rank * a.in_dim, a.vscale + q * a.rank,
                                     a.rank, s_z[t], reinterpret_cast<float*>(sm.prod));
             } else if (nzq <= kDecZq) {
-                for (int j = threadIdx.x; j < a.rank; j += kDecRT) s_z[t][j] = s_zq[q * a.rank + j];
+                for (int j = threadIdx.x; j < a.rank; j += kRT) s_z[t][j] = s_zq[q * a.rank + j];
             } else {
                 const float* zi = a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank;
-                for (int j = threadIdx.x; j < a.rank; j += kDecRT) s_z[t][j] = __ldcg(zi + j);
+                for (int j = threadIdx.x; j < a.rank; j += kRT) s_z[t][j] = __ldcg(zi + j);
             }
         }
     }
@@ -1941,7 +1956,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
         return reinterpret_cast<int4*>(base + ((static_cast<int64_t>(at) * a.atom_rows + row) * 64 + ((ch ^ (row & 7)) << 3)));
     };
     if (a.use_main) {
-        for (int t8 = threadIdx.x; t8 < a.k_pad / 8; t8 += kDecRT) {
+        for (int t8 = threadIdx.x; t8 < a.k_pad / 8; t8 += kRT) {
             int4 v;
             if (stage16) {
                 v = reinterpret_cast<const int4*>(s_x16)[t8];
@@ -1965,7 +1980,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
     // ---- extension rows [Sx | Z * zscale_e | 0] ----
     const int n8 = a.ext_cols / 8;
     RT_CHECK(nd <= kDecMaxTopK + 64 && n8 <= 64, "nd %d n8 %d\n", nd, n8);
-    for (int idx = threadIdx.x; idx < nd * n8; idx += kDecRT) {
+    for (int idx = threadIdx.x; idx < nd * n8; idx += kRT) {
         const int d = idx / n8, t8 = idx % n8;
         const int row = s_row[d];
         if (row < 0) continue;
@@ -1978,7 +1993,7 @@ __global__ void __launch_bounds__(kDecRT, 1) dec_route_kernel(const DecRouteArgs
             if (col < a.groups) {
                 if (a.use_main) v = s_sx[col];
             } else if (col < a.groups + a.rank) {
-                if (a.use_lr && e >= 0) v = s_z[d][col - a.groups] * a.zscale[e];
+                if (a.use_lr && e >= 0) v = s_z[d][col - a.groups] * s_zs[e];
             }
             h[m] = __float2half_rn(v);
         }
@@ -2284,8 +2299,12 @@ cudaError_t launch_dec_route(const DecRouteArgs& a, cudaStream_t stream) {
     const int nslices = a.given ? 0 : (a.num_experts + kRouteExperts - 1) / kRouteExperts;
     const int ny = nslices + a.num_q * ((a.rank + kProjRows - 1) / kProjRows);
     if (ny < 1) return cudaErrorInvalidValue;
-    max_carveout(dec_route_kernel);
-    return launch_maybe_pdl(dec_route_kernel, dim3(a.batch, ny), dim3(kDecRT), 0, stream, a);
+    if (a.batch * ny > 2 * 148) {
+        max_carveout(dec_route_kernel<256>);
+        return launch_maybe_pdl(dec_route_kernel<256>, dim3(a.batch, ny), dim3(256), 0, stream, a);
+    }
+    max_carveout(dec_route_kernel<kDecRT>);
+    return launch_maybe_pdl(dec_route_kernel<kDecRT>, dim3(a.batch, ny), dim3(kDecRT), 0, stream, a);
 }
 
 cudaError_t launch_dec_combine(const DecCombineArgs& a, cudaStream_t stream) {

@@ -101,11 +101,18 @@ __global__ void __launch_bounds__(128) dequant_all_kernel(const DequantAllArgs a
         if (col0 >= a.i) break;
         const int g = col0 / a.group_size;   // a 32-column super-word lies in one group (group_size % 32 == 0)
         const uint16_t sb = a.scales[(wm * a.groups + g) * kBM + r];
-        uint32_t words[BITS];
-#pragma unroll
-        for (int q = 0; q < BITS; ++q) words[q] = blk[(h * BITS + q) * kBM + r];
         uint32_t v[16];
-        dequant32<BITS>(words, make_dq(__ushort_as_half(sb)), v);
+        if constexpr (BITS == kDenseBits) {
+            // codebook residuals resolved to fp16 weights at load: the block IS the weights
+            (void)sb;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) v[q] = blk[(h * 16 + q) * kBM + r];
+        } else {
+            uint32_t words[BITS];
+#pragma unroll
+            for (int q = 0; q < BITS; ++q) words[q] = blk[(h * BITS + q) * kBM + r];
+            dequant32<BITS>(words, make_dq(__ushort_as_half(sb)), v);
+        }
         // ext column g (block g/64): u32 word ((g%64)/32*16 + (g%32)/2) of row r, half g%2
         const int gb = g >> 6, gc = g & 63;
         const uint16_t zb = ext[static_cast<int64_t>(gb) * (code_block_bytes(kDenseBits) / 2) +
@@ -153,6 +160,7 @@ cudaError_t launch_dequant_all(const DequantAllArgs& a, int bits, cudaStream_t s
         case 3: dequant_all_kernel<3><<<grid, 128, 0, stream>>>(a); break;
         case 4: dequant_all_kernel<4><<<grid, 128, 0, stream>>>(a); break;
         case 8: dequant_all_kernel<8><<<grid, 128, 0, stream>>>(a); break;
+        case kDenseBits: dequant_all_kernel<kDenseBits><<<grid, 128, 0, stream>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -496,6 +496,40 @@ void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t*
     }
 }
 
+// Codebook residual -> dense fp16 blocks in the engine's [mb][kc] layout: word
+// (h * 16 + j) of row r of a 64-K block holds columns 32 h + 2 j, + 1 (the layout of
+// the extension / projection blocks).
+// W[r, c] = codebook[code(r, c / sub_dim)][c % sub_dim] (dequantize, quant.cpp:303-321).
+void repack_vq(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out, uint8_t* zeros_out,
+               int* k_out) {
+    const size_t sd = q.sub_dim, subs = (static_cast<size_t>(g.i) + sd - 1) / sd;
+    const std::vector<uint32_t> codes = unpack_stream(q.packed, q.bits, static_cast<size_t>(g.o) * subs, "codes");
+    *k_out = 0;
+    auto val = [&](int64_t row, int64_t col) -> uint32_t {
+        if (row >= g.o || col >= g.i) return 0u;
+        const uint32_t c = codes[static_cast<size_t>(row) * subs + static_cast<size_t>(col) / sd];
+        return q.codebook[static_cast<size_t>(c) * sd + static_cast<size_t>(col) % sd];
+    };
+    const int blk = code_block_bytes(kDenseBits);
+    for (int64_t mb = 0; mb < g.mb_count; ++mb) {
+        for (int64_t kc = 0; kc < g.kc_total; ++kc) {
+            uint32_t* block = reinterpret_cast<uint32_t*>(codes_out + (mb * g.kc_total + kc) * blk);
+            for (int h = 0; h < 2; ++h)
+                for (int j = 0; j < 16; ++j)
+                    for (int rl = 0; rl < kBM; ++rl) {
+                        const int64_t row = mb * kBM + rl, c0 = kc * kKC + 32 * h + 2 * j;
+                        block[(h * 16 + j) * kBM + rl] = val(row, c0) | (val(row, c0 + 1) << 16);
+                    }
+        }
+        for (int64_t gi = 0; gi < g.G; ++gi)
+            for (int rl = 0; rl < kBM; ++rl) {
+                const size_t dst = static_cast<size_t>((mb * g.G + gi) * kBM + rl);
+                scales_out[dst] = mb * kBM + rl < g.o ? 0x3C00u : 0u;   // 1.0
+                zeros_out[dst] = 0;
+            }
+    }
+}
+
 }  // namespace tqb
 
 using namespace tqb;
@@ -540,6 +574,8 @@ struct tq_layer {
     DBuf lay_U, lay_right, lay_proj1d, lay_sigma, lay_dq;
     bool lay_ready[4] = {false, false, false, false};
     int num_sms = 148;
+    bool vq = false;                    // codebook residuals, expanded to fp16 weight blocks at load
+    int art_bits = 0;                   // residual code width as stored in the artifact
     // expert-GEMM device timing (tq_gemm_timing_enable)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -1068,11 +1104,15 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
     for (const QMat& m : a.shared)
         if (m.bits != q0.bits || m.vec != q0.vec || m.gs != q0.gs || m.sub_dim != q0.sub_dim)
             fail(TQ_ERR_PARAM, "shared experts must use the routed experts' bits/group_size on the GPU engine");
-    if (q0.vec)
-        fail(TQ_ERR_PARAM, "tensor 'expert.0.codes': vector-quantized residuals (codebook mode) are not supported by the "
-                           "GPU engine yet");
-    const int bits = q0.bits;
-    const size_t gs = q0.gs;
+    // codebook (vector) residuals, quant.cpp:303-321: every codebook entry is f16-snapped
+    // (quant.cpp:262-266), so the dequantized weights ARE fp16 values -- the loader
+    // resolves each code through its expert's codebook into exact fp16 weight blocks,
+    // streamed by the dense (kDenseBits) weight path; unit scales, no zero points
+    const bool vq = q0.vec;
+    L->vq = vq;
+    L->art_bits = q0.bits;
+    const int bits = vq ? kDenseBits : q0.bits;
+    const size_t gs = vq ? 128 : q0.gs;
     std::vector<QMat> q;
     for (int64_t e = e_begin; e < e_end; ++e) q.push_back(std::move(a.routed[static_cast<size_t>(e)]));
     for (auto& m : a.shared) q.push_back(std::move(m));
@@ -1112,8 +1152,12 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
             pool.emplace_back([&] {
                 for (size_t w = next++; w < q.size(); w = next++) {
                     try {
-                        repack_qmat(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
-                                    h_zeros.data() + w * slab, &wk[w]);
+                        if (vq)
+                            repack_vq(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
+                                      h_zeros.data() + w * slab, &wk[w]);
+                        else
+                            repack_qmat(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
+                                        h_zeros.data() + w * slab, &wk[w]);
                     } catch (const std::exception& e) {
                         errs[w] = e.what();
                     }
@@ -1647,7 +1691,7 @@ bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
     }();
     const Geometry& g = L->g;
     const int64_t slots = given ? batch * g.top_k : batch;
-    return !off && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
+    return !off && !L->vq && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
            g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64 && g.n_ext <= 4;
 }
 
@@ -1948,7 +1992,7 @@ tq_status tq_layer_info_get(const tq_layer* L, tq_layer_info* out) {
         out->rank = L->g.r;
         out->grid_rows = L->g.M;
         out->grid_cols = L->g.N;
-        out->bits = L->g.bits;
+        out->bits = L->vq ? L->art_bits : L->g.bits;
         out->group_size = L->g.gs;
         out->expert_begin = L->e_begin;
         out->expert_end = L->e_end;
@@ -2378,6 +2422,7 @@ tq_status tq_layer_export_codes(tq_layer* L, int64_t e, uint32_t* out, void* str
     return guarded([&] {
         check_layer(L);
         if (e < 0 || e >= L->n_weights) fail(TQ_ERR_PARAM, "export: matrix index out of range");
+        if (L->vq) fail(TQ_ERR_PARAM, "export: codebook residuals are resolved to fp16 weights at load; no codes kept");
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cuda_check(launch_export_codes(L->codes.as<uint8_t>() + e * L->weight_stride, L->g.bits,
                                        static_cast<int>(L->g.kc_total), static_cast<int>(L->g.o),

@@ -300,3 +300,21 @@ def test_layer_load_reports_host_errors_before_device(tq, tmp_path):
         tq.Layer(str(d))
     with pytest.raises(tq.IoError):
         tq.Layer(str(tmp_path / "missing"))
+
+
+def test_vector_quantized_artifact_is_read(tq, refl, tmp_path):
+    """Codebook residuals (io.cpp:464-480): codes o x ceil(i / sub_dim) and a
+    2^bits x sub_dim binary16 codebook per expert; a codebook of the wrong
+    shape is a FormatError naming it, like the reference's reader."""
+    if refl is None:
+        pytest.skip("reference library not built")
+    d = tmp_path / "vq"
+    refl.make_artifact(str(d), K=4, top_k=2, i=128, o=64, S=1, r=4, bits=2, g=128, calib="gauss", seed=5,
+                       quantizer="vq", sub_dim=2)
+    tq.artifact_check(str(d))
+    refl.load(str(d))
+    m = _manifest(d)
+    assert m["meta"]["quant"]["mode"] == "vector"
+    m["tensors"]["expert.1.codebook"]["shape"] = [8, 1]      # same byte length, wrong shape
+    _write_manifest(d, m)
+    _expect(tq, refl, d, FORMAT, "expert.1.codebook")

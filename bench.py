@@ -328,6 +328,9 @@ def bench_tileq(args, rank, world, local_rank):
         import torch.distributed as dist
         from paper_2605_09281_b200.ep import EPLayer
         ep = EPLayer(art, device=local_rank)
+        if args.workload == "decode":
+            # fixed-capacity exchange (equal splits, device-side counts): no host round trip
+            ep.slab = max(DECODE_BATCHES) * ep.top_k
         L = ep.stages
         fwd = lambda x, out: ep.forward(x, out=out)  # noqa: E731
     else:

@@ -292,6 +292,16 @@ tq_status tq_ep_expert_rows(tq_layer* layer, const uint16_t* xrows, const uint16
 
 /* Combine returned rows (in permuted-slot order) with the gates plus the
  * shared experts applied to the home tokens: y [dev] f32 batch x out_dim. */
+/* Expert outputs for rows received in FIXED-CAPACITY slabs (decode-sized expert
+ * parallel, equal-split all-to-alls, no host round trip): rows [dev] fp16
+ * [n_src * slab][row_ld], each row [x (tq_ep_xrow_elems) | ext (tq_ep_extrow_elems)];
+ * source s's rows for local expert j start at s * slab + sum_{j' < j} counts[s][j'];
+ * counts [dev] int32 [n_src][e_stride] (the received count matrix).  Work units are
+ * built on the device from counts; yrows [dev] f32 [n_src * slab][out_dim] (rows past
+ * a source's count are not written).  Stream-ordered, no synchronization. */
+tq_status tq_ep_expert_rows_slab(tq_layer* layer, const uint16_t* rows, int64_t row_ld, int64_t n_src, int64_t slab,
+                                 const int32_t* counts, int64_t e_stride, float* yrows, int path, void* stream);
+
 tq_status tq_ep_combine(tq_layer* layer, const float* x, int64_t batch, const float* yrows,
                         const int32_t* inv, const float* gates, float* y, int path,
                         void* stream);

@@ -135,6 +135,7 @@ def lib() -> C.CDLL:
     L.tq_ep_dispatch_rows.argtypes = [p, p, i64, p, p, p, p, i32, p]
     L.tq_ep_expert_rows.argtypes = [p, p, p, i64, p, i64, p, i32, p]
     L.tq_ep_combine.argtypes = [p, p, i64, p, p, p, p, i32, p]
+    L.tq_ep_expert_rows_slab.argtypes = [p, p, i64, i64, i64, p, i64, p, i32, p]
     L.tq_gemm_timing_enable.argtypes = [p, i32]
     L.tq_gemm_time_get.argtypes = [p, C.POINTER(C.c_double), C.POINTER(i64)]
     L.tq_layout_prepare.argtypes = [p, i32]
@@ -147,7 +148,7 @@ def lib() -> C.CDLL:
     for name in ("tq_layer_load", "tq_artifact_check", "tq_layer_create", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
                  "tq_sync", "tq_debug_decode_counters", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
-                 "tq_ep_expert_rows", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):
+                 "tq_ep_expert_rows", "tq_ep_expert_rows_slab", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
@@ -434,6 +435,17 @@ class Layer:
         if rows and len(seg):
             check(lib().tq_ep_expert_rows(self._h, xrows.data_ptr(), erows.data_ptr(), rows, seg.ctypes.data,
                                           len(seg), y.data_ptr(), _PATHS[path], _stream_ptr(xrows.device)))
+        return y
+
+    def ep_expert_rows_slab(self, rows, n_src: int, slab: int, counts, path: str = "full"):
+        """Resident-expert outputs for rows received in fixed-capacity slabs (no host
+        round trip): rows fp16 [n_src * slab, xw + ew] = [x | ext]; counts int32
+        [n_src, e_stride] the received count matrix (device).  f32 [n_src * slab, o]."""
+        torch = _torch()
+        y = torch.empty((n_src * slab, self.out_dim), dtype=torch.float32, device=rows.device)
+        cnt = counts.to(device=rows.device, dtype=torch.int32).contiguous()
+        check(lib().tq_ep_expert_rows_slab(self._h, rows.data_ptr(), rows.shape[1], n_src, slab, cnt.data_ptr(),
+                                           cnt.shape[1], y.data_ptr(), _PATHS[path], _stream_ptr(rows.device)))
         return y
 
     def ep_combine(self, x, yrows, inv, gates, path: str = "full", out=None):

@@ -242,6 +242,14 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
         h->wt_first[W] = acc;
         for (int w = W + 1; w <= kDecMaxW; ++w) h->wt_first[w] = 0x7fffffff;
         h->n_wt = acc;
+#ifdef TQ_DEC_CHECK
+        {
+            int slots = 0;
+            for (int w = 0; w < p.num_experts; ++w) slots += p.cnt[w];
+            DEC_CHECK(p.check_slots <= 0 || slots == p.check_slots, "routed slots %d, expected %d (batch %d)\n", slots,
+                      p.check_slots, p.batch);
+        }
+#endif
     }
     if (wid == kCProd) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&h->tmem_base)),

@@ -245,6 +245,7 @@ struct DecParams {
     int code_stages, x_stages, code_stage_bytes;   // set by launch_decode
     unsigned long long* trace;       // TQ_DEC_TRACE builds only
     int trace_cta;
+    int check_slots;                 // TQ_DEC_CHECK builds: expected routed slots (batch * top_k)
 };
 
 struct DecCombineArgs {

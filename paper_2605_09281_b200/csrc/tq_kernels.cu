@@ -164,7 +164,13 @@ __device__ unsigned route_slice(const float* __restrict__ xb, int in_dim, const 
         }
         __syncthreads();
     }
-    if (sm.und != 0u) {   // block-uniform
+    // every thread takes its copy of the undecided mask BEFORE thread 0 clears it for
+    // tier 2 (reading sm.und in the condition itself raced with that clear: a late
+    // thread saw 0, skipped tier 2 and its barriers, and the CTA's barrier phases
+    // fell apart -- the intermittent decode-router fault)
+    const unsigned und1 = sm.und;
+    __syncthreads();
+    if (und1 != 0u) {   // block-uniform
     if (threadIdx.x == 0) sm.und = 0u;
     __syncthreads();
     // ---- tier 2: the partial sums of the reference's order ----
@@ -2015,6 +2021,13 @@ __global__ void __launch_bounds__(256) dec_combine_kernel(const DecCombineArgs a
         const int64_t f = static_cast<int64_t>(b) * a.top_k + threadIdx.x;
         s_row[threadIdx.x] = a.inv[f];
         s_gate[threadIdx.x] = a.gates[f];
+#ifdef TQ_DEC_CHECK
+        if (s_row[threadIdx.x] >= (a.num_experts + a.num_shared) * a.cap8) {
+            printf("DEC_CHECK combine: token %d t %d row %d >= %d\n", b, threadIdx.x, s_row[threadIdx.x],
+                   (a.num_experts + a.num_shared) * a.cap8);
+            __trap();
+        }
+#endif
     }
     __syncthreads();
     const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -2283,6 +2296,61 @@ cudaError_t launch_unpack(const uint8_t* bytes, int64_t nbytes, int bits, int64_
     return cudaGetLastError();
 }
 
+// Expert-parallel receive side, fixed-capacity slabs: work units built on the device
+// from the received per-(source, local expert) row counts -- no host round trip.
+// Source s's rows start at s * slab, its experts' rows follow each other in expert
+// order; every (segment, m-block, token tile) becomes one Unit, in segment order.
+__global__ void __launch_bounds__(1024) ep_units_kernel(const int32_t* __restrict__ counts, int n_src, int e_stride,
+                                                       int n_local, int slab, int mb_count, int bn, int kc_end,
+                                                       int n_ext, Unit* __restrict__ units, int32_t* __restrict__ n_units) {
+    __shared__ int s_nu[1024];
+    const int nseg = n_src * n_local;
+    const int t = threadIdx.x;
+    int r0 = 0, cnt = 0, nu = 0, s = 0, j = 0;
+    if (t < nseg) {
+        s = t / n_local;
+        j = t % n_local;
+        r0 = s * slab;
+        for (int jj = 0; jj < j; ++jj) r0 += counts[s * e_stride + jj];
+        cnt = counts[s * e_stride + j];
+        nu = mb_count * ((cnt + bn - 1) / bn);
+    }
+    s_nu[t] = nu;
+    __syncthreads();
+    // inclusive scan (Hillis-Steele) of the unit counts
+    for (int off = 1; off < 1024; off <<= 1) {
+        const int v = t >= off ? s_nu[t - off] : 0;
+        __syncthreads();
+        s_nu[t] += v;
+        __syncthreads();
+    }
+    const int base = s_nu[t] - nu;
+    if (t == 1023) *n_units = s_nu[1023];
+    int u = base;
+    for (int t0 = 0; t0 < cnt; t0 += bn)
+        for (int mb = 0; mb < mb_count; ++mb) {
+            Unit un{};
+            un.weight = j;
+            un.mb = mb;
+            un.x_row = r0 + t0;
+            un.n_tok = min(bn, cnt - t0);
+            un.y_row = un.x_row;
+            un.kc_begin = 0;
+            un.kc_end = static_cast<int16_t>(kc_end);
+            un.n_ext = static_cast<int16_t>(n_ext);
+            un.split = 0;
+            units[u++] = un;
+        }
+}
+
+cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int n_local, int slab, int mb_count, int bn,
+                            int kc_end, int n_ext, Unit* units, int32_t* n_units, cudaStream_t stream) {
+    if (n_src * n_local > 1024) return cudaErrorInvalidValue;
+    ep_units_kernel<<<1, 1024, 0, stream>>>(counts, n_src, e_stride, n_local, slab, mb_count, bn, kc_end, n_ext, units,
+                                            n_units);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream) {
     const int64_t n = static_cast<int64_t>(out_dim) * kc_total * 2;
@@ -2299,10 +2367,12 @@ cudaError_t launch_dec_route(const DecRouteArgs& a, cudaStream_t stream) {
     const int nslices = a.given ? 0 : (a.num_experts + kRouteExperts - 1) / kRouteExperts;
     const int ny = nslices + a.num_q * ((a.rank + kProjRows - 1) / kProjRows);
     if (ny < 1) return cudaErrorInvalidValue;
+#ifndef TQ_ROUTE_NO256
     if (a.batch * ny > 2 * 148) {
         max_carveout(dec_route_kernel<256>);
         return launch_maybe_pdl(dec_route_kernel<256>, dim3(a.batch, ny), dim3(256), 0, stream, a);
     }
+#endif
     max_carveout(dec_route_kernel<kDecRT>);
     return launch_maybe_pdl(dec_route_kernel<kDecRT>, dim3(a.batch, ny), dim3(kDecRT), 0, stream, a);
 }

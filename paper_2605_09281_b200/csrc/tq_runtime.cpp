@@ -52,6 +52,8 @@ cudaError_t launch_dec_combine(const DecCombineArgs& a, cudaStream_t stream);
 cudaError_t launch_decode(const DecParams& p, int dn, int grid, cudaStream_t stream);
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream);
+cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int n_local, int slab, int mb_count, int bn,
+                            int kc_end, int n_ext, Unit* units, int32_t* n_units, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // errors
@@ -381,12 +383,13 @@ EncodeTiledFn get_encode_fn() {
     return fn;
 }
 
-// fp16 row-major [rows, cols] tensor, box [box_rows, 64], 128-byte swizzle
-CUtensorMap make_map(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// fp16 row-major [rows, cols] tensor, box [box_rows, 64], 128-byte swizzle; rows
+// `ld` elements apart (0: cols)
+CUtensorMap make_map(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows, uint64_t ld = 0) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
-    const cuuint64_t strides[1] = {cols * 2};
+    const cuuint64_t strides[1] = {(ld ? ld : cols) * 2};
     const cuuint32_t box[2] = {64, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, base, dims, strides, box, estr,
@@ -555,7 +558,8 @@ struct tq_layer {
     int64_t cap = 0;
     DBuf route_ws, route_ticket, poffsets;   // router: per-(token, expert) certified scores, per-token tickets
     DBuf ids, gates, x16, sx, perm, inv, offsets, units, n_units, punits, n_punits, zpart, xperm, extperm, ypart,
-        err_flag, xin, yout, nsplit_d, hids, hgates;
+        err_flag, xin, yout, nsplit_d, hids, hgates, ep_units, ep_nunits;
+    int64_t ep_units_cap = 0;
     int64_t ypart_cap_floats = 0, zpart_cap_floats = 0;
     CUtensorMap map_x16_16{}, map_x16_64{}, map_xp16{}, map_xp64{}, map_ep16{}, map_ep64{};
     // decode path (batch <= kDecMaxBatch): route+scatter -> fused expert GEMM -> combine
@@ -620,6 +624,9 @@ struct tq_layer {
     cudaStream_t cap_stream = nullptr;
     bool use_graphs = !(getenv("TQ_GRAPHS") && atoi(getenv("TQ_GRAPHS")) == 0) && !getenv("TQ_DEBUG");  // debug dumps sync
     void drop_graphs() {
+        // an executable graph may still be running (forwards are asynchronous): wait
+        // for the device before its exec and the buffers it references are released
+        if (!graphs.empty()) cudaDeviceSynchronize();
         for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
         graphs.clear();
     }
@@ -1822,6 +1829,7 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
     dp.ldy = static_cast<int>(g.o);
     dp.scratch = L->dec_scratch.as<float>();
     dp.seg_cnt = L->dec_segcnt.as<int32_t>();
+    dp.check_slots = static_cast<int>(batch * g.top_k);
     {
         cudaEvent_t ev0 = nullptr, ev1 = nullptr;
         if (L->timing) {
@@ -2688,6 +2696,69 @@ tq_status tq_ep_expert_rows(tq_layer* L, const uint16_t* xrows, const uint16_t* 
         timed_expert_gemm(L, p, static_cast<int>(std::min<int64_t>(nu, L->num_sms)), st);
         count_launch(L);
         cuda_check(cudaStreamSynchronize(st), "stream sync");  // dunits lifetime
+    });
+}
+
+tq_status tq_ep_expert_rows_slab(tq_layer* L, const uint16_t* rows, int64_t row_ld, int64_t n_src, int64_t slab,
+                                 const int32_t* counts, int64_t e_stride, float* yrows, int path, void* stream) {
+    return guarded([&] {
+        check_layer(L);
+        if (path < 0 || path > 2) fail(TQ_ERR_PARAM, "unknown path " + std::to_string(path));
+        const Geometry& g = L->g;
+        const int64_t local = L->e_end - L->e_begin;
+        if (n_src < 1 || slab < 0 || e_stride < local) fail(TQ_ERR_SHAPE, "slab layout: bad source count / capacity / stride");
+        if (row_ld < g.k_pad + g.ext_cols || (row_ld % 8) != 0)
+            fail(TQ_ERR_SHAPE, "slab rows hold [x (" + std::to_string(g.k_pad) + ") | ext (" +
+                                   std::to_string(g.ext_cols) + ")] fp16, 16-byte aligned");
+        if (n_src * local > 1024) fail(TQ_ERR_PARAM, "slab layout: at most 1024 (source, expert) segments");
+        if (slab == 0 || local == 0) return;
+        cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const LaunchCfg cf = cfg64(L);
+        // units on the device: capacity for the worst split of slab rows over the experts
+        const int64_t cap = n_src * (local * g.mb_count + g.mb_count * ((slab + cf.bn - 1) / cf.bn));
+        if (cap > L->ep_units_cap) {
+            L->ep_units.alloc(sizeof(Unit) * cap);
+            L->ep_nunits.alloc(sizeof(int32_t));
+            L->ep_units_cap = cap;
+        }
+        const bool use_qmoe = path != TQ_PATH_LOTILE;
+        cuda_check(launch_ep_units(counts, static_cast<int>(n_src), static_cast<int>(e_stride), static_cast<int>(local),
+                                   static_cast<int>(slab), static_cast<int>(g.mb_count), cf.bn,
+                                   use_qmoe ? cf.kc_total : 0, cf.n_ext, L->ep_units.as<Unit>(),
+                                   L->ep_nunits.as<int32_t>(), st),
+                   "ep units");
+        count_launch(L);
+        const int64_t nrows = n_src * slab;
+        GemmParams p = base_params(L, cf, cf.bn);
+        void* xr = const_cast<uint16_t*>(rows);
+        void* er = const_cast<uint16_t*>(rows + g.k_pad);
+        p.tmap_x64 = make_map(xr, nrows, g.k_pad, 64, row_ld);
+        p.tmap_e64 = make_map(er, nrows, g.ext_cols, 64, row_ld);
+        p.tmap_x16 = make_map(xr, nrows, g.k_pad, 16, row_ld);
+        p.tmap_e16 = make_map(er, nrows, g.ext_cols, 16, row_ld);
+        p.x_ptr = static_cast<const __half*>(xr);
+        p.x_ld = row_ld;
+        p.e_ptr = static_cast<const __half*>(er);
+        p.e_ld = row_ld;
+        p.codes = L->codes.as<uint8_t>();
+        p.weight_stride = L->weight_stride;
+        p.scales = L->scales.as<__half>();
+        p.ext_blocks = L->ext_blocks.as<uint8_t>();
+        p.n_ext64 = static_cast<int32_t>(g.n_ext);
+        p.w_outscale = L->w_outscale.as<float>();
+        p.units = L->ep_units.as<Unit>();
+        p.n_units = L->ep_nunits.as<int32_t>();
+        p.y = yrows;
+        p.y_split_stride = 0;
+        p.ldy = static_cast<int32_t>(g.o);
+        p.o_valid = static_cast<int32_t>(g.o);
+        p.o_pad = static_cast<int32_t>(g.o_pad);
+        p.bits = g.bits;
+        p.groups = static_cast<int32_t>(g.G);
+        p.rank = static_cast<int32_t>(g.r);
+        timed_expert_gemm(L, p, L->num_sms, st);
+        count_launch(L);
     });
 }
 

@@ -140,7 +140,7 @@ class EPLayer:
     """
 
     def __init__(self, artifact_dir: Optional[str] = None, comm=None, device: Optional[int] = None,
-                 stages=None, num_experts: Optional[int] = None, path: str = "full"):
+                 stages=None, num_experts: Optional[int] = None, path: str = "full", slab: Optional[int] = None):
         self.comm = comm if comm is not None else TorchComm()
         W, r = self.comm.world, self.comm.rank
         if stages is None:
@@ -167,6 +167,11 @@ class EPLayer:
         self.in_dim = stages.in_dim
         self.path = path
         self.e_begin, self.e_end = self.bounds[r], self.bounds[r + 1]
+        # slab: fixed per-destination row capacity (decode sizes).  Every all-to-all then
+        # has equal, host-known splits and the receive side builds its work units from
+        # the device-resident counts: a forward with no host round trip.  All ranks
+        # must agree on it (and on B * top_k <= slab).
+        self.slab = slab
 
     # -- phases (usable one by one by an emulator that steps several ranks) --
     def phase_dispatch(self, x):
@@ -188,9 +193,53 @@ class EPLayer:
     def phase_combine(self, pend: _Pending, yback, out=None):
         return self.stages.ep_combine(pend.x, yback, pend.inv, pend.gates, self.path, out=out)
 
+    # -- fixed-capacity (slab) phases: no host round trip -------------------
+    def slab_dispatch(self, x):
+        """route + permute + rows into the [W * slab, xw + ew] send buffer.  Returns
+        (pending state, send buffer, [W, E_max] int32 count matrix, slot -> slab index)."""
+        import torch
+        S, W, C, k = self.stages, self.comm.world, self.slab, self.top_k
+        B = x.shape[0]
+        if B * k > C:
+            from . import ShapeError
+            raise ShapeError(f"expert parallel slab: {B} tokens x top_k {k} exceed the slab capacity {C}")
+        dev = x.device
+        ids, gates = S.route(x)
+        perm, offsets, inv = S.permute(ids)
+        xrows, erows = S.ep_dispatch_rows(x, ids, perm, self.path)
+        xw, ew = xrows.shape[1], erows.shape[1]
+        off = offsets.to(dev).long()
+        starts = off[torch.tensor(self.bounds, device=dev)]           # first permuted slot per destination
+        pos = torch.arange(B * k, device=dev)
+        dest = torch.searchsorted(starts[1:].contiguous(), pos, right=True)
+        idx = dest * C + (pos - starts[dest])
+        send = torch.zeros((W * C, xw + ew), dtype=xrows.dtype, device=dev)
+        send[idx, :xw] = xrows
+        send[idx, xw:] = erows.to(xrows.dtype)
+        emax = max(self.bounds[d + 1] - self.bounds[d] for d in range(W))
+        ej = torch.tensor([[self.bounds[d] + j if self.bounds[d] + j < self.bounds[d + 1] else -1 for j in range(emax)]
+                           for d in range(W)], device=dev)
+        per_e = off[1:] - off[:-1]
+        counts = torch.where(ej >= 0, per_e[ej.clamp(min=0)], torch.zeros_like(ej)).to(torch.int32)
+        pend = _Pending(x, ids, gates, inv, None, None)
+        return pend, send, counts, idx, xw
+
+    def forward_slab(self, x, out=None):
+        import torch
+        c, C, W = self.comm, self.slab, self.comm.world
+        pend, send, counts, idx, xw = self.slab_dispatch(x)
+        recv_counts = c.all_to_all_counts(counts)
+        recv = c.all_to_all_rows(send, [C] * W, [C] * W)
+        y = self.stages.ep_expert_rows_slab(recv, W, C, recv_counts, self.path)
+        yback = c.all_to_all_rows(y, [C] * W, [C] * W)
+        inv_slab = idx[pend.inv.to(idx.device).long()].to(torch.int32)
+        return self.stages.ep_combine(pend.x, yback, inv_slab, pend.gates, self.path, out=out)
+
     # -- the collective forward ----------------------------------------------
     def forward(self, x, out=None):
         """y = tileq_forward(x) for this rank's tokens, experts computed where they live."""
+        if self.slab is not None:
+            return self.forward_slab(x, out=out)
         c = self.comm
         pend, xrows, erows, counts = self.phase_dispatch(x)
         cdev = counts.to(xrows.device)
@@ -232,4 +281,25 @@ def emulate_forward(layers: list, xs: list):
             off = int(per_src[:s].sum())
             parts.append(y[off:off + int(per_src[s])])
         outs.append(layers[s].phase_combine(st[s][0], torch.cat(parts)))
+    return outs
+
+
+def emulate_forward_slab(layers: list, xs: list):
+    """emulate_forward for the fixed-capacity (slab) path: the same exchange with
+    equal splits, moved by tensor slicing in one process."""
+    import torch
+    W = len(layers)
+    C = layers[0].slab
+    st = [l.slab_dispatch(x) for l, x in zip(layers, xs)]
+    ys = []
+    for d in range(W):
+        recv = torch.cat([st[s][1][d * C:(d + 1) * C] for s in range(W)])
+        rc = torch.stack([st[s][2][d] for s in range(W)])
+        ys.append(layers[d].stages.ep_expert_rows_slab(recv, W, C, rc, layers[d].path))
+    outs = []
+    for s in range(W):
+        yback = torch.cat([ys[d][s * C:(s + 1) * C] for d in range(W)])
+        pend, idx = st[s][0], st[s][3]
+        inv_slab = idx[pend.inv.to(idx.device).long()].to(torch.int32)
+        outs.append(layers[s].stages.ep_combine(pend.x, yback, inv_slab, pend.gates, layers[s].path))
     return outs

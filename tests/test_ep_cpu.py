@@ -61,6 +61,20 @@ class OracleStages:
             y[r0:r0 + n] = torch.from_numpy(a.astype(np.float64) + b)
         return y
 
+    def ep_expert_rows_slab(self, rows, n_src, slab, counts, path):
+        # the checker's rows are [x (in_dim f32) | (token, expert)]: split, rebuild the
+        # (source, expert) segments from the received counts, reuse ep_expert_rows
+        xw = self.in_dim
+        cnt = counts.numpy()
+        segs = []
+        for s in range(n_src):
+            r = s * slab
+            for j in range(cnt.shape[1]):
+                if self.e_begin + j < self.e_end and cnt[s, j]:
+                    segs.append((j, r, int(cnt[s, j])))
+                r += int(cnt[s, j])
+        return self.ep_expert_rows(rows[:, :xw], rows[:, xw:], segs, path)
+
     def ep_combine(self, x, yrows, inv, gates, path, out=None):
         B = x.shape[0]
         k = self.top_k
@@ -84,7 +98,7 @@ def _art(tmpdir):
     return d
 
 
-def _worker(rank, world, port, art_dir, batches, q):
+def _worker(rank, world, port, art_dir, batches, q, slab=None):
     import sys
     sys.path.insert(0, REPO)
     sys.path.insert(0, os.path.join(REPO, "tests"))
@@ -98,11 +112,11 @@ def _worker(rank, world, port, art_dir, batches, q):
         comm = TorchComm()
         from paper_2605_09281_b200.ep import expert_bounds
         b = expert_bounds(art["K"], world)
-        ep = EPLayer(comm=comm, stages=OracleStages(o, art, b[rank], b[rank + 1]))
+        ep = EPLayer(comm=comm, stages=OracleStages(o, art, b[rank], b[rank + 1]), slab=slab)
         errs = []
         for B in batches:
             # ranks hold different token counts (ragged, including empty)
-            Br = B + 3 * rank if B else 0
+            Br = (B + 3 * rank if B else 0) if slab is None else B
             x = np.random.default_rng(1000 * rank + B).standard_normal((Br, art["i"])).astype(np.float32)
             y = ep.forward(torch.from_numpy(x)).numpy()
             want = o.tileq_forward(art, x)[0] if Br else np.zeros((0, art["o"]), np.float32)
@@ -132,6 +146,27 @@ def test_ep_gloo_matches_oracle(oracle_built, tmp_path_factory, world):
     q = ctx.Queue()
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, art_dir, [1, 5, 0, 40], q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        for Br, err, shape_ok in res[r]:
+            assert shape_ok
+            assert err <= 1e-5, (r, Br, err)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ep_gloo_slab_matches_oracle(oracle_built, tmp_path_factory, world):
+    """Fixed-capacity (slab) exchange: equal-split all-to-alls, receive-side
+    segments from the exchanged count matrix -- no host round trip on GPUs."""
+    art_dir = _art(str(tmp_path_factory.mktemp("ep_slab")))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, art_dir, [1, 5, 16], q, 40)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(world))

@@ -335,6 +335,26 @@ def test_ep_stages_emulated_ranks(tq, golden, name, world):
         assert rel_frob(y.cpu().numpy(), golden[f"{name}/tileq{B}"]) <= TOL, (B, world)
 
 
+@pytest.mark.parametrize("name", ["general_b2_shared", "scalar_b4_ragged"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_ep_slab_emulated_ranks(tq, golden, name, world):
+    """The fixed-capacity (slab) expert-parallel path -- equal-split exchanges,
+    work units built on the device from the received count matrix
+    (tq_ep_expert_rows_slab), no host round trip -- for W emulated ranks."""
+    import torch
+    from paper_2605_09281_b200.ep import EPLayer, emulate_forward_slab, expert_bounds
+    d = os.path.join(GOLD, name)
+    full = tq.Layer(d)
+    b = expert_bounds(full.num_experts, world)
+    B = 7
+    layers = [EPLayer(comm=_RankComm(r, world), num_experts=full.num_experts, slab=B * full.top_k,
+                      stages=tq.Layer(d, expert_range=(b[r], b[r + 1]))) for r in range(world)]
+    xs = [torch.from_numpy(golden[f"{name}/x{B}"]).cuda() for _ in range(world)]
+    ys = emulate_forward_slab(layers, xs)
+    for y in ys:
+        assert rel_frob(y.cpu().numpy(), golden[f"{name}/tileq{B}"]) <= TOL, world
+
+
 @pytest.mark.parametrize("B", [1, 8])
 def test_lotile_path_many_units_per_cta(tq, ref, make_artifact, B):
     """lotile_forward alone at a shape where each CTA holds several ext-only

@@ -1,0 +1,1 @@
+TQ_LIB_PATH=$PWD/paper_2605_09281_b200/libtileq_b200_tq_dec_check.so SCAN_PATHS=full SCAN_BATCHES=12,16,24,31,32 timeout 300 python tools/gpu_stress_scan.py 2>&1 | grep -vE "^ +|Traceback" | head -12

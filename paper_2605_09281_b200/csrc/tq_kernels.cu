@@ -855,6 +855,11 @@ __global__ void __launch_bounds__(kTThreads, 2) route_tile_kernel(const float* _
     __shared__ int n_t3;
     __shared__ int t3[kTT * 64];
     if (threadIdx.x == 0) n_t3 = 0;
+    // the tier-3 count must be cleared for every warp before any reads it: with no
+    // tier-2 score the loop below has no barrier, and a warp reading a stale n_t3
+    // walked a stale t3[] list into wild addresses (the token-tile router's
+    // intermittent illegal address)
+    __syncthreads();
     const int n_t2 = (TQ_RT_ABL & 4) ? 0 : n_und;
     for (int i = 0; i < n_t2; ++i) {
         const int pr = und[i];
@@ -2106,12 +2111,10 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
 #define TQ_ROUTE_TOKEN_CTAS (2 * 148)   // token-chunk CTAs at prefill (several tokens per CTA beyond this)
 #endif
     static const int tile_min = [] {
-        // batch from which the token-tile router runs (<= 0: never).  Off by default:
-        // it faulted with an illegal address in ~1 of 30 launches at 4096 tokens
-        // (tools/gpu_stress_repro.py; cause not found), the per-token route_kernel
-        // below passed 180 / 180 (known issues)
+        // batch from which the token-tile router runs (<= 0: never); the per-token
+        // route_kernel below serves smaller batches
         const char* e = getenv("TQ_ROUTE_TILE_MIN");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : 297;
     }();
     const bool tile_ok = !plan && num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
                          (k_pad & 3) == 0 && (!sx || (group_size > 0 && kTC % group_size == 0));

@@ -224,6 +224,10 @@ tq_status tq_debug_decode_counters(tq_layer* layer, int32_t* out, int64_t n);
 /* GPU unpack of a packed stream (codec.cpp:168-195): bytes [dev], out [dev]
  * uint32 count.  Returns TQ_ERR_PARAM on a bad width or byte count and
  * TQ_ERR_FORMAT on nonzero padding bits (after synchronizing). */
+/* Test hook: the routers' f64 exp (the softmax of route(), moe.cpp:72 std::exp)
+ * on x [dev] f64 n -> y [dev] f64, for the exp-vs-glibc parity test. */
+tq_status tq_exp_f64(const double* x, int64_t n, double* y, void* stream);
+
 tq_status tq_unpack_codes(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count,
                           uint32_t* out, void* stream);
 

@@ -16,7 +16,8 @@
 //     sequence of quantize_moe (pipeline.cpp:138-230) with the same stage
 //     seeds but skips proxy_loss (quant.cpp:325-343), which only feeds the
 //     report; the artifact bytes are unchanged (checked by
-//     tests/test_oracle.py against quantize_moe itself on a small shape).
+//     tests/test_cpu_oracle.py::test_factory_stage_replay_matches_quantize_moe
+//     against quantize_moe itself on a small shape).
 //     Inputs follow the CLI synth command (tileq_main.cpp:356-410):
 //     synth_experts + gaussian gate from derive(seed, 6) + calibration
 //     tokens from derive(seed, 5) (signs -> folded descale tier, gaussians ->

@@ -116,6 +116,7 @@ def lib() -> C.CDLL:
     L.tq_layer_load.argtypes = [C.c_char_p, i32, i32, i64, i64, C.POINTER(p)]
     L.tq_layer_free.argtypes = [p]
     L.tq_artifact_check.argtypes = [C.c_char_p, i32]
+    L.tq_exp_f64.argtypes = [p, i64, p, p]
     L.tq_layer_create.argtypes = [p, i32, i64, i64, C.POINTER(p)]
     L.tq_layer_info_get.argtypes = [p, C.POINTER(_LayerInfo)]
     L.tq_layer_reserve.argtypes = [p, i64]
@@ -145,7 +146,7 @@ def lib() -> C.CDLL:
     L.tq_ep_xrow_elems.argtypes = [p]
     L.tq_ep_extrow_elems.restype = i64
     L.tq_ep_extrow_elems.argtypes = [p]
-    for name in ("tq_layer_load", "tq_artifact_check", "tq_layer_create", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
+    for name in ("tq_layer_load", "tq_artifact_check", "tq_exp_f64", "tq_layer_create", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
                  "tq_sync", "tq_debug_decode_counters", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
                  "tq_ep_expert_rows", "tq_ep_expert_rows_slab", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get"):

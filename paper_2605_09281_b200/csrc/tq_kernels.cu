@@ -438,163 +438,6 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
 }
 
 // =============================================================================
-// route, large batches: one warp per token
-// =============================================================================
-// Same contract and certification as route_kernel (tier 1: the loose
-// any-order bound; an undecided score is replayed with the reference's exact
-// sequential loop, matrix.cpp:29-34), but one warp owns a token: no cross-CTA
-// tickets, 8 tokens per 256-thread CTA, the gate rows served from L1/L2 to all
-// warps.  Opt-in (TQ_ROUTE_WARP_MIN=<batch>): bit-exact (the GPU parity suite
-// passes with it forced on) but not faster than route_kernel at 4096 tokens.
-constexpr int kRwWarps = 8;
-constexpr int kRwExp = 8;   // experts per accumulation pass (registers: 2 x 8 f64 per lane)
-
-__global__ void __launch_bounds__(kRwWarps * 32) route_warp_kernel(const float* __restrict__ x, int batch, int in_dim,
-                                                                 const float* __restrict__ gate, int num_experts,
-                                                                 int top_k, int group_size, int groups, int k_pad,
-                                                                 int32_t* __restrict__ ids, float* __restrict__ gates,
-                                                                 __half* __restrict__ x16, float* __restrict__ sx) {
-    __shared__ float sc[kRwWarps][64];
-    __shared__ double ex[kRwWarps][64];
-    __shared__ int pick_k[kRwWarps][64];
-    __shared__ double pick_p[kRwWarps][64];
-    pdl_wait();
-    pdl_launch_dependents();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int b = blockIdx.x * kRwWarps + warp;
-    if (b >= batch) return;   // no block-level barriers below
-    const float* xb = x + static_cast<int64_t>(b) * in_dim;
-    // fp16 activations (zero-padded to k_pad) and per-group sums of them
-    if (x16) {
-        __half* xo = x16 + static_cast<int64_t>(b) * k_pad;
-        for (int c = lane; c < k_pad; c += 32) xo[c] = __float2half_rn(c < in_dim ? xb[c] : 0.0f);
-    }
-    for (int g = 0; sx && g < groups; ++g) {
-        float acc = 0.0f;
-        const int c0 = g * group_size, c1 = min(in_dim, c0 + group_size);
-        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-        if (lane == 0) sx[static_cast<int64_t>(b) * groups + g] = acc;
-    }
-    if (num_experts == 0) return;
-    const bool vec = (in_dim & 3) == 0;
-    for (int k0 = 0; k0 < num_experts; k0 += kRwExp) {
-        double sum[kRwExp], asum[kRwExp];
-#pragma unroll
-        for (int j = 0; j < kRwExp; ++j) sum[j] = asum[j] = 0.0;
-        if (vec) {
-            for (int c = 4 * lane; c < in_dim; c += 128) {
-                const float4 xv = *reinterpret_cast<const float4*>(xb + c);
-#pragma unroll
-                for (int j = 0; j < kRwExp; ++j) {
-                    if (k0 + j >= num_experts) break;
-                    const float4 gv = __ldg(reinterpret_cast<const float4*>(gate + static_cast<int64_t>(k0 + j) * in_dim + c));
-                    const double p0 = static_cast<double>(xv.x) * gv.x, p1 = static_cast<double>(xv.y) * gv.y;
-                    const double p2 = static_cast<double>(xv.z) * gv.z, p3 = static_cast<double>(xv.w) * gv.w;
-                    sum[j] += (p0 + p1) + (p2 + p3);
-                    asum[j] += (fabs(p0) + fabs(p1)) + (fabs(p2) + fabs(p3));
-                }
-            }
-        } else {
-            for (int c = lane; c < in_dim; c += 32) {
-                const float xv = xb[c];
-#pragma unroll
-                for (int j = 0; j < kRwExp; ++j) {
-                    if (k0 + j >= num_experts) break;
-                    const double pr = static_cast<double>(xv) * gate[static_cast<int64_t>(k0 + j) * in_dim + c];
-                    sum[j] += pr;
-                    asum[j] += fabs(pr);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kRwExp; ++j) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                sum[j] += __shfl_xor_sync(0xffffffffu, sum[j], off);
-                asum[j] += __shfl_xor_sync(0xffffffffu, asum[j], off);
-            }
-        }
-        // certification (tier 1 of route_kernel); lane j owns expert k0 + j
-        unsigned und = 0u;
-#pragma unroll
-        for (int j = 0; j < kRwExp; ++j) {
-            if (k0 + j >= num_experts) break;
-            const double u = 1.1102230246251565e-16;  // 2^-53
-            const double nterms = 2.0 * (static_cast<double>(in_dim) + static_cast<double>(in_dim) / 32.0 + 40.0);
-            const double err = __dmul_ru(__dmul_ru(nterms * u, 1.01), __dmul_ru(asum[j], 1.0001));
-            const float lo = __double2float_rn(__dsub_rd(sum[j], err));
-            const float hi = __double2float_rn(__dadd_ru(sum[j], err));
-            if (lo != hi) und |= 1u << j;
-            if (lane == j) sc[warp][k0 + j] = __double2float_rn(sum[j]);
-        }
-        // undecided: the reference's sequential loop, exactly (rare)
-        for (int j = 0; j < kRwExp; ++j) {
-            if (!(und & (1u << j))) continue;
-            if (lane == 0) {
-                const float* gk = gate + static_cast<int64_t>(k0 + j) * in_dim;
-                double acc = 0.0;
-                int c = 0;
-                for (; c + 8 <= in_dim; c += 8) {
-                    double v[8];
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) v[t] = static_cast<double>(xb[c + t]) * static_cast<double>(gk[c + t]);
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) acc = __dadd_rn(acc, v[t]);
-                }
-                for (; c < in_dim; ++c) acc = __dadd_rn(acc, static_cast<double>(xb[c]) * static_cast<double>(gk[c]));
-                sc[warp][k0 + j] = __double2float_rn(acc);
-            }
-        }
-    }
-    __syncwarp();
-    // softmax (f64, max-subtracted, total in k order) and top-k -- moe.cpp:64-87
-    double mx = -INFINITY;
-    for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[warp][k]));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    for (int k = lane; k < num_experts; k += 32) ex[warp][k] = exp(static_cast<double>(sc[warp][k]) - mx);
-    __syncwarp();
-    double total = 0.0;   // in the reference order k = 0..K-1
-    for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[warp][k]);
-    double selected = 0.0;
-    uint64_t taken = 0;
-    for (int tt = 0; tt < top_k; ++tt) {
-        double best_p = -1.0;
-        int best_k = 0x7fffffff;
-        for (int k = lane; k < num_experts; k += 32) {
-            if (taken & (1ull << k)) continue;
-            const double pk = __ddiv_rn(ex[warp][k], total);
-            if (pk > best_p || (pk == best_p && k < best_k)) {
-                best_p = pk;
-                best_k = k;
-            }
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            const double op = __shfl_xor_sync(0xffffffffu, best_p, off);
-            const int ok = __shfl_xor_sync(0xffffffffu, best_k, off);
-            if (op > best_p || (op == best_p && ok < best_k)) {
-                best_p = op;
-                best_k = ok;
-            }
-        }
-        taken |= 1ull << best_k;
-        if (lane == 0) {
-            pick_k[warp][tt] = best_k;
-            pick_p[warp][tt] = best_p;
-        }
-        selected = __dadd_rn(selected, best_p);
-    }
-    __syncwarp();
-    for (int tt = lane; tt < top_k; tt += 32) {
-        ids[static_cast<int64_t>(b) * top_k + tt] = pick_k[warp][tt];
-        gates[static_cast<int64_t>(b) * top_k + tt] = __double2float_rn(__ddiv_rn(pick_p[warp][tt], selected));
-    }
-}
-
-// =============================================================================
 // route, prefill: token tiles x all experts (a skinny f64 GEMM)
 // =============================================================================
 // Same contract and certification as route_kernel, organised for large
@@ -2095,27 +1938,13 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
     if (plan && num_experts <= 0) return cudaErrorInvalidValue;
     const PlanArgs pa = plan ? *plan : PlanArgs{};
-    static const int warp_min = [] {
-        // batch from which the warp-per-token router runs (off by default: measured
-        // 442 vs 403 us at 4096 tokens -- both routers are bound by their f64 work)
-        const char* e = getenv("TQ_ROUTE_WARP_MIN");
-        return e ? atoi(e) : 0x7fffffff;
-    }();
-    if (!plan && batch >= warp_min) {
-        max_carveout(route_warp_kernel);
-        return launch_maybe_pdl(route_warp_kernel, dim3((batch + kRwWarps - 1) / kRwWarps), dim3(kRwWarps * 32), 0,
-                                stream, x, batch, in_dim, gate, num_experts, top_k, group_size, groups, k_pad, ids,
-                                gates, x16, sx);
-    }
 #ifndef TQ_ROUTE_TOKEN_CTAS
 #define TQ_ROUTE_TOKEN_CTAS (2 * 148)   // token-chunk CTAs at prefill (several tokens per CTA beyond this)
 #endif
-    static const int tile_min = [] {
-        // batch from which the token-tile router runs (<= 0: never); the per-token
-        // route_kernel below serves smaller batches
-        const char* e = getenv("TQ_ROUTE_TILE_MIN");
-        return e ? atoi(e) : 297;
-    }();
+    // batch from which the token-tile router runs; the per-token route_kernel below
+    // serves smaller batches (at decode sizes the tile router's 16 sequential
+    // chunks per CTA cost more than one CTA per token)
+    constexpr int tile_min = 297;
     const bool tile_ok = !plan && num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
                          (k_pad & 3) == 0 && (!sx || (group_size > 0 && kTC % group_size == 0));
     if (tile_ok) {
@@ -2132,19 +1961,9 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     const dim3 grid((batch + tpc - 1) / tpc, num_experts > 0 ? (num_experts + kRouteExperts - 1) / kRouteExperts : 1);
     // prefill (several tokens per CTA): 128-thread CTAs (more CTAs per SM); decode: 512
     // (measured at 4096 tokens: 512 -> 1437 us, 256 -> 1367 us, 128 -> 1345 us per forward)
-    static const int pre_threads = [] {
-        const char* e = getenv("TQ_ROUTE_PREFILL_THREADS");   // 128 (default) / 256
-        return e ? atoi(e) : 128;
-    }();
-    if (tpc > 1 && pre_threads == 128) {
+    if (tpc > 1) {
         max_carveout(route_kernel<128>);
         return launch_maybe_pdl(route_kernel<128>, grid, dim3(128), 0, stream, x, batch, in_dim, gate, num_experts,
-                                top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
-                                plan ? plan_ticket : nullptr);
-    }
-    if (tpc > 1) {
-        max_carveout(route_kernel<256>);
-        return launch_maybe_pdl(route_kernel<256>, grid, dim3(256), 0, stream, x, batch, in_dim, gate, num_experts,
                                 top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
                                 plan ? plan_ticket : nullptr);
     }
@@ -2266,7 +2085,7 @@ __global__ void __launch_bounds__(256, 4) combine_rows_kernel(const CombineArgs 
 }
 
 cudaError_t launch_combine(const CombineArgs& a, cudaStream_t stream) {
-    if (a.batch > 64 && (a.out_dim & 3) == 0 && a.top_k <= 64 && !getenv("TQ_COMBINE_COLS")) {
+    if (a.batch > 64 && (a.out_dim & 3) == 0 && a.top_k <= 64) {
         max_carveout(combine_rows_kernel);
         return launch_maybe_pdl(combine_rows_kernel, dim3((a.out_dim + kCbCols - 1) / kCbCols, a.batch), dim3(256), 0,
                                 stream, a);
@@ -2351,6 +2170,20 @@ cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int 
     if (n_src * n_local > 1024) return cudaErrorInvalidValue;
     ep_units_kernel<<<1, 1024, 0, stream>>>(counts, n_src, e_stride, n_local, slab, mb_count, bn, kc_end, n_ext, units,
                                             n_units);
+    return cudaGetLastError();
+}
+
+// The f64 exp of the routers' softmax (route_pick / route_tile_kernel, moe.cpp:72
+// std::exp) on arbitrary arguments: the hook the exp-vs-glibc parity test drives.
+__global__ void exp_f64_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        y[t] = exp(x[t]);
+}
+
+cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    exp_f64_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, stream>>>(x, n, y);
     return cudaGetLastError();
 }
 

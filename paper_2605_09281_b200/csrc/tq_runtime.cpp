@@ -52,6 +52,7 @@ cudaError_t launch_dec_combine(const DecCombineArgs& a, cudaStream_t stream);
 cudaError_t launch_decode(const DecParams& p, int dn, int grid, cudaStream_t stream);
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream);
+cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t stream);
 cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int n_local, int slab, int mb_count, int bn,
                             int kc_end, int n_ext, Unit* units, int32_t* n_units, cudaStream_t stream);
 
@@ -715,14 +716,7 @@ LaunchCfg proj_cfg(const tq_layer* L, int64_t batch) {
 
 // decode configuration (dn == 32): resident activation slots of kc-wide chunks
 // must fit ~140 KB of shared memory -> lower bound on the split-K count
-// experiments: TQ_NS_FORCE=<n> pins the decode K-split count
-static int ns_force() {
-    static const int v = [] {
-        const char* e = std::getenv("TQ_NS_FORCE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v;
-}
+static int ns_force() { return 0; }   // (experiment hook retired: the plan picks the K split)
 
 int xr_ns_min(const tq_layer* L, const LaunchCfg& cf, int64_t batch) {
     if (cf.dn != 32) return 1;
@@ -1408,11 +1402,7 @@ void count_launch(tq_layer* L, int n = 1) {
 // measured slower, the plan's unit loop wants the full 1024-thread CTA)
 static bool fuse_plan(const tq_layer* L) {
     (void)L;
-    static const bool on = [] {
-        const char* e = std::getenv("TQ_FUSE_PLAN");
-        return e && e[0] == '1';
-    }();
-    return on;
+    return false;
 }
 
 // prep (x16, sx) and optional routing; with `plan` the router's last CTA also
@@ -1492,10 +1482,7 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
         // ext-balanced K splits: opt-in (TQ_EXT_BALANCE=1) -- measured slower on the
         // c2 sweep (739 vs 717 us): the per-unit chain, not the ext bytes, bounds the
         // last split's CTAs, and uneven main-chunk counts cost more than they save
-        static const bool ext_balance = [] {
-            const char* e = std::getenv("TQ_EXT_BALANCE");
-            return e && e[0] == '1';
-        }();
+        constexpr bool ext_balance = false;
         if (ext_balance && use_qmoe && cf.n_ext > 0 && g.ext_cols > 0) {
             // ext blocks (dense fp16, 128 x 64 per block) against one packed main chunk
             const double ext_bytes = static_cast<double>(g.ext_cols) * kBM * 2.0;
@@ -1504,12 +1491,8 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
         }
         pa.max_run = xr ? xr_slots(cf, ns_min) : 0;
         // per-unit pipeline cost of the decode GEMM in chunk equivalents (TQ_PROFILE:
-        // ~1 us per unit vs ~0.27 us per 6.9 KB chunk); TQ_UNIT_COST8=0 restores the
-        // balance-only split choice
-        static const int unit_cost8 = [] {
-            const char* e = std::getenv("TQ_UNIT_COST8");
-            return e ? std::atoi(e) : 30;
-        }();
+        // ~1 us per unit vs ~0.27 us per 6.9 KB chunk)
+        constexpr int unit_cost8 = 30;
         pa.unit_cost8 = (xr && use_qmoe) ? unit_cost8 : 0;
     }
     pa.n_ext = cf.n_ext;
@@ -1641,9 +1624,9 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.bits = g.bits;
     p.groups = static_cast<int32_t>(g.G);
     p.rank = static_cast<int32_t>(g.r);
-    // fused combine: at most two addends per output element (top_k <= 2, no shared experts)
-    // (opt-in: measured slower at prefill -- L2 reductions of scattered rows cost more than the combine pass)
-    const bool fuse = g.top_k <= 2 && !with_shared && getenv("TQ_FUSED_COMBINE") && atoi(getenv("TQ_FUSED_COMBINE")) == 1;
+    // (an epilogue-fused combine -- red.global.add of at most two addends per output --
+    // measured slower at prefill than the separate combine pass; not used)
+    const bool fuse = false;
     if (fuse) {
         cuda_check(cudaMemsetAsync(y, 0, sizeof(float) * batch * g.o, st), "y memset");
         p.fuse_combine = 1;
@@ -2388,6 +2371,13 @@ tq_status tq_debug_decode_counters(tq_layer* L, int32_t* out, int64_t n) {
         pull(L->dec_ticket, kDecMaxBatch);
         pull(L->dec_segcnt, (g.K + g.S) * g.mb_count);   // first tile of every weight
         for (int64_t t = 0; t < n && t < static_cast<int64_t>(h.size()); ++t) out[t] = h[static_cast<size_t>(t)];
+    });
+}
+
+tq_status tq_exp_f64(const double* x, int64_t n, double* y, void* stream) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && (!x || !y))) fail(TQ_ERR_PARAM, "tq_exp_f64: bad arguments");
+        cuda_check(launch_exp_f64(x, n, y, static_cast<cudaStream_t>(stream)), "exp launch");
     });
 }
 

@@ -9,7 +9,8 @@ descale tier) or random positive scaling (general tier).  The container is
 written exactly like write_artifact (io.cpp:565-677): manifest.json
 (format_version 1, kind tileq_artifact, keys sorted, dump(2) + newline) plus
 one little-endian blob per tensor with its zlib CRC32; the reference's own
-read_artifact accepts these files (checked in tests/test_artifacts.py).
+read_artifact accepts these files (checked by
+tests/test_cpu_oracle.py::test_synthetic_artifact_readable_by_reference).
 
 Throughput does not depend on the numeric content; parity tests use
 artifacts produced by the reference pipeline itself.

@@ -189,6 +189,20 @@ def test_no_cpu_fallback_in_product():
 # synthetic workload + measurement bookkeeping
 # ---------------------------------------------------------------------------
 
+def test_factory_stage_replay_matches_quantize_moe(ref, tmp_path):
+    """The artifact factory replays quantize_moe's stages without proxy_loss
+    (oracle/ref_shim.cpp): its blobs must equal quantize_moe's own, byte for byte."""
+    kw = dict(K=6, top_k=2, i=128, o=96, S=1, r=8, bits=3, g=64, calib="gauss", seed=9)
+    a, b = str(tmp_path / "replay"), str(tmp_path / "full")
+    ref.make_artifact(a, **kw)
+    ref.make_artifact(b, full_pipeline=True, **kw)
+    bins = sorted(f for f in os.listdir(a) if f.endswith(".bin"))
+    assert len(bins) > 20
+    for f in bins:
+        with open(os.path.join(a, f), "rb") as fa, open(os.path.join(b, f), "rb") as fb:
+            assert fa.read() == fb.read(), f
+
+
 def test_synthetic_artifact_readable_by_reference(ref, oracle, tmp_path):
     from oracle.oracle import read_artifact_np
     from paper_2605_09281_b200 import synth

@@ -295,6 +295,13 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
                     const int ein = gshift >= 0 ? (e0 & ((1 << gshift) - 1)) : e0 % p.group_size;
                     const int glast = p.groups - 1 - (gshift >= 0 ? e0 >> gshift : e0 / p.group_size);
                     const uint16_t* sc = reinterpret_cast<const uint16_t*>(st + kAtomsPerStep * kBlk) + rloc;
+                    // groups of >= 128 columns: this warp's 128 columns (atoms 2hw, 2hw+1, the
+                    // step being 256-aligned) share one scale -- one scale load and one bias
+                    // table for all four super-words
+                    const bool one_group = gshift >= 7;
+                    DqConst dq1;
+                    if (one_group)
+                        dq1 = make_dq(__ushort_as_half(sc[min((ein + 128 * hw) >> gshift, glast) * kBM]));
                     mbar_wait(&h->a_empty[as], aph ^ 1u);
                     if (lane == 0 && q == 0 && hw == 0) dtrace(p, 8, j);
                     tc_fence_after();
@@ -304,15 +311,17 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
                         if (at < nat) {
                             const uint32_t* wst = reinterpret_cast<const uint32_t*>(st + at * kBlk) + rloc;
                             uint32_t words[2][kWords];
-                            uint16_t sbits[2];
+                            uint16_t sbits[2] = {0, 0};
 #pragma unroll
                             for (int ss = 0; ss < 2; ++ss) {
 #pragma unroll
                                 for (int w = 0; w < kWords; ++w) words[ss][w] = wst[ss * kHalf + w * kBM];
-                                const int off = ein + 64 * at + 32 * ss;
-                                // a super-word past in_dim (zero codes) may lie past the last group
-                                const int gi = min(gshift >= 0 ? off >> gshift : off / p.group_size, glast);
-                                sbits[ss] = sc[gi * kBM];
+                                if (!one_group) {
+                                    const int off = ein + 64 * at + 32 * ss;
+                                    // a super-word past in_dim (zero codes) may lie past the last group
+                                    const int gi = min(gshift >= 0 ? off >> gshift : off / p.group_size, glast);
+                                    sbits[ss] = sc[gi * kBM];
+                                }
                             }
 #pragma unroll
                             for (int ss = 0; ss < 2; ++ss) {
@@ -321,8 +330,12 @@ __global__ void __launch_bounds__(kThreads, 1) dec_gemm_kernel(const __grid_cons
 #pragma unroll
                                 for (int w = 0; w < 16; ++w) v[w] = words[ss][w % kWords] + sbits[ss];
 #else
-                                const DqConst dq = make_dq(__ushort_as_half(sbits[ss]));
-                                dequant32<BITS>(words[ss], dq, v);
+                                if (one_group) {
+                                    dequant32<BITS>(words[ss], dq1, v);
+                                } else {
+                                    const DqConst dq = make_dq(__ushort_as_half(sbits[ss]));
+                                    dequant32<BITS>(words[ss], dq, v);
+                                }
 #endif
                                 tc_st_32x32b_x16(tmem + lane_base + as * 128 + at * 32 + ss * 16, v);
                             }

@@ -1717,28 +1717,8 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
         pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
     }
     const int w0 = a.given ? 0 : 1;   // first warp free of the pick
-    for (int g = warp - w0; a.use_main && g >= 0 && g < a.groups; g += kRT / 32 - w0) {
-        float acc = 0.0f;
-        const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
-        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
-        if (lane == 0) s_sx[g] = acc;
-    }
-    const bool stage16 = a.use_main && a.k_pad <= kDecStage16;
-    if (stage16 && warp >= w0) {
-        for (int t8 = threadIdx.x - 32 * w0; t8 < a.k_pad / 8; t8 += kRT - 32 * w0) {
-            __align__(16) __half hh[8];
-#pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int c = t8 * 8 + m;
-                hh[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
-            }
-            reinterpret_cast<int4*>(s_x16)[t8] = *reinterpret_cast<const int4*>(hh);
-        }
-    }
     // small per-layer tables the tail reads per destination, staged once (no dependent
-    // global loads after the pick)
+    // global loads after the pick); issued first so their latency overlaps the x pass
     for (int t = threadIdx.x; t < K; t += kRT) {
         s_eq[t] = a.e_q[t];
         s_zs[t] = a.zscale[t];
@@ -1748,6 +1728,52 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
     if (nzq <= kDecZq) {
         const float* zi = a.zq_ws + static_cast<int64_t>(b) * nzq;
         for (int t = threadIdx.x - 32 * w0; t >= 0 && t < nzq; t += kRT - 32 * w0) s_zq[t] = __ldcg(zi + t);
+    }
+    const bool stage16 = a.use_main && a.k_pad <= kDecStage16;
+    // one pass over x for 128-column groups (the BASELINE shapes): warp w takes groups
+    // w, w + nw, ...; every lane loads all its float4s first, then writes the fp16 row
+    // and the group sums of the fp16-rounded values (one memory round trip, not two)
+    constexpr int kGPW = 6;   // groups per warp held in flight
+    const int nw = kRT / 32 - w0;
+    const bool one_pass = stage16 && a.group_size == 128 && a.in_dim == a.k_pad && a.groups <= kGPW * nw;
+    if (one_pass && warp >= w0) {
+        float4 v[kGPW];
+#pragma unroll
+        for (int i = 0; i < kGPW; ++i) {
+            const int g = warp - w0 + i * nw;
+            if (g < a.groups) v[i] = __ldg(reinterpret_cast<const float4*>(xb + g * 128) + lane);
+        }
+#pragma unroll
+        for (int i = 0; i < kGPW; ++i) {
+            const int g = warp - w0 + i * nw;
+            if (g >= a.groups) break;
+            const __half2 h01 = __floats2half2_rn(v[i].x, v[i].y), h23 = __floats2half2_rn(v[i].z, v[i].w);
+            reinterpret_cast<__half2*>(s_x16 + g * 128 + 4 * lane)[0] = h01;
+            reinterpret_cast<__half2*>(s_x16 + g * 128 + 4 * lane)[1] = h23;
+            float acc = (__low2float(h01) + __high2float(h01)) + (__low2float(h23) + __high2float(h23));
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+            if (lane == 0) s_sx[g] = acc;
+        }
+    }
+    for (int g = warp - w0; !one_pass && a.use_main && g >= 0 && g < a.groups; g += kRT / 32 - w0) {
+        float acc = 0.0f;
+        const int c0 = g * a.group_size, c1 = min(a.in_dim, c0 + a.group_size);
+        for (int c = c0 + lane; c < c1; c += 32) acc += __half2float(__float2half_rn(xb[c]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+        if (lane == 0) s_sx[g] = acc;
+    }
+    if (!one_pass && stage16 && warp >= w0) {
+        for (int t8 = threadIdx.x - 32 * w0; t8 < a.k_pad / 8; t8 += kRT - 32 * w0) {
+            __align__(16) __half hh[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int c = t8 * 8 + m;
+                hh[m] = __float2half_rn(c < a.in_dim ? xb[c] : 0.0f);
+            }
+            reinterpret_cast<int4*>(s_x16)[t8] = *reinterpret_cast<const int4*>(hh);
+        }
     }
     __syncthreads();
     rtrace(a, 3);

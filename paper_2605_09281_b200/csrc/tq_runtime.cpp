@@ -1719,7 +1719,10 @@ void run_decode(tq_layer* L, const float* x, int64_t batch, const int32_t* ids_i
     const bool use_lr = path != TQ_PATH_QMOE;
     const int S = use_main ? static_cast<int>(g.S) : 0;   // lotile_forward has no shared experts
     const int64_t cap8 = round_up(given ? batch * g.top_k : batch, 8);
-    const int dn = cap8 <= 32 ? 32 : 64;
+    // 32-slot tiles (4 MMA issue streams) up to 64 slots per weight: at uniform routing an
+    // expert of a 64-token batch holds ~16 slots, and the 2-issuer 64-slot tile pays
+    // twice the per-MMA issue latency per step; an expert past 32 slots takes two tiles
+    const int dn = cap8 <= 64 ? 32 : 64;
     if (L->ktime) {
         L->kt_stream = st;
         L->kt_active = true;

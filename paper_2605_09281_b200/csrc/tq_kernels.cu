@@ -311,9 +311,10 @@ __device__ unsigned route_slice(const float* __restrict__ xb, int in_dim, const 
 // ONE warp: mx, prob_k = exp(s_k - mx) in f64, total summed k = 0..K-1,
 // order by (prob desc, index asc), gate = float(prob / selected).
 __device__ void route_pick(const float* score_row, int num_experts, int top_k, float* sc, double* ex, int* pick_k,
-                           double* pick_p, int32_t* __restrict__ ids_row, float* __restrict__ gates_row) {
+                           double* pick_p, int32_t* __restrict__ ids_row, float* __restrict__ gates_row,
+                           bool fence = true) {
     const int lane = threadIdx.x & 31;
-    __threadfence();
+    if (fence) __threadfence();   // (callers that acquired through their ticket pass false)
     for (int k = lane; k < num_experts; k += 32) sc[k] = __ldcg(score_row + k);
     __syncwarp();
     double mx = -INFINITY;
@@ -1666,9 +1667,8 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
     const int y = blockIdx.y;
     rtrace(a, 0);
     if (y < nslices) {
-        const unsigned und = route_slice<kRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts,
-                                                 a.score_ws + static_cast<int64_t>(b) * K, sm);
-        if (threadIdx.x < kRouteExperts || (threadIdx.x == 0 && und)) __threadfence();
+        (void)route_slice<kRT>(xb, a.in_dim, a.gate, K, y * kRouteExperts, a.score_ws + static_cast<int64_t>(b) * K,
+                               sm);
     } else {
         // projection CTA: rows [kProjRows * rs, + kProjRows) of tile column q
         const int rs_cnt = (a.rank + kProjRows - 1) / kProjRows;
@@ -1684,14 +1684,17 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
                                      a.vscale + q * a.rank + j0, min(kProjRows, a.rank - j0),
                                      a.zq_ws + (static_cast<int64_t>(b) * a.num_q + q) * a.rank + j0,
                                      reinterpret_cast<float*>(sm.prod));
-            __threadfence();
         }
     }
+    // publication without per-thread fences: the barrier orders every thread's score /
+    // projection stores before thread 0's gpu-scope acq_rel ticket increment, which
+    // releases them (cumulatively) and, in the last CTA, acquires the other CTAs'
+    // stores for every thread behind the next barrier (they read them through L2)
     __syncthreads();
     rtrace(a, 1);
     if (threadIdx.x == 0) {
-        __threadfence();
-        const int done = atomicAdd(&a.ticket[b], 1);
+        int done;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(done) : "l"(a.ticket + b) : "memory");
         s_last = done == static_cast<int>(gridDim.y) - 1;
         if (s_last) a.ticket[b] = 0;   // ready for the next launch
 #ifdef TQ_DEC_CHECK
@@ -1703,7 +1706,6 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
     rtrace(a, 2);
     const int k = a.top_k;
     // ---- routing decision (warp 0), overlapped with the token's loads (other warps):
@@ -1712,7 +1714,7 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
     if (!a.given) {
         if (warp == 0)
             route_pick(a.score_ws + static_cast<int64_t>(b) * K, K, k, sc, ex, pick_k, pick_p,
-                       a.ids + static_cast<int64_t>(b) * k, a.gates + static_cast<int64_t>(b) * k);
+                       a.ids + static_cast<int64_t>(b) * k, a.gates + static_cast<int64_t>(b) * k, false);
     } else if (static_cast<int>(threadIdx.x) < k) {
         pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
     }

@@ -6,8 +6,9 @@
 //   * bitwise CPU identities become the north_star bar where the GPU computes
 //     in fp16 x fp16 -> fp32 (rel. Frobenius <= 2e-3), and stay BITWISE where
 //     both sides are the same engine (artifact round trip, determinism);
-//   * group_size 5 / 16 become 32: the engine dequantizes 32-code super-words
-//     per scale group (group_size % 32 == 0 is a documented engine limit).
+//   * the layers keep the reference tests' own shapes and group sizes (16, 5): the
+//     engine serves group sizes that are not a multiple of 32 from fp16 weights it
+//     dequantizes once at load.
 //
 //   test_infer.cpp:117-143  fused forward vs naive reconstruction, 24 configs x 4 scaling regimes
 //   test_infer.cpp:145-159  zero gates -> exactly zero output
@@ -128,7 +129,7 @@ TileQLayer make_quantized(std::uint64_t seed, std::size_t i, std::size_t o, int 
     cfg.grid_cols = 3;
     cfg.rank = 8;
     cfg.bits = bits;
-    cfg.group_size = 32;
+    cfg.group_size = 16;
     cfg.sub_dim = 2;
     cfg.quantizer = qz;
     cfg.seed = seed + 2;
@@ -253,9 +254,9 @@ TEST_CASE("dispatch count is independent of the batch size") {
 
 TEST_CASE("qmoe_forward equals the reference over dequantized experts") {
     for (int bits : {3, 2, 4, 8}) {
-        const TileQLayer layer = make_quantized(131 + bits, 64, 48, bits, 1);
+        const TileQLayer layer = make_quantized(131 + bits, 16, 12, bits, 1);   // test_infer.cpp:321
         CounterRng rng(132);
-        const DenseMatrix x = gaussian_matrix(5, 64, rng);
+        const DenseMatrix x = gaussian_matrix(5, 16, rng);
         const RoutingDecision routing = route(x, layer.gate_weights, 2);
         ExpertSet dq;
         dq.spec = layer.spec;
@@ -265,10 +266,13 @@ TEST_CASE("qmoe_forward equals the reference over dequantized experts") {
         const double g1 = relative_gap(qm, reference_forward(x, dq, routing));
         CAPTURE(bits);
         CHECK(g1 < kTol);
-        // the combined path is the sum of its halves (one accumulator on the GPU: fp32 rounding only)
+        // the combined path is the sum of its halves.  (group_size 16 -> fp16 weights at
+        // load, served by the grouped path, while the lotile-only layer takes the decode
+        // path: the two round the projected activations to fp16 at different points, so
+        // the bar is the north_star one rather than fp32 rounding)
         const DenseMatrix total = gpu::tileq_forward(x, layer, routing);
         const double g2 = relative_gap(total, add(qm, gpu::lotile_forward(x, layer.tiled, routing)));
-        CHECK(g2 < 1e-5);
+        CHECK(g2 < kTol);
         // and it matches the reference's own tileq_forward
         const double g3 = relative_gap(total, tileq_forward(x, layer, routing));
         CHECK(g3 < kTol);
@@ -283,12 +287,12 @@ TEST_CASE("qmoe_forward equals the reference over dequantized experts") {
 }
 
 TEST_CASE("artifact round trip: forward from the directory equals forward from memory, bitwise") {
-    const TileQLayer layer = make_quantized(21, 64, 40, 4, 1);
+    const TileQLayer layer = make_quantized(21, 16, 40, 4, 1);
     const std::string dir = scratch("roundtrip");
     write_artifact(dir, layer, nlohmann::json{{"run", "test"}});
     const LoadedArtifact back = read_artifact(dir);
     CounterRng rng(22);
-    const DenseMatrix x = gaussian_matrix(6, 64, rng);
+    const DenseMatrix x = gaussian_matrix(6, 16, rng);
     const RoutingDecision routing = gpu::route(x, layer.gate_weights, 2);
     const DenseMatrix from_mem = gpu::tileq_forward(x, layer, routing);
     CHECK(max_abs_diff(gpu::tileq_forward(x, back.layer, routing), from_mem) == 0.0);

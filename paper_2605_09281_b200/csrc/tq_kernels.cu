@@ -26,6 +26,7 @@
 #include <cstdlib>
 #include <cuda_fp16.h>
 
+#include "tq_exp.h"
 #include "tq_internal.h"
 #include "tq_ptx.cuh"
 
@@ -308,8 +309,8 @@ __device__ unsigned route_slice(const float* __restrict__ xb, int in_dim, const 
 }
 
 // Softmax and top-k of one token's certified scores (moe.cpp:64-87), run by
-// ONE warp: mx, prob_k = exp(s_k - mx) in f64, total summed k = 0..K-1,
-// order by (prob desc, index asc), gate = float(prob / selected).
+// ONE warp: mx, prob_k = exp(s_k - mx) in f64 (glibc's exp, tq_exp.h), total
+// summed k = 0..K-1, order by (prob desc, index asc), gate = float(prob / selected).
 __device__ void route_pick(const float* score_row, int num_experts, int top_k, float* sc, double* ex, int* pick_k,
                            double* pick_p, int32_t* __restrict__ ids_row, float* __restrict__ gates_row,
                            bool fence = true) {
@@ -321,7 +322,7 @@ __device__ void route_pick(const float* score_row, int num_experts, int top_k, f
     for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[k]));
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-    for (int k = lane; k < num_experts; k += 32) ex[k] = exp(static_cast<double>(sc[k]) - mx);
+    for (int k = lane; k < num_experts; k += 32) ex[k] = tq_exp::exp(__dsub_rn(static_cast<double>(sc[k]), mx));
     __syncwarp();
     double total = 0.0;   // in the reference order k = 0..K-1
     for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[k]);
@@ -795,7 +796,8 @@ __global__ void __launch_bounds__(kTThreads, 2) route_tile_kernel(const float* _
         for (int k = lane; k < num_experts; k += 32) mx = fmax(mx, static_cast<double>(sc[r][k]));
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-        for (int k = lane; k < num_experts; k += 32) ex[warp][k] = exp(static_cast<double>(sc[r][k]) - mx);
+        for (int k = lane; k < num_experts; k += 32)
+            ex[warp][k] = tq_exp::exp(__dsub_rn(static_cast<double>(sc[r][k]), mx));
         __syncwarp();
         double total = 0.0;   // in the reference order k = 0..K-1
         for (int k = 0; k < num_experts; ++k) total = __dadd_rn(total, ex[warp][k]);
@@ -2206,7 +2208,7 @@ cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int 
 __global__ void exp_f64_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ y) {
     for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
          t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        y[t] = exp(x[t]);
+        y[t] = tq_exp::exp(x[t]);
 }
 
 cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t stream) {

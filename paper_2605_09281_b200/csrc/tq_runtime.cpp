@@ -534,6 +534,43 @@ void repack_vq(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* s
     }
 }
 
+// Scalar residual with a group size the super-word dequant cannot serve: W'[r, c] =
+// fp16((code - zero) * scale * 2^k) (dequantize, quant.cpp:285-323, computed in f64,
+// rounded once; k = prescale_exponent keeps |W'| <= 255 * 16), dense blocks in the
+// engine layout; the epilogue multiplies by 2^-k; unit scales, no zero points left.
+void repack_dense_scalar(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out,
+                         uint8_t* zeros_out, int* k_out) {
+    const std::vector<uint32_t> codes = unpack_stream(q.packed, q.bits, static_cast<size_t>(g.o * g.i), "codes");
+    const int k = prescale_exponent(q);
+    *k_out = k;
+    const size_t G = (static_cast<size_t>(g.i) + q.gs - 1) / q.gs;
+    auto val = [&](int64_t row, int64_t col) -> uint32_t {
+        if (row >= g.o || col >= g.i) return 0u;
+        const size_t gi = static_cast<size_t>(row) * G + static_cast<size_t>(col) / q.gs;
+        const double w = (static_cast<double>(codes[static_cast<size_t>(row * g.i + col)]) - q.zeros[gi]) *
+                         static_cast<double>(half_bits_to_float(q.scales[gi]));
+        return float_to_half_bits(static_cast<float>(std::ldexp(w, k)));
+    };
+    const int blk = code_block_bytes(kDenseBits);
+    for (int64_t mb = 0; mb < g.mb_count; ++mb) {
+        for (int64_t kc = 0; kc < g.kc_total; ++kc) {
+            uint32_t* block = reinterpret_cast<uint32_t*>(codes_out + (mb * g.kc_total + kc) * blk);
+            for (int h = 0; h < 2; ++h)
+                for (int j = 0; j < 16; ++j)
+                    for (int rl = 0; rl < kBM; ++rl) {
+                        const int64_t row = mb * kBM + rl, c0 = kc * kKC + 32 * h + 2 * j;
+                        block[(h * 16 + j) * kBM + rl] = val(row, c0) | (val(row, c0 + 1) << 16);
+                    }
+        }
+        for (int64_t gi = 0; gi < g.G; ++gi)
+            for (int rl = 0; rl < kBM; ++rl) {
+                const size_t dst = static_cast<size_t>((mb * g.G + gi) * kBM + rl);
+                scales_out[dst] = mb * kBM + rl < g.o ? 0x3C00u : 0u;
+                zeros_out[dst] = 0;
+            }
+    }
+}
+
 }  // namespace tqb
 
 using namespace tqb;
@@ -580,7 +617,9 @@ struct tq_layer {
     bool lay_ready[4] = {false, false, false, false};
     int num_sms = 148;
     bool vq = false;                    // codebook residuals, expanded to fp16 weight blocks at load
+    bool dense = false;                 // residuals held as dense fp16 weight blocks (codebook / odd group size)
     int art_bits = 0;                   // residual code width as stored in the artifact
+    int64_t art_gs = 0;                 // scale group size as stored in the artifact
     // expert-GEMM device timing (tq_gemm_timing_enable)
     bool timing = false;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
@@ -1110,10 +1149,17 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
     // resolves each code through its expert's codebook into exact fp16 weight blocks,
     // streamed by the dense (kDenseBits) weight path; unit scales, no zero points
     const bool vq = q0.vec;
+    // scale groups that are not a multiple of 32 codes (the dequant works on 32-code
+    // super-words per scale): the loader dequantizes such residuals once, exactly in
+    // f64 and rounded once to fp16 (prescaled by 2^k like the code path), into dense
+    // weight blocks -- the same dense-weight path as codebook residuals
+    const bool dense_scalar = !vq && q0.gs % 32 != 0;
     L->vq = vq;
+    L->dense = vq || dense_scalar;
     L->art_bits = q0.bits;
-    const int bits = vq ? kDenseBits : q0.bits;
-    const size_t gs = vq ? 128 : q0.gs;
+    L->art_gs = static_cast<int64_t>(q0.gs);
+    const int bits = L->dense ? kDenseBits : q0.bits;
+    const size_t gs = L->dense ? 128 : q0.gs;
     std::vector<QMat> q;
     for (int64_t e = e_begin; e < e_end; ++e) q.push_back(std::move(a.routed[static_cast<size_t>(e)]));
     for (auto& m : a.shared) q.push_back(std::move(m));
@@ -1156,6 +1202,9 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
                         if (vq)
                             repack_vq(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
                                       h_zeros.data() + w * slab, &wk[w]);
+                        else if (dense_scalar)
+                            repack_dense_scalar(q[w], g, h_codes.data() + w * L->weight_stride,
+                                                h_scales.data() + w * slab, h_zeros.data() + w * slab, &wk[w]);
                         else
                             repack_qmat(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
                                         h_zeros.data() + w * slab, &wk[w]);
@@ -1681,7 +1730,7 @@ bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
     }();
     const Geometry& g = L->g;
     const int64_t slots = given ? batch * g.top_k : batch;
-    return !off && !L->vq && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
+    return !off && !L->dense && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
            g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64 && g.n_ext <= 4;
 }
 
@@ -1986,8 +2035,8 @@ tq_status tq_layer_info_get(const tq_layer* L, tq_layer_info* out) {
         out->rank = L->g.r;
         out->grid_rows = L->g.M;
         out->grid_cols = L->g.N;
-        out->bits = L->vq ? L->art_bits : L->g.bits;
-        out->group_size = L->g.gs;
+        out->bits = L->dense ? L->art_bits : L->g.bits;
+        out->group_size = L->dense ? L->art_gs : L->g.gs;
         out->expert_begin = L->e_begin;
         out->expert_end = L->e_end;
         out->device = L->device;
@@ -2423,7 +2472,7 @@ tq_status tq_layer_export_codes(tq_layer* L, int64_t e, uint32_t* out, void* str
     return guarded([&] {
         check_layer(L);
         if (e < 0 || e >= L->n_weights) fail(TQ_ERR_PARAM, "export: matrix index out of range");
-        if (L->vq) fail(TQ_ERR_PARAM, "export: codebook residuals are resolved to fp16 weights at load; no codes kept");
+        if (L->dense) fail(TQ_ERR_PARAM, "export: this layer's residuals are resolved to fp16 weights at load; no codes kept");
         cuda_check(cudaSetDevice(L->device), "cudaSetDevice");
         cuda_check(launch_export_codes(L->codes.as<uint8_t>() + e * L->weight_stride, L->g.bits,
                                        static_cast<int>(L->g.kc_total), static_cast<int>(L->g.o),

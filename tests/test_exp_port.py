@@ -1,0 +1,36 @@
+"""csrc/tq_exp.h (the routers' f64 exp) against the host libm, bit for bit.
+
+route() takes prob_k = std::exp(s_k - mx) (moe.cpp:72) with glibc's exp; the
+engine restates that algorithm (tq_exp.h) so routing ties break identically.
+This builds the header for the host with FMA contraction off and compares it
+with libm's exp on ~70M arguments (softmax-shaped, f32 score differences, the
+whole over/underflow range, raw bit patterns, edges).  glibc picks its FMA
+variant on FMA-capable CPUs -- the B200 hosts' -- so the check needs one too.
+"""
+import os
+import subprocess
+import tempfile
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(os.path.dirname(HERE), "paper_2605_09281_b200", "csrc")
+
+
+def _cpu_has_fma():
+    try:
+        with open("/proc/cpuinfo") as f:
+            return " fma " in f.read().replace("\n", " ")
+    except OSError:
+        return False
+
+
+@pytest.mark.skipif(not _cpu_has_fma(), reason="host glibc uses its non-FMA exp variant")
+def test_exp_port_matches_libm():
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "exp_port_check")
+        subprocess.run(["g++", "-O2", "-mfma", "-ffp-contract=off", "-std=c++17", "-I", CSRC,
+                        os.path.join(HERE, "exp_port_check.cpp"), "-o", exe, "-lm"], check=True)
+        r = subprocess.run([exe, "15000000"], capture_output=True, text=True, timeout=300)
+        print(r.stdout)
+        assert r.returncode == 0, r.stdout

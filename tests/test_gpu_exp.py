@@ -1,12 +1,11 @@
 """The routers' f64 exp against glibc's (SURVEY hard part 1).
 
 route() takes prob_k = std::exp(s_k - mx) in f64 (moe.cpp:72) -- glibc on the
-reference's host; the engine's routers use CUDA's exp(double).  The ids only
-depend on the order of the probabilities and the gates are compared within
-1 f32 ulp, so the contract is: exp agrees with glibc to within 1 f64 ulp on
-every argument the softmax can see (s - mx in [-745, 0]), and we record how
-often it is bit-identical.  Arguments: a dense log-uniform sweep of [-745, 0],
-differences of f32 scores (the form s - mx takes), and the edges.
+reference's host.  The engine's routers run the same algorithm (csrc/tq_exp.h,
+a restatement of glibc's table-driven exp), so the contract is bit-identity on
+every argument: a dense log-uniform sweep of [-745, 0] (the softmax's range),
+differences of f32 scores (the form s - mx takes), the over/underflow range,
+and the edges.
 """
 import ctypes
 import ctypes.util
@@ -40,7 +39,8 @@ def test_router_exp_matches_glibc():
     diffs = (s.min(axis=1).astype(np.float64) - s.max(axis=1).astype(np.float64))
     edges = np.array([0.0, -0.0, -1e-300, -5e-324, -1.0, -0.5, -708.39, -708.40, -744.44, -745.0, -745.13,
                       -745.2, -746.0], np.float64)
-    x = np.concatenate([sweep, diffs, edges])
+    wide = rng.uniform(-1100.0, 800.0, n // 4)
+    x = np.concatenate([sweep, diffs, wide, edges, -edges])
     xd = torch.from_numpy(x).cuda()
     yd = torch.empty_like(xd)
     tq.check(tq.lib().tq_exp_f64(xd.data_ptr(), x.size, yd.data_ptr(), None))
@@ -50,5 +50,4 @@ def test_router_exp_matches_glibc():
     u = _ulps(y, want)
     exact = float((u == 0).mean())
     print(f"\nexp vs glibc: {x.size} arguments, {exact * 100:.4f}% bit-identical, max {int(u.max())} ulp")
-    assert int(u.max()) <= 1
-    assert exact >= 0.99
+    assert int(u.max()) == 0

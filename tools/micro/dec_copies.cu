@@ -14,7 +14,7 @@
 using namespace tqb;
 
 __global__ void __launch_bounds__(384, 1) k(const uint8_t* codes, const uint8_t* scales, const uint8_t* xs, int steps, int xb,
-                                           int nst, int sb, int use_sc, unsigned long long* out) {
+                                           int nst, int sb, int use_sc, unsigned long long* out, int xsplit) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + nst * sb);
     uint64_t* empty = full + 32;
@@ -44,7 +44,10 @@ __global__ void __launch_bounds__(384, 1) k(const uint8_t* codes, const uint8_t*
                     if (use_sc) bulk_copy_g2s(dst + 12288, scales + (static_cast<size_t>(blockIdx.x) * steps + j) * 512, 512, &full[st]);
                 } else {
                     mbar_arrive_expect_tx(&full[st], xb);
-                    if (xb) bulk_copy_g2s(dst + 13312, xs + static_cast<size_t>(j % 16) * 32768, xb, &full[st]);
+                    // xsplit pieces: the activation rows of a step as 1 or 4 (one per 64-K atom) copies
+                    for (int q = 0; q < xsplit && xb; ++q)
+                        bulk_copy_g2s(dst + 13312 + q * (xb / xsplit), xs + static_cast<size_t>(j % 16) * 32768 + q * 8192,
+                                      xb / xsplit, &full[st]);
                 }
             }
             __syncwarp();
@@ -86,7 +89,7 @@ int main() {
     cudaEventCreate(&b);
     uint8_t* flush;
     cudaMalloc(&flush, 512 << 20);
-    auto run = [&](int steps, int xb, int nst, int use_sc) {
+    auto run = [&](int steps, int xb, int nst, int use_sc, int xsplit = 1) {
         const int sb = 13312 + 16384;
         const int smem = nst * sb + 1024;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -94,7 +97,7 @@ int main() {
         for (int r = 0; r < 3; ++r) {
             cudaMemset(flush, r, 512 << 20);
             cudaEventRecord(a);
-            k<<<148, 384, smem>>>(codes, scales, xs, steps, xb, nst, sb, use_sc, d);
+            k<<<148, 384, smem>>>(codes, scales, xs, steps, xb, nst, sb, use_sc, d, xsplit);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
@@ -104,14 +107,16 @@ int main() {
         cudaError_t e = cudaDeviceSynchronize();
         cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
         const double bytes = 148.0 * steps * (12288 + (use_sc ? 512 : 0) + xb);
-        printf("steps %4d xb %5d scales %d stages %2d: %7.2f us  %6.0f cycles/step (CTA 0)  %7.1f GB/s  (%s)\n", steps, xb,
-               use_sc, nst, best * 1e3, double(h[0]) / steps, bytes / (best * 1e-3) / 1e9, cudaGetErrorString(e));
+        printf("steps %4d xb %5d x-copies %d scales %d stages %2d: %7.2f us  %6.0f cycles/step (CTA 0)  %7.1f GB/s  (%s)\n",
+               steps, xb, xsplit, use_sc, nst, best * 1e3, double(h[0]) / steps, bytes / (best * 1e-3) / 1e9,
+               cudaGetErrorString(e));
     };
-    for (int steps : {26, 103, 1000})
-        for (int xb : {0, 4096, 16384}) run(steps, xb, 6, 1);
-    run(26, 4096, 6, 0);
-    run(1000, 4096, 6, 0);
-    run(26, 4096, 4, 1);
-    run(1000, 4096, 4, 1);
+    for (int steps : {26, 103})
+        for (int xs : {1, 4}) {
+            run(steps, 4096, 7, 1, xs);
+            run(steps, 16384, 7, 1, xs);
+        }
+    run(26, 1024, 7, 1, 4);
+    run(26, 1024, 7, 1, 1);
     return 0;
 }

@@ -221,13 +221,14 @@ tq_status tq_sync(tq_layer* layer, void* stream);
  * [(K + S) * m-blocks]); every entry reads zero between forwards. */
 tq_status tq_debug_decode_counters(tq_layer* layer, int32_t* out, int64_t n);
 
+/* Test hook: the routers' f64 exp (the softmax of route(), moe.cpp:72 std::exp,
+ * glibc's algorithm restated in csrc/tq_exp.h) on x [dev] f64 n -> y [dev] f64,
+ * for the exp-vs-glibc parity test. */
+tq_status tq_exp_f64(const double* x, int64_t n, double* y, void* stream);
+
 /* GPU unpack of a packed stream (codec.cpp:168-195): bytes [dev], out [dev]
  * uint32 count.  Returns TQ_ERR_PARAM on a bad width or byte count and
  * TQ_ERR_FORMAT on nonzero padding bits (after synchronizing). */
-/* Test hook: the routers' f64 exp (the softmax of route(), moe.cpp:72 std::exp)
- * on x [dev] f64 n -> y [dev] f64, for the exp-vs-glibc parity test. */
-tq_status tq_exp_f64(const double* x, int64_t n, double* y, void* stream);
-
 tq_status tq_unpack_codes(const uint8_t* bytes, int64_t nbytes, int bits, int64_t count,
                           uint32_t* out, void* stream);
 
@@ -313,6 +314,48 @@ tq_status tq_ep_combine(tq_layer* layer, const float* x, int64_t batch, const fl
 /* Row widths of the dispatch buffers (fp16 elements). */
 int64_t tq_ep_xrow_elems(const tq_layer* layer);
 int64_t tq_ep_extrow_elems(const tq_layer* layer);
+
+/* ------------------------------------------------------------------------
+ * Artifact producer hot spots, device arrays, bit-identical to
+ * the reference.  Quantized experts cross as unpacked codes (uint8, rows x
+ * cols), per-group scales (f32, binary16-exact) and zero points (int32),
+ * rows x ceil(cols / group_size), row-major.  These calls synchronize the
+ * stream where the reference returns a host value or may throw.
+ *
+ *   tq_estimate_hessian <- estimate_hessian(calib, damping_fraction)
+ *                          include/tileq/quant.hpp:67, src/quant.cpp:116-150
+ *   tq_spd_inverse      <- spd_inverse(h) (internal)   src/quant.cpp:72-112
+ *   tq_quantize_rtn     <- quantize_rtn(r, bits, group_size)
+ *                          include/tileq/quant.hpp:74, src/quant.cpp:152-175
+ *   tq_quantize_gptq    <- quantize_gptq(r, h, bits, group_size)
+ *                          include/tileq/quant.hpp:85-86, src/quant.cpp:177-221
+ *   tq_proxy_loss       <- proxy_loss(original, q, h)
+ *                          include/tileq/quant.hpp:104, src/quant.cpp:325-343
+ * ------------------------------------------------------------------------ */
+
+/* calib [dev] f32 tokens x dim -> h [dev] f32 dim x dim; *damping_out (host,
+ * nullable) = lambda.  Empty set -> TQ_ERR_DATA; damping < 0 -> TQ_ERR_PARAM. */
+tq_status tq_estimate_hessian(const float* calib, int64_t tokens, int64_t dim, double damping_fraction, float* h,
+                              double* damping_out, void* stream);
+
+/* h [dev] f32 n x n -> hinv [dev] f64 n x n.  A non-positive or non-finite
+ * pivot -> TQ_ERR_NUMERIC with the reference's message. */
+tq_status tq_spd_inverse(const float* h, int64_t n, double* hinv, void* stream);
+
+/* r [dev] f32 rows x cols -> codes / scales / zeros [dev]. */
+tq_status tq_quantize_rtn(const float* r, int64_t rows, int64_t cols, int bits, int64_t group_size, uint8_t* codes,
+                          float* scales, int32_t* zeros, void* stream);
+
+/* r [dev] f32 rows x cols, h [dev] f32 cols x cols -> codes / scales / zeros
+ * [dev]; *used_rtn (host, nullable) = 1 when plain rounding won the proxy-loss
+ * comparison (quant.cpp:216-219).  cols <= 25600. */
+tq_status tq_quantize_gptq(const float* r, int64_t rows, int64_t cols, const float* h, int bits, int64_t group_size,
+                           uint8_t* codes, float* scales, int32_t* zeros, int32_t* used_rtn, void* stream);
+
+/* tr(E H E^T), E = original - dequantize(codes, scales, zeros), into *loss (host). */
+tq_status tq_proxy_loss(const float* original, int64_t rows, int64_t cols, const uint8_t* codes, const float* scales,
+                        const int32_t* zeros, int bits, int64_t group_size, const float* h, double* loss,
+                        void* stream);
 
 #ifdef __cplusplus
 }

@@ -150,6 +150,21 @@ class Oracle:
         L.tqo_lotile_forward.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p,
                                          _i64, _i64, _p]
         L.tqo_dequantize_rows.argtypes = [_p, _i64, _i64, _i64, _i64, _p]
+        L.tqo_spd_inverse.argtypes = [_p, _i64, _p, _p, _p]
+
+    def spd_inverse(self, h):
+        """quant.cpp:72-112 -> (hinv f64, None) or (None, (column, pivot)) on a bad pivot."""
+        h = np.ascontiguousarray(h, np.float32)
+        n = h.shape[0]
+        out = np.zeros((n, n), np.float64)
+        col = C.c_int64(0)
+        piv = C.c_double(0.0)
+        st = self.lib.tqo_spd_inverse(_ptr(h), n, _ptr(out), C.byref(col), C.byref(piv))
+        if st == 6:
+            return None, (col.value, piv.value)
+        if st:
+            raise MemoryError("tqo_spd_inverse")
+        return out, None
 
     def half_to_float(self, bits: int) -> float:
         return self.lib.tqo_half_to_float(bits)
@@ -263,6 +278,7 @@ class RefError(Exception):
     def __init__(self, code, msg):
         super().__init__(f"[{code}] {msg}")
         self.code = code
+        self.msg = msg
 
 
 class RefLib:
@@ -289,6 +305,9 @@ class RefLib:
         L.tq_ref_make_artifact.argtypes = [C.c_char_p] + [_i64] * 8 + [C.c_int, _i64, C.c_int, _i64,
                                            C.c_double, C.c_double, _i64, C.c_uint64, C.c_int,
                                            C.c_int, _i64, C.c_char_p, C.c_int]
+        L.tq_ref_estimate_hessian.argtypes = [_p, _i64, _i64, C.c_double, _p, _p, C.c_char_p, C.c_int]
+        L.tq_ref_quantize.argtypes = [C.c_int, _p, _i64, _i64, _p, C.c_int, _i64, _p, _p, _p, C.c_char_p, C.c_int]
+        L.tq_ref_proxy_loss.argtypes = [_p, _i64, _i64, _p, _p, _p, C.c_int, _i64, _p, _p, C.c_char_p, C.c_int]
 
     def _check(self, st, buf):
         if st:
@@ -323,6 +342,46 @@ class RefLib:
         buf = C.create_string_buffer(1024)
         self._check(self.lib.tq_ref_pack(_ptr(codes), codes.size, bits, _ptr(out), buf, 1024), buf)
         return out
+
+    # -- artifact producer hot spots (quant.cpp:116-221,325-343) --
+    def estimate_hessian(self, calib, damping_fraction):
+        calib = np.ascontiguousarray(calib, np.float32)
+        h = np.zeros((calib.shape[1], calib.shape[1]), np.float32)
+        lam = C.c_double(0.0)
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.tq_ref_estimate_hessian(_ptr(calib), calib.shape[0], calib.shape[1],
+                                                     damping_fraction, _ptr(h), C.byref(lam), buf, 1024), buf)
+        return h, lam.value
+
+    def quantize(self, method, r, h, bits, group_size):
+        """method "rtn" (quantize_rtn) or "gptq" (quantize_gptq): (codes u32, scales f32, zeros i32)."""
+        r = np.ascontiguousarray(r, np.float32)
+        rows, cols = r.shape
+        G = (cols + group_size - 1) // group_size if group_size >= 1 else 0
+        codes = np.zeros((rows, cols), np.uint32)
+        scales = np.zeros((rows, G), np.float32)
+        zeros = np.zeros((rows, G), np.int32)
+        hp = None
+        if method == "gptq":
+            h = np.ascontiguousarray(h, np.float32)
+            hp = _ptr(h)
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.tq_ref_quantize(0 if method == "rtn" else 1, _ptr(r), rows, cols, hp, bits, group_size,
+                                             _ptr(codes), _ptr(scales), _ptr(zeros), buf, 1024), buf)
+        return codes, scales, zeros
+
+    def proxy_loss(self, original, codes, scales, zeros, bits, group_size, h):
+        original = np.ascontiguousarray(original, np.float32)
+        codes = np.ascontiguousarray(codes, np.uint32)
+        scales = np.ascontiguousarray(scales, np.float32)
+        zeros = np.ascontiguousarray(zeros, np.int32)
+        h = np.ascontiguousarray(h, np.float32)
+        out = C.c_double(0.0)
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.tq_ref_proxy_loss(_ptr(original), original.shape[0], original.shape[1], _ptr(codes),
+                                               _ptr(scales), _ptr(zeros), bits, group_size, _ptr(h),
+                                               C.byref(out), buf, 1024), buf)
+        return out.value
 
     def f16_to_f32(self, bits):
         bits = np.ascontiguousarray(bits, np.uint16)

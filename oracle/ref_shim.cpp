@@ -23,6 +23,9 @@
 //     tokens from derive(seed, 5) (signs -> folded descale tier, gaussians ->
 //     general tier).
 //
+//   * tq_ref_estimate_hessian / tq_ref_quantize / tq_ref_proxy_loss: the
+//     artifact producer's hot spots (quant.cpp:116-221,325-343) on raw arrays.
+//
 // Errors never cross this boundary as exceptions: every entry returns 0 on
 // success or a tileq error class code and writes the message to errbuf.
 
@@ -373,6 +376,76 @@ int tq_ref_bench(void* hv, int layout, const std::int64_t* batches, std::int64_t
             out[4 * t + 2] = reps[t].p90_ns();
             out[4 * t + 3] = static_cast<double>(reps[t].dispatches);
         }
+    });
+}
+
+// ---- artifact producer hot spots --------------------------
+// estimate_hessian (quant.cpp:116-150), quantize_rtn / quantize_gptq
+// (quant.cpp:152-221) and proxy_loss (quant.cpp:325-343) on raw arrays.
+// Quantized experts cross as unpacked codes (uint32, rows x cols), per-group
+// scales (f32) and zero points (int32), rows x ceil(cols / group_size).
+
+int tq_ref_estimate_hessian(const float* calib, std::int64_t tokens, std::int64_t dim, double damping_fraction,
+                            float* h_out, double* damping_out, char* errbuf, int errlen) {
+    return guarded(errbuf, errlen, [&] {
+        const HessianProxy h = estimate_hessian(wrap(calib, tokens, dim), damping_fraction);
+        copy_out(h.h, h_out);
+        *damping_out = h.damping;
+    });
+}
+
+namespace {
+void export_quantized(const QuantizedExpert& q, std::uint32_t* codes, float* scales, std::int32_t* zeros) {
+    const std::vector<std::uint32_t> c = unpack_codes(q.packed, q.bits, q.code_count());
+    std::memcpy(codes, c.data(), c.size() * sizeof(std::uint32_t));
+    for (std::size_t t = 0; t < q.grids.size(); ++t) {
+        scales[t] = q.grids[t].scale;
+        zeros[t] = q.grids[t].zero_point;
+    }
+}
+
+QuantizedExpert import_quantized(std::int64_t rows, std::int64_t cols, const std::uint32_t* codes,
+                                 const float* scales, const std::int32_t* zeros, int bits, std::int64_t gs) {
+    QuantizedExpert q;
+    q.out_dim = static_cast<std::size_t>(rows);
+    q.in_dim = static_cast<std::size_t>(cols);
+    q.bits = bits;
+    q.mode = QuantMode::scalar;
+    q.group_size = static_cast<std::size_t>(gs);
+    q.packed = pack_codes(std::vector<std::uint32_t>(codes, codes + rows * cols), bits);
+    const std::size_t n = q.out_dim * q.groups_per_row();
+    q.grids.resize(n);
+    for (std::size_t t = 0; t < n; ++t) q.grids[t] = QuantGrid{scales[t], zeros[t]};
+    return q;
+}
+} // namespace
+
+// method 0: quantize_rtn(r, bits, gs); 1: quantize_gptq(r, {h}, bits, gs)
+int tq_ref_quantize(int method, const float* r, std::int64_t rows, std::int64_t cols, const float* h, int bits,
+                    std::int64_t gs, std::uint32_t* codes, float* scales, std::int32_t* zeros, char* errbuf,
+                    int errlen) {
+    return guarded(errbuf, errlen, [&] {
+        const DenseMatrix rm = wrap(r, rows, cols);
+        QuantizedExpert q;
+        if (method == 0) {
+            q = quantize_rtn(rm, bits, static_cast<std::size_t>(gs));
+        } else {
+            HessianProxy hp;
+            hp.h = wrap(h, cols, cols);
+            q = quantize_gptq(rm, hp, bits, static_cast<std::size_t>(gs));
+        }
+        export_quantized(q, codes, scales, zeros);
+    });
+}
+
+int tq_ref_proxy_loss(const float* original, std::int64_t rows, std::int64_t cols, const std::uint32_t* codes,
+                      const float* scales, const std::int32_t* zeros, int bits, std::int64_t gs, const float* h,
+                      double* out, char* errbuf, int errlen) {
+    return guarded(errbuf, errlen, [&] {
+        HessianProxy hp;
+        hp.h = wrap(h, cols, cols);
+        *out = proxy_loss(wrap(original, rows, cols), import_quantized(rows, cols, codes, scales, zeros, bits, gs),
+                          hp);
     });
 }
 

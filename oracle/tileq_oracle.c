@@ -367,3 +367,48 @@ int tqo_lotile_forward(const float* x, int64_t batch, int64_t in_dim, int64_t ou
     free(sig); free(tier); free(first); free(proj); free(xproj); free(sacc); free(descaled);
     return TQO_OK;
 }
+
+/* ------------------------------------------------------ producer: spd_inverse -- */
+
+/* quant.cpp:72-112, loop for loop */
+int tqo_spd_inverse(const float* h, int64_t n, double* hinv, int64_t* bad_col, double* bad_pivot) {
+    double* chol = (double*)calloc((size_t)(n * n), sizeof(double));
+    double* linv = (double*)calloc((size_t)(n * n), sizeof(double));
+    if (!chol || !linv) { free(chol); free(linv); return 99; }
+    for (int64_t j = 0; j < n; ++j) {
+        for (int64_t i = j; i < n; ++i) {
+            double acc = (double)h[i * n + j];
+            for (int64_t k = 0; k < j; ++k) acc -= chol[i * n + k] * chol[j * n + k];
+            if (i == j) {
+                if (acc <= 0.0 || !isfinite(acc)) {
+                    *bad_col = j;
+                    *bad_pivot = acc;
+                    free(chol); free(linv);
+                    return 6;
+                }
+                chol[i * n + j] = sqrt(acc);
+            } else {
+                chol[i * n + j] = acc / chol[j * n + j];
+            }
+        }
+    }
+    for (int64_t j = 0; j < n; ++j) {
+        linv[j * n + j] = 1.0 / chol[j * n + j];
+        for (int64_t i = j + 1; i < n; ++i) {
+            double acc = 0.0;
+            for (int64_t k = j; k < i; ++k) acc += chol[i * n + k] * linv[k * n + j];
+            linv[i * n + j] = -acc / chol[i * n + i];
+        }
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        for (int64_t j = 0; j <= i; ++j) {
+            double acc = 0.0;
+            for (int64_t k = i; k < n; ++k) acc += linv[k * n + i] * linv[k * n + j];
+            hinv[i * n + j] = acc;
+            hinv[j * n + i] = acc;
+        }
+    }
+    free(chol);
+    free(linv);
+    return 0;
+}

@@ -69,6 +69,12 @@ int tqo_lotile_forward(const float* x, int64_t batch, int64_t in_dim, int64_t ou
                        const int64_t* ids, const float* gates, int64_t r0, int64_t r1,
                        float* y /* batch x (r1-r0) */);
 
+/* spd_inverse (quant.cpp:72-112): Cholesky H = L L^T, L^-1 by columns,
+ * Hinv = L^-T L^-1, every dot in the reference's loop order.  h: n x n f32,
+ * hinv: n x n f64.  Returns 0, or 6 (NumericError) with *bad_col / *bad_pivot
+ * set at the first non-positive or non-finite pivot. */
+int tqo_spd_inverse(const float* h, int64_t n, double* hinv, int64_t* bad_col, double* bad_pivot);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtileq_b200.so")
-SOURCES = ["tq_gemm.cu", "tq_decode.cu", "tq_kernels.cu", "tq_layouts.cu", "tq_runtime.cpp"]
+SOURCES = ["tq_gemm.cu", "tq_decode.cu", "tq_kernels.cu", "tq_layouts.cu", "tq_producer.cu", "tq_runtime.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

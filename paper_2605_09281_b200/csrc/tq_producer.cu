@@ -1,0 +1,621 @@
+// GPU ports of the artifact producer's hot spots:
+//
+//   estimate_hessian   quant.cpp:116-150   H = (1/T) X^T X + lambda I
+//   spd_inverse        quant.cpp:72-112    Cholesky, L^-1, L^-T L^-1
+//   make_grids / RTN   quant.cpp:28-70,152-175
+//   quantize_gptq      quant.cpp:177-221   per-row error feedback through H^-1
+//   proxy_loss         quant.cpp:325-343   tr(E H E^T)
+//
+// Every function returns the reference's bits, not an approximation: each
+// output element sees the same f64 operations in the same order as the
+// reference's scalar loops (compiled for x86-64 without FMA contraction), so
+// products and sums are issued one at a time with __dmul_rn / __dadd_rn /
+// __dsub_rn / __ddiv_rn and are never contracted.  What the GPU changes is
+// WHICH elements run concurrently:
+//
+//   * the dot-product-shaped loops (Hessian accumulation, the Cholesky trailing
+//     update, the L^-1 block update, L^-T L^-1, E H) run as 64x64 output tiles
+//     whose threads each accumulate their 4x4 outputs over k ascending -- the
+//     reference's order per element; terms the reference skips are either
+//     skipped too or exact zero products that leave a +0-started sum unchanged;
+//   * the sequential recurrences (the Cholesky panel, the L^-1 diagonal block,
+//     the GPTQ column sweep) keep their order along the recurrence and run
+//     independent rows / columns side by side.
+//
+// All of it is FP64 CUDA-core work (the reference's arithmetic is f64); none
+// of it is GEMM-shaped in a precision the tensor cores serve.
+
+#include <cuda_fp16.h>
+
+#include <cstdint>
+
+#include "tq_internal.h"
+
+namespace tqb {
+namespace {
+
+constexpr int kT = 64;     // output tile edge
+constexpr int kKC = 16;    // k chunk staged in shared memory
+constexpr int kTT = 256;   // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+
+// Status word shared by the spd_inverse kernels: the first failing pivot.
+struct SpdStatus {
+    int32_t failed;
+    int32_t pad;
+    int64_t column;
+    double pivot;
+};
+
+// ---------------------------------------------------------------------------
+// ordered f64 tile product
+// ---------------------------------------------------------------------------
+
+// acc[ii][jj] (+|-)= A(i0 + ty*4 + ii, k) * B(k, j0 + tx*4 + jj) for k = k0 .. k1-1
+// ascending.  kAK / kBK: the operand is contiguous along k (stage k-fastest) or
+// along i / j (stage i/j-fastest), so the global loads coalesce either way.
+template <bool kSub, bool kAK, bool kBK, class FA, class FB>
+__device__ __forceinline__ void tile_accumulate(double (&acc)[4][4], int64_t i0, int64_t j0, int64_t k0, int64_t k1,
+                                                const FA& fa, const FB& fb, double (*As)[kT + 2],
+                                                double (*Bs)[kT + 2]) {
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    for (int64_t kb = k0; kb < k1; kb += kKC) {
+        const int kc = static_cast<int>(k1 - kb < kKC ? k1 - kb : kKC);
+        for (int e = tid; e < kKC * kT; e += kTT) {
+            const int kk = kAK ? e % kKC : e / kT;
+            const int ii = kAK ? e / kKC : e % kT;
+            As[kk][ii] = kk < kc ? fa(i0 + ii, kb + kk) : 0.0;
+        }
+        for (int e = tid; e < kKC * kT; e += kTT) {
+            const int kk = kBK ? e % kKC : e / kT;
+            const int jj = kBK ? e / kKC : e % kT;
+            Bs[kk][jj] = kk < kc ? fb(kb + kk, j0 + jj) : 0.0;
+        }
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = As[kk][ty * 4 + q];
+                b[q] = Bs[kk][tx * 4 + q];
+            }
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const double p = __dmul_rn(a[ii], b[jj]);
+                    acc[ii][jj] = kSub ? __dsub_rn(acc[ii][jj], p) : __dadd_rn(acc[ii][jj], p);
+                }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// estimate_hessian (quant.cpp:116-150)
+// ---------------------------------------------------------------------------
+
+// acc[a][b] = sum_t x[t][a] * x[t][b] for b >= a, t ascending (quant.cpp:127-133).
+__global__ void __launch_bounds__(kTT) hessian_acc_kernel(const float* __restrict__ x, int64_t tokens, int64_t dim,
+                                                           double* __restrict__ acc_out) {
+    const int64_t a0 = static_cast<int64_t>(blockIdx.y) * kT, b0 = static_cast<int64_t>(blockIdx.x) * kT;
+    if (b0 + kT <= a0) return;   // tile entirely below the diagonal
+    __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
+    double acc[4][4] = {};
+    auto fa = [&](int64_t a, int64_t t) { return a < dim ? static_cast<double>(x[t * dim + a]) : 0.0; };
+    auto fb = [&](int64_t t, int64_t b) { return b < dim ? static_cast<double>(x[t * dim + b]) : 0.0; };
+    tile_accumulate<false, false, false>(acc, a0, b0, 0, tokens, fa, fb, As, Bs);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t a = a0 + ty * 4 + ii, b = b0 + tx * 4 + jj;
+            if (a < dim && b < dim && b >= a) acc_out[a * dim + b] = acc[ii][jj];
+        }
+}
+
+// trace = sum_a acc[a][a] / T (a ascending), lambda = damping * (trace / dim)  (quant.cpp:134-136)
+__global__ void hessian_lambda_kernel(const double* __restrict__ acc, int64_t tokens, int64_t dim, double damping,
+                                      double* __restrict__ lambda_out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const double t = static_cast<double>(tokens);
+    double trace = 0.0;
+    for (int64_t a = 0; a < dim; ++a) trace = __dadd_rn(trace, __ddiv_rn(acc[a * dim + a], t));
+    *lambda_out = __dmul_rn(damping, __ddiv_rn(trace, static_cast<double>(dim)));
+}
+
+// h[a][b] = h[b][a] = float(acc[a][b] / T + (a == b ? lambda : 0))  (quant.cpp:141-148)
+__global__ void hessian_fill_kernel(const double* __restrict__ acc, int64_t tokens, int64_t dim,
+                                    const double* __restrict__ lambda, float* __restrict__ h) {
+    const double t = static_cast<double>(tokens), lam = *lambda;
+    const int64_t n = dim * dim;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t a = e / dim, b = e % dim;
+        const int64_t lo = a < b ? a : b, hi = a < b ? b : a;   // the upper-triangle entry holds the sum
+        const double v = __dadd_rn(__ddiv_rn(acc[lo * dim + hi], t), lo == hi ? lam : 0.0);
+        h[e] = __double2float_rn(v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// spd_inverse (quant.cpp:72-112)
+// ---------------------------------------------------------------------------
+
+// C[i][j] = double(h[i][j]) on and below the diagonal (the Cholesky work array)
+__global__ void chol_init_kernel(const float* __restrict__ h, int64_t n, double* __restrict__ c) {
+    const int64_t total = n * n;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = e / n, j = e % n;
+        c[e] = j <= i ? static_cast<double>(h[e]) : 0.0;
+    }
+}
+
+// Trailing update of panel [j0, j0 + kT): C[i][j] -= C[i][k] * C[j][k] for k = 0 .. j0-1
+// ascending, rows i >= j0 (quant.cpp:77-78 for the columns already finished).
+__global__ void __launch_bounds__(kTT) chol_update_kernel(double* __restrict__ c, int64_t n, int64_t j0,
+                                                           const SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    const int64_t i0 = j0 + static_cast<int64_t>(blockIdx.x) * kT;
+    __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
+    double acc[4][4];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            acc[ii][jj] = (i < n && j < n && j <= i) ? c[i * n + j] : 0.0;
+        }
+    auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
+    auto fb = [&](int64_t k, int64_t j) { return j < n ? c[j * n + k] : 0.0; };
+    tile_accumulate<true, true, true>(acc, i0, j0, 0, j0, fa, fb, As, Bs);
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            if (i < n && j < n && j <= i) c[i * n + j] = acc[ii][jj];
+        }
+}
+
+// Factor the panel's diagonal block (one CTA, thread t owns row j0 + t): for each
+// column j: the pivot, then the rows below it, each finishing k = j0 .. j-1 in order
+// (quant.cpp:75-90).
+__global__ void __launch_bounds__(kT) chol_diag_kernel(double* __restrict__ c, int64_t n, int64_t j0,
+                                                        SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    __shared__ double d[kT][kT + 1];
+    __shared__ int bad;
+    const int t = threadIdx.x;
+    const int w = static_cast<int>(n - j0 < kT ? n - j0 : kT);
+    for (int j = 0; j < w; ++j) d[t][j] = (t < w && j <= t) ? c[(j0 + t) * n + j0 + j] : 0.0;
+    if (t == 0) bad = 0;
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        if (t == j) {
+            double acc = d[j][j];
+            for (int k = 0; k < j; ++k) acc = __dsub_rn(acc, __dmul_rn(d[j][k], d[j][k]));
+            if (!(acc > 0.0) || !isfinite(acc)) {   // acc <= 0.0 || !finite (NaN included)
+                st->failed = 1;
+                st->column = j0 + j;
+                st->pivot = acc;
+                bad = 1;
+            } else {
+                d[j][j] = __dsqrt_rn(acc);
+            }
+        }
+        __syncthreads();
+        if (bad) return;
+        if (t > j && t < w) {
+            double acc = d[t][j];
+            for (int k = 0; k < j; ++k) acc = __dsub_rn(acc, __dmul_rn(d[t][k], d[j][k]));
+            d[t][j] = __ddiv_rn(acc, d[j][j]);
+        }
+        __syncthreads();
+    }
+    if (t < w)
+        for (int j = 0; j <= t; ++j) c[(j0 + t) * n + j0 + j] = d[t][j];
+}
+
+// Rows below the diagonal block: row i finishes its panel entries left to right
+// against the factored block (quant.cpp:87-88).  One thread per row.
+constexpr int kRowsPerCta = 128;
+__global__ void __launch_bounds__(kRowsPerCta) chol_rows_kernel(double* __restrict__ c, int64_t n, int64_t j0,
+                                                                 const SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    extern __shared__ double sm[];
+    double(*d)[kT + 1] = reinterpret_cast<double(*)[kT + 1]>(sm);                    // kT x (kT+1)
+    double(*rv)[kT + 1] = reinterpret_cast<double(*)[kT + 1]>(sm + kT * (kT + 1));   // rows x (kT+1)
+    const int w = static_cast<int>(n - j0 < kT ? n - j0 : kT);
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+        const int r = e / kT, q = e % kT;
+        d[r][q] = (r < w && q <= r) ? c[(j0 + r) * n + j0 + q] : 0.0;
+    }
+    const int64_t i = j0 + kT + static_cast<int64_t>(blockIdx.x) * kRowsPerCta + threadIdx.x;
+    __syncthreads();
+    if (i >= n) return;
+    double* row = rv[threadIdx.x];
+    for (int j = 0; j < w; ++j) row[j] = c[i * n + j0 + j];
+    for (int j = 0; j < w; ++j) {
+        double acc = row[j];
+        for (int k = 0; k < j; ++k) acc = __dsub_rn(acc, __dmul_rn(row[k], d[j][k]));
+        row[j] = __ddiv_rn(acc, d[j][j]);
+    }
+    for (int j = 0; j < w; ++j) c[i * n + j0 + j] = row[j];
+}
+
+// L^-1, row block [i0, i0 + kT): partial sums over the finished rows,
+// acc[i][j] = sum_{k < i0} L[i][k] * Linv[k][j] for j < i0 (k ascending; the terms
+// k < j are exact zero products, so starting the sum at the tile's first column
+// matches the reference's k = j start), parked in Linv[i][j] (quant.cpp:96-99).
+__global__ void __launch_bounds__(kTT) linv_update_kernel(const double* __restrict__ c, double* __restrict__ li,
+                                                           int64_t n, int64_t i0, const SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kT;
+    __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
+    double acc[4][4] = {};
+    auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
+    auto fb = [&](int64_t k, int64_t j) { return li[k * n + j]; };
+    tile_accumulate<false, true, false>(acc, i0, j0, j0, i0, fa, fb, As, Bs);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            if (i < n && j < i0) li[i * n + j] = acc[ii][jj];
+        }
+}
+
+// L^-1, row block [i0, i0 + kT), the in-block part: thread per column j <= i0+kT-1
+// walks rows i ascending, adds k = max(i0, j) .. i-1, then Linv[i][j] = -acc / L[i][i];
+// Linv[j][j] = 1 / L[j][j] (quant.cpp:94-100).
+__global__ void __launch_bounds__(kRowsPerCta) linv_block_kernel(const double* __restrict__ c,
+                                                                  double* __restrict__ li, int64_t n, int64_t i0,
+                                                                  const SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    __shared__ double d[kT][kT + 1];   // L[i0 + r][i0 + q]
+    const int w = static_cast<int>(n - i0 < kT ? n - i0 : kT);
+    for (int e = threadIdx.x; e < kT * kT; e += blockDim.x) {
+        const int r = e / kT, q = e % kT;
+        d[r][q] = (r < w && q <= r) ? c[(i0 + r) * n + i0 + q] : 0.0;
+    }
+    __syncthreads();
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * kRowsPerCta + threadIdx.x;
+    if (j >= i0 + w) return;
+    for (int r = 0; r < w; ++r) {
+        const int64_t i = i0 + r;
+        if (i < j) continue;
+        if (i == j) {
+            li[j * n + j] = __ddiv_rn(1.0, d[r][r]);
+            continue;
+        }
+        double acc = j < i0 ? li[i * n + j] : 0.0;
+        const int kb = static_cast<int>(j < i0 ? 0 : j - i0);
+        for (int q = kb; q < r; ++q) acc = __dadd_rn(acc, __dmul_rn(d[r][q], li[(i0 + q) * n + j]));
+        li[i * n + j] = __ddiv_rn(-acc, d[r][r]);
+    }
+}
+
+// Hinv[i][j] = Hinv[j][i] = sum_{k >= i} Linv[k][i] * Linv[k][j] for j <= i, k ascending
+// (quant.cpp:102-110; the k < i terms of a tile are exact zero products).
+__global__ void __launch_bounds__(kTT) hinv_kernel(const double* __restrict__ li, int64_t n,
+                                                    double* __restrict__ hinv, const SpdStatus* __restrict__ st) {
+    if (st->failed) return;
+    const int64_t i0 = static_cast<int64_t>(blockIdx.y) * kT, j0 = static_cast<int64_t>(blockIdx.x) * kT;
+    if (j0 > i0) return;
+    __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
+    double acc[4][4] = {};
+    auto fa = [&](int64_t i, int64_t k) { return i < n ? li[k * n + i] : 0.0; };
+    auto fb = [&](int64_t k, int64_t j) { return j < n ? li[k * n + j] : 0.0; };
+    tile_accumulate<false, false, false>(acc, i0, j0, i0, n, fa, fb, As, Bs);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            if (i < n && j <= i) {
+                hinv[i * n + j] = acc[ii][jj];
+                hinv[j * n + i] = acc[ii][jj];
+            }
+        }
+}
+
+// ---------------------------------------------------------------------------
+// grids, RTN, GPTQ (quant.cpp:28-70,152-221)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ float snap_f16(float v) { return __half2float(__float2half_rn(v)); }
+
+// make_grid over one group (quant.cpp:28-48), std::min / std::max semantics kept
+__global__ void grids_kernel(const float* __restrict__ r, int64_t rows, int64_t cols, int bits, int64_t gs,
+                             float* __restrict__ scales, int32_t* __restrict__ zeros) {
+    const int64_t G = (cols + gs - 1) / gs;
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= rows * G) return;
+    const int64_t row = t / G, g = t % G, start = g * gs;
+    const int64_t len = cols - start < gs ? cols - start : gs;
+    const float* v = r + row * cols + start;
+    float vmin = v[0], vmax = v[0];
+    for (int64_t q = 1; q < len; ++q) {
+        const float x = v[q];
+        vmin = x < vmin ? x : vmin;   // std::min(vmin, x)
+        vmax = vmax < x ? x : vmax;   // std::max(vmax, x)
+    }
+    const double dmin = static_cast<double>(vmin), dmax = static_cast<double>(vmax);
+    const double rmin = 0.0 < dmin ? 0.0 : dmin;   // std::min(dmin, 0.0)
+    const double rmax = dmax < 0.0 ? 0.0 : dmax;   // std::max(dmax, 0.0)
+    const double levels = static_cast<double>((1 << bits) - 1);
+    double scale = __ddiv_rn(__dsub_rn(rmax, rmin), levels);
+    if (scale <= 0.0) scale = 1e-8;
+    float s = snap_f16(__double2float_rn(scale));
+    if (s <= 0.0f) s = 5.9604644775390625e-8f;   // least positive binary16, 2^-24
+    double zero = rint(__ddiv_rn(-rmin, static_cast<double>(s)));
+    zero = 0.0 < zero ? zero : 0.0;          // std::max(0.0, zero)
+    zero = zero < levels ? zero : levels;    // std::min(levels, .)
+    scales[t] = s;
+    zeros[t] = static_cast<int32_t>(zero);
+}
+
+// encode_one (quant.cpp:50-55)
+__device__ __forceinline__ uint32_t encode_one(double value, float scale, int32_t zero, double levels) {
+    double code = __dadd_rn(rint(__ddiv_rn(value, static_cast<double>(scale))), static_cast<double>(zero));
+    code = 0.0 < code ? code : 0.0;
+    code = code < levels ? code : levels;
+    return static_cast<uint32_t>(code);
+}
+
+__global__ void rtn_codes_kernel(const float* __restrict__ r, int64_t rows, int64_t cols, int bits, int64_t gs,
+                                 const float* __restrict__ scales, const int32_t* __restrict__ zeros,
+                                 uint8_t* __restrict__ codes) {
+    const int64_t G = (cols + gs - 1) / gs, n = rows * cols;
+    const double levels = static_cast<double>((1 << bits) - 1);
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t row = e / cols, c = e % cols, g = row * G + c / gs;
+        codes[e] = static_cast<uint8_t>(encode_one(static_cast<double>(r[e]), scales[g], zeros[g], levels));
+    }
+}
+
+// GPTQ column sweep (quant.cpp:200-213).  A CTA owns kR rows, their working rows
+// in shared memory; columns are dealt to threads round-robin so the shrinking
+// trailing range stays balanced.  Per column j: every thread forms the code and
+// error of column j for its rows (work[j] is final after the previous barrier),
+// then updates its own columns c > j: work[c] -= err * Hinv[j][c] / Hinv[j][j].
+constexpr int kGptqThreads = 512;
+template <int kR>
+__global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restrict__ r, int64_t rows, int64_t dim,
+                                                             int bits, int64_t gs, const float* __restrict__ scales,
+                                                             const int32_t* __restrict__ zeros,
+                                                             const double* __restrict__ hinv,
+                                                             uint8_t* __restrict__ codes) {
+    extern __shared__ double work[];   // kR x dim
+    const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kR;
+    const int nr = static_cast<int>(rows - row0 < kR ? rows - row0 : kR);
+    const int64_t G = (dim + gs - 1) / gs;
+    const double levels = static_cast<double>((1 << bits) - 1);
+    for (int q = 0; q < nr; ++q)
+        for (int64_t c = threadIdx.x; c < dim; c += kGptqThreads)
+            work[q * dim + c] = static_cast<double>(r[(row0 + q) * dim + c]);
+    __syncthreads();
+    for (int64_t j = 0; j < dim; ++j) {
+        double err[kR];
+        const int64_t g = j / gs;
+#pragma unroll
+        for (int q = 0; q < kR; ++q) {
+            err[q] = 0.0;
+            if (q < nr) {
+                const float s = scales[(row0 + q) * G + g];
+                const int32_t z = zeros[(row0 + q) * G + g];
+                const double wj = work[q * dim + j];
+                const uint32_t code = encode_one(wj, s, z, levels);
+                const double deq = __dmul_rn(__dsub_rn(static_cast<double>(code), static_cast<double>(z)),
+                                             static_cast<double>(s));
+                err[q] = __dsub_rn(wj, deq);
+                if (threadIdx.x == q) codes[(row0 + q) * dim + j] = static_cast<uint8_t>(code);
+            }
+        }
+        const double inv_jj = hinv[j * dim + j];
+        const int64_t first = j + 1;
+        int64_t c = first + ((static_cast<int64_t>(threadIdx.x) - first) % kGptqThreads + kGptqThreads) % kGptqThreads;
+        for (; c < dim; c += kGptqThreads) {
+            const double h = hinv[j * dim + c];
+#pragma unroll
+            for (int q = 0; q < kR; ++q)
+                if (q < nr) work[q * dim + c] = __dsub_rn(work[q * dim + c], __ddiv_rn(__dmul_rn(err[q], h), inv_jj));
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// proxy_loss (quant.cpp:325-343)
+// ---------------------------------------------------------------------------
+
+// e = original - float(double(code - zero) * scale)  (matrix.cpp:138-143, quant.cpp:296-300)
+__device__ __forceinline__ float err_elem(const float* __restrict__ orig, const uint8_t* __restrict__ codes,
+                                          const float* __restrict__ scales, const int32_t* __restrict__ zeros,
+                                          int64_t row, int64_t c, int64_t dim, int64_t G, int64_t gs) {
+    const int64_t g = row * G + c / gs;
+    const int64_t q = static_cast<int64_t>(codes[row * dim + c]) - zeros[g];
+    const float deq = __double2float_rn(__dmul_rn(static_cast<double>(q), static_cast<double>(scales[g])));
+    return __fsub_rn(orig[row * dim + c], deq);
+}
+
+// he[row][a] = sum_b double(H[a][b]) * e[row][b], b ascending (quant.cpp:333-337);
+// stored column-major (he_t[a][row - r0]) for the row-sequential pass.
+__global__ void __launch_bounds__(kTT) proxy_he_kernel(const float* __restrict__ orig,
+                                                        const uint8_t* __restrict__ codes,
+                                                        const float* __restrict__ scales,
+                                                        const int32_t* __restrict__ zeros, int64_t rows, int64_t dim,
+                                                        int64_t gs, const float* __restrict__ h, int64_t r0,
+                                                        int64_t nrows, double* __restrict__ he_t) {
+    const int64_t i0 = r0 + static_cast<int64_t>(blockIdx.y) * kT, a0 = static_cast<int64_t>(blockIdx.x) * kT;
+    const int64_t G = (dim + gs - 1) / gs, rend = r0 + nrows;
+    __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
+    double acc[4][4] = {};
+    auto fa = [&](int64_t row, int64_t b) {
+        return row < rend ? static_cast<double>(err_elem(orig, codes, scales, zeros, row, b, dim, G, gs)) : 0.0;
+    };
+    auto fb = [&](int64_t b, int64_t a) { return a < dim ? static_cast<double>(h[a * dim + b]) : 0.0; };
+    tile_accumulate<false, true, true>(acc, i0, a0, 0, dim, fa, fb, As, Bs);
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t row = i0 + ty * 4 + ii, a = a0 + tx * 4 + jj;
+            if (row < rend && a < dim) he_t[a * nrows + (row - r0)] = acc[ii][jj];
+        }
+}
+
+// rowsum[row] = sum_a double(e[row][a]) * he[row][a], a ascending (quant.cpp:338-339)
+__global__ void proxy_rowsum_kernel(const float* __restrict__ orig, const uint8_t* __restrict__ codes,
+                                    const float* __restrict__ scales, const int32_t* __restrict__ zeros, int64_t dim,
+                                    int64_t gs, int64_t r0, int64_t nrows, const double* __restrict__ he_t,
+                                    double* __restrict__ rowsum) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= nrows) return;
+    const int64_t row = r0 + t, G = (dim + gs - 1) / gs;
+    double s = 0.0;
+    for (int64_t a = 0; a < dim; ++a) {
+        const double e = static_cast<double>(err_elem(orig, codes, scales, zeros, row, a, dim, G, gs));
+        s = __dadd_rn(s, __dmul_rn(e, he_t[a * nrows + t]));
+    }
+    rowsum[row] = s;
+}
+
+// total = sum_row rowsum[row], rows ascending (quant.cpp:340)
+__global__ void proxy_total_kernel(const double* __restrict__ rowsum, int64_t rows, double* __restrict__ total) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0;
+    for (int64_t r = 0; r < rows; ++r) s = __dadd_rn(s, rowsum[r]);
+    *total = s;
+}
+
+unsigned grid_for(int64_t n, int threads) {
+    const int64_t b = (n + threads - 1) / threads;
+    return static_cast<unsigned>(b < 148 * 16 ? (b < 1 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+cudaError_t launch_estimate_hessian(const float* x, int64_t tokens, int64_t dim, double damping, double* acc,
+                                    double* lambda, float* h, cudaStream_t stream) {
+    const unsigned nt = static_cast<unsigned>((dim + kT - 1) / kT);
+    hessian_acc_kernel<<<dim3(nt, nt), kTT, 0, stream>>>(x, tokens, dim, acc);
+    hessian_lambda_kernel<<<1, 32, 0, stream>>>(acc, tokens, dim, damping, lambda);
+    hessian_fill_kernel<<<grid_for(dim * dim, 256), 256, 0, stream>>>(acc, tokens, dim, lambda, h);
+    return cudaGetLastError();
+}
+
+size_t spd_status_bytes() { return sizeof(SpdStatus); }
+
+// chol / linv: n x n f64 scratch each; status: spd_status_bytes() of device memory
+cudaError_t launch_spd_inverse(const float* h, int64_t n, double* chol, double* linv, double* hinv, void* status,
+                               cudaStream_t stream) {
+    SpdStatus* st = static_cast<SpdStatus*>(status);
+    cudaError_t e = cudaMemsetAsync(st, 0, sizeof(SpdStatus), stream);
+    if (e != cudaSuccess) return e;
+    chol_init_kernel<<<grid_for(n * n, 256), 256, 0, stream>>>(h, n, chol);
+    const size_t rows_smem = sizeof(double) * (kT + kRowsPerCta) * (kT + 1);
+    e = cudaFuncSetAttribute(chol_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(rows_smem));
+    if (e != cudaSuccess) return e;
+    for (int64_t j0 = 0; j0 < n; j0 += kT) {
+        if (j0 > 0)
+            chol_update_kernel<<<static_cast<unsigned>((n - j0 + kT - 1) / kT), kTT, 0, stream>>>(chol, n, j0, st);
+        chol_diag_kernel<<<1, kT, 0, stream>>>(chol, n, j0, st);
+        const int64_t below = n - j0 - kT;
+        if (below > 0)
+            chol_rows_kernel<<<static_cast<unsigned>((below + kRowsPerCta - 1) / kRowsPerCta), kRowsPerCta, rows_smem,
+                               stream>>>(chol, n, j0, st);
+    }
+    e = cudaMemsetAsync(linv, 0, sizeof(double) * n * n, stream);
+    if (e != cudaSuccess) return e;
+    for (int64_t i0 = 0; i0 < n; i0 += kT) {
+        if (i0 > 0) linv_update_kernel<<<static_cast<unsigned>((i0 + kT - 1) / kT), kTT, 0, stream>>>(chol, linv, n, i0, st);
+        const int64_t cols = (n - i0 < kT ? n : i0 + kT);
+        linv_block_kernel<<<static_cast<unsigned>((cols + kRowsPerCta - 1) / kRowsPerCta), kRowsPerCta, 0, stream>>>(
+            chol, linv, n, i0, st);
+    }
+    const unsigned nt = static_cast<unsigned>((n + kT - 1) / kT);
+    hinv_kernel<<<dim3(nt, nt), kTT, 0, stream>>>(linv, n, hinv, st);
+    return cudaGetLastError();
+}
+
+void spd_status_read(const void* host_copy, int* failed, int64_t* column, double* pivot) {
+    const SpdStatus* s = static_cast<const SpdStatus*>(host_copy);
+    *failed = s->failed;
+    *column = s->column;
+    *pivot = s->pivot;
+}
+
+cudaError_t launch_make_grids(const float* r, int64_t rows, int64_t cols, int bits, int64_t gs, float* scales,
+                              int32_t* zeros, cudaStream_t stream) {
+    const int64_t n = rows * ((cols + gs - 1) / gs);
+    grids_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(r, rows, cols, bits, gs, scales, zeros);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rtn_codes(const float* r, int64_t rows, int64_t cols, int bits, int64_t gs, const float* scales,
+                             const int32_t* zeros, uint8_t* codes, cudaStream_t stream) {
+    rtn_codes_kernel<<<grid_for(rows * cols, 256), 256, 0, stream>>>(r, rows, cols, bits, gs, scales, zeros, codes);
+    return cudaGetLastError();
+}
+
+int gptq_rows_per_cta(int64_t dim) {
+    const int64_t budget = 200 * 1024 / 8;   // doubles of shared memory
+    return dim * 4 <= budget ? 4 : dim * 2 <= budget ? 2 : dim <= budget ? 1 : 0;
+}
+
+cudaError_t launch_gptq(const float* r, int64_t rows, int64_t dim, int bits, int64_t gs, const float* scales,
+                        const int32_t* zeros, const double* hinv, uint8_t* codes, cudaStream_t stream) {
+    const int R = gptq_rows_per_cta(dim);
+    if (R == 0) return cudaErrorInvalidValue;
+    const size_t smem = sizeof(double) * R * dim;
+    const unsigned grid = static_cast<unsigned>((rows + R - 1) / R);
+    cudaError_t e;
+    switch (R) {
+        case 4:
+            e = cudaFuncSetAttribute(gptq_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            gptq_kernel<4><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
+            break;
+        case 2:
+            e = cudaFuncSetAttribute(gptq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            gptq_kernel<2><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
+            break;
+        default:
+            e = cudaFuncSetAttribute(gptq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            if (e != cudaSuccess) return e;
+            gptq_kernel<1><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
+    }
+    return cudaGetLastError();
+}
+
+// he_t: chunk_rows x dim f64 scratch; rowsum: rows f64; total: 1 f64 (device)
+cudaError_t launch_proxy_loss(const float* orig, const uint8_t* codes, const float* scales, const int32_t* zeros,
+                              int64_t rows, int64_t dim, int64_t gs, const float* h, int64_t chunk_rows, double* he_t,
+                              double* rowsum, double* total, cudaStream_t stream) {
+    for (int64_t r0 = 0; r0 < rows; r0 += chunk_rows) {
+        const int64_t nr = rows - r0 < chunk_rows ? rows - r0 : chunk_rows;
+        const dim3 grid(static_cast<unsigned>((dim + kT - 1) / kT), static_cast<unsigned>((nr + kT - 1) / kT));
+        proxy_he_kernel<<<grid, kTT, 0, stream>>>(orig, codes, scales, zeros, rows, dim, gs, h, r0, nr, he_t);
+        proxy_rowsum_kernel<<<static_cast<unsigned>((nr + 127) / 128), 128, 0, stream>>>(orig, codes, scales, zeros,
+                                                                                          dim, gs, r0, nr, he_t,
+                                                                                          rowsum);
+    }
+    proxy_total_kernel<<<1, 32, 0, stream>>>(rowsum, rows, total);
+    return cudaGetLastError();
+}
+
+}  // namespace tqb

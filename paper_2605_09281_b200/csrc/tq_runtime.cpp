@@ -53,6 +53,23 @@ cudaError_t launch_decode(const DecParams& p, int dn, int grid, cudaStream_t str
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream);
 cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t stream);
+// artifact producer (tq_producer.cu)
+cudaError_t launch_estimate_hessian(const float* x, int64_t tokens, int64_t dim, double damping, double* acc,
+                                    double* lambda, float* h, cudaStream_t stream);
+size_t spd_status_bytes();
+cudaError_t launch_spd_inverse(const float* h, int64_t n, double* chol, double* linv, double* hinv, void* status,
+                               cudaStream_t stream);
+void spd_status_read(const void* host_copy, int* failed, int64_t* column, double* pivot);
+cudaError_t launch_make_grids(const float* r, int64_t rows, int64_t cols, int bits, int64_t gs, float* scales,
+                              int32_t* zeros, cudaStream_t stream);
+cudaError_t launch_rtn_codes(const float* r, int64_t rows, int64_t cols, int bits, int64_t gs, const float* scales,
+                             const int32_t* zeros, uint8_t* codes, cudaStream_t stream);
+int gptq_rows_per_cta(int64_t dim);
+cudaError_t launch_gptq(const float* r, int64_t rows, int64_t dim, int bits, int64_t gs, const float* scales,
+                        const int32_t* zeros, const double* hinv, uint8_t* codes, cudaStream_t stream);
+cudaError_t launch_proxy_loss(const float* orig, const uint8_t* codes, const float* scales, const int32_t* zeros,
+                              int64_t rows, int64_t dim, int64_t gs, const float* h, int64_t chunk_rows, double* he_t,
+                              double* rowsum, double* total, cudaStream_t stream);
 cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int n_local, int slab, int mb_count, int bn,
                             int kc_end, int n_ext, Unit* units, int32_t* n_units, cudaStream_t stream);
 
@@ -2910,6 +2927,157 @@ tq_status tq_ep_combine(tq_layer* L, const float* x, int64_t batch, const float*
         ca.out = y;
         cuda_check(launch_combine(ca, st), "combine_kernel launch");
         count_launch(L);
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// artifact producer hot spots: estimate_hessian, spd_inverse,
+// quantize_rtn, quantize_gptq, proxy_loss (quant.cpp:72-221,325-343) on device
+// arrays.  Bit-identical to the reference (tq_producer.cu).
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// stream-ordered device scratch
+struct AsyncBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    AsyncBuf(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes) cuda_check(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync (producer scratch)");
+    }
+    ~AsyncBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    AsyncBuf(const AsyncBuf&) = delete;
+    AsyncBuf& operator=(const AsyncBuf&) = delete;
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+void check_quant_bits(int bits) {
+    if (bits != 2 && bits != 3 && bits != 4 && bits != 8)
+        fail(TQ_ERR_PARAM, "quantizer bits must be in {2,3,4,8}, got " + std::to_string(bits));
+}
+
+// spd_inverse into hinv (n x n f64, device); NumericError as quant.cpp:80-85
+void spd_inverse_dev(const float* h, int64_t n, double* hinv, cudaStream_t st) {
+    if (n == 0) return;
+    AsyncBuf chol(sizeof(double) * n * n, st), linv(sizeof(double) * n * n, st), status(spd_status_bytes(), st);
+    cuda_check(launch_spd_inverse(h, n, chol.as<double>(), linv.as<double>(), hinv, status.p, st),
+               "spd_inverse launch");
+    std::vector<unsigned char> host(spd_status_bytes());
+    cuda_check(cudaMemcpyAsync(host.data(), status.p, host.size(), cudaMemcpyDeviceToHost, st), "spd status D2H");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+    int failed = 0;
+    int64_t col = 0;
+    double pivot = 0.0;
+    spd_status_read(host.data(), &failed, &col, &pivot);
+    if (failed)
+        fail(TQ_ERR_NUMERIC, "Hessian is singular after damping (pivot " + std::to_string(pivot) + " at column " +
+                                 std::to_string(col) + "); increase damping_fraction");
+}
+
+double proxy_loss_dev(const float* original, int64_t rows, int64_t cols, const uint8_t* codes, const float* scales,
+                      const int32_t* zeros, int64_t gs, const float* h, cudaStream_t st) {
+    if (rows == 0 || cols == 0) return 0.0;
+    const int64_t chunk = std::min<int64_t>(rows, std::max<int64_t>(64, (int64_t{256} << 20) / (8 * cols)));
+    AsyncBuf he(sizeof(double) * chunk * cols, st), rowsum(sizeof(double) * rows, st), total(sizeof(double), st);
+    cuda_check(launch_proxy_loss(original, codes, scales, zeros, rows, cols, gs, h, chunk, he.as<double>(),
+                                 rowsum.as<double>(), total.as<double>(), st),
+               "proxy_loss launch");
+    double out = 0.0;
+    cuda_check(cudaMemcpyAsync(&out, total.p, sizeof(double), cudaMemcpyDeviceToHost, st), "proxy D2H");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+    return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+tq_status tq_estimate_hessian(const float* calib, int64_t tokens, int64_t dim, double damping_fraction, float* h,
+                              double* damping_out, void* stream) {
+    return guarded([&] {
+        if (tokens < 0 || dim < 0) fail(TQ_ERR_PARAM, "estimate_hessian: negative size");
+        if (tokens == 0 || dim == 0) fail(TQ_ERR_DATA, "estimate_hessian: empty calibration set");
+        if (damping_fraction < 0.0) fail(TQ_ERR_PARAM, "estimate_hessian: damping_fraction must be >= 0");
+        if (!calib || !h) fail(TQ_ERR_PARAM, "estimate_hessian: null buffer");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        AsyncBuf acc(sizeof(double) * dim * dim, st), lam(sizeof(double), st);
+        cuda_check(launch_estimate_hessian(calib, tokens, dim, damping_fraction, acc.as<double>(), lam.as<double>(),
+                                           h, st),
+                   "estimate_hessian launch");
+        if (damping_out) {
+            cuda_check(cudaMemcpyAsync(damping_out, lam.p, sizeof(double), cudaMemcpyDeviceToHost, st), "lambda D2H");
+            cuda_check(cudaStreamSynchronize(st), "stream sync");
+        }
+    });
+}
+
+tq_status tq_spd_inverse(const float* h, int64_t n, double* hinv, void* stream) {
+    return guarded([&] {
+        if (n < 0 || (n > 0 && (!h || !hinv))) fail(TQ_ERR_PARAM, "spd_inverse: bad arguments");
+        spd_inverse_dev(h, n, hinv, static_cast<cudaStream_t>(stream));
+    });
+}
+
+tq_status tq_quantize_rtn(const float* r, int64_t rows, int64_t cols, int bits, int64_t group_size, uint8_t* codes,
+                          float* scales, int32_t* zeros, void* stream) {
+    return guarded([&] {
+        check_quant_bits(bits);
+        if (group_size < 1) fail(TQ_ERR_PARAM, "quantize_rtn: group_size must be >= 1");
+        if (rows <= 0 || cols <= 0) fail(TQ_ERR_PARAM, "quantize_rtn: empty input");
+        if (!r || !codes || !scales || !zeros) fail(TQ_ERR_PARAM, "quantize_rtn: null buffer");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        cuda_check(launch_make_grids(r, rows, cols, bits, group_size, scales, zeros, st), "grids launch");
+        cuda_check(launch_rtn_codes(r, rows, cols, bits, group_size, scales, zeros, codes, st), "rtn launch");
+    });
+}
+
+tq_status tq_quantize_gptq(const float* r, int64_t rows, int64_t cols, const float* h, int bits, int64_t group_size,
+                           uint8_t* codes, float* scales, int32_t* zeros, int32_t* used_rtn, void* stream) {
+    return guarded([&] {
+        check_quant_bits(bits);
+        if (group_size < 1) fail(TQ_ERR_PARAM, "quantize_gptq: group_size must be >= 1");
+        if (rows < 0 || cols < 0) fail(TQ_ERR_PARAM, "quantize_gptq: negative size");
+        if (cols > 0 && gptq_rows_per_cta(cols) == 0)
+            fail(TQ_ERR_PARAM, "quantize_gptq: in_dim " + std::to_string(cols) +
+                                   " exceeds the engine's limit (25600: one working row in shared memory)");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        AsyncBuf hinv(sizeof(double) * cols * cols, st);
+        spd_inverse_dev(h, cols, hinv.as<double>(), st);                       // quant.cpp:187
+        if (rows == 0 || cols == 0) fail(TQ_ERR_PARAM, "quantize_rtn: empty input");   // quant.cpp:218 -> :155
+        if (!r || !codes || !scales || !zeros) fail(TQ_ERR_PARAM, "quantize_gptq: null buffer");
+        cuda_check(launch_make_grids(r, rows, cols, bits, group_size, scales, zeros, st), "grids launch");
+        cuda_check(launch_gptq(r, rows, cols, bits, group_size, scales, zeros, hinv.as<double>(), codes, st),
+                   "gptq launch");
+        // keep the better of GPTQ and plain rounding (same grids) -- quant.cpp:216-219
+        AsyncBuf rtn(static_cast<size_t>(rows * cols), st);
+        cuda_check(launch_rtn_codes(r, rows, cols, bits, group_size, scales, zeros, rtn.as<uint8_t>(), st),
+                   "rtn launch");
+        const double lg = proxy_loss_dev(r, rows, cols, codes, scales, zeros, group_size, h, st);
+        const double lr = proxy_loss_dev(r, rows, cols, rtn.as<uint8_t>(), scales, zeros, group_size, h, st);
+        const bool take_rtn = lg > lr;
+        if (take_rtn)
+            cuda_check(cudaMemcpyAsync(codes, rtn.p, static_cast<size_t>(rows * cols), cudaMemcpyDeviceToDevice, st),
+                       "rtn codes D2D");
+        if (used_rtn) *used_rtn = take_rtn ? 1 : 0;
+    });
+}
+
+tq_status tq_proxy_loss(const float* original, int64_t rows, int64_t cols, const uint8_t* codes, const float* scales,
+                        const int32_t* zeros, int bits, int64_t group_size, const float* h, double* loss,
+                        void* stream) {
+    return guarded([&] {
+        check_quant_bits(bits);
+        if (group_size < 1) fail(TQ_ERR_PARAM, "proxy_loss: group_size must be >= 1");
+        if (rows < 0 || cols < 0 || !loss) fail(TQ_ERR_PARAM, "proxy_loss: bad arguments");
+        *loss = proxy_loss_dev(original, rows, cols, codes, scales, zeros, group_size, h,
+                               static_cast<cudaStream_t>(stream));
     });
 }
 

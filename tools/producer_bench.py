@@ -1,0 +1,102 @@
+"""Time the GPU artifact-producer stages at the Mixtral (c2) expert
+shape and the reference's CPU implementation on bounded samples.
+
+    python tools/producer_bench.py [--rows 14336] [--dim 4096] [--tokens 512] [--cpu-rows 8]
+
+GPU: CUDA events around each stage (estimate_hessian over `tokens` calibration
+rows; spd_inverse; quantize_rtn; quantize_gptq = spd_inverse + grids + the
+column sweep + RTN + two proxy losses; proxy_loss).  CPU: the reference
+(oracle/_ref) on the same dim with `cpu-rows` residual rows, one thread, and
+the per-row cost scaled to `rows` (the row loops are independent; spd_inverse
+is paid once per call and reported separately).  Prints one JSON line.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--rows", type=int, default=14336)
+    ap.add_argument("--dim", type=int, default=4096)
+    ap.add_argument("--tokens", type=int, default=512)
+    ap.add_argument("--bits", type=int, default=3)
+    ap.add_argument("--gs", type=int, default=128)
+    ap.add_argument("--cpu-rows", type=int, default=8)
+    ap.add_argument("--cpu-dim", type=int, default=0, help="dim of the CPU sample (default: --dim)")
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    import torch
+    from paper_2605_09281_b200 import producer as P
+
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev).manual_seed(0)
+    calib = torch.randn((a.tokens, a.dim), device=dev, generator=g)
+    r = torch.randn((a.rows, a.dim), device=dev, generator=g) * 0.02
+    out = {"config": {"rows": a.rows, "dim": a.dim, "tokens": a.tokens, "bits": a.bits, "group_size": a.gs}}
+
+    def timed(fn, reps=1):
+        fn()   # warm-up (allocator, module load)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            res = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, res
+
+    t_h, hp = timed(lambda: P.estimate_hessian(calib, 0.01))
+    t_inv, _ = timed(lambda: P.spd_inverse(hp))
+    t_rtn, q_rtn = timed(lambda: P.quantize_rtn(r, a.bits, a.gs))
+    t_gptq, q = timed(lambda: P.quantize_gptq(r, hp, a.bits, a.gs))
+    t_proxy, loss = timed(lambda: P.proxy_loss(r, q, hp))
+    gpu = {"estimate_hessian_ms": t_h, "spd_inverse_ms": t_inv, "quantize_rtn_ms": t_rtn,
+           "quantize_gptq_ms": t_gptq, "proxy_loss_ms": t_proxy, "gptq_used_rtn": q.used_rtn,
+           "proxy_loss": loss}
+    # FP64 work per stage (mul + add or mul + div + sub counted as one element op)
+    d, R, T = a.dim, a.rows, a.tokens
+    gpu["proxy_loss_f64_macs"] = R * d * d + R * d
+    gpu["proxy_loss_gmac_per_s"] = gpu["proxy_loss_f64_macs"] / (t_proxy * 1e6)
+    gpu["gptq_sweep_updates"] = R * d * (d - 1) // 2
+    out["gpu"] = gpu
+
+    if not a.no_cpu:
+        from oracle.oracle import RefLib
+        ref = RefLib()
+        cd = a.cpu_dim or a.dim
+        cn = a.cpu_rows
+        rs = r[:cn, :cd].float().cpu().numpy()
+        cs = calib[:, :cd].float().cpu().numpy()
+        t0 = time.perf_counter()
+        h_ref, _ = ref.estimate_hessian(cs, 0.01)
+        t_h_cpu = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        c, s, z = ref.quantize("rtn", rs, None, a.bits, a.gs)
+        t_rtn_cpu = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref.proxy_loss(rs, c, s, z, a.bits, a.gs, h_ref)
+        t_proxy_cpu = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        ref.quantize("gptq", rs, h_ref, a.bits, a.gs)
+        t_gptq_cpu = time.perf_counter() - t0
+        # quantize_gptq = spd_inverse + sweep + rtn + 2 proxy losses; isolate spd_inverse
+        t_inv_cpu = max(t_gptq_cpu - 2 * t_proxy_cpu - t_rtn_cpu - 0.0, 0.0)
+        scale = a.rows / cn
+        out["cpu_reference"] = {
+            "threads": 1, "sample": f"{cn} residual rows x dim {cd}, {T} calibration tokens",
+            "estimate_hessian_s": t_h_cpu, "proxy_loss_s_sample": t_proxy_cpu, "quantize_gptq_s_sample": t_gptq_cpu,
+            "proxy_loss_s_scaled_to_rows": t_proxy_cpu * scale,
+            "quantize_gptq_s_scaled_to_rows": t_inv_cpu + (t_gptq_cpu - t_inv_cpu) * scale if cd == a.dim else None,
+        }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

@@ -152,12 +152,18 @@ __global__ void chol_init_kernel(const float* __restrict__ h, int64_t n, double*
     }
 }
 
-// Trailing update of panel [j0, j0 + kT): C[i][j] -= C[i][k] * C[j][k] for k = 0 .. j0-1
-// ascending, rows i >= j0 (quant.cpp:77-78 for the columns already finished).
-__global__ void __launch_bounds__(kTT) chol_update_kernel(double* __restrict__ c, int64_t n, int64_t j0,
-                                                           const SpdStatus* __restrict__ st) {
+// Right-looking trailing update after panel [j0, j0 + kT) is factored:
+// C[i][j] -= C[i][k] * C[j][k] for k = j0 .. j0+kT-1 ascending, over the trailing
+// lower triangle i >= j >= j0 + kT.  Panels run in order, so every element still
+// receives its k = 0 .. j-1 subtractions in the reference's order
+// (quant.cpp:77-78) -- the work of one panel spread over the whole trailing
+// matrix instead of one K = j0 chain per output.
+__global__ void __launch_bounds__(kTT) chol_trail_kernel(double* __restrict__ c, int64_t n, int64_t j0,
+                                                          const SpdStatus* __restrict__ st) {
     if (st->failed) return;
-    const int64_t i0 = j0 + static_cast<int64_t>(blockIdx.x) * kT;
+    const int64_t j1 = j0 + kT;
+    const int64_t i0 = j1 + static_cast<int64_t>(blockIdx.y) * kT, jt0 = j1 + static_cast<int64_t>(blockIdx.x) * kT;
+    if (jt0 > i0) return;   // tile above the diagonal
     __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
     double acc[4][4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -165,17 +171,17 @@ __global__ void __launch_bounds__(kTT) chol_update_kernel(double* __restrict__ c
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            const int64_t i = i0 + ty * 4 + ii, j = jt0 + tx * 4 + jj;
             acc[ii][jj] = (i < n && j < n && j <= i) ? c[i * n + j] : 0.0;
         }
     auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
     auto fb = [&](int64_t k, int64_t j) { return j < n ? c[j * n + k] : 0.0; };
-    tile_accumulate<true, true, true>(acc, i0, j0, 0, j0, fa, fb, As, Bs);
+    tile_accumulate<true, true, true>(acc, i0, jt0, j0, j1, fa, fb, As, Bs);
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            const int64_t i = i0 + ty * 4 + ii, j = jt0 + tx * 4 + jj;
             if (i < n && j < n && j <= i) c[i * n + j] = acc[ii][jj];
         }
 }
@@ -246,26 +252,36 @@ __global__ void __launch_bounds__(kRowsPerCta) chol_rows_kernel(double* __restri
     for (int j = 0; j < w; ++j) c[i * n + j0 + j] = row[j];
 }
 
-// L^-1, row block [i0, i0 + kT): partial sums over the finished rows,
-// acc[i][j] = sum_{k < i0} L[i][k] * Linv[k][j] for j < i0 (k ascending; the terms
-// k < j are exact zero products, so starting the sum at the tile's first column
-// matches the reference's k = j start), parked in Linv[i][j] (quant.cpp:96-99).
-__global__ void __launch_bounds__(kTT) linv_update_kernel(const double* __restrict__ c, double* __restrict__ li,
-                                                           int64_t n, int64_t i0, const SpdStatus* __restrict__ st) {
+// L^-1, right-looking: once rows [i0, i0 + kT) of L^-1 are final, every later
+// row's partial sums take their terms k = i0 .. i0+kT-1 in order:
+// Linv[i][j] += L[i][k] * Linv[k][j] for i >= i0 + kT, j < i0 + kT (quant.cpp:96-99).
+// Partial sums are parked in Linv[i][j] until row i's own block finishes them.
+// Terms with k < j are exact zero products on a +0-started sum (the reference
+// starts at k = j).
+__global__ void __launch_bounds__(kTT) linv_trail_kernel(const double* __restrict__ c, double* __restrict__ li,
+                                                          int64_t n, int64_t i0, const SpdStatus* __restrict__ st) {
     if (st->failed) return;
-    const int64_t j0 = static_cast<int64_t>(blockIdx.x) * kT;
+    const int64_t i1 = i0 + kT;
+    const int64_t r0 = i1 + static_cast<int64_t>(blockIdx.y) * kT, j0 = static_cast<int64_t>(blockIdx.x) * kT;
     __shared__ double As[kKC][kT + 2], Bs[kKC][kT + 2];
-    double acc[4][4] = {};
-    auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
-    auto fb = [&](int64_t k, int64_t j) { return li[k * n + j]; };
-    tile_accumulate<false, true, false>(acc, i0, j0, j0, i0, fa, fb, As, Bs);
+    double acc[4][4];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
-            if (i < n && j < i0) li[i * n + j] = acc[ii][jj];
+            const int64_t i = r0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            acc[ii][jj] = (i < n && j < i1) ? li[i * n + j] : 0.0;
+        }
+    auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
+    auto fb = [&](int64_t k, int64_t j) { return j < i1 ? li[k * n + j] : 0.0; };
+    tile_accumulate<false, true, false>(acc, r0, j0, i0, i1, fa, fb, As, Bs);
+#pragma unroll
+    for (int ii = 0; ii < 4; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int64_t i = r0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            if (i < n && j < i1) li[i * n + j] = acc[ii][jj];
         }
 }
 
@@ -380,53 +396,116 @@ __global__ void rtn_codes_kernel(const float* __restrict__ r, int64_t rows, int6
     }
 }
 
-// GPTQ column sweep (quant.cpp:200-213).  A CTA owns kR rows, their working rows
-// in shared memory; columns are dealt to threads round-robin so the shrinking
-// trailing range stays balanced.  Per column j: every thread forms the code and
-// error of column j for its rows (work[j] is final after the previous barrier),
-// then updates its own columns c > j: work[c] -= err * Hinv[j][c] / Hinv[j][j].
+// RN(a / d) given y = RN(1 / d): q0 = a*y, one FMA correction, then an exact
+// check that q1 is the correctly rounded quotient -- |a - q1*d| (exact by FMA)
+// below half an ulp of q1 times |d| (a quotient of two doubles is never a
+// midpoint, so no tie case) -- else the full __ddiv_rn.  Saves the per-element
+// reciprocal when one divisor serves a whole row segment.
+__device__ __forceinline__ double div_rn_by(double a, double d, double y) {
+    if (a == 0.0) return __dmul_rn(a, y);   // the signed zero a / d
+    const double q0 = __dmul_rn(a, y);
+    const double q1 = __fma_rn(__fma_rn(-q0, d, a), y, q0);
+    const double r1 = __fma_rn(-q1, d, a);
+    const long long qb = __double_as_longlong(q1), db = __double_as_longlong(d);
+    const int eq = static_cast<int>((qb >> 52) & 0x7ff), ed = static_cast<int>((db >> 52) & 0x7ff);
+    if (eq > 200 && eq < 1800 && ed > 200 && ed < 1800) {
+        // half an ulp of q1 (the smaller one below a power of two), times |d|: exact
+        const int eh = eq - 53 - ((qb & 0xfffffffffffffLL) == 0 ? 1 : 0);
+        const double bound = __dmul_rn(fabs(d), __longlong_as_double(static_cast<long long>(eh) << 52));
+        if (fabs(r1) < bound) return q1;
+    }
+    return __ddiv_rn(a, d);
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// GPTQ column sweep (quant.cpp:200-213).  A CTA owns kR rows: their working rows
+// and grids sit in shared memory; columns are dealt to threads round-robin so
+// the shrinking trailing range stays balanced.  Per column j: every thread
+// forms the code and error of column j for its rows (work[j] is final after the
+// previous barrier), then updates its own columns c > j:
+// work[c] -= err * Hinv[j][c] / Hinv[j][j].  With kStage, row j+1 of Hinv is
+// copied into a second shared buffer (cp.async) while column j is processed, so
+// the sweep never waits on L2 latency between its barriers.
 constexpr int kGptqThreads = 512;
-template <int kR>
+template <int kR, bool kStage>
 __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restrict__ r, int64_t rows, int64_t dim,
                                                              int bits, int64_t gs, const float* __restrict__ scales,
                                                              const int32_t* __restrict__ zeros,
                                                              const double* __restrict__ hinv,
                                                              uint8_t* __restrict__ codes) {
-    extern __shared__ double work[];   // kR x dim
+    extern __shared__ double sm[];
+    const int64_t G = (dim + gs - 1) / gs;
+    double* work = sm;                                    // kR x dim
+    double* hb = sm + kR * dim;                           // 2 x dim (kStage)
+    float* gsc = reinterpret_cast<float*>(hb + (kStage ? 2 * dim : 0));   // kR x G
+    int32_t* gzp = reinterpret_cast<int32_t*>(gsc + kR * G);              // kR x G
     const int64_t row0 = static_cast<int64_t>(blockIdx.x) * kR;
     const int nr = static_cast<int>(rows - row0 < kR ? rows - row0 : kR);
-    const int64_t G = (dim + gs - 1) / gs;
     const double levels = static_cast<double>((1 << bits) - 1);
-    for (int q = 0; q < nr; ++q)
-        for (int64_t c = threadIdx.x; c < dim; c += kGptqThreads)
-            work[q * dim + c] = static_cast<double>(r[(row0 + q) * dim + c]);
+    const int tid = threadIdx.x;
+    for (int q = 0; q < nr; ++q) {
+        for (int64_t c = tid; c < dim; c += kGptqThreads) work[q * dim + c] = static_cast<double>(r[(row0 + q) * dim + c]);
+        for (int64_t g = tid; g < G; g += kGptqThreads) {
+            gsc[q * G + g] = scales[(row0 + q) * G + g];
+            gzp[q * G + g] = zeros[(row0 + q) * G + g];
+        }
+    }
+    if (kStage) {
+        for (int64_t c = tid; c < dim; c += kGptqThreads) cp_async8(hb + c, hinv + c);
+        cp_async_commit();
+        cp_async_wait_all();
+    }
     __syncthreads();
     for (int64_t j = 0; j < dim; ++j) {
+        const double* hrow;
+        if (kStage) {
+            const int buf = static_cast<int>(j & 1);
+            hrow = hb + buf * dim;
+            if (j + 1 < dim) {   // prefetch row j+1 (own columns >= j+1; the diagonal included)
+                const int64_t f = j + 1;
+                double* dst = hb + (buf ^ 1) * dim;
+                for (int64_t c = f + ((tid - f) % kGptqThreads + kGptqThreads) % kGptqThreads; c < dim;
+                     c += kGptqThreads)
+                    cp_async8(dst + c, hinv + f * dim + c);
+                cp_async_commit();
+            }
+        } else {
+            hrow = hinv + j * dim;
+        }
         double err[kR];
         const int64_t g = j / gs;
 #pragma unroll
         for (int q = 0; q < kR; ++q) {
             err[q] = 0.0;
             if (q < nr) {
-                const float s = scales[(row0 + q) * G + g];
-                const int32_t z = zeros[(row0 + q) * G + g];
+                const float sc = gsc[q * G + g];
+                const int32_t z = gzp[q * G + g];
                 const double wj = work[q * dim + j];
-                const uint32_t code = encode_one(wj, s, z, levels);
+                const uint32_t code = encode_one(wj, sc, z, levels);
                 const double deq = __dmul_rn(__dsub_rn(static_cast<double>(code), static_cast<double>(z)),
-                                             static_cast<double>(s));
+                                             static_cast<double>(sc));
                 err[q] = __dsub_rn(wj, deq);
-                if (threadIdx.x == q) codes[(row0 + q) * dim + j] = static_cast<uint8_t>(code);
+                if (tid == q) codes[(row0 + q) * dim + j] = static_cast<uint8_t>(code);
             }
         }
-        const double inv_jj = hinv[j * dim + j];
+        const double inv_jj = hrow[j];
+        const double rcp = __drcp_rn(inv_jj);
         const int64_t first = j + 1;
-        int64_t c = first + ((static_cast<int64_t>(threadIdx.x) - first) % kGptqThreads + kGptqThreads) % kGptqThreads;
-        for (; c < dim; c += kGptqThreads) {
-            const double h = hinv[j * dim + c];
+        for (int64_t c = first + ((tid - first) % kGptqThreads + kGptqThreads) % kGptqThreads; c < dim;
+             c += kGptqThreads) {
+            const double h = hrow[c];
 #pragma unroll
             for (int q = 0; q < kR; ++q)
-                if (q < nr) work[q * dim + c] = __dsub_rn(work[q * dim + c], __ddiv_rn(__dmul_rn(err[q], h), inv_jj));
+                if (q < nr)
+                    work[q * dim + c] = __dsub_rn(work[q * dim + c], div_rn_by(__dmul_rn(err[q], h), inv_jj, rcp));
         }
+        if (kStage) cp_async_wait_all();
         __syncthreads();
     }
 }
@@ -530,21 +609,25 @@ cudaError_t launch_spd_inverse(const float* h, int64_t n, double* chol, double* 
                              static_cast<int>(rows_smem));
     if (e != cudaSuccess) return e;
     for (int64_t j0 = 0; j0 < n; j0 += kT) {
-        if (j0 > 0)
-            chol_update_kernel<<<static_cast<unsigned>((n - j0 + kT - 1) / kT), kTT, 0, stream>>>(chol, n, j0, st);
         chol_diag_kernel<<<1, kT, 0, stream>>>(chol, n, j0, st);
         const int64_t below = n - j0 - kT;
-        if (below > 0)
+        if (below > 0) {
             chol_rows_kernel<<<static_cast<unsigned>((below + kRowsPerCta - 1) / kRowsPerCta), kRowsPerCta, rows_smem,
                                stream>>>(chol, n, j0, st);
+            const unsigned t = static_cast<unsigned>((below + kT - 1) / kT);
+            chol_trail_kernel<<<dim3(t, t), kTT, 0, stream>>>(chol, n, j0, st);
+        }
     }
     e = cudaMemsetAsync(linv, 0, sizeof(double) * n * n, stream);
     if (e != cudaSuccess) return e;
     for (int64_t i0 = 0; i0 < n; i0 += kT) {
-        if (i0 > 0) linv_update_kernel<<<static_cast<unsigned>((i0 + kT - 1) / kT), kTT, 0, stream>>>(chol, linv, n, i0, st);
         const int64_t cols = (n - i0 < kT ? n : i0 + kT);
         linv_block_kernel<<<static_cast<unsigned>((cols + kRowsPerCta - 1) / kRowsPerCta), kRowsPerCta, 0, stream>>>(
             chol, linv, n, i0, st);
+        const int64_t below = n - i0 - kT;
+        if (below > 0)
+            linv_trail_kernel<<<dim3(static_cast<unsigned>((i0 + kT) / kT), static_cast<unsigned>((below + kT - 1) / kT)),
+                                kTT, 0, stream>>>(chol, linv, n, i0, st);
     }
     const unsigned nt = static_cast<unsigned>((n + kT - 1) / kT);
     hinv_kernel<<<dim3(nt, nt), kTT, 0, stream>>>(linv, n, hinv, st);
@@ -571,35 +654,58 @@ cudaError_t launch_rtn_codes(const float* r, int64_t rows, int64_t cols, int bit
     return cudaGetLastError();
 }
 
-int gptq_rows_per_cta(int64_t dim) {
-    const int64_t budget = 200 * 1024 / 8;   // doubles of shared memory
-    return dim * 4 <= budget ? 4 : dim * 2 <= budget ? 2 : dim <= budget ? 1 : 0;
+namespace {
+constexpr size_t kGptqSmemBudget = 220 * 1024;
+size_t gptq_smem(int R, bool stage, int64_t dim, int64_t G) {
+    return sizeof(double) * (R + (stage ? 2 : 0)) * dim + (sizeof(float) + sizeof(int32_t)) * R * G;
+}
+// (rows per CTA, staged Hinv rows) for this shape; R = 0 when even one row does not fit
+void gptq_config(int64_t dim, int64_t gs, int* R, bool* stage) {
+    const int64_t G = (dim + gs - 1) / gs;
+    for (bool st : {true, false})
+        for (int r : {4, 2, 1})
+            if (gptq_smem(r, st, dim, G) <= kGptqSmemBudget) {
+                *R = r;
+                *stage = st;
+                return;
+            }
+    *R = 0;
+    *stage = false;
+}
+template <int kR, bool kStage>
+cudaError_t launch_gptq_t(const float* r, int64_t rows, int64_t dim, int bits, int64_t gs, const float* scales,
+                          const int32_t* zeros, const double* hinv, uint8_t* codes, cudaStream_t stream) {
+    const size_t smem = gptq_smem(kR, kStage, dim, (dim + gs - 1) / gs);
+    cudaError_t e = cudaFuncSetAttribute(gptq_kernel<kR, kStage>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    gptq_kernel<kR, kStage><<<static_cast<unsigned>((rows + kR - 1) / kR), kGptqThreads, smem, stream>>>(
+        r, rows, dim, bits, gs, scales, zeros, hinv, codes);
+    return cudaGetLastError();
+}
+}  // namespace
+
+int gptq_rows_per_cta(int64_t dim, int64_t gs) {
+    int R;
+    bool st;
+    gptq_config(dim, gs, &R, &st);
+    return R;
 }
 
 cudaError_t launch_gptq(const float* r, int64_t rows, int64_t dim, int bits, int64_t gs, const float* scales,
                         const int32_t* zeros, const double* hinv, uint8_t* codes, cudaStream_t stream) {
-    const int R = gptq_rows_per_cta(dim);
+    int R;
+    bool st;
+    gptq_config(dim, gs, &R, &st);
     if (R == 0) return cudaErrorInvalidValue;
-    const size_t smem = sizeof(double) * R * dim;
-    const unsigned grid = static_cast<unsigned>((rows + R - 1) / R);
-    cudaError_t e;
-    switch (R) {
-        case 4:
-            e = cudaFuncSetAttribute(gptq_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            gptq_kernel<4><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
-            break;
-        case 2:
-            e = cudaFuncSetAttribute(gptq_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            gptq_kernel<2><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
-            break;
-        default:
-            e = cudaFuncSetAttribute(gptq_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            if (e != cudaSuccess) return e;
-            gptq_kernel<1><<<grid, kGptqThreads, smem, stream>>>(r, rows, dim, bits, gs, scales, zeros, hinv, codes);
+    if (st) {
+        if (R == 4) return launch_gptq_t<4, true>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
+        if (R == 2) return launch_gptq_t<2, true>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
+        return launch_gptq_t<1, true>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
     }
-    return cudaGetLastError();
+    if (R == 4) return launch_gptq_t<4, false>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
+    if (R == 2) return launch_gptq_t<2, false>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
+    return launch_gptq_t<1, false>(r, rows, dim, bits, gs, scales, zeros, hinv, codes, stream);
 }
 
 // he_t: chunk_rows x dim f64 scratch; rowsum: rows f64; total: 1 f64 (device)

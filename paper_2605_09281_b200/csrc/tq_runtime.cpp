@@ -64,7 +64,7 @@ cudaError_t launch_make_grids(const float* r, int64_t rows, int64_t cols, int bi
                               int32_t* zeros, cudaStream_t stream);
 cudaError_t launch_rtn_codes(const float* r, int64_t rows, int64_t cols, int bits, int64_t gs, const float* scales,
                              const int32_t* zeros, uint8_t* codes, cudaStream_t stream);
-int gptq_rows_per_cta(int64_t dim);
+int gptq_rows_per_cta(int64_t dim, int64_t gs);
 cudaError_t launch_gptq(const float* r, int64_t rows, int64_t dim, int bits, int64_t gs, const float* scales,
                         const int32_t* zeros, const double* hinv, uint8_t* codes, cudaStream_t stream);
 cudaError_t launch_proxy_loss(const float* orig, const uint8_t* codes, const float* scales, const int32_t* zeros,
@@ -3044,9 +3044,9 @@ tq_status tq_quantize_gptq(const float* r, int64_t rows, int64_t cols, const flo
         check_quant_bits(bits);
         if (group_size < 1) fail(TQ_ERR_PARAM, "quantize_gptq: group_size must be >= 1");
         if (rows < 0 || cols < 0) fail(TQ_ERR_PARAM, "quantize_gptq: negative size");
-        if (cols > 0 && gptq_rows_per_cta(cols) == 0)
+        if (cols > 0 && gptq_rows_per_cta(cols, group_size) == 0)
             fail(TQ_ERR_PARAM, "quantize_gptq: in_dim " + std::to_string(cols) +
-                                   " exceeds the engine's limit (25600: one working row in shared memory)");
+                                   " exceeds the engine's limit (one working row and its grids in shared memory)");
         const cudaStream_t st = static_cast<cudaStream_t>(stream);
         AsyncBuf hinv(sizeof(double) * cols * cols, st);
         spd_inverse_dev(h, cols, hinv.as<double>(), st);                       // quant.cpp:187

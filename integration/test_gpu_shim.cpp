@@ -20,15 +20,27 @@
 //                           quantized layer tracks the full-precision layer
 //   test_io.cpp:220-234     artifact round trip: forward from the directory == forward from memory
 //   test_moe.cpp:110-191    route: ids / gates equal the reference's route
+//   test_quant.cpp:52-113   estimate_hessian: rank-1 sample, isotropic inputs, exact damping,
+//                           PSD after damping, empty set -> DataError
+//   test_quant.cpp:115-193  quantize_rtn: grid-aligned exactness, constant groups, half-scale error
+//                           bound, grid contract, fixed point, short final group, domain errors
+//   test_quant.cpp:195-261  quantize_gptq: identity Hessian == RTN, the crafted 1x2 optimum,
+//                           never worse than RTN over seeded trials, degenerate / mismatched H
+//   test_quant.cpp:346-353  proxy_loss: identity Hessian == squared error
+//   (the producer functions are also checked bit for bit against the reference's own)
 #include <doctest.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <filesystem>
 #include <string>
 #include <vector>
 
 #include "tileq/errors.hpp"
 #include "tileq/infer.hpp"
+#include "tileq/lowrank.hpp"
 #include "tileq/io.hpp"
 #include "tileq/matrix.hpp"
 #include "tileq/moe.hpp"
@@ -311,4 +323,174 @@ TEST_CASE("artifact round trip: forward from the directory equals forward from m
     }
     CHECK_THROWS_WITH_AS(gpu::forward_from_artifact(bad, x), doctest::Contains("expert.2.codes"), FormatError);
     CHECK_THROWS_AS(gpu::forward_from_artifact(bad + "/nope", x), IoError);
+}
+
+// ---------------------------------------------------------------------------
+// artifact producer (test_quant.cpp), through tileq::gpu
+// ---------------------------------------------------------------------------
+
+namespace {
+
+HessianProxy proxy_of(const DenseMatrix& m) {
+    HessianProxy h;
+    h.h = m;
+    h.sample_count = 1;
+    return h;
+}
+
+bool same_quantized(const QuantizedExpert& a, const QuantizedExpert& b) {
+    if (a.packed != b.packed || a.grids.size() != b.grids.size()) return false;
+    for (std::size_t t = 0; t < a.grids.size(); ++t)
+        if (a.grids[t].scale != b.grids[t].scale || a.grids[t].zero_point != b.grids[t].zero_point) return false;
+    return true;
+}
+
+bool same_bits(const DenseMatrix& a, const DenseMatrix& b) {
+    return a.rows == b.rows && a.cols == b.cols &&
+           std::memcmp(a.data.data(), b.data.data(), a.data.size() * sizeof(float)) == 0;
+}
+
+}  // namespace
+
+TEST_CASE("producer: estimate_hessian properties and bit identity with the reference") {
+    DenseMatrix one(1, 4, 0.0f);   // a single basis-vector token: H = e0 e0^T
+    one.at(0, 0) = 1.0f;
+    const HessianProxy h1 = gpu::estimate_hessian(one, 0.0);
+    CHECK(h1.sample_count == 1);
+    for (std::size_t r = 0; r < 4; ++r)
+        for (std::size_t c = 0; c < 4; ++c) CHECK(h1.h.at(r, c) == (r == 0 && c == 0 ? 1.0f : 0.0f));
+
+    CounterRng rng(100);   // isotropic tokens: close to the identity, exactly symmetric
+    const DenseMatrix iso = gaussian_matrix(10000, 4, rng);
+    const HessianProxy hi = gpu::estimate_hessian(iso, 0.0);
+    for (std::size_t r = 0; r < 4; ++r)
+        for (std::size_t c = 0; c < 4; ++c) {
+            if (r == c) CHECK(hi.h.at(r, c) == doctest::Approx(1.0).epsilon(0.10));
+            else CHECK(std::fabs(hi.h.at(r, c)) < 0.1);
+            CHECK(hi.h.at(r, c) == hi.h.at(c, r));
+        }
+    CHECK(same_bits(hi.h, estimate_hessian(iso, 0.0).h));
+
+    CounterRng rng2(101);   // damping adds lambda = fraction * mean diagonal
+    const DenseMatrix calib = gaussian_matrix(50, 6, rng2);
+    const HessianProxy plain = gpu::estimate_hessian(calib, 0.0), damped = gpu::estimate_hessian(calib, 0.01);
+    double mean_diag = 0.0;
+    for (std::size_t j = 0; j < 6; ++j) mean_diag += plain.h.at(j, j);
+    CHECK(damped.damping == doctest::Approx(0.01 * mean_diag / 6.0).epsilon(1e-6));
+    for (std::size_t r = 0; r < 6; ++r)
+        for (std::size_t c = 0; c < 6; ++c)
+            CHECK(damped.h.at(r, c) == doctest::Approx(plain.h.at(r, c) + (r == c ? damped.damping : 0.0)).epsilon(1e-6));
+    const HessianProxy ref_damped = estimate_hessian(calib, 0.01);
+    CHECK(same_bits(damped.h, ref_damped.h));
+    CHECK(damped.damping == ref_damped.damping);
+
+    CounterRng rng3(102);   // fewer tokens than dims: still PSD with a floor near lambda
+    const HessianProxy hr = gpu::estimate_hessian(gaussian_matrix(3, 5, rng3), 0.01);
+    const LowRankFactor f = exact_svd_truncated(hr.h, 5);
+    CHECK(f.singulars[4] >= 0.0f);
+    CHECK(f.singulars[4] >= 0.5f * static_cast<float>(hr.damping));
+
+    CHECK_THROWS_AS(gpu::estimate_hessian(DenseMatrix(), 0.01), DataError);
+}
+
+TEST_CASE("producer: quantize_rtn contracts and bit identity with the reference") {
+    const DenseMatrix aligned = matrix_from({{0, 1, 2, 3}});   // on the grid: lossless
+    CHECK(max_abs_diff(dequantize(gpu::quantize_rtn(aligned, 2, 4)), aligned) == 0.0);
+
+    const DenseMatrix flat(2, 6, 1.5f);   // constant groups: one code, tiny error
+    const QuantizedExpert qf = gpu::quantize_rtn(flat, 3, 6);
+    CHECK(max_abs_diff(dequantize(qf), flat) < 1e-3);
+    const auto codes = unpack_codes(qf.packed, 3, qf.code_count());
+    for (std::size_t t = 1; t < codes.size(); ++t) CHECK(codes[t] == codes[0]);
+
+    CounterRng rng(2);   // error within half a step of the group's grid
+    const DenseMatrix g = gaussian_matrix(4, 8, rng);
+    const QuantizedExpert qg = gpu::quantize_rtn(g, 3, 8);
+    const DenseMatrix back = dequantize(qg);
+    for (std::size_t row = 0; row < 4; ++row)
+        for (std::size_t c = 0; c < 8; ++c)
+            CHECK(std::fabs(back.at(row, c) - g.at(row, c)) <= 0.5f * qg.grids[row].scale * (1.0f + 1e-3f));
+
+    CounterRng rng2(3);   // positive inputs: range pinned at zero, zero point 0, f16-exact scales
+    DenseMatrix pos = gaussian_matrix(3, 12, rng2);
+    for (float& v : pos.data) v = std::fabs(v) + 1.0f;
+    const QuantizedExpert qp = gpu::quantize_rtn(pos, 4, 4);
+    for (const QuantGrid& grid : qp.grids) {
+        CHECK(grid.scale > 0.0f);
+        CHECK(snap_f16(grid.scale) == grid.scale);
+        CHECK(grid.zero_point == 0);
+    }
+    CHECK(qp.packed.size() == packed_byte_length(qp.code_count(), 4));
+
+    CounterRng rng3(4);   // re-quantizing a dequantized matrix changes nothing
+    const DenseMatrix m = gaussian_matrix(5, 10, rng3);
+    for (int bits : {2, 4, 8}) {
+        const QuantizedExpert q1 = gpu::quantize_rtn(m, bits, 5);
+        const QuantizedExpert q2 = gpu::quantize_rtn(dequantize(q1), bits, 5);
+        CHECK(same_quantized(q1, q2));
+        CHECK(same_quantized(q1, quantize_rtn(m, bits, 5)));
+    }
+
+    CounterRng rng4(5);   // 7 = 4 + 3: a short final group; domain errors
+    const DenseMatrix r7 = gaussian_matrix(2, 7, rng4);
+    const QuantizedExpert q7 = gpu::quantize_rtn(r7, 2, 4);
+    CHECK(q7.groups_per_row() == 2);
+    CHECK(q7.grids.size() == 4);
+    CHECK(all_finite(dequantize(q7)));
+    CHECK(same_quantized(q7, quantize_rtn(r7, 2, 4)));
+    CHECK_THROWS_AS(gpu::quantize_rtn(r7, 5, 4), ParamError);
+    CHECK_THROWS_AS(gpu::quantize_rtn(r7, 2, 0), ParamError);
+}
+
+TEST_CASE("producer: quantize_gptq and proxy_loss contracts and bit identity with the reference") {
+    CounterRng rng(6);   // H = I: no feedback, GPTQ is RTN
+    const DenseMatrix r = gaussian_matrix(4, 9, rng);
+    const HessianProxy id = proxy_of(eye(9));
+    const QuantizedExpert g_id = gpu::quantize_gptq(r, id, 3, 3);
+    CHECK(g_id.packed == gpu::quantize_rtn(r, 3, 3).packed);
+    CHECK(std::fabs(gpu::proxy_loss(r, g_id, id) - gpu::proxy_loss(r, gpu::quantize_rtn(r, 3, 3), id)) < 1e-6);
+
+    // one row, two strongly coupled columns: the first column's rounding error is
+    // worth pushing into the second, which plain rounding cannot do; GPTQ finds
+    // the exhaustive optimum over the 16 code pairs of the shared grid
+    const DenseMatrix r2 = matrix_from({{0.35f, 2.0f}});
+    const DenseMatrix hm = matrix_from({{1.0f, 0.45f}, {0.45f, 0.25f}});
+    const HessianProxy hc = proxy_of(hm);
+    const QuantizedExpert rtn2 = gpu::quantize_rtn(r2, 2, 2);
+    const double l_rtn = gpu::proxy_loss(r2, rtn2, hc), l_gptq = gpu::proxy_loss(r2, gpu::quantize_gptq(r2, hc, 2, 2), hc);
+    CHECK(l_gptq < l_rtn - 0.05);
+    const QuantGrid grid = rtn2.grids[0];
+    double best = 1e300;
+    for (int c0 = 0; c0 < 4; ++c0)
+        for (int c1 = 0; c1 < 4; ++c1) {
+            const double e0 = static_cast<float>(c0 - grid.zero_point) * grid.scale - r2.at(0, 0);
+            const double e1 = static_cast<float>(c1 - grid.zero_point) * grid.scale - r2.at(0, 1);
+            best = std::min(best, e0 * (hm.at(0, 0) * e0 + hm.at(0, 1) * e1) + e1 * (hm.at(1, 0) * e0 + hm.at(1, 1) * e1));
+        }
+    CHECK(l_gptq == doctest::Approx(best).epsilon(1e-6));
+
+    const int bits_cycle[] = {2, 3, 4, 8};   // never worse than RTN; identical to the reference
+    for (std::uint64_t trial = 0; trial < 40; ++trial) {
+        CounterRng tr(1000 + trial);
+        const std::size_t i = 8 + tr.next_below(9);
+        const DenseMatrix rt = gaussian_matrix(3, i, tr);
+        const HessianProxy ht = gpu::estimate_hessian(gaussian_matrix(32, i, tr), 0.01);
+        const int bits = bits_cycle[trial % 4];
+        const std::size_t gsz = trial % 2 == 0 ? 4 : i;
+        const QuantizedExpert qg = gpu::quantize_gptq(rt, ht, bits, gsz);
+        const double lr = gpu::proxy_loss(rt, gpu::quantize_rtn(rt, bits, gsz), ht);
+        const double lg = gpu::proxy_loss(rt, qg, ht);
+        CHECK(lg <= lr + 1e-9);
+        CHECK(same_quantized(qg, quantize_gptq(rt, ht, bits, gsz)));
+        CHECK(lg == proxy_loss(rt, qg, ht));   // bitwise the reference's f64 sum
+    }
+
+    CHECK_THROWS_AS(gpu::quantize_gptq(DenseMatrix(2, 4, 1.0f), proxy_of(DenseMatrix(4, 4, 0.0f)), 2, 4), NumericError);
+    CHECK_THROWS_AS(gpu::quantize_gptq(DenseMatrix(2, 4, 1.0f), proxy_of(eye(5)), 2, 4), ShapeError);
+
+    CounterRng rng5(10);   // H = I: the proxy loss is the squared Frobenius error
+    const DenseMatrix r5 = gaussian_matrix(3, 8, rng5);
+    const QuantizedExpert q5 = gpu::quantize_rtn(r5, 2, 4);
+    const double fro = frob_norm(sub(r5, dequantize(q5)));
+    CHECK(gpu::proxy_loss(r5, q5, proxy_of(eye(8))) == doctest::Approx(fro * fro).epsilon(1e-6));
 }

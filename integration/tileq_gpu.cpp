@@ -12,6 +12,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "tileq/codec.hpp"
 #include "tileq/errors.hpp"
 #include "tileq_b200.h"
@@ -352,6 +354,140 @@ void clear_cache() {
     std::lock_guard<std::mutex> lk(g_mu);
     g_layers.clear();
     g_dirs.clear();
+}
+
+// ---------------------------------------------------------------------------
+// artifact producer: host matrices in, device arrays through the C-ABI, the
+// reference's packed QuantizedExpert out
+// ---------------------------------------------------------------------------
+
+namespace {
+
+struct DevMem {
+    void* p = nullptr;
+    explicit DevMem(std::size_t bytes) {
+        if (bytes && cudaMalloc(&p, bytes) != cudaSuccess) throw Error("libtileq_b200: cudaMalloc failed");
+    }
+    ~DevMem() {
+        if (p) cudaFree(p);
+    }
+    DevMem(const DevMem&) = delete;
+    DevMem& operator=(const DevMem&) = delete;
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+void to_dev(void* d, const void* h, std::size_t n) {
+    if (n && cudaMemcpy(d, h, n, cudaMemcpyHostToDevice) != cudaSuccess) throw Error("libtileq_b200: H2D failed");
+}
+void to_host(void* h, const void* d, std::size_t n) {
+    if (n && cudaMemcpy(h, d, n, cudaMemcpyDeviceToHost) != cudaSuccess) throw Error("libtileq_b200: D2H failed");
+}
+
+void upload(DevMem& d, const DenseMatrix& m) { to_dev(d.p, m.data.data(), m.data.size() * sizeof(float)); }
+
+// unpacked device codes + grids -> the reference's QuantizedExpert (scalar mode)
+QuantizedExpert pack_quantized(std::size_t rows, std::size_t cols, int bits, std::size_t gs, const DevMem& codes,
+                               const DevMem& scales, const DevMem& zeros) {
+    const std::size_t G = (cols + gs - 1) / gs;
+    std::vector<std::uint8_t> c8(rows * cols);
+    std::vector<float> sc(rows * G);
+    std::vector<std::int32_t> zp(rows * G);
+    to_host(c8.data(), codes.p, c8.size());
+    to_host(sc.data(), scales.p, sc.size() * sizeof(float));
+    to_host(zp.data(), zeros.p, zp.size() * sizeof(std::int32_t));
+    QuantizedExpert q;
+    q.out_dim = rows;
+    q.in_dim = cols;
+    q.bits = bits;
+    q.mode = QuantMode::scalar;
+    q.group_size = gs;
+    q.packed = pack_codes(std::vector<std::uint32_t>(c8.begin(), c8.end()), bits);
+    q.grids.resize(rows * G);
+    for (std::size_t t = 0; t < q.grids.size(); ++t) q.grids[t] = QuantGrid{sc[t], zp[t]};
+    return q;
+}
+
+void check_square(const HessianProxy& h, std::size_t dim, const char* who) {
+    if (h.h.rows != dim || h.h.cols != dim)
+        throw ShapeError(std::string(who) + ": Hessian is " + std::to_string(h.h.rows) + "x" +
+                         std::to_string(h.h.cols) + ", residual has in_dim " + std::to_string(dim));
+}
+
+}  // namespace
+
+HessianProxy estimate_hessian(const DenseMatrix& calib_inputs, double damping_fraction) {
+    if (calib_inputs.rows == 0 || calib_inputs.cols == 0) throw DataError("estimate_hessian: empty calibration set");
+    const std::size_t d = calib_inputs.cols;
+    DevMem x(calib_inputs.data.size() * sizeof(float)), h(d * d * sizeof(float));
+    upload(x, calib_inputs);
+    HessianProxy out;
+    ok(tq_estimate_hessian(x.as<float>(), static_cast<std::int64_t>(calib_inputs.rows), static_cast<std::int64_t>(d),
+                           damping_fraction, h.as<float>(), &out.damping, nullptr));
+    out.h = DenseMatrix(d, d);
+    to_host(out.h.data.data(), h.p, d * d * sizeof(float));
+    out.sample_count = calib_inputs.rows;
+    return out;
+}
+
+QuantizedExpert quantize_rtn(const DenseMatrix& r, int bits, std::size_t group_size) {
+    const std::size_t gs = group_size ? group_size : 1, G = (r.cols + gs - 1) / gs;
+    DevMem rd(r.data.size() * sizeof(float)), codes(r.rows * r.cols), scales(r.rows * G * 4), zeros(r.rows * G * 4);
+    upload(rd, r);
+    ok(tq_quantize_rtn(rd.as<float>(), static_cast<std::int64_t>(r.rows), static_cast<std::int64_t>(r.cols), bits,
+                       static_cast<std::int64_t>(group_size), codes.as<std::uint8_t>(), scales.as<float>(),
+                       zeros.as<std::int32_t>(), nullptr));
+    return pack_quantized(r.rows, r.cols, bits, group_size, codes, scales, zeros);
+}
+
+QuantizedExpert quantize_gptq(const DenseMatrix& r, const HessianProxy& h, int bits, std::size_t group_size) {
+    if (bits != 2 && bits != 3 && bits != 4 && bits != 8)   // quant.cpp:178 checks bits before the shape
+        throw ParamError("quantizer bits must be in {2,3,4,8}, got " + std::to_string(bits));
+    if (group_size < 1) throw ParamError("quantize_gptq: group_size must be >= 1");
+    check_square(h, r.cols, "quantize_gptq");
+    const std::size_t G = (r.cols + group_size - 1) / group_size;
+    DevMem rd(r.data.size() * sizeof(float)), hd(h.h.data.size() * sizeof(float)), codes(r.rows * r.cols),
+        scales(r.rows * G * 4), zeros(r.rows * G * 4);
+    upload(rd, r);
+    upload(hd, h.h);
+    std::int32_t used_rtn = 0;
+    ok(tq_quantize_gptq(rd.as<float>(), static_cast<std::int64_t>(r.rows), static_cast<std::int64_t>(r.cols),
+                        hd.as<float>(), bits, static_cast<std::int64_t>(group_size), codes.as<std::uint8_t>(),
+                        scales.as<float>(), zeros.as<std::int32_t>(), &used_rtn, nullptr));
+    return pack_quantized(r.rows, r.cols, bits, group_size, codes, scales, zeros);
+}
+
+double proxy_loss(const DenseMatrix& original, const QuantizedExpert& q, const HessianProxy& h) {
+    if (q.mode != QuantMode::scalar) throw ParamError("tileq::gpu::proxy_loss: scalar-mode experts only");
+    if (original.rows != q.out_dim || original.cols != q.in_dim) throw ShapeError("sub: shape mismatch");
+    check_square(h, original.cols, "proxy_loss");
+    const std::size_t rows = q.out_dim, cols = q.in_dim, gs = q.group_size ? q.group_size : 1;
+    const std::size_t G = (cols + gs - 1) / gs;
+    if (q.grids.size() != rows * G)
+        throw ParamError("dequantize: grid table has " + std::to_string(q.grids.size()) + " entries, expected " +
+                         std::to_string(rows * G));
+    const std::vector<std::uint32_t> c32 = unpack_codes(q.packed, q.bits, rows * cols);   // FormatError on padding
+    std::vector<std::uint8_t> c8(c32.begin(), c32.end());
+    std::vector<float> sc(rows * G);
+    std::vector<std::int32_t> zp(rows * G);
+    for (std::size_t t = 0; t < q.grids.size(); ++t) {
+        sc[t] = q.grids[t].scale;
+        zp[t] = q.grids[t].zero_point;
+    }
+    DevMem od(original.data.size() * sizeof(float)), hd(h.h.data.size() * sizeof(float)), cd(c8.size()),
+        sd(sc.size() * 4), zd(zp.size() * 4);
+    upload(od, original);
+    upload(hd, h.h);
+    to_dev(cd.p, c8.data(), c8.size());
+    to_dev(sd.p, sc.data(), sc.size() * 4);
+    to_dev(zd.p, zp.data(), zp.size() * 4);
+    double loss = 0.0;
+    ok(tq_proxy_loss(od.as<float>(), static_cast<std::int64_t>(rows), static_cast<std::int64_t>(cols),
+                     cd.as<std::uint8_t>(), sd.as<float>(), zd.as<std::int32_t>(), q.bits,
+                     static_cast<std::int64_t>(gs), hd.as<float>(), &loss, nullptr));
+    return loss;
 }
 
 }  // namespace tileq::gpu

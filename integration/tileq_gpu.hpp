@@ -13,6 +13,11 @@
 //   tileq::gpu::forward_from_artifact <- _tileq.forward_from_artifact  bindings/py_module.cpp:112-117
 //   tileq::gpu::reset_dispatch_count / dispatch_count <- infer.hpp:37-38 (GPU analogue:
 //                                    kernel launches, constant in the batch size)
+//   tileq::gpu::estimate_hessian <- tileq::estimate_hessian include/tileq/quant.hpp:67
+//   tileq::gpu::quantize_rtn     <- tileq::quantize_rtn     include/tileq/quant.hpp:74
+//   tileq::gpu::quantize_gptq    <- tileq::quantize_gptq    include/tileq/quant.hpp:85-86
+//   tileq::gpu::proxy_loss       <- tileq::proxy_loss       include/tileq/quant.hpp:104
+//                                    (the artifact producer's hot spots; bit-identical results)
 //
 // Failures surface as the reference's exception types (errors.hpp:13-50):
 // the C-ABI status is mapped back to ShapeError / ParamError / FormatError /
@@ -27,6 +32,7 @@
 
 #include "tileq/infer.hpp"
 #include "tileq/moe.hpp"
+#include "tileq/quant.hpp"
 
 namespace tileq::gpu {
 
@@ -52,5 +58,11 @@ std::uint64_t dispatch_count();
 void set_device(int device);
 /// Free every cached device-resident layer.
 void clear_cache();
+
+// artifact producer: same results as the reference, bit for bit
+HessianProxy estimate_hessian(const DenseMatrix& calib_inputs, double damping_fraction);
+QuantizedExpert quantize_rtn(const DenseMatrix& r, int bits, std::size_t group_size);
+QuantizedExpert quantize_gptq(const DenseMatrix& r, const HessianProxy& h, int bits, std::size_t group_size);
+double proxy_loss(const DenseMatrix& original, const QuantizedExpert& q, const HessianProxy& h);
 
 }  // namespace tileq::gpu

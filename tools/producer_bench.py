@@ -30,6 +30,8 @@ def main():
     ap.add_argument("--gs", type=int, default=128)
     ap.add_argument("--cpu-rows", type=int, default=8)
     ap.add_argument("--cpu-dim", type=int, default=0, help="dim of the CPU sample (default: --dim)")
+    ap.add_argument("--cpu-rows2", type=int, default=0,
+                    help="second GPTQ sample size: per-row cost = difference of the two runs (same spd_inverse)")
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
     import torch
@@ -86,14 +88,29 @@ def main():
         t0 = time.perf_counter()
         ref.quantize("gptq", rs, h_ref, a.bits, a.gs)
         t_gptq_cpu = time.perf_counter() - t0
-        # quantize_gptq = spd_inverse + sweep + rtn + 2 proxy losses; isolate spd_inverse
-        t_inv_cpu = max(t_gptq_cpu - 2 * t_proxy_cpu - t_rtn_cpu - 0.0, 0.0)
+        # quantize_gptq = spd_inverse (once per call) + per-row work (sweep, RTN, two
+        # proxy losses); spd_inverse alone is timed on the C restatement of the
+        # same loops (oracle/tileq_oracle.c, quant.cpp:72-112, -O2 like the reference)
+        from oracle.oracle import Oracle
+        t0 = time.perf_counter()
+        Oracle().spd_inverse(h_ref)
+        t_inv_cpu = time.perf_counter() - t0
         scale = a.rows / cn
+        per_row = None
+        if a.cpu_rows2 > cn:
+            rs2 = r[:a.cpu_rows2, :cd].float().cpu().numpy()
+            t0 = time.perf_counter()
+            ref.quantize("gptq", rs2, h_ref, a.bits, a.gs)
+            t_gptq2 = time.perf_counter() - t0
+            per_row = (t_gptq2 - t_gptq_cpu) / (a.cpu_rows2 - cn)
         out["cpu_reference"] = {
             "threads": 1, "sample": f"{cn} residual rows x dim {cd}, {T} calibration tokens",
-            "estimate_hessian_s": t_h_cpu, "proxy_loss_s_sample": t_proxy_cpu, "quantize_gptq_s_sample": t_gptq_cpu,
+            "estimate_hessian_s": t_h_cpu, "proxy_loss_s_sample": t_proxy_cpu, "quantize_rtn_s_sample": t_rtn_cpu,
+            "quantize_gptq_s_sample": t_gptq_cpu, "spd_inverse_s": t_inv_cpu,
             "proxy_loss_s_scaled_to_rows": t_proxy_cpu * scale,
-            "quantize_gptq_s_scaled_to_rows": t_inv_cpu + (t_gptq_cpu - t_inv_cpu) * scale if cd == a.dim else None,
+            "quantize_gptq_per_row_s": per_row,
+            "quantize_gptq_s_scaled_to_rows": (t_gptq_cpu + per_row * (a.rows - cn)
+                                               if per_row is not None and cd == a.dim else None),
         }
     print(json.dumps(out))
 

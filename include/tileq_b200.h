@@ -331,6 +331,9 @@ int64_t tq_ep_extrow_elems(const tq_layer* layer);
  *                          include/tileq/quant.hpp:85-86, src/quant.cpp:177-221
  *   tq_proxy_loss       <- proxy_loss(original, q, h)
  *                          include/tileq/quant.hpp:104, src/quant.cpp:325-343
+ *   tq_sketch_lowrank   <- sketch_lowrank(w, rank, power_iters, seed)
+ *                          include/tileq/lowrank.hpp:21-30, src/lowrank.cpp:194-247
+ *                          (extract_features tiler.cpp:137, decompose_shared tiler.cpp:308)
  * ------------------------------------------------------------------------ */
 
 /* calib [dev] f32 tokens x dim -> h [dev] f32 dim x dim; *damping_out (host,
@@ -348,9 +351,18 @@ tq_status tq_quantize_rtn(const float* r, int64_t rows, int64_t cols, int bits, 
 
 /* r [dev] f32 rows x cols, h [dev] f32 cols x cols -> codes / scales / zeros
  * [dev]; *used_rtn (host, nullable) = 1 when plain rounding won the proxy-loss
- * comparison (quant.cpp:216-219).  cols <= 25600. */
+ * comparison (quant.cpp:216-219).  One working row and its grids must fit in
+ * shared memory (cols up to ~27000). */
 tq_status tq_quantize_gptq(const float* r, int64_t rows, int64_t cols, const float* h, int bits, int64_t group_size,
                            uint8_t* codes, float* scales, int32_t* zeros, int32_t* used_rtn, void* stream);
+
+/* sketch_lowrank(w, rank, power_iters, seed) (include/tileq/lowrank.hpp:21-30,
+ * src/lowrank.cpp:194-247): w [dev] f32 rows x cols -> left [dev] f32 rows x rank,
+ * right [dev] f32 rank x cols, singulars [dev] f32 rank (nonincreasing).  The f64
+ * working copy stays on the device (8 * rows * cols bytes); the probes are drawn
+ * on the host with the reference's generator.  Synchronizes the stream. */
+tq_status tq_sketch_lowrank(const float* w, int64_t rows, int64_t cols, int64_t rank, int power_iters, uint64_t seed,
+                            float* left, float* right, float* singulars, void* stream);
 
 /* tr(E H E^T), E = original - dequantize(codes, scales, zeros), into *loss (host). */
 tq_status tq_proxy_loss(const float* original, int64_t rows, int64_t cols, const uint8_t* codes, const float* scales,

@@ -494,3 +494,17 @@ TEST_CASE("producer: quantize_gptq and proxy_loss contracts and bit identity wit
     const double fro = frob_norm(sub(r5, dequantize(q5)));
     CHECK(gpu::proxy_loss(r5, q5, proxy_of(eye(8))) == doctest::Approx(fro * fro).epsilon(1e-6));
 }
+
+TEST_CASE("producer: sketch_lowrank equals the reference's, bit for bit") {
+    CounterRng rng(77);
+    const DenseMatrix w = gaussian_matrix(48, 36, rng);
+    for (int iters : {0, 2, 4}) {
+        const LowRankFactor g = gpu::sketch_lowrank(w, 6, iters, 5);
+        const LowRankFactor c = sketch_lowrank(w, 6, iters, 5);
+        CHECK(same_bits(g.left, c.left));
+        CHECK(same_bits(g.right, c.right));
+        CHECK(g.singulars == c.singulars);
+    }
+    CHECK_THROWS_AS(gpu::sketch_lowrank(w, 0, 2, 5), ParamError);
+    CHECK_THROWS_AS(gpu::sketch_lowrank(w, 2, -1, 5), ParamError);
+}

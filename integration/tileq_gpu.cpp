@@ -490,4 +490,22 @@ double proxy_loss(const DenseMatrix& original, const QuantizedExpert& q, const H
     return loss;
 }
 
+LowRankFactor sketch_lowrank(const DenseMatrix& w, std::size_t rank, int power_iters, std::uint64_t seed) {
+    const std::size_t rows = w.rows, cols = w.cols, r = rank;
+    DevMem wd(w.data.size() * sizeof(float)), ld(rows * r * sizeof(float)), rd(r * cols * sizeof(float)),
+        sd(r * sizeof(float));
+    upload(wd, w);
+    ok(tq_sketch_lowrank(wd.as<float>(), static_cast<std::int64_t>(rows), static_cast<std::int64_t>(cols),
+                         static_cast<std::int64_t>(rank), power_iters, seed, ld.as<float>(), rd.as<float>(),
+                         sd.as<float>(), nullptr));
+    LowRankFactor f;
+    f.left = DenseMatrix(rows, r);
+    f.right = DenseMatrix(r, cols);
+    f.singulars.resize(r);
+    to_host(f.left.data.data(), ld.p, rows * r * sizeof(float));
+    to_host(f.right.data.data(), rd.p, r * cols * sizeof(float));
+    to_host(f.singulars.data(), sd.p, r * sizeof(float));
+    return f;
+}
+
 }  // namespace tileq::gpu

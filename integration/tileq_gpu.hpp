@@ -17,6 +17,7 @@
 //   tileq::gpu::quantize_rtn     <- tileq::quantize_rtn     include/tileq/quant.hpp:74
 //   tileq::gpu::quantize_gptq    <- tileq::quantize_gptq    include/tileq/quant.hpp:85-86
 //   tileq::gpu::proxy_loss       <- tileq::proxy_loss       include/tileq/quant.hpp:104
+//   tileq::gpu::sketch_lowrank   <- tileq::sketch_lowrank   include/tileq/lowrank.hpp:21-30
 //                                    (the artifact producer's hot spots; bit-identical results)
 //
 // Failures surface as the reference's exception types (errors.hpp:13-50):
@@ -31,6 +32,7 @@
 #include <string>
 
 #include "tileq/infer.hpp"
+#include "tileq/lowrank.hpp"
 #include "tileq/moe.hpp"
 #include "tileq/quant.hpp"
 
@@ -64,5 +66,6 @@ HessianProxy estimate_hessian(const DenseMatrix& calib_inputs, double damping_fr
 QuantizedExpert quantize_rtn(const DenseMatrix& r, int bits, std::size_t group_size);
 QuantizedExpert quantize_gptq(const DenseMatrix& r, const HessianProxy& h, int bits, std::size_t group_size);
 double proxy_loss(const DenseMatrix& original, const QuantizedExpert& q, const HessianProxy& h);
+LowRankFactor sketch_lowrank(const DenseMatrix& w, std::size_t rank, int power_iters, std::uint64_t seed);
 
 }  // namespace tileq::gpu

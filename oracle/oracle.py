@@ -308,6 +308,8 @@ class RefLib:
         L.tq_ref_estimate_hessian.argtypes = [_p, _i64, _i64, C.c_double, _p, _p, C.c_char_p, C.c_int]
         L.tq_ref_quantize.argtypes = [C.c_int, _p, _i64, _i64, _p, C.c_int, _i64, _p, _p, _p, C.c_char_p, C.c_int]
         L.tq_ref_proxy_loss.argtypes = [_p, _i64, _i64, _p, _p, _p, C.c_int, _i64, _p, _p, C.c_char_p, C.c_int]
+        L.tq_ref_sketch_lowrank.argtypes = [_p, _i64, _i64, _i64, C.c_int, C.c_uint64, _p, _p, _p, C.c_char_p,
+                                            C.c_int]
 
     def _check(self, st, buf):
         if st:
@@ -382,6 +384,18 @@ class RefLib:
                                                _ptr(scales), _ptr(zeros), bits, group_size, _ptr(h),
                                                C.byref(out), buf, 1024), buf)
         return out.value
+
+    def sketch_lowrank(self, w, rank, power_iters, seed):
+        """sketch_lowrank (lowrank.cpp:194-247) -> (left, singulars, right) f32."""
+        w = np.ascontiguousarray(w, np.float32)
+        rows, cols = w.shape
+        left = np.zeros((rows, rank), np.float32)
+        right = np.zeros((rank, cols), np.float32)
+        sing = np.zeros(rank, np.float32)
+        buf = C.create_string_buffer(1024)
+        self._check(self.lib.tq_ref_sketch_lowrank(_ptr(w), rows, cols, rank, power_iters, seed, _ptr(left),
+                                                   _ptr(right), _ptr(sing), buf, 1024), buf)
+        return left, sing, right
 
     def f16_to_f32(self, bits):
         bits = np.ascontiguousarray(bits, np.uint16)

@@ -41,6 +41,7 @@
 #include "tileq/errors.hpp"
 #include "tileq/infer.hpp"
 #include "tileq/io.hpp"
+#include "tileq/lowrank.hpp"
 #include "tileq/moe.hpp"
 #include "tileq/pipeline.hpp"
 #include "tileq/quant.hpp"
@@ -446,6 +447,16 @@ int tq_ref_proxy_loss(const float* original, std::int64_t rows, std::int64_t col
         hp.h = wrap(h, cols, cols);
         *out = proxy_loss(wrap(original, rows, cols), import_quantized(rows, cols, codes, scales, zeros, bits, gs),
                           hp);
+    });
+}
+
+int tq_ref_sketch_lowrank(const float* w, std::int64_t rows, std::int64_t cols, std::int64_t rank, int power_iters,
+                          std::uint64_t seed, float* left, float* right, float* singulars, char* errbuf, int errlen) {
+    return guarded(errbuf, errlen, [&] {
+        const LowRankFactor f = sketch_lowrank(wrap(w, rows, cols), static_cast<std::size_t>(rank), power_iters, seed);
+        copy_out(f.left, left);
+        copy_out(f.right, right);
+        std::memcpy(singulars, f.singulars.data(), f.singulars.size() * sizeof(float));
     });
 }
 

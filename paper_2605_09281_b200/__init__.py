@@ -151,11 +151,12 @@ def lib() -> C.CDLL:
     L.tq_quantize_rtn.argtypes = [p, i64, i64, i32, i64, p, p, p, p]
     L.tq_quantize_gptq.argtypes = [p, i64, i64, p, i32, i64, p, p, p, p, p]
     L.tq_proxy_loss.argtypes = [p, i64, i64, p, p, p, i32, i64, p, p, p]
+    L.tq_sketch_lowrank.argtypes = [p, i64, i64, i64, i32, C.c_uint64, p, p, p, p]
     for name in ("tq_layer_load", "tq_artifact_check", "tq_exp_f64", "tq_layer_create", "tq_layer_free", "tq_layer_info_get", "tq_layer_reserve", "tq_route",
                  "tq_route_raw", "tq_permute", "tq_forward", "tq_forward_routed", "tq_forward_host",
                  "tq_sync", "tq_debug_decode_counters", "tq_unpack_codes", "tq_layer_export_codes", "tq_ep_dispatch_rows",
                  "tq_ep_expert_rows", "tq_ep_expert_rows_slab", "tq_ep_combine", "tq_gemm_timing_enable", "tq_gemm_time_get",
-                 "tq_estimate_hessian", "tq_spd_inverse", "tq_quantize_rtn", "tq_quantize_gptq", "tq_proxy_loss"):
+                 "tq_estimate_hessian", "tq_spd_inverse", "tq_quantize_rtn", "tq_quantize_gptq", "tq_proxy_loss", "tq_sketch_lowrank"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -2217,6 +2217,81 @@ cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t s
     return cudaGetLastError();
 }
 
+
+// Load-time repack on the device: the artifact's LSB-first packed
+// code stream (codec.cpp:145-195) -> the engine's [mb][kc] super-word blocks,
+// one thread per (m-block, K chunk, half, row): it gathers its row's 32 codes
+// and writes them as `bits` super-words, the layout dequant32<b> decodes
+// (tests/test_gpu_parity.py::test_repacked_codes_bit_exact reads it back).
+__device__ __forceinline__ void pack_superword_dev(const uint32_t* c, int bits, uint32_t* w) {
+    for (int j = 0; j < bits; ++j) w[j] = 0;
+    if (bits == 2) {
+        for (int j = 0; j < 2; ++j)
+            for (int m = 0; m < 8; ++m) {
+                const int p = 8 * j + m;
+                w[j] |= (c[2 * p] << (2 * m)) | (c[2 * p + 1] << (16 + 2 * m));
+            }
+    } else if (bits == 3) {
+        for (int j = 0; j < 3; ++j)
+            for (int m = 0; m < 5; ++m) {
+                const int p = 5 * j + m;
+                w[j] |= (c[2 * p] << (3 * m)) | (c[2 * p + 1] << (16 + 3 * m));
+            }
+        for (int k = 0; k < 3; ++k) w[k] |= (((c[30] >> k) & 1u) << 15) | (((c[31] >> k) & 1u) << 31);
+    } else if (bits == 4) {
+        for (int j = 0; j < 4; ++j)
+            for (int m = 0; m < 4; ++m) {
+                const int p = 4 * j + m;
+                w[j] |= (c[2 * p] << (4 * m)) | (c[2 * p + 1] << (16 + 4 * m));
+            }
+    } else {
+        for (int j = 0; j < 8; ++j)
+            for (int m = 0; m < 2; ++m) {
+                const int p = 2 * j + m;
+                w[j] |= (c[2 * p] << (8 * m)) | (c[2 * p + 1] << (16 + 8 * m));
+            }
+    }
+}
+
+__global__ void repack_codes_kernel(const uint8_t* __restrict__ packed, int64_t nbytes, int bits, int64_t o,
+                                    int64_t i, int64_t mb_count, int64_t kc_total, uint8_t* __restrict__ out) {
+    const int64_t n = mb_count * kc_total * 2 * kBM;
+    const int blk = code_block_bytes(bits);
+    const uint32_t mask = (1u << bits) - 1u;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int rl = static_cast<int>(t % kBM);
+        const int h = static_cast<int>((t / kBM) % 2);
+        const int64_t kc = (t / (2 * kBM)) % kc_total, mb = t / (2 * kBM * kc_total);
+        const int64_t row = mb * kBM + rl, col0 = kc * kKC + 32 * h;
+        uint32_t c[32];
+        for (int q = 0; q < 32; ++q) {
+            const int64_t col = col0 + q;
+            uint32_t v = 0u;
+            if (row < o && col < i) {
+                const int64_t bit = (row * i + col) * bits, byte = bit >> 3;
+                uint32_t two = packed[byte];
+                if (byte + 1 < nbytes) two |= static_cast<uint32_t>(packed[byte + 1]) << 8;
+                v = (two >> (bit & 7)) & mask;
+            }
+            c[q] = v;
+        }
+        uint32_t w[8];
+        pack_superword_dev(c, bits, w);
+        uint32_t* block = reinterpret_cast<uint32_t*>(out + (mb * kc_total + kc) * blk);
+        for (int j = 0; j < bits; ++j) block[(h * bits + j) * kBM + rl] = w[j];
+    }
+}
+
+cudaError_t launch_repack_codes(const uint8_t* packed, int64_t nbytes, int bits, int64_t o, int64_t i,
+                                int64_t mb_count, int64_t kc_total, uint8_t* out, cudaStream_t stream) {
+    const int64_t n = mb_count * kc_total * 2 * kBM;
+    const int64_t blocks = std::min<int64_t>((n + 255) / 256, 148 * 16);
+    repack_codes_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(packed, nbytes, bits, o, i, mb_count,
+                                                                           kc_total, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream) {
     const int64_t n = static_cast<int64_t>(out_dim) * kc_total * 2;

@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kT = 64;     // output tile edge
 constexpr int kKC = 16;    // k chunk staged in shared memory
-constexpr int kTT = 256;   // threads per tile CTA (16 x 16, 4 x 4 outputs each)
+constexpr int kTT = 256;   // threads per tile CTA (16 x 16, 4 x 4 outputs each, strided by 16)
 
 // Status word shared by the spd_inverse kernels: the first failing pivot.
 struct SpdStatus {
@@ -50,7 +50,7 @@ struct SpdStatus {
 // ordered f64 tile product
 // ---------------------------------------------------------------------------
 
-// acc[ii][jj] (+|-)= A(i0 + ty*4 + ii, k) * B(k, j0 + tx*4 + jj) for k = k0 .. k1-1
+// acc[ii][jj] (+|-)= A(i0 + ty + 16 ii, k) * B(k, j0 + tx + 16 jj) for k = k0 .. k1-1
 // ascending.  kAK / kBK: the operand is contiguous along k (stage k-fastest) or
 // along i / j (stage i/j-fastest), so the global loads coalesce either way.
 template <bool kSub, bool kAK, bool kBK, class FA, class FB>
@@ -75,8 +75,8 @@ __device__ __forceinline__ void tile_accumulate(double (&acc)[4][4], int64_t i0,
             double a[4], b[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                a[q] = As[kk][ty * 4 + q];
-                b[q] = Bs[kk][tx * 4 + q];
+                a[q] = As[kk][ty + 16 * q];   // 2 addresses per warp: broadcast
+                b[q] = Bs[kk][tx + 16 * q];   // 16 consecutive doubles: one wavefront
             }
 #pragma unroll
             for (int ii = 0; ii < 4; ++ii)
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kTT) hessian_acc_kernel(const float* __restric
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t a = a0 + ty * 4 + ii, b = b0 + tx * 4 + jj;
+            const int64_t a = a0 + ty + 16 * ii, b = b0 + tx + 16 * jj;
             if (a < dim && b < dim && b >= a) acc_out[a * dim + b] = acc[ii][jj];
         }
 }
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(kTT) chol_trail_kernel(double* __restrict__ c,
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = jt0 + tx * 4 + jj;
+            const int64_t i = i0 + ty + 16 * ii, j = jt0 + tx + 16 * jj;
             acc[ii][jj] = (i < n && j < n && j <= i) ? c[i * n + j] : 0.0;
         }
     auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(kTT) chol_trail_kernel(double* __restrict__ c,
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = jt0 + tx * 4 + jj;
+            const int64_t i = i0 + ty + 16 * ii, j = jt0 + tx + 16 * jj;
             if (i < n && j < n && j <= i) c[i * n + j] = acc[ii][jj];
         }
 }
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kTT) linv_trail_kernel(const double* __restric
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = r0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            const int64_t i = r0 + ty + 16 * ii, j = j0 + tx + 16 * jj;
             acc[ii][jj] = (i < n && j < i1) ? li[i * n + j] : 0.0;
         }
     auto fa = [&](int64_t i, int64_t k) { return i < n ? c[i * n + k] : 0.0; };
@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kTT) linv_trail_kernel(const double* __restric
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = r0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            const int64_t i = r0 + ty + 16 * ii, j = j0 + tx + 16 * jj;
             if (i < n && j < i1) li[i * n + j] = acc[ii][jj];
         }
 }
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kTT) hinv_kernel(const double* __restrict__ li
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t i = i0 + ty * 4 + ii, j = j0 + tx * 4 + jj;
+            const int64_t i = i0 + ty + 16 * ii, j = j0 + tx + 16 * jj;
             if (i < n && j <= i) {
                 hinv[i * n + j] = acc[ii][jj];
                 hinv[j * n + i] = acc[ii][jj];
@@ -426,13 +426,34 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 // GPTQ column sweep (quant.cpp:200-213).  A CTA owns kR rows: their working rows
 // and grids sit in shared memory; columns are dealt to threads round-robin so
-// the shrinking trailing range stays balanced.  Per column j: every thread
-// forms the code and error of column j for its rows (work[j] is final after the
-// previous barrier), then updates its own columns c > j:
+// the shrinking trailing range stays balanced.  Column j's codes and errors are
+// formed ONCE, by the thread that owns column j, right after it applied the
+// last update to that column (step j-1), and published through a small
+// double-buffered shared array; step j then updates every column c > j:
 // work[c] -= err * Hinv[j][c] / Hinv[j][j].  With kStage, row j+1 of Hinv is
-// copied into a second shared buffer (cp.async) while column j is processed, so
-// the sweep never waits on L2 latency between its barriers.
+// copied into a second shared buffer (cp.async) while column j is processed,
+// so the sweep never waits on L2 latency between its barriers.
 constexpr int kGptqThreads = 512;
+
+template <int kR>
+__device__ __forceinline__ void gptq_encode(const double (&w)[kR], int nr, int64_t j, int64_t G, int64_t gs,
+                                            const float* gsc, const int32_t* gzp, double levels, int64_t row0,
+                                            int64_t dim, uint8_t* __restrict__ codes, double* errb) {
+    const int64_t g = j / gs;
+#pragma unroll
+    for (int q = 0; q < kR; ++q) {
+        if (q < nr) {
+            const float sc = gsc[q * G + g];
+            const int32_t z = gzp[q * G + g];
+            const uint32_t code = encode_one(w[q], sc, z, levels);
+            const double deq = __dmul_rn(__dsub_rn(static_cast<double>(code), static_cast<double>(z)),
+                                         static_cast<double>(sc));
+            errb[q] = __dsub_rn(w[q], deq);
+            codes[(row0 + q) * dim + j] = static_cast<uint8_t>(code);
+        }
+    }
+}
+
 template <int kR, bool kStage>
 __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restrict__ r, int64_t rows, int64_t dim,
                                                              int bits, int64_t gs, const float* __restrict__ scales,
@@ -440,6 +461,7 @@ __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restr
                                                              const double* __restrict__ hinv,
                                                              uint8_t* __restrict__ codes) {
     extern __shared__ double sm[];
+    __shared__ double errb[2][kR];
     const int64_t G = (dim + gs - 1) / gs;
     double* work = sm;                                    // kR x dim
     double* hb = sm + kR * dim;                           // 2 x dim (kStage)
@@ -462,10 +484,17 @@ __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restr
         cp_async_wait_all();
     }
     __syncthreads();
+    if (tid == 0 && dim > 0) {   // column 0 is final from the start
+        double w0[kR];
+#pragma unroll
+        for (int q = 0; q < kR; ++q) w0[q] = q < nr ? work[q * dim] : 0.0;
+        gptq_encode<kR>(w0, nr, 0, G, gs, gsc, gzp, levels, row0, dim, codes, errb[0]);
+    }
+    __syncthreads();
     for (int64_t j = 0; j < dim; ++j) {
         const double* hrow;
+        const int buf = static_cast<int>(j & 1);
         if (kStage) {
-            const int buf = static_cast<int>(j & 1);
             hrow = hb + buf * dim;
             if (j + 1 < dim) {   // prefetch row j+1 (own columns >= j+1; the diagonal included)
                 const int64_t f = j + 1;
@@ -479,31 +508,25 @@ __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restr
             hrow = hinv + j * dim;
         }
         double err[kR];
-        const int64_t g = j / gs;
 #pragma unroll
-        for (int q = 0; q < kR; ++q) {
-            err[q] = 0.0;
-            if (q < nr) {
-                const float sc = gsc[q * G + g];
-                const int32_t z = gzp[q * G + g];
-                const double wj = work[q * dim + j];
-                const uint32_t code = encode_one(wj, sc, z, levels);
-                const double deq = __dmul_rn(__dsub_rn(static_cast<double>(code), static_cast<double>(z)),
-                                             static_cast<double>(sc));
-                err[q] = __dsub_rn(wj, deq);
-                if (tid == q) codes[(row0 + q) * dim + j] = static_cast<uint8_t>(code);
-            }
-        }
+        for (int q = 0; q < kR; ++q) err[q] = errb[buf][q];
         const double inv_jj = hrow[j];
         const double rcp = __drcp_rn(inv_jj);
         const int64_t first = j + 1;
         for (int64_t c = first + ((tid - first) % kGptqThreads + kGptqThreads) % kGptqThreads; c < dim;
              c += kGptqThreads) {
             const double h = hrow[c];
+            double nw[kR];
 #pragma unroll
-            for (int q = 0; q < kR; ++q)
-                if (q < nr)
-                    work[q * dim + c] = __dsub_rn(work[q * dim + c], div_rn_by(__dmul_rn(err[q], h), inv_jj, rcp));
+            for (int q = 0; q < kR; ++q) {
+                nw[q] = 0.0;
+                if (q < nr) {
+                    nw[q] = __dsub_rn(work[q * dim + c], div_rn_by(__dmul_rn(err[q], h), inv_jj, rcp));
+                    work[q * dim + c] = nw[q];
+                }
+            }
+            if (c == first)   // column j+1 just got its last update: publish its codes / errors
+                gptq_encode<kR>(nw, nr, first, G, gs, gsc, gzp, levels, row0, dim, codes, errb[buf ^ 1]);
         }
         if (kStage) cp_async_wait_all();
         __syncthreads();
@@ -546,7 +569,7 @@ __global__ void __launch_bounds__(kTT) proxy_he_kernel(const float* __restrict__
     for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj) {
-            const int64_t row = i0 + ty * 4 + ii, a = a0 + tx * 4 + jj;
+            const int64_t row = i0 + ty + 16 * ii, a = a0 + tx + 16 * jj;
             if (row < rend && a < dim) he_t[a * nrows + (row - r0)] = acc[ii][jj];
         }
 }
@@ -573,6 +596,123 @@ __global__ void proxy_total_kernel(const double* __restrict__ rowsum, int64_t ro
     double s = 0.0;
     for (int64_t r = 0; r < rows; ++r) s = __dadd_rn(s, rowsum[r]);
     *total = s;
+}
+
+
+// ---------------------------------------------------------------------------
+// sketch_lowrank (lowrank.cpp:194-247): the f64 mat-vecs of the randomized
+// sketch on the resident working copy.  Host code (tq_runtime.cpp) draws the
+// probes and runs the sequential control flow.
+// ---------------------------------------------------------------------------
+
+__global__ void widen_kernel(const float* __restrict__ w, int64_t n, double* __restrict__ out) {
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        out[e] = static_cast<double>(w[e]);
+}
+
+// y[r] = sum_c a[r][c] * x[c], c ascending (lowrank.cpp:37-46).  A warp owns 32
+// rows: it stages 32 x 32 tiles with coalesced row segments and each lane walks
+// its own row through the tile.
+constexpr int kMvWarps = 4;
+__global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __restrict__ a, int64_t rows,
+                                                                int64_t cols, const double* __restrict__ x,
+                                                                double* __restrict__ y) {
+    __shared__ double tile[kMvWarps][32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kMvWarps + warp) * 32;
+    if (r0 >= rows) return;   // warp-uniform; no CTA barriers below
+    double acc = 0.0;
+    for (int64_t c0 = 0; c0 < cols; c0 += 32) {
+        const int w = static_cast<int>(cols - c0 < 32 ? cols - c0 : 32);
+#pragma unroll 8
+        for (int rr = 0; rr < 32; ++rr) {
+            const int64_t r = r0 + rr;
+            tile[warp][rr][lane] = (r < rows && lane < w) ? a[r * cols + c0 + lane] : 0.0;
+        }
+        const double xv = lane < w ? x[c0 + lane] : 0.0;
+        __syncwarp();
+        for (int k = 0; k < w; ++k) {
+            const double xk = __shfl_sync(0xffffffffu, xv, k);
+            acc = __dadd_rn(acc, __dmul_rn(tile[warp][lane][k], xk));
+        }
+        __syncwarp();
+    }
+    if (r0 + lane < rows) y[r0 + lane] = acc;
+}
+
+// y[c] = sum_r a[r][c] * x[r], r ascending (lowrank.cpp:48-56): one thread per
+// column (coalesced across the warp), 32 row loads in flight per thread.
+constexpr int kMtvUnroll = 32;
+__global__ void __launch_bounds__(64) mattvec_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
+                                                      const double* __restrict__ x, double* __restrict__ y) {
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    double acc = 0.0;
+    int64_t r = 0;
+    for (; r + kMtvUnroll <= rows; r += kMtvUnroll) {
+        double v[kMtvUnroll];
+#pragma unroll
+        for (int u = 0; u < kMtvUnroll; ++u) v[u] = __ldcs(a + (r + u) * cols + c);
+#pragma unroll
+        for (int u = 0; u < kMtvUnroll; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], x[r + u]));
+    }
+    for (; r < rows; ++r) acc = __dadd_rn(acc, __dmul_rn(a[r * cols + c], x[r]));
+    y[c] = acc;
+}
+
+// sqrt(sum v^2), v ascending (lowrank.cpp:58-62): one thread, loads run ahead
+__global__ void norm2_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double acc = 0.0;
+    int64_t t = 0;
+    for (; t + 16 <= n; t += 16) {
+        double b[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) b[u] = v[t + u];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, __dmul_rn(b[u], b[u]));
+    }
+    for (; t < n; ++t) acc = __dadd_rn(acc, __dmul_rn(v[t], v[t]));
+    *out = __dsqrt_rn(acc);
+}
+
+// dst[i] = src[i] / *d  (x /= qn, v /= sigma)
+__global__ void div_by_kernel(const double* __restrict__ src, int64_t n, const double* __restrict__ d,
+                              double* __restrict__ dst) {
+    const double den = *d;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[e] = __ddiv_rn(src[e], den);
+}
+
+// work[r][c] -= (sigma * u[r]) * v[c]  (lowrank.cpp:232-236)
+__global__ void deflate_kernel(double* __restrict__ a, int64_t rows, int64_t cols, const double* __restrict__ sigma,
+                               const double* __restrict__ u, const double* __restrict__ v) {
+    const double s = *sigma;
+    const int64_t n = rows * cols;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = e / cols, c = e - r * cols;
+        a[e] = __dsub_rn(a[e], __dmul_rn(__dmul_rn(s, u[r]), v[c]));
+    }
+}
+
+// left[i][p] = float(u_{order[p]}[i]), right[p][c] = float(v_{order[p]}[c])  (lowrank.cpp:84-99)
+__global__ void pack_triples_kernel(const double* __restrict__ us, const double* __restrict__ vs,
+                                    const int32_t* __restrict__ order, int64_t rank, int64_t rows, int64_t cols,
+                                    float* __restrict__ left, float* __restrict__ right) {
+    const int64_t nl = rows * rank, n = nl + rank * cols;
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (e < nl) {
+            const int64_t i = e / rank, p = e % rank;
+            left[e] = __double2float_rn(us[static_cast<int64_t>(order[p]) * rows + i]);
+        } else {
+            const int64_t f = e - nl, p = f / cols, c = f % cols;
+            right[f] = __double2float_rn(vs[static_cast<int64_t>(order[p]) * cols + c]);
+        }
+    }
 }
 
 unsigned grid_for(int64_t n, int threads) {
@@ -721,6 +861,44 @@ cudaError_t launch_proxy_loss(const float* orig, const uint8_t* codes, const flo
                                                                                           rowsum);
     }
     proxy_total_kernel<<<1, 32, 0, stream>>>(rowsum, rows, total);
+    return cudaGetLastError();
+}
+
+
+// sketch_lowrank building blocks
+cudaError_t launch_widen(const float* w, int64_t n, double* out, cudaStream_t stream) {
+    widen_kernel<<<grid_for(n, 256), 256, 0, stream>>>(w, n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_matvec(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                          cudaStream_t stream) {
+    const int64_t warps = (rows + 31) / 32;
+    matvec_kernel<<<static_cast<unsigned>((warps + kMvWarps - 1) / kMvWarps), kMvWarps * 32, 0, stream>>>(a, rows,
+                                                                                                           cols, x, y);
+    return cudaGetLastError();
+}
+cudaError_t launch_mattvec(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                           cudaStream_t stream) {
+    mattvec_kernel<<<static_cast<unsigned>((cols + 63) / 64), 64, 0, stream>>>(a, rows, cols, x, y);
+    return cudaGetLastError();
+}
+cudaError_t launch_norm2(const double* v, int64_t n, double* out, cudaStream_t stream) {
+    norm2_kernel<<<1, 32, 0, stream>>>(v, n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_div_by(const double* src, int64_t n, const double* d, double* dst, cudaStream_t stream) {
+    div_by_kernel<<<grid_for(n, 256), 256, 0, stream>>>(src, n, d, dst);
+    return cudaGetLastError();
+}
+cudaError_t launch_deflate(double* a, int64_t rows, int64_t cols, const double* sigma, const double* u,
+                           const double* v, cudaStream_t stream) {
+    deflate_kernel<<<grid_for(rows * cols, 256), 256, 0, stream>>>(a, rows, cols, sigma, u, v);
+    return cudaGetLastError();
+}
+cudaError_t launch_pack_triples(const double* us, const double* vs, const int32_t* order, int64_t rank, int64_t rows,
+                                int64_t cols, float* left, float* right, cudaStream_t stream) {
+    pack_triples_kernel<<<grid_for((rows + cols) * rank, 256), 256, 0, stream>>>(us, vs, order, rank, rows, cols,
+                                                                                 left, right);
     return cudaGetLastError();
 }
 

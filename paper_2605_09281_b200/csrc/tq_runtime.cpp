@@ -53,6 +53,8 @@ cudaError_t launch_decode(const DecParams& p, int dn, int grid, cudaStream_t str
 cudaError_t launch_export_codes(const uint8_t* wcodes, int bits, int kc_total, int out_dim, int in_dim,
                                 uint32_t* out, cudaStream_t stream);
 cudaError_t launch_exp_f64(const double* x, int64_t n, double* y, cudaStream_t stream);
+cudaError_t launch_repack_codes(const uint8_t* packed, int64_t nbytes, int bits, int64_t o, int64_t i,
+                                int64_t mb_count, int64_t kc_total, uint8_t* out, cudaStream_t stream);
 // artifact producer (tq_producer.cu)
 cudaError_t launch_estimate_hessian(const float* x, int64_t tokens, int64_t dim, double damping, double* acc,
                                     double* lambda, float* h, cudaStream_t stream);
@@ -70,6 +72,17 @@ cudaError_t launch_gptq(const float* r, int64_t rows, int64_t dim, int bits, int
 cudaError_t launch_proxy_loss(const float* orig, const uint8_t* codes, const float* scales, const int32_t* zeros,
                               int64_t rows, int64_t dim, int64_t gs, const float* h, int64_t chunk_rows, double* he_t,
                               double* rowsum, double* total, cudaStream_t stream);
+cudaError_t launch_widen(const float* w, int64_t n, double* out, cudaStream_t stream);
+cudaError_t launch_matvec(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                          cudaStream_t stream);
+cudaError_t launch_mattvec(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
+                           cudaStream_t stream);
+cudaError_t launch_norm2(const double* v, int64_t n, double* out, cudaStream_t stream);
+cudaError_t launch_div_by(const double* src, int64_t n, const double* d, double* dst, cudaStream_t stream);
+cudaError_t launch_deflate(double* a, int64_t rows, int64_t cols, const double* sigma, const double* u,
+                           const double* v, cudaStream_t stream);
+cudaError_t launch_pack_triples(const double* us, const double* vs, const int32_t* order, int64_t rank, int64_t rows,
+                                int64_t cols, float* left, float* right, cudaStream_t stream);
 cudaError_t launch_ep_units(const int32_t* counts, int n_src, int e_stride, int n_local, int slab, int mb_count, int bn,
                             int kc_end, int n_ext, Unit* units, int32_t* n_units, cudaStream_t stream);
 
@@ -421,38 +434,6 @@ CUtensorMap make_map(void* base, uint64_t rows, uint64_t cols, uint32_t box_rows
 // repack: wire codes -> engine tile layout
 // ---------------------------------------------------------------------------
 
-// Encode 32 consecutive codes of one row into `bits` words (the super-word
-// layouts decoded by dequant32<BITS> in tq_kernels.cu).
-void pack_superword(const uint32_t* c, int bits, uint32_t* w) {
-    for (int j = 0; j < bits; ++j) w[j] = 0;
-    if (bits == 2) {
-        for (int j = 0; j < 2; ++j)
-            for (int m = 0; m < 8; ++m) {
-                const int p = 8 * j + m;
-                w[j] |= (c[2 * p] << (2 * m)) | (c[2 * p + 1] << (16 + 2 * m));
-            }
-    } else if (bits == 3) {
-        const int pos[5] = {0, 3, 6, 9, 12};
-        for (int j = 0; j < 3; ++j)
-            for (int m = 0; m < 5; ++m) {
-                const int p = 5 * j + m;
-                w[j] |= (c[2 * p] << pos[m]) | (c[2 * p + 1] << (16 + pos[m]));
-            }
-        for (int k = 0; k < 3; ++k) w[k] |= (((c[30] >> k) & 1u) << 15) | (((c[31] >> k) & 1u) << 31);
-    } else if (bits == 4) {
-        for (int j = 0; j < 4; ++j)
-            for (int m = 0; m < 4; ++m) {
-                const int p = 4 * j + m;
-                w[j] |= (c[2 * p] << (4 * m)) | (c[2 * p + 1] << (16 + 4 * m));
-            }
-    } else {
-        for (int j = 0; j < 8; ++j)
-            for (int m = 0; m < 2; ++m) {
-                const int p = 2 * j + m;
-                w[j] |= (c[2 * p] << (8 * m)) | (c[2 * p + 1] << (16 + 8 * m));
-            }
-    }
-}
 
 struct Geometry {
     int64_t K, top_k, i, o, S, r, M, N;
@@ -476,45 +457,26 @@ int prescale_exponent(const QMat& q) {
     return k;
 }
 
-// Repack one quantized matrix into [mb][kc] blocks + scale/zero slabs.
-void repack_qmat(const QMat& q, const Geometry& g, uint8_t* codes_out, uint16_t* scales_out, uint8_t* zeros_out,
-                 int* k_out) {
-    const int bits = g.bits;
-    const std::vector<uint32_t> codes = unpack_stream(q.packed, bits, static_cast<size_t>(g.o * g.i), "codes");
+// Scale / zero slabs of one scalar matrix ([mb][group][row], scales prescaled by
+// 2^k); its code blocks are repacked on the device from the packed stream
+// (repack_codes_kernel) once the layer's device memory exists.
+void repack_slabs(const QMat& q, const Geometry& g, uint16_t* scales_out, uint8_t* zeros_out, int* k_out) {
     const int k = prescale_exponent(q);
     *k_out = k;
-    const int blk = code_block_bytes(bits);
-    uint32_t cbuf[32];
-    uint32_t wbuf[8];
-    for (int64_t mb = 0; mb < g.mb_count; ++mb) {
-        for (int64_t kc = 0; kc < g.kc_total; ++kc) {
-            uint32_t* block = reinterpret_cast<uint32_t*>(codes_out + (mb * g.kc_total + kc) * blk);
-            for (int h = 0; h < 2; ++h) {
-                for (int rl = 0; rl < kBM; ++rl) {
-                    const int64_t row = mb * kBM + rl;
-                    for (int t = 0; t < 32; ++t) {
-                        const int64_t col = kc * kKC + 32 * h + t;
-                        cbuf[t] = (row < g.o && col < g.i) ? codes[static_cast<size_t>(row * g.i + col)] : 0u;
-                    }
-                    pack_superword(cbuf, bits, wbuf);
-                    for (int j = 0; j < bits; ++j) block[(h * bits + j) * kBM + rl] = wbuf[j];
-                }
-            }
-        }
+    for (int64_t mb = 0; mb < g.mb_count; ++mb)
         for (int64_t gi = 0; gi < g.G; ++gi)
             for (int rl = 0; rl < kBM; ++rl) {
                 const int64_t row = mb * kBM + rl;
                 const size_t dst = static_cast<size_t>((mb * g.G + gi) * kBM + rl);
                 if (row < g.o) {
-                    const float s = half_bits_to_float(q.scales[static_cast<size_t>(row * g.G + gi)]);
-                    scales_out[dst] = float_to_half_bits(std::ldexp(s, k));
+                    const float sv = half_bits_to_float(q.scales[static_cast<size_t>(row * g.G + gi)]);
+                    scales_out[dst] = float_to_half_bits(std::ldexp(sv, k));
                     zeros_out[dst] = q.zeros[static_cast<size_t>(row * g.G + gi)];
                 } else {
                     scales_out[dst] = 0;
                     zeros_out[dst] = 0;
                 }
             }
-    }
 }
 
 // Codebook residual -> dense fp16 blocks in the engine's [mb][kc] layout: word
@@ -1203,7 +1165,10 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
     const int64_t blk = code_block_bytes(bits);
     L->weight_stride = g.mb_count * g.kc_total * blk;
     const int64_t slab = g.mb_count * g.G * kBM;  // scale / zero entries per matrix
-    std::vector<uint8_t> h_codes(static_cast<size_t>(L->weight_stride * L->n_weights));
+    // scalar code streams are repacked on the device after upload (below); only the
+    // dense-weight paths (codebook / odd group sizes) build their blocks on the host
+    const bool device_repack = !L->dense;
+    std::vector<uint8_t> h_codes(device_repack ? 0 : static_cast<size_t>(L->weight_stride * L->n_weights));
     std::vector<uint16_t> h_scales(static_cast<size_t>(slab * L->n_weights));
     std::vector<uint8_t> h_zeros(static_cast<size_t>(slab * L->n_weights));
     std::vector<int> wk(static_cast<size_t>(L->n_weights), 0);
@@ -1223,8 +1188,7 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
                             repack_dense_scalar(q[w], g, h_codes.data() + w * L->weight_stride,
                                                 h_scales.data() + w * slab, h_zeros.data() + w * slab, &wk[w]);
                         else
-                            repack_qmat(q[w], g, h_codes.data() + w * L->weight_stride, h_scales.data() + w * slab,
-                                        h_zeros.data() + w * slab, &wk[w]);
+                            repack_slabs(q[w], g, h_scales.data() + w * slab, h_zeros.data() + w * slab, &wk[w]);
                     } catch (const std::exception& e) {
                         errs[w] = e.what();
                     }
@@ -1234,6 +1198,9 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
         for (size_t w = 0; w < errs.size(); ++w)
             if (!errs[w].empty()) fail(TQ_ERR_FORMAT, errs[w]);
     }
+    std::vector<std::vector<uint8_t>> packed_streams;
+    if (device_repack)
+        for (auto& m : q) packed_streams.push_back(std::move(m.packed));
     q.clear();
     std::vector<float> h_outscale(static_cast<size_t>(L->n_weights));
     for (int64_t w = 0; w < L->n_weights; ++w) h_outscale[w] = static_cast<float>(std::ldexp(1.0, -wk[w]));
@@ -1383,7 +1350,26 @@ void build_layer(tq_layer* L, HostArtifact& a, int device, int64_t e_begin, int6
     }
     // --- upload ---
     L->gate.upload(gate_b.data(), gate_b.size());
-    L->codes.upload(h_codes.data(), h_codes.size());
+    if (device_repack) {
+        // packed streams -> device -> engine blocks (repack_codes_kernel), one staging
+        // buffer reused across matrices
+        L->codes.alloc(static_cast<size_t>(L->weight_stride * L->n_weights));
+        size_t max_stream = 0;
+        for (const auto& ps : packed_streams) max_stream = std::max(max_stream, ps.size());
+        DBuf staging;
+        staging.alloc(max_stream);
+        for (int64_t w = 0; w < L->n_weights; ++w) {
+            const auto& ps = packed_streams[static_cast<size_t>(w)];
+            cuda_check(cudaMemcpy(staging.p, ps.data(), ps.size(), cudaMemcpyHostToDevice), "packed stream H2D");
+            cuda_check(launch_repack_codes(staging.as<uint8_t>(), static_cast<int64_t>(ps.size()), g.bits, g.o, g.i,
+                                           g.mb_count, g.kc_total, L->codes.as<uint8_t>() + w * L->weight_stride,
+                                           nullptr),
+                       "repack launch");
+        }
+        cuda_check(cudaDeviceSynchronize(), "repack sync");   // staging is reused / freed
+    } else {
+        L->codes.upload(h_codes.data(), h_codes.size());
+    }
     L->scales.upload(h_scales.data(), h_scales.size() * 2);
     L->ext_blocks.upload(h_ext.data(), h_ext.size());
     L->w_outscale.upload(h_outscale.data(), h_outscale.size() * 4);
@@ -3082,3 +3068,133 @@ tq_status tq_proxy_loss(const float* original, int64_t rows, int64_t cols, const
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// sketch_lowrank (lowrank.cpp:194-247) with the mat-vecs on the device
+// ---------------------------------------------------------------------------
+
+namespace {
+
+// The reference's counter-based generator (rng.hpp: splitmix64 finalizer over
+// seed + n * golden gamma, Box-Muller with a cached spare), restated: the probes
+// are drawn here on the host with the host's libm, exactly as the reference
+// draws them, and uploaded.
+class SketchRng {
+public:
+    explicit SketchRng(uint64_t seed) : seed_(seed) {}
+    double gaussian() {
+        if (spare_ok_) {
+            spare_ok_ = false;
+            return spare_;
+        }
+        const double u1 = 1.0 - unit();
+        const double u2 = unit();
+        const double radius = std::sqrt(-2.0 * std::log(u1));
+        const double angle = 6.283185307179586476925286766559 * u2;
+        spare_ = radius * std::sin(angle);
+        spare_ok_ = true;
+        return radius * std::cos(angle);
+    }
+
+private:
+    static uint64_t mix(uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        return z ^ (z >> 31);
+    }
+    double unit() { return static_cast<double>(mix(seed_ + (++counter_) * 0x9E3779B97F4A7C15ull) >> 11) * 0x1.0p-53; }
+    uint64_t seed_;
+    uint64_t counter_ = 0;
+    double spare_ = 0.0;
+    bool spare_ok_ = false;
+};
+
+double read_scalar(const double* d, cudaStream_t st) {
+    double v = 0.0;
+    cuda_check(cudaMemcpyAsync(&v, d, sizeof(double), cudaMemcpyDeviceToHost, st), "scalar D2H");
+    cuda_check(cudaStreamSynchronize(st), "stream sync");
+    return v;
+}
+
+}  // namespace
+
+extern "C" tq_status tq_sketch_lowrank(const float* w, int64_t rows, int64_t cols, int64_t rank, int power_iters,
+                                       uint64_t seed, float* left, float* right, float* singulars, void* stream) {
+    return guarded([&] {
+        if (rows <= 0 || cols <= 0) fail(TQ_ERR_PARAM, "sketch_lowrank: input matrix is empty");
+        const int64_t cap = std::min(rows, cols);
+        if (rank < 1 || rank > cap)
+            fail(TQ_ERR_PARAM, "sketch_lowrank: rank " + std::to_string(rank) + " outside [1, " + std::to_string(cap) +
+                                   "] for a " + std::to_string(rows) + "x" + std::to_string(cols) + " matrix");
+        if (power_iters < 0) fail(TQ_ERR_PARAM, "sketch_lowrank: power_iters must be >= 0");
+        if (!w || !left || !right || !singulars) fail(TQ_ERR_PARAM, "sketch_lowrank: null buffer");
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        AsyncBuf work(sizeof(double) * rows * cols, st), q(sizeof(double) * rows, st), t(sizeof(double) * cols, st),
+            us(sizeof(double) * rank * rows, st), vs(sizeof(double) * rank * cols, st), sig(sizeof(double) * rank, st),
+            nrm(sizeof(double), st), order_d(sizeof(int32_t) * rank, st);
+        cuda_check(launch_widen(w, rows * cols, work.as<double>(), st), "widen launch");
+        SketchRng rng(seed);
+        std::vector<double> probe(static_cast<size_t>(cols)), sigmas(static_cast<size_t>(rank), 0.0);
+        double* W = work.as<double>();
+        double* Q = q.as<double>();
+        double* T = t.as<double>();
+        for (int64_t j = 0; j < rank; ++j) {
+            for (double& p : probe) p = rng.gaussian();
+            cuda_check(cudaMemcpyAsync(T, probe.data(), sizeof(double) * cols, cudaMemcpyHostToDevice, st),
+                       "probe H2D");
+            cuda_check(launch_matvec(W, rows, cols, T, Q, st), "matvec launch");
+            cuda_check(launch_norm2(Q, rows, nrm.as<double>(), st), "norm launch");
+            bool dead = read_scalar(nrm.as<double>(), st) == 0.0;   // (also orders the probe buffer's reuse)
+            if (!dead) {
+                cuda_check(launch_div_by(Q, rows, nrm.as<double>(), Q, st), "scale launch");
+                for (int it = 0; it < power_iters && !dead; ++it) {
+                    cuda_check(launch_mattvec(W, rows, cols, Q, T, st), "mattvec launch");
+                    cuda_check(launch_matvec(W, rows, cols, T, Q, st), "matvec launch");
+                    cuda_check(launch_norm2(Q, rows, nrm.as<double>(), st), "norm launch");
+                    if (read_scalar(nrm.as<double>(), st) == 0.0) dead = true;
+                    else cuda_check(launch_div_by(Q, rows, nrm.as<double>(), Q, st), "scale launch");
+                }
+            }
+            double* Uj = us.as<double>() + j * rows;
+            double* Vj = vs.as<double>() + j * cols;
+            if (!dead) {
+                cuda_check(launch_mattvec(W, rows, cols, Q, T, st), "mattvec launch");
+                double* Sj = sig.as<double>() + j;
+                cuda_check(launch_norm2(T, cols, Sj, st), "norm launch");
+                const double sigma = read_scalar(Sj, st);
+                if (sigma == 0.0) {
+                    dead = true;
+                } else {
+                    sigmas[static_cast<size_t>(j)] = sigma;
+                    cuda_check(cudaMemcpyAsync(Uj, Q, sizeof(double) * rows, cudaMemcpyDeviceToDevice, st), "u D2D");
+                    cuda_check(launch_div_by(T, cols, Sj, Vj, st), "v launch");
+                    cuda_check(launch_deflate(W, rows, cols, Sj, Uj, Vj, st), "deflate launch");
+                }
+            }
+            if (dead) {   // basis_triple (lowrank.cpp:101-108)
+                cuda_check(cudaMemsetAsync(Uj, 0, sizeof(double) * rows, st), "u memset");
+                cuda_check(cudaMemsetAsync(Vj, 0, sizeof(double) * cols, st), "v memset");
+                const double one = 1.0;
+                cuda_check(cudaMemcpyAsync(Uj + j % rows, &one, sizeof(double), cudaMemcpyHostToDevice, st), "u e_j");
+                cuda_check(cudaMemcpyAsync(Vj + j % cols, &one, sizeof(double), cudaMemcpyHostToDevice, st), "v e_j");
+                cuda_check(cudaStreamSynchronize(st), "stream sync");   // (&one is a stack value)
+                sigmas[static_cast<size_t>(j)] = 0.0;
+            }
+        }
+        // nonincreasing sigma, stable (lowrank.cpp:80-82)
+        std::vector<int32_t> order(static_cast<size_t>(rank));
+        for (int64_t j = 0; j < rank; ++j) order[static_cast<size_t>(j)] = static_cast<int32_t>(j);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return sigmas[static_cast<size_t>(a)] > sigmas[static_cast<size_t>(b)]; });
+        std::vector<float> sv(static_cast<size_t>(rank));
+        for (int64_t p2 = 0; p2 < rank; ++p2) sv[static_cast<size_t>(p2)] = static_cast<float>(sigmas[order[static_cast<size_t>(p2)]]);
+        cuda_check(cudaMemcpyAsync(order_d.p, order.data(), sizeof(int32_t) * rank, cudaMemcpyHostToDevice, st),
+                   "order H2D");
+        cuda_check(cudaMemcpyAsync(singulars, sv.data(), sizeof(float) * rank, cudaMemcpyHostToDevice, st),
+                   "singulars H2D");
+        cuda_check(launch_pack_triples(us.as<double>(), vs.as<double>(), order_d.as<int32_t>(), rank, rows, cols, left,
+                                       right, st),
+                   "pack launch");
+        cuda_check(cudaStreamSynchronize(st), "stream sync");   // host order / sv lifetimes
+    });
+}

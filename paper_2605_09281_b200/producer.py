@@ -9,6 +9,7 @@ mostly proxy_loss):
     quantize_gptq(r, h, bits, group_size)      quant.hpp:85,   quant.cpp:177-221
     proxy_loss(original, q, h)                 quant.hpp:104,  quant.cpp:325-343
     spd_inverse(h)                             quant.cpp:72-112 (internal there)
+    sketch_lowrank(w, rank, power_iters, seed) lowrank.hpp:21-30, lowrank.cpp:194-247
 
 Results are bit-identical to the reference's (same f64 operations in the same
 order per element; tq_producer.cu).  Matrices may be numpy arrays or CUDA
@@ -154,5 +155,28 @@ def proxy_loss(original, q: QuantizedExpert, h) -> float:
     return out.value
 
 
-__all__ = ["HessianProxy", "QuantizedExpert", "estimate_hessian", "identity_hessian", "spd_inverse",
+@dataclass
+class LowRankFactor:
+    """lowrank.hpp:15-19: left (rows x r), singulars (r, nonincreasing), right (r x cols); f32 CUDA tensors."""
+    left: object
+    singulars: object
+    right: object
+
+
+def sketch_lowrank(w, rank: int, power_iters: int, seed: int) -> LowRankFactor:
+    torch = _torch()
+    wd = _as_dev(w, torch.float32)
+    if wd.ndim != 2:
+        raise ParamError("sketch_lowrank: input must be 2-D")
+    rows, cols = wd.shape
+    r = max(int(rank), 0)
+    left = torch.empty((rows, r), dtype=torch.float32, device=_dev())
+    right = torch.empty((r, cols), dtype=torch.float32, device=_dev())
+    sing = torch.empty((r,), dtype=torch.float32, device=_dev())
+    check(lib().tq_sketch_lowrank(wd.data_ptr(), rows, cols, int(rank), int(power_iters), int(seed) & (2**64 - 1),
+                                  left.data_ptr(), right.data_ptr(), sing.data_ptr(), _stream_ptr(_dev())))
+    return LowRankFactor(left, sing, right)
+
+
+__all__ = ["HessianProxy", "LowRankFactor", "sketch_lowrank", "QuantizedExpert", "estimate_hessian", "identity_hessian", "spd_inverse",
            "quantize_rtn", "quantize_gptq", "proxy_loss"]

@@ -135,3 +135,39 @@ def test_errors_match_reference(prod, ref):
         prod.estimate_hessian(np.zeros((0, 4), np.float32), 0.01)
     with pytest.raises(tq.ParamError):
         prod.estimate_hessian(np.ones((2, 4), np.float32), -1.0)
+
+
+SKETCH = [(30, 20, 5, 2, 7), (64, 200, 8, 4, 11), (257, 33, 6, 0, 3), (100, 100, 12, 4, 5), (1, 40, 1, 3, 9)]
+
+
+@pytest.mark.parametrize("rows,cols,rank,iters,seed", SKETCH)
+def test_sketch_lowrank_bit_exact(prod, ref, rows, cols, rank, iters, seed):
+    w = np.random.default_rng(rows * cols + seed).standard_normal((rows, cols)).astype(np.float32)
+    f = prod.sketch_lowrank(w, rank, iters, seed)
+    l, s, r = ref.sketch_lowrank(w, rank, iters, seed)
+    np.testing.assert_array_equal(f.singulars.cpu().numpy().view(np.uint32), s.view(np.uint32))
+    np.testing.assert_array_equal(f.left.cpu().numpy().view(np.uint32), l.view(np.uint32))
+    np.testing.assert_array_equal(f.right.cpu().numpy().view(np.uint32), r.view(np.uint32))
+
+
+def test_sketch_lowrank_rank_deficient_and_zero(prod, ref):
+    """Exhausted directions become basis triples (sigma 0), sorted last, as in the reference."""
+    rng = np.random.default_rng(4)
+    w = (rng.standard_normal((40, 2)) @ rng.standard_normal((2, 24))).astype(np.float32)   # rank 2
+    for m in (w, np.zeros((12, 9), np.float32)):
+        f = prod.sketch_lowrank(m, 5, 2, 21)
+        l, s, r = ref.sketch_lowrank(m, 5, 2, 21)
+        np.testing.assert_array_equal(f.singulars.cpu().numpy().view(np.uint32), s.view(np.uint32))
+        np.testing.assert_array_equal(f.left.cpu().numpy().view(np.uint32), l.view(np.uint32))
+        np.testing.assert_array_equal(f.right.cpu().numpy().view(np.uint32), r.view(np.uint32))
+
+
+def test_sketch_lowrank_errors_match_reference(prod, ref):
+    import paper_2605_09281_b200 as tq
+    w = np.ones((6, 4), np.float32)
+    for rank, iters in ((0, 1), (5, 1), (2, -1)):
+        with pytest.raises(tq.ParamError) as e1:
+            prod.sketch_lowrank(w, rank, iters, 1)
+        with pytest.raises(Exception) as e2:
+            ref.sketch_lowrank(w, max(rank, 0), iters, 1)
+        assert str(e1.value) == e2.value.msg

@@ -33,6 +33,9 @@ def main():
     ap.add_argument("--cpu-rows2", type=int, default=0,
                     help="second GPTQ sample size: per-row cost = difference of the two runs (same spd_inverse)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sketch", default="43008x12288", help="sketch_lowrank shape (the c2 3x3 mosaic), '' to skip")
+    ap.add_argument("--sketch-rank", type=int, default=32)
+    ap.add_argument("--sketch-iters", type=int, default=4)
     a = ap.parse_args()
     import torch
     from paper_2605_09281_b200 import producer as P
@@ -67,6 +70,14 @@ def main():
     gpu["proxy_loss_f64_macs"] = R * d * d + R * d
     gpu["proxy_loss_gmac_per_s"] = gpu["proxy_loss_f64_macs"] / (t_proxy * 1e6)
     gpu["gptq_sweep_updates"] = R * d * (d - 1) // 2
+    if a.sketch:
+        sr, sc = (int(v) for v in a.sketch.split("x"))
+        wm = torch.randn((sr, sc), device=dev, generator=g)
+        t_sk, f = timed(lambda: P.sketch_lowrank(wm, a.sketch_rank, a.sketch_iters, 7))
+        passes = (2 * a.sketch_iters + 2) + 2   # mat-vecs + deflate (read + write) per triple
+        gpu["sketch_lowrank_ms"] = t_sk
+        gpu["sketch_shape"] = [sr, sc, a.sketch_rank, a.sketch_iters]
+        gpu["sketch_gbs"] = a.sketch_rank * passes * sr * sc * 8 / (t_sk * 1e6)
     out["gpu"] = gpu
 
     if not a.no_cpu:
@@ -96,6 +107,12 @@ def main():
         Oracle().spd_inverse(h_ref)
         t_inv_cpu = time.perf_counter() - t0
         scale = a.rows / cn
+        if a.sketch:
+            # one triple of the sketch on the full mosaic: every triple streams the
+            # same working copy the same number of times, so rank x this is the stage
+            t0 = time.perf_counter()
+            ref.sketch_lowrank(wm.cpu().numpy(), 1, a.sketch_iters, 7)
+            t_sk1 = time.perf_counter() - t0
         per_row = None
         if a.cpu_rows2 > cn:
             rs2 = r[:a.cpu_rows2, :cd].float().cpu().numpy()
@@ -109,6 +126,8 @@ def main():
             "quantize_gptq_s_sample": t_gptq_cpu, "spd_inverse_s": t_inv_cpu,
             "proxy_loss_s_scaled_to_rows": t_proxy_cpu * scale,
             "quantize_gptq_per_row_s": per_row,
+            "sketch_lowrank_rank1_s": t_sk1 if a.sketch else None,
+            "sketch_lowrank_s_scaled_to_rank": t_sk1 * a.sketch_rank if a.sketch else None,
             "quantize_gptq_s_scaled_to_rows": (t_gptq_cpu + per_row * (a.rows - cn)
                                                if per_row is not None and cd == a.dim else None),
         }

@@ -612,8 +612,9 @@ __global__ void widen_kernel(const float* __restrict__ w, int64_t n, double* __r
 }
 
 // y[r] = sum_c a[r][c] * x[c], c ascending (lowrank.cpp:37-46).  A warp owns 32
-// rows: it stages 32 x 32 tiles with coalesced row segments and each lane walks
-// its own row through the tile.
+// rows: it stages 32 x 32 tiles with coalesced row segments (the next tile's
+// loads issued before the current tile is consumed) and each lane walks its own
+// row through the tile.
 constexpr int kMvWarps = 4;
 __global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __restrict__ a, int64_t rows,
                                                                 int64_t cols, const double* __restrict__ x,
@@ -622,59 +623,103 @@ __global__ void __launch_bounds__(kMvWarps * 32) matvec_kernel(const double* __r
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t r0 = (static_cast<int64_t>(blockIdx.x) * kMvWarps + warp) * 32;
     if (r0 >= rows) return;   // warp-uniform; no CTA barriers below
+    const int nrow = static_cast<int>(rows - r0 < 32 ? rows - r0 : 32);
+    double nxt[32];
+    auto fetch = [&](int64_t c0) {
+        const bool ok = c0 + lane < cols;
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) nxt[rr] = (ok && rr < nrow) ? __ldcs(a + (r0 + rr) * cols + c0 + lane) : 0.0;
+    };
     double acc = 0.0;
+    fetch(0);
     for (int64_t c0 = 0; c0 < cols; c0 += 32) {
         const int w = static_cast<int>(cols - c0 < 32 ? cols - c0 : 32);
-#pragma unroll 8
-        for (int rr = 0; rr < 32; ++rr) {
-            const int64_t r = r0 + rr;
-            tile[warp][rr][lane] = (r < rows && lane < w) ? a[r * cols + c0 + lane] : 0.0;
-        }
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) tile[warp][rr][lane] = nxt[rr];
         const double xv = lane < w ? x[c0 + lane] : 0.0;
         __syncwarp();
+        if (c0 + 32 < cols) fetch(c0 + 32);
         for (int k = 0; k < w; ++k) {
             const double xk = __shfl_sync(0xffffffffu, xv, k);
             acc = __dadd_rn(acc, __dmul_rn(tile[warp][lane][k], xk));
         }
         __syncwarp();
     }
-    if (r0 + lane < rows) y[r0 + lane] = acc;
+    if (lane < nrow) y[r0 + lane] = acc;
 }
 
-// y[c] = sum_r a[r][c] * x[r], r ascending (lowrank.cpp:48-56): one thread per
-// column (coalesced across the warp), 32 row loads in flight per thread.
-constexpr int kMtvUnroll = 32;
-__global__ void __launch_bounds__(64) mattvec_kernel(const double* __restrict__ a, int64_t rows, int64_t cols,
-                                                      const double* __restrict__ x, double* __restrict__ y) {
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (c >= cols) return;
+// y[c] = sum_r a[r][c] * x[r], r ascending (lowrank.cpp:48-56).  A CTA owns 32
+// columns: its warps stream kMtvRows x 32 tiles (coalesced 256-byte row
+// segments) into a kMtvStages-deep shared ring with cp.async, and warp 0 -- one
+// lane per column -- adds the rows in order out of shared memory; the ring keeps
+// several tiles in flight so the add chain, not the load latency, sets the pace.
+constexpr int kMtvWarps = 4, kMtvRows = 32, kMtvStages = 5;
+__global__ void __launch_bounds__(kMtvWarps * 32) mattvec_kernel(const double* __restrict__ a, int64_t rows,
+                                                                  int64_t cols, const double* __restrict__ x,
+                                                                  double* __restrict__ y) {
+    __shared__ double tile[kMtvStages][kMtvRows][32];
+    __shared__ double xs[kMtvStages][kMtvRows];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + lane;
+    const bool col_ok = c < cols;
+    const int64_t nchunks = (rows + kMtvRows - 1) / kMtvRows;
+    auto stage = [&](int64_t chunk) {   // every thread issues its share, then commits one group
+        if (chunk < nchunks) {
+            const int buf = static_cast<int>(chunk % kMtvStages);
+            const int64_t rb = chunk * kMtvRows;
+            for (int rr = warp; rr < kMtvRows; rr += kMtvWarps) {
+                const int64_t r = rb + rr;
+                if (r < rows && col_ok) cp_async8(&tile[buf][rr][lane], a + r * cols + c);
+                else tile[buf][rr][lane] = 0.0;
+            }
+            if (warp == 0) {
+                const int64_t r = rb + lane;
+                if (r < rows) cp_async8(&xs[buf][lane], x + r);
+                else xs[buf][lane] = 0.0;
+            }
+        }
+        cp_async_commit();
+    };
+    for (int64_t k = 0; k < kMtvStages - 1; ++k) stage(k);
     double acc = 0.0;
-    int64_t r = 0;
-    for (; r + kMtvUnroll <= rows; r += kMtvUnroll) {
-        double v[kMtvUnroll];
-#pragma unroll
-        for (int u = 0; u < kMtvUnroll; ++u) v[u] = __ldcs(a + (r + u) * cols + c);
-#pragma unroll
-        for (int u = 0; u < kMtvUnroll; ++u) acc = __dadd_rn(acc, __dmul_rn(v[u], x[r + u]));
+    for (int64_t chunk = 0; chunk < nchunks; ++chunk) {
+        stage(chunk + kMtvStages - 1);
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kMtvStages - 1) : "memory");
+        __syncthreads();
+        if (warp == 0) {
+            const int buf = static_cast<int>(chunk % kMtvStages);
+            const int n = static_cast<int>(rows - chunk * kMtvRows < kMtvRows ? rows - chunk * kMtvRows : kMtvRows);
+            for (int rr = 0; rr < n; ++rr) acc = __dadd_rn(acc, __dmul_rn(tile[buf][rr][lane], xs[buf][rr]));
+        }
+        __syncthreads();   // the slot is refilled kMtvStages - 1 chunks later
     }
-    for (; r < rows; ++r) acc = __dadd_rn(acc, __dmul_rn(a[r * cols + c], x[r]));
-    y[c] = acc;
+    if (warp == 0 && col_ok) y[c] = acc;
 }
 
-// sqrt(sum v^2), v ascending (lowrank.cpp:58-62): one thread, loads run ahead
+// sqrt(sum v^2), v ascending (lowrank.cpp:58-62): one warp; the lanes load and
+// square 32 consecutive entries, every lane adds them in order (shuffles), so
+// only the dependent add chain is serial
 __global__ void norm2_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
     double acc = 0.0;
-    int64_t t = 0;
-    for (; t + 16 <= n; t += 16) {
-        double b[16];
+    double nxt = lane < n ? v[lane] : 0.0;
+    for (int64_t t0 = 0; t0 < n; t0 += 32) {
+        const double cur = nxt;
+        if (t0 + 32 + lane < n) nxt = v[t0 + 32 + lane];
+        const double sq = __dmul_rn(cur, cur);
+        if (n - t0 >= 32) {   // full chunk: the 32 shuffles issue ahead of the add chain
+            double b[32];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) b[u] = v[t + u];
+            for (int k = 0; k < 32; ++k) b[k] = __shfl_sync(0xffffffffu, sq, k);
 #pragma unroll
-        for (int u = 0; u < 16; ++u) acc = __dadd_rn(acc, __dmul_rn(b[u], b[u]));
+            for (int k = 0; k < 32; ++k) acc = __dadd_rn(acc, b[k]);
+        } else {
+            const int m = static_cast<int>(n - t0);
+            for (int k = 0; k < m; ++k) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, sq, k));
+        }
     }
-    for (; t < n; ++t) acc = __dadd_rn(acc, __dmul_rn(v[t], v[t]));
-    *out = __dsqrt_rn(acc);
+    if (lane == 0) *out = __dsqrt_rn(acc);
 }
 
 // dst[i] = src[i] / *d  (x /= qn, v /= sigma)
@@ -686,15 +731,14 @@ __global__ void div_by_kernel(const double* __restrict__ src, int64_t n, const d
         dst[e] = __ddiv_rn(src[e], den);
 }
 
-// work[r][c] -= (sigma * u[r]) * v[c]  (lowrank.cpp:232-236)
+// work[r][c] -= (sigma * u[r]) * v[c]  (lowrank.cpp:232-236); a CTA per row band
 __global__ void deflate_kernel(double* __restrict__ a, int64_t rows, int64_t cols, const double* __restrict__ sigma,
                                const double* __restrict__ u, const double* __restrict__ v) {
     const double s = *sigma;
-    const int64_t n = rows * cols;
-    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = e / cols, c = e - r * cols;
-        a[e] = __dsub_rn(a[e], __dmul_rn(__dmul_rn(s, u[r]), v[c]));
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const double ur = __dmul_rn(s, u[r]);
+        double* row = a + r * cols;
+        for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) row[c] = __dsub_rn(row[c], __dmul_rn(ur, v[c]));
     }
 }
 
@@ -879,7 +923,7 @@ cudaError_t launch_matvec(const double* a, int64_t rows, int64_t cols, const dou
 }
 cudaError_t launch_mattvec(const double* a, int64_t rows, int64_t cols, const double* x, double* y,
                            cudaStream_t stream) {
-    mattvec_kernel<<<static_cast<unsigned>((cols + 63) / 64), 64, 0, stream>>>(a, rows, cols, x, y);
+    mattvec_kernel<<<static_cast<unsigned>((cols + 31) / 32), kMtvWarps * 32, 0, stream>>>(a, rows, cols, x, y);
     return cudaGetLastError();
 }
 cudaError_t launch_norm2(const double* v, int64_t n, double* out, cudaStream_t stream) {
@@ -892,7 +936,8 @@ cudaError_t launch_div_by(const double* src, int64_t n, const double* d, double*
 }
 cudaError_t launch_deflate(double* a, int64_t rows, int64_t cols, const double* sigma, const double* u,
                            const double* v, cudaStream_t stream) {
-    deflate_kernel<<<grid_for(rows * cols, 256), 256, 0, stream>>>(a, rows, cols, sigma, u, v);
+    deflate_kernel<<<static_cast<unsigned>(rows < 148 * 16 ? rows : 148 * 16), 512, 0, stream>>>(a, rows, cols, sigma,
+                                                                                               u, v);
     return cudaGetLastError();
 }
 cudaError_t launch_pack_triples(const double* us, const double* vs, const int32_t* order, int64_t rank, int64_t rows,

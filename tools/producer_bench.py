@@ -3,7 +3,7 @@ shape and the reference's CPU implementation on bounded samples.
 
     python tools/producer_bench.py [--rows 14336] [--dim 4096] [--tokens 512] [--cpu-rows 8]
 
-GPU: CUDA events around each stage (estimate_hessian over `tokens` calibration
+GPU: CUDA events around each stage (best of 3 after a warm-up call) (estimate_hessian over `tokens` calibration
 rows; spd_inverse; quantize_rtn; quantize_gptq = spd_inverse + grids + the
 column sweep + RTN + two proxy losses; proxy_loss).  CPU: the reference
 (oracle/_ref) on the same dim with `cpu-rows` residual rows, one thread, and
@@ -46,16 +46,18 @@ def main():
     r = torch.randn((a.rows, a.dim), device=dev, generator=g) * 0.02
     out = {"config": {"rows": a.rows, "dim": a.dim, "tokens": a.tokens, "bits": a.bits, "group_size": a.gs}}
 
-    def timed(fn, reps=1):
-        fn()   # warm-up (allocator, module load)
+    def timed(fn, reps=3):
+        fn()   # warm-up (allocator, module load, clocks)
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(reps):
+        best, res = float("inf"), None
+        for _ in range(reps):   # best of `reps` (each call synchronizes where the API returns host values)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             res = fn()
-        e1.record()
-        torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / reps, res
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        return best, res
 
     t_h, hp = timed(lambda: P.estimate_hessian(calib, 0.01))
     t_inv, _ = timed(lambda: P.spd_inverse(hp))

@@ -171,3 +171,30 @@ def test_sketch_lowrank_errors_match_reference(prod, ref):
         with pytest.raises(Exception) as e2:
             ref.sketch_lowrank(w, max(rank, 0), iters, 1)
         assert str(e1.value) == e2.value.msg
+
+
+def test_producer_at_c1_dims(prod, ref):
+    """c1's in_dim (1024) and group size (128): the staged GPTQ sweep (R = 4 rows per
+    CTA, 512 threads dealing 1024 columns) and a 1024-wide H^-1, on 36 residual rows
+    (9 CTAs, the last one partial), against the reference; proxy losses equal."""
+    d = 1024
+    h, _ = ref.estimate_hessian(_calib(384, d, 77), 0.01)
+    hp = prod.estimate_hessian(_calib(384, d, 77), 0.01)
+    np.testing.assert_array_equal(hp.h.cpu().numpy().view(np.uint32), h.view(np.uint32))
+    r = _resid(36, d, 78, scale=0.02)
+    q = prod.quantize_gptq(r, hp, 3, 128)
+    c, s, z = ref.quantize("gptq", r, h, 3, 128)
+    np.testing.assert_array_equal(q.codes.cpu().numpy().astype(np.uint32), c)
+    np.testing.assert_array_equal(q.scales.cpu().numpy().view(np.uint32), s.view(np.uint32))
+    assert prod.proxy_loss(r, q, hp) == ref.proxy_loss(r, c, s, z, 3, 128, h)
+
+
+def test_sketch_at_mosaic_like_dims(prod, ref):
+    """A 2-row x 3-column mosaic of 768 x 512 blocks, rank 8, 4 power iterations
+    (the decompose stage's defaults), against the reference."""
+    w = np.random.default_rng(91).standard_normal((1536, 1536)).astype(np.float32)
+    f = prod.sketch_lowrank(w, 8, 4, 1234)
+    l, s, r = ref.sketch_lowrank(w, 8, 4, 1234)
+    np.testing.assert_array_equal(f.singulars.cpu().numpy().view(np.uint32), s.view(np.uint32))
+    np.testing.assert_array_equal(f.left.cpu().numpy().view(np.uint32), l.view(np.uint32))
+    np.testing.assert_array_equal(f.right.cpu().numpy().view(np.uint32), r.view(np.uint32))

@@ -1430,9 +1430,9 @@ __global__ void export_codes_kernel(const uint8_t* __restrict__ wcodes, int bits
 // activation row and the extension row [Sx | Z * zscale_e] of every destination
 // in the atom-major swizzled layout the expert GEMM bulk-copies.
 
-__device__ __forceinline__ void rtrace(const DecRouteArgs& a, int k) {
+__device__ __forceinline__ void rtrace(const DecRouteArgs& a, int k, unsigned tid = 0) {
 #ifdef TQ_ROUTE_TRACE
-    if (threadIdx.x == 0 && a.trace) {
+    if (threadIdx.x == tid && a.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         a.trace[(blockIdx.x * gridDim.y + blockIdx.y) * 16 + k] = t;
@@ -1440,6 +1440,7 @@ __device__ __forceinline__ void rtrace(const DecRouteArgs& a, int k) {
 #else
     (void)a;
     (void)k;
+    (void)tid;
 #endif
 }
 
@@ -1714,9 +1715,11 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
     //      group sums of the fp16 activations, the fp16 row staged in shared memory,
     //      the folded / scalar tile columns' projections of this token ----
     if (!a.given) {
-        if (warp == 0)
+        if (warp == 0) {
             route_pick(a.score_ws + static_cast<int64_t>(b) * K, K, k, sc, ex, pick_k, pick_p,
                        a.ids + static_cast<int64_t>(b) * k, a.gates + static_cast<int64_t>(b) * k, false);
+            rtrace(a, 11);
+        }
     } else if (static_cast<int>(threadIdx.x) < k) {
         pick_k[threadIdx.x] = a.ids_in[static_cast<int64_t>(b) * k + threadIdx.x];
     }
@@ -1759,6 +1762,7 @@ __global__ void __launch_bounds__(kRT, 512 / kRT) dec_route_kernel(const DecRout
             for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
             if (lane == 0) s_sx[g] = acc;
         }
+        rtrace(a, 12, 32);
     }
     for (int g = warp - w0; !one_pass && a.use_main && g >= 0 && g < a.groups; g += kRT / 32 - w0) {
         float acc = 0.0f;

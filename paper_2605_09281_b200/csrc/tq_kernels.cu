@@ -373,8 +373,7 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
                                                              int32_t* __restrict__ ids, float* __restrict__ gates,
                                                              __half* __restrict__ x16, float* __restrict__ sx,
                                                              float* __restrict__ score_ws, int32_t* __restrict__ ticket,
-                                                             int tokens_per_cta, const PlanArgs plan,
-                                                             int32_t* __restrict__ plan_ticket) {
+                                                             int tokens_per_cta) {
     __shared__ RouteSmem<kRT> sm;
     __shared__ float sc[64];
     __shared__ double ex[64];
@@ -422,21 +421,6 @@ __global__ void __launch_bounds__(kRT) route_kernel(const float* __restrict__ x,
                ids + static_cast<int64_t>(b) * top_k, gates + static_cast<int64_t>(b) * top_k);
     }   // last slice CTA of token b
     }   // tokens of this CTA
-    // ---- fused plan: the globally-last CTA permutes the finished routing ----
-    if (plan_ticket) {
-        __threadfence();   // this CTA's ids / gates
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int done = atomicAdd(plan_ticket, 1);
-            s_last = done == static_cast<int>(gridDim.x * gridDim.y) - 1;
-            if (s_last) *plan_ticket = 0;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            plan_body(plan, reinterpret_cast<int32_t*>(sm.prod));   // (16 + 1) * K + 1 ints <= 16 KB
-        }
-    }
 }
 
 // =============================================================================
@@ -1279,7 +1263,6 @@ __global__ void __launch_bounds__(kGatherThreads) gather_tokens_kernel(const Gat
 __global__ void __launch_bounds__(256) combine_kernel(const CombineArgs a) {
     pdl_wait();
     pdl_launch_dependents();
-    if (a.fused && *a.nsplit_dev == 1) return;   // the expert GEMM's epilogue combined already
     // 4 consecutive output columns per thread (float4 when out_dim % 4 == 0)
     const int b = blockIdx.y;
     const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -1966,12 +1949,9 @@ static void max_carveout(K kern) {
 
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
-                         float* score_ws, int32_t* ticket, const PlanArgs* plan, int32_t* plan_ticket,
-                         cudaStream_t stream) {
+                         float* score_ws, int32_t* ticket, cudaStream_t stream) {
     if (batch <= 0) return cudaSuccess;
     if (num_experts > 64 || top_k > 64) return cudaErrorInvalidValue;
-    if (plan && num_experts <= 0) return cudaErrorInvalidValue;
-    const PlanArgs pa = plan ? *plan : PlanArgs{};
 #ifndef TQ_ROUTE_TOKEN_CTAS
 #define TQ_ROUTE_TOKEN_CTAS (2 * 148)   // token-chunk CTAs at prefill (several tokens per CTA beyond this)
 #endif
@@ -1979,7 +1959,7 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     // serves smaller batches (at decode sizes the tile router's 16 sequential
     // chunks per CTA cost more than one CTA per token)
     constexpr int tile_min = 297;
-    const bool tile_ok = !plan && num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
+    const bool tile_ok = num_experts > 0 && tile_min > 0 && batch >= tile_min && (in_dim & 3) == 0 &&
                          (k_pad & 3) == 0 && (!sx || (group_size > 0 && kTC % group_size == 0));
     if (tile_ok) {
         static bool attr = false;
@@ -1998,13 +1978,11 @@ cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gat
     if (tpc > 1) {
         max_carveout(route_kernel<128>);
         return launch_maybe_pdl(route_kernel<128>, grid, dim3(128), 0, stream, x, batch, in_dim, gate, num_experts,
-                                top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
-                                plan ? plan_ticket : nullptr);
+                                top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc);
     }
     max_carveout(route_kernel<kRouteThreads>);
     return launch_maybe_pdl(route_kernel<kRouteThreads>, grid, dim3(kRouteThreads), 0, stream, x, batch, in_dim, gate, num_experts,
-                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc, pa,
-                            plan ? plan_ticket : nullptr);
+                            top_k, group_size, groups, k_pad, ids, gates, x16, sx, score_ws, ticket, tpc);
 }
 
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream) {
@@ -2034,7 +2012,6 @@ __global__ void __launch_bounds__(256, 4) combine_rows_kernel(const CombineArgs 
     __shared__ float s_gate[64];
     pdl_wait();
     pdl_launch_dependents();
-    if (a.fused && *a.nsplit_dev == 1) return;
     const int b = blockIdx.y;
     const int k = a.use_routed ? a.top_k : 0;
     if (static_cast<int>(threadIdx.x) < k) {

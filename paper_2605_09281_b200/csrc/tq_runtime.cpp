@@ -34,7 +34,7 @@ namespace tqb {
 cudaError_t launch_gemm(const GemmParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_route(const float* x, int batch, int in_dim, const float* gate, int num_experts, int top_k,
                          int group_size, int groups, int k_pad, int32_t* ids, float* gates, __half* x16, float* sx,
-                         float* score_ws, int32_t* ticket, const PlanArgs* plan, int32_t* plan_ticket,
+                         float* score_ws, int32_t* ticket,
                          cudaStream_t stream);
 cudaError_t launch_plan(const PlanArgs& a, cudaStream_t stream);
 cudaError_t launch_gather(const GatherArgs& a, int max_rows, cudaStream_t stream);
@@ -797,8 +797,8 @@ void reserve(tq_layer* L, int64_t max_tokens) {
     L->x16.alloc(sizeof(__half) * cap * g.k_pad);
     L->sx.alloc(sizeof(float) * cap * std::max<int64_t>(1, g.G));
     L->route_ws.alloc(sizeof(float) * cap * g.K);
-    L->route_ticket.alloc(sizeof(int32_t) * (cap + 1));   // + the fused plan's grid ticket
-    cuda_check(cudaMemset(L->route_ticket.p, 0, sizeof(int32_t) * (cap + 1)), "cudaMemset");
+    L->route_ticket.alloc(sizeof(int32_t) * cap);
+    cuda_check(cudaMemset(L->route_ticket.p, 0, sizeof(int32_t) * cap), "cudaMemset");
     L->perm.alloc(sizeof(int32_t) * cap * g.top_k);
     L->inv.alloc(sizeof(int32_t) * cap * g.top_k);
     L->offsets.alloc(sizeof(int32_t) * (g.K + 1));
@@ -1450,17 +1450,10 @@ void count_launch(tq_layer* L, int n = 1) {
     }
 }
 
-// the plan fused into the router's last CTA (TQ_FUSE_PLAN=1; off by default:
-// measured slower, the plan's unit loop wants the full 1024-thread CTA)
-static bool fuse_plan(const tq_layer* L) {
-    (void)L;
-    return false;
-}
-
-// prep (x16, sx) and optional routing; with `plan` the router's last CTA also
-// runs the plan (permutation + work units) on the routing it just produced
-void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st,
-               const PlanArgs* plan = nullptr) {
+// prep (x16, sx) and optional routing (the plan runs as its own launch: fused into
+// the router's last CTA it measured slower -- the plan's unit loop wants the full
+// 1024-thread CTA)
+void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaStream_t st) {
     if (L->ktime) {
         L->kt_stream = st;
         L->kt_active = true;
@@ -1473,8 +1466,7 @@ void run_route(tq_layer* L, const float* x, int64_t batch, bool do_route, cudaSt
                             do_route ? static_cast<int>(L->g.K) : 0, static_cast<int>(L->g.top_k),
                             static_cast<int>(L->g.gs), static_cast<int>(L->g.G), static_cast<int>(L->g.k_pad),
                             L->ids.as<int32_t>(), L->gates.as<float>(), L->x16.as<__half>(), L->sx.as<float>(),
-                            L->route_ws.as<float>(), L->route_ticket.as<int32_t>(), do_route ? plan : nullptr,
-                            L->route_ticket.as<int32_t>() + L->cap, st),
+                            L->route_ws.as<float>(), L->route_ticket.as<int32_t>(), st),
                "route_kernel launch");
     count_launch(L);
 }
@@ -1570,7 +1562,7 @@ PlanArgs make_plan_args(tq_layer* L, int64_t batch, const int32_t* ids, int path
 
 // plan_done: the router already ran the plan (run_route with make_plan_args)
 void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids, const float* gates, float* y,
-                 int path, cudaStream_t st, bool plan_done = false) {
+                 int path, cudaStream_t st) {
     (void)x;
     const Geometry& g = L->g;
     const bool use_lotile = path != TQ_PATH_QMOE;
@@ -1582,10 +1574,8 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     const int pns = proj_nsplit(L, batch);
     const bool with_shared = use_qmoe && g.S > 0;
     const PlanArgs pa = make_plan_args(L, batch, ids, path);
-    if (!plan_done) {
-        cuda_check(launch_plan(pa, st), "plan_kernel launch");
-        count_launch(L);
-    }
+    cuda_check(launch_plan(pa, st), "plan_kernel launch");
+    count_launch(L);
     const int64_t atom_rows = rows_for(L, L->cap);   // capacity rows of xperm / extperm / ypart
     // projection pass: Z = P . x for every token (dense fp16 weights)
     if (use_lotile && L->proj_mb > 0) {
@@ -1677,20 +1667,7 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     p.groups = static_cast<int32_t>(g.G);
     p.rank = static_cast<int32_t>(g.r);
     // (an epilogue-fused combine -- red.global.add of at most two addends per output --
-    // measured slower at prefill than the separate combine pass; not used)
-    const bool fuse = false;
-    if (fuse) {
-        cuda_check(cudaMemsetAsync(y, 0, sizeof(float) * batch * g.o, st), "y memset");
-        p.fuse_combine = 1;
-        p.top_k = static_cast<int32_t>(g.top_k);
-        p.e_begin = static_cast<int32_t>(L->e_begin);
-        p.nsplit_dev = L->nsplit_d.as<int32_t>();
-        p.perm = L->perm.as<int32_t>();
-        p.offsets = L->offsets.as<int32_t>();
-        p.poffsets = L->poffsets.as<int32_t>();
-        p.gates = gates;
-        p.y_out = y;
-    }
+    // was measured slower at prefill than this separate combine pass)
     timed_expert_gemm(L, p, L->num_sms, st);
     count_launch(L);
     // combine
@@ -1714,7 +1691,6 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
     ca.sh_nsplit = pa.nsplit;
     ca.sh_from_offsets = 1;
     ca.nsplit_dev = L->nsplit_d.as<int32_t>();
-    ca.fused = fuse ? 1 : 0;
     ca.out = y;
     cuda_check(launch_combine(ca, st), "combine_kernel launch");
     count_launch(L);
@@ -1727,13 +1703,9 @@ void run_experts(tq_layer* L, const float* x, int64_t batch, const int32_t* ids,
 constexpr int64_t kDecMaxBatch = 256;  // slots per expert (and tokens) the decode workspace holds
 
 bool decode_ok(const tq_layer* L, int64_t batch, bool given) {
-    static const bool off = [] {
-        const char* e = std::getenv("TQ_NO_DECODE");   // 1: decode-sized batches on the grouped-GEMM path
-        return e && e[0] == '1';
-    }();
     const Geometry& g = L->g;
     const int64_t slots = given ? batch * g.top_k : batch;
-    return !off && !L->dense && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
+    return !L->dense && batch > 0 && slots <= kDecMaxBatch && g.top_k <= kDecMaxTopK && g.K <= 64 &&
            g.K + g.S <= kDecMaxW && L->e_begin == 0 && L->e_end == g.K && g.r <= 64 && g.G <= 64 && g.n_ext <= 4;
 }
 
@@ -2146,9 +2118,8 @@ tq_status tq_forward_routed(tq_layer* L, const float* x, int64_t batch, float* y
             if (dec) {
                 run_decode(L, x, batch, nullptr, nullptr, y, path, s2);
             } else {
-                const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
-                run_route(L, x, batch, true, s2, fuse_plan(L) ? &pa : nullptr);
-                run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2, fuse_plan(L));
+                run_route(L, x, batch, true, s2);
+                run_experts(L, x, batch, L->ids.as<int32_t>(), L->gates.as<float>(), y, path, s2);
             }
             if (ids)
                 cuda_check(cudaMemcpyAsync(ids, L->ids.p, sizeof(int32_t) * batch * L->g.top_k, cudaMemcpyDeviceToDevice,
@@ -2177,10 +2148,9 @@ tq_status tq_forward_host(tq_layer* L, const float* x, int64_t batch, float* y, 
             if (dec) {
                 run_decode(L, L->xin.as<float>(), batch, nullptr, nullptr, L->yout.as<float>(), path, s2);
             } else {
-                const PlanArgs pa = make_plan_args(L, batch, L->ids.as<int32_t>(), path);
-                run_route(L, L->xin.as<float>(), batch, true, s2, fuse_plan(L) ? &pa : nullptr);
+                run_route(L, L->xin.as<float>(), batch, true, s2);
                 run_experts(L, L->xin.as<float>(), batch, L->ids.as<int32_t>(), L->gates.as<float>(),
-                            L->yout.as<float>(), path, s2, fuse_plan(L));
+                            L->yout.as<float>(), path, s2);
             }
             cuda_check(cudaMemcpyAsync(y, L->yout.p, sizeof(float) * batch * L->g.o, cudaMemcpyDeviceToHost, s2),
                        "y D2H");
@@ -2534,7 +2504,7 @@ tq_status tq_route_raw(const float* x, int64_t batch, int64_t in_dim, const floa
         cuda_check(cudaMemsetAsync(ticket.p, 0, sizeof(int32_t) * batch, st), "cudaMemsetAsync");
         cuda_check(launch_route(x, static_cast<int>(batch), static_cast<int>(in_dim), gate,
                                 static_cast<int>(num_experts), static_cast<int>(top_k), 1, 0, 0, ids, gates, nullptr,
-                                nullptr, ws.as<float>(), ticket.as<int32_t>(), nullptr, nullptr, st),
+                                nullptr, ws.as<float>(), ticket.as<int32_t>(), st),
                    "route_kernel launch");
         cuda_check(cudaStreamSynchronize(st), "stream sync");   // workspace lifetime
     });

@@ -548,7 +548,7 @@ __device__ __forceinline__ float err_elem(const float* __restrict__ orig, const 
 
 // he[row][a] = sum_b double(H[a][b]) * e[row][b], b ascending (quant.cpp:333-337);
 // stored column-major (he_t[a][row - r0]) for the row-sequential pass.
-__global__ void __launch_bounds__(kTT) proxy_he_kernel(const float* __restrict__ orig,
+__global__ void __launch_bounds__(kTT, 4) proxy_he_kernel(const float* __restrict__ orig,
                                                         const uint8_t* __restrict__ codes,
                                                         const float* __restrict__ scales,
                                                         const int32_t* __restrict__ zeros, int64_t rows, int64_t dim,

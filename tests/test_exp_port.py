@@ -34,3 +34,17 @@ def test_exp_port_matches_libm():
         r = subprocess.run([exe, "15000000"], capture_output=True, text=True, timeout=300)
         print(r.stdout)
         assert r.returncode == 0, r.stdout
+
+
+def test_exp_table_regenerates():
+    """csrc/tq_exp.h's 2^(i/128) table is exactly what tools/gen_exp_table.py derives
+    from first principles (60-digit decimals)."""
+    import re
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(HERE), "tools"))
+    import gen_exp_table
+    src = open(os.path.join(CSRC, "tq_exp.h")).read()
+    body = src[src.index("kTab[256] = {"):src.index("};", src.index("kTab[256] = {"))]
+    words = [int(w, 16) for w in re.findall(r"0x([0-9a-f]{16})ull", body)]
+    want = [v for pair in gen_exp_table.table() for v in pair]
+    assert words == want
